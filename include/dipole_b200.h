@@ -1,0 +1,176 @@
+/* dipole_b200.h — C-ABI of the B200-native Barnes-Hut dipole-sum engine.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ * (`dipole::DipoleTree`, proj/include/dipole/bhtree.hpp:51-130, and the render
+ * step proj/include/dipole/renderer.hpp:365-385). The reference is a C++20
+ * library with no FFI; a maintainer swapping the CPU tree for this engine binds
+ * these symbols from C++ (include/dipole_b200.hpp re-exposes the reference
+ * class API on top of them) or from Python via ctypes.
+ *
+ * Conventions
+ *  - Every function returns an int status: 0 ok, 1 usage, 2 data
+ *    (reference DataError, util.hpp:35), 3 numerical (NumericalError), 4 CUDA.
+ *    dpl_last_error() returns the message of the calling thread's last failure.
+ *  - Array arguments may be HOST or DEVICE pointers (detected per call with
+ *    cudaPointerGetAttributes). Host arrays are staged through the handle's
+ *    stream; device arrays are used in place. Results are complete when the
+ *    call returns for host outputs; device outputs are ordered on the handle's
+ *    stream (dpl_tree_sync() waits).
+ *  - A handle is not thread-safe (as the reference: build / update_moments /
+ *    flush need exclusive access). One handle = one GPU + stream.
+ *  - Layouts are row-major: positions N x 3, moments N x C with channel 0 the
+ *    geometry moment and 1..C-1 the appearance moments (bhtree.cpp:31-32).
+ *  - There is no CPU fallback: every entry point runs sm_100a kernels.
+ */
+#ifndef DIPOLE_B200_H_
+#define DIPOLE_B200_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DPL_OK 0
+#define DPL_ERR_USAGE 1
+#define DPL_ERR_DATA 2
+#define DPL_ERR_NUMERICAL 3
+#define DPL_ERR_CUDA 4
+
+/* ChannelKernel (bhtree.hpp:13) */
+#define DPL_DIPOLE 0
+#define DPL_RADIAL 1
+
+typedef struct dpl_tree_s* dpl_tree_t;
+typedef struct dpl_gradbuf_s* dpl_gradbuf_t;
+typedef struct dpl_tape_s* dpl_tape_t;
+
+/* KernelParams (kernels.hpp:156-161); epsilon <= 0 selects the singular kernel */
+typedef struct {
+  double epsilon;
+  int32_t desingularized;
+  int32_t reserved;
+  double desing_delta;
+  double coincident_value;
+} dpl_kernel_params;
+
+/* Counters of one query, replaying the reference's decisions (visited is
+ * bhtree.cpp:201): nodes popped, far-field accepts (area > 0) with t < 6.5 and
+ * t >= 6.5, leaf-point interactions with t < 6.5 and t >= 6.5. */
+typedef struct {
+  int64_t visited, far_near, far_far, pt_near, pt_far;
+} dpl_counters;
+
+const char* dpl_last_error(void);
+int dpl_version(void);
+/* Number of kernel launches this process has issued through the library. */
+int64_t dpl_launch_count(void);
+
+/* ---- tree lifecycle: DipoleTree::build / update_moments / set_channel_kernels */
+/* stream: a cudaStream_t, or NULL for a library-owned non-blocking stream. */
+int dpl_tree_create(int device, void* stream, dpl_tree_t* out);
+int dpl_tree_destroy(dpl_tree_t tree);
+int dpl_tree_set_stream(dpl_tree_t tree, void* stream);
+int dpl_tree_sync(dpl_tree_t tree);
+
+/* DipoleTree::build (bhtree.cpp:158-169): GPU Morton-digit sort + level-by-level
+ * BFS numbering reproduces build_structure (:36-105) bit-exactly; geometry
+ * (:107-134) and moments (:136-156) follow. Channel kernels reset to Dipole. */
+int dpl_tree_build(dpl_tree_t tree, const double* pos, const double* nrm, const double* area,
+                   const double* mu, int64_t n, int32_t channels, int32_t max_leaf_size,
+                   int32_t max_depth);
+/* DipoleTree::update_moments (bhtree.cpp:171-176): refreshes point data
+ * (positions too, as refresh_point_data does) and node moments. */
+int dpl_tree_update_moments(dpl_tree_t tree, const double* pos, const double* nrm,
+                            const double* area, const double* mu, int64_t n, int32_t channels);
+/* DipoleTree::set_channel_kernels (bhtree.cpp:178-182); kinds[c] in {DPL_DIPOLE, DPL_RADIAL}. */
+int dpl_tree_set_channel_kernels(dpl_tree_t tree, const uint8_t* kinds, int32_t channels);
+
+int dpl_tree_channels(dpl_tree_t tree, int32_t* channels);
+int dpl_tree_point_count(dpl_tree_t tree, int64_t* n);
+int dpl_tree_node_count(dpl_tree_t tree, int64_t* nodes);
+/* nodes() / point_order() / point_leaf (bhtree.hpp:69-70,119): geo nodes x 5
+ * (cx, cy, cz, area, radius), topo nodes x 6 (begin, end, child_begin,
+ * child_count, parent, leaf), order N, leaf_of N. Any pointer may be NULL. */
+int dpl_tree_export(dpl_tree_t tree, double* geo, int32_t* topo, int32_t* point_order,
+                    int32_t* point_leaf);
+/* Node moments (moments_v_ nodes x C x 3, moments_s_ nodes x C), fp32 as stored. */
+int dpl_tree_export_moments(dpl_tree_t tree, float* moments_v, float* moments_s);
+/* DipoleTree::dump "DPLT" v1 byte format (bhtree.cpp:465-494). */
+int dpl_tree_dump(dpl_tree_t tree, const char* path);
+
+/* ---- forward queries -------------------------------------------------------
+ * DipoleTree::primal / primal_with_gradient (bhtree.cpp:188-234,276-334) for a
+ * batch of q query points xs (q x 3, fp64 like Vec3). out: q x C fp32.
+ * grad: NULL (values only) or q x C x 3. counters: NULL or q records.
+ * Opening decisions are evaluated in fp64 exactly as the reference does
+ * (d = centroid - x; (dx*dx + dy*dy) + dz*dz > (beta^2 * r) * r), so the
+ * far-field/leaf sets match the reference's; interaction arithmetic is fp32. */
+int dpl_primal(dpl_tree_t tree, const dpl_kernel_params* params, double beta_bh,
+               const double* xs, int64_t q, float* out, float* grad, dpl_counters* counters);
+/* DipoleTree::primal_channel (bhtree.cpp:236-274): one channel, out q. */
+int dpl_primal_channel(dpl_tree_t tree, const dpl_kernel_params* params, double beta_bh,
+                       const double* xs, int64_t q, int32_t channel, float* out);
+/* Same as dpl_primal but only the gradient of the FIRST channel is produced
+ * (grad0: q x 3); this is what the render step consumes (renderer.cpp:125-127). */
+int dpl_primal_grad0(dpl_tree_t tree, const dpl_kernel_params* params, double beta_bh,
+                     const double* xs, int64_t q, float* out, float* grad0);
+
+/* ---- adjoint (two-stage) ---------------------------------------------------
+ * GradientBuffer (bhtree.hpp:40-49): device fp64 accumulators node_v, node_s,
+ * point_mu, point_n, d_epsilon. */
+int dpl_gradbuf_create(dpl_tree_t tree, dpl_gradbuf_t* out);
+int dpl_gradbuf_destroy(dpl_gradbuf_t buf);
+int dpl_gradbuf_zero(dpl_gradbuf_t buf);
+/* DipoleTree::adjoint (bhtree.cpp:345-417) for q queries: d_out q x C,
+ * d_grad NULL or q x C x 3 (radial channels ignore d_grad, as the reference).
+ * Warp-aggregated accumulation into node / leaf-point buffers; no per-point
+ * ancestor walk here. */
+int dpl_adjoint(dpl_tree_t tree, const dpl_kernel_params* params, double beta_bh,
+                const double* xs, int64_t q, const float* d_out, const float* d_grad,
+                dpl_gradbuf_t buf);
+/* DipoleTree::flush_gradients (bhtree.cpp:419-463): sums nbuf buffers, pushes
+ * node accumulators down to points (top-down, O(nodes*C + N*C)), zeroes the
+ * buffers. moments N x C, normals N x 3 (fp32, any may be NULL), d_epsilon. */
+int dpl_flush(dpl_tree_t tree, dpl_gradbuf_t* bufs, int32_t nbuf, float* moments,
+              float* normals, double* d_epsilon);
+
+/* ---- render step (renderer.cpp:106-231) ------------------------------------
+ * Rays are (origin, dir) fp64 (R x 6). Samples per ray: S; when ts is NULL the
+ * stratified sampler t_j = t_near + (t_far - t_near) * ((j + u_j) / S) with
+ * u_j = dpl_uniform(seed, ray * S + j) is used (identical bits in the oracle);
+ * otherwise ts / deltas are R x S fp64 (RaySamples, renderer.hpp:322-326).
+ * The head is direct-rgb (radiance.cpp:133-145): rgb = logistic(D_1..3). */
+typedef struct {
+  double lambda_scale;   /* SceneModel::lambda_scale (fields.hpp:17) */
+  double beta_bh;        /* SceneModel::beta_bh */
+  double background[3];  /* SceneModel::background */
+  double t_near, t_far;  /* sampler range (used when ts == NULL) */
+  uint64_t seed;         /* sampler seed (used when ts == NULL) */
+} dpl_render_params;
+
+int dpl_tape_create(dpl_tape_t* out);
+int dpl_tape_destroy(dpl_tape_t tape);
+/* render_ray for R rays (tape recorded on device). rgb: R x 3 fp32 output. */
+int dpl_render_forward(dpl_tree_t tree, const dpl_kernel_params* params,
+                       const dpl_render_params* rp, const double* rays, int64_t R, int32_t S,
+                       const double* ts, const double* deltas, float* rgb, dpl_tape_t tape);
+/* render_ray_backward with d_weight = 0: d_rgb R x 3 fp32; emits the adjoint
+ * queries into buf; d_lambda / d_background (3) are summed over rays (fp64). */
+int dpl_render_backward(dpl_tree_t tree, const dpl_kernel_params* params,
+                        const dpl_render_params* rp, dpl_tape_t tape, const float* d_rgb,
+                        dpl_gradbuf_t buf, double* d_lambda, double* d_background);
+/* The sampler's uniform draw, exported so host code can reproduce it. */
+double dpl_uniform(uint64_t seed, uint64_t counter);
+
+/* ---- Adam (optimizer.cpp:65-81) on device parameter groups ------------------ */
+/* In-place Adam on n fp32 params with fp32 grads and fp32 m/v state; step t is
+ * the 1-based iteration after increment. */
+int dpl_adam_step(dpl_tree_t tree, float* params, const float* grads, float* m, float* v,
+                  int64_t n, double lr, double beta1, double beta2, double eps, int64_t t);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DIPOLE_B200_H_ */

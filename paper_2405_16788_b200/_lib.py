@@ -1,0 +1,129 @@
+"""ctypes binding of libdipole_b200.so (include/dipole_b200.h).
+
+The shared library is built in-tree by ``__graft_entry__.build()``. There is no
+fallback: if it is missing, importing the engine raises immediately.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdipole_b200.so")
+
+DPL_OK, DPL_ERR_USAGE, DPL_ERR_DATA, DPL_ERR_NUMERICAL, DPL_ERR_CUDA = range(5)
+DPL_DIPOLE, DPL_RADIAL = 0, 1
+
+
+class DataError(RuntimeError):
+    """dipole::DataError (util.hpp:35): bad input — empty cloud, size mismatch."""
+
+
+class NumericalError(RuntimeError):
+    """dipole::NumericalError (util.hpp:38)."""
+
+
+class UsageError(ValueError):
+    pass
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+class KernelParams(C.Structure):
+    """KernelParams (kernels.hpp:156-161) == dpl_kernel_params."""
+
+    _fields_ = [("epsilon", C.c_double), ("desingularized", C.c_int32), ("reserved", C.c_int32),
+                ("desing_delta", C.c_double), ("coincident_value", C.c_double)]
+
+    def __init__(self, epsilon=0.0, desingularized=False, desing_delta=0.0, coincident_value=0.0):
+        super().__init__(float(epsilon), int(bool(desingularized)), 0, float(desing_delta),
+                         float(coincident_value))
+
+
+class Counters(C.Structure):
+    _fields_ = [(n, C.c_int64) for n in ("visited", "far_near", "far_far", "pt_near", "pt_far")]
+
+
+class RenderParams(C.Structure):
+    _fields_ = [("lambda_scale", C.c_double), ("beta_bh", C.c_double),
+                ("background", C.c_double * 3), ("t_near", C.c_double), ("t_far", C.c_double),
+                ("seed", C.c_uint64)]
+
+
+_lib = None
+
+_vp = C.c_void_p
+_sig = {
+    "dpl_last_error": (C.c_char_p, []),
+    "dpl_version": (C.c_int, []),
+    "dpl_launch_count": (C.c_int64, []),
+    "dpl_tree_create": (C.c_int, [C.c_int, _vp, C.POINTER(_vp)]),
+    "dpl_tree_destroy": (C.c_int, [_vp]),
+    "dpl_tree_set_stream": (C.c_int, [_vp, _vp]),
+    "dpl_tree_sync": (C.c_int, [_vp]),
+    "dpl_tree_build": (C.c_int, [_vp, _vp, _vp, _vp, _vp, C.c_int64, C.c_int32, C.c_int32,
+                                 C.c_int32]),
+    "dpl_tree_update_moments": (C.c_int, [_vp, _vp, _vp, _vp, _vp, C.c_int64, C.c_int32]),
+    "dpl_tree_set_channel_kernels": (C.c_int, [_vp, _vp, C.c_int32]),
+    "dpl_tree_channels": (C.c_int, [_vp, C.POINTER(C.c_int32)]),
+    "dpl_tree_point_count": (C.c_int, [_vp, C.POINTER(C.c_int64)]),
+    "dpl_tree_node_count": (C.c_int, [_vp, C.POINTER(C.c_int64)]),
+    "dpl_tree_export": (C.c_int, [_vp, _vp, _vp, _vp, _vp]),
+    "dpl_tree_export_moments": (C.c_int, [_vp, _vp, _vp]),
+    "dpl_tree_dump": (C.c_int, [_vp, C.c_char_p]),
+    "dpl_primal": (C.c_int, [_vp, C.POINTER(KernelParams), C.c_double, _vp, C.c_int64, _vp, _vp,
+                             _vp]),
+    "dpl_primal_channel": (C.c_int, [_vp, C.POINTER(KernelParams), C.c_double, _vp, C.c_int64,
+                                     C.c_int32, _vp]),
+    "dpl_primal_grad0": (C.c_int, [_vp, C.POINTER(KernelParams), C.c_double, _vp, C.c_int64,
+                                   _vp, _vp]),
+    "dpl_gradbuf_create": (C.c_int, [_vp, C.POINTER(_vp)]),
+    "dpl_gradbuf_destroy": (C.c_int, [_vp]),
+    "dpl_gradbuf_zero": (C.c_int, [_vp]),
+    "dpl_adjoint": (C.c_int, [_vp, C.POINTER(KernelParams), C.c_double, _vp, C.c_int64, _vp, _vp,
+                              _vp]),
+    "dpl_flush": (C.c_int, [_vp, C.POINTER(_vp), C.c_int32, _vp, _vp, C.POINTER(C.c_double)]),
+    "dpl_tape_create": (C.c_int, [C.POINTER(_vp)]),
+    "dpl_tape_destroy": (C.c_int, [_vp]),
+    "dpl_render_forward": (C.c_int, [_vp, C.POINTER(KernelParams), C.POINTER(RenderParams), _vp,
+                                     C.c_int64, C.c_int32, _vp, _vp, _vp, _vp]),
+    "dpl_render_backward": (C.c_int, [_vp, C.POINTER(KernelParams), C.POINTER(RenderParams), _vp,
+                                      _vp, _vp, C.POINTER(C.c_double), _vp]),
+    "dpl_uniform": (C.c_double, [C.c_uint64, C.c_uint64]),
+    "dpl_adam_step": (C.c_int, [_vp, _vp, _vp, _vp, _vp, C.c_int64, C.c_double, C.c_double,
+                                C.c_double, C.c_double, C.c_int64]),
+}
+
+EXPORTED_SYMBOLS = tuple(_sig)
+
+
+def lib():
+    """Load the CUDA engine; raises if it has not been built (no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: build the sm_100a engine with "
+                "`python -c 'import __graft_entry__ as g; g.build()'` (there is no CPU fallback)")
+        lb = C.CDLL(LIB_PATH)
+        for name, (res, args) in _sig.items():
+            f = getattr(lb, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = lb
+    return _lib
+
+
+def check(rc):
+    if rc == DPL_OK:
+        return
+    msg = lib().dpl_last_error().decode(errors="replace")
+    if rc == DPL_ERR_DATA:
+        raise DataError(msg)
+    if rc == DPL_ERR_NUMERICAL:
+        raise NumericalError(msg)
+    if rc == DPL_ERR_CUDA:
+        raise CudaError(msg)
+    raise UsageError(msg)

@@ -1,0 +1,311 @@
+"""Python mirror of ``dipole::DipoleTree`` (proj/include/dipole/bhtree.hpp:51-130).
+
+Same method names, argument meaning and error behaviour as the reference, with
+batched queries: where the reference takes one ``Vec3 x`` per call, these take
+``xs`` of shape (Q, 3) and return (Q, C) outputs. Arrays may be numpy arrays
+(host) or torch tensors (host or CUDA); outputs follow the query array's
+device unless ``out=`` is given. Every call runs the sm_100a kernels of
+libdipole_b200.so — there is no CPU path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from ._lib import (DPL_DIPOLE, DPL_RADIAL, Counters, DataError, KernelParams, NumericalError,
+                   check, lib)
+
+try:  # torch is optional plumbing (device memory, streams)
+    import torch
+except Exception:  # pragma: no cover
+    torch = None
+
+Dipole, Radial = DPL_DIPOLE, DPL_RADIAL
+
+
+def _is_torch(a):
+    return torch is not None and isinstance(a, torch.Tensor)
+
+
+def _in(a, np_dtype, shape=None):
+    """(pointer, keepalive) for an input array."""
+    if a is None:
+        return None, None
+    if _is_torch(a):
+        tdt = {np.float64: torch.float64, np.float32: torch.float32, np.uint8: torch.uint8}[np_dtype]
+        t = a.detach().to(tdt).contiguous()
+        if shape is not None:
+            t = t.reshape(shape)
+        return t.data_ptr(), t
+    arr = np.ascontiguousarray(a, dtype=np_dtype)
+    if shape is not None:
+        arr = arr.reshape(shape)
+    return arr.ctypes.data, arr
+
+
+def _out_like(ref, shape, np_dtype):
+    """Allocate an output on the device of `ref`."""
+    if _is_torch(ref) and ref.is_cuda:
+        tdt = {np.float32: torch.float32, np.float64: torch.float64, np.int64: torch.int64}[np_dtype]
+        t = torch.empty(shape, dtype=tdt, device=ref.device)
+        return t.data_ptr(), t
+    arr = np.empty(shape, dtype=np_dtype)
+    return arr.ctypes.data, arr
+
+
+@dataclass
+class OrientedPointCloud:
+    """OrientedPointCloud (pointcloud.hpp:19-35) in SoA form: moments[:, 0] is the
+    geometry moment and moments[:, 1:] the k_appearance appearance moments."""
+
+    positions: object
+    normals: object
+    areas: object
+    moments: object
+
+    @property
+    def size(self):
+        return int(self.positions.shape[0])
+
+    @property
+    def channels(self):
+        return int(self.moments.shape[1]) if len(self.moments.shape) > 1 else 1
+
+    @property
+    def k_appearance(self):
+        return self.channels - 1
+
+
+@dataclass
+class PointGradients:
+    """PointGradients (bhtree.hpp:28-36)."""
+
+    channels: int
+    moments: object   # N x C
+    normals: object   # N x 3
+    d_epsilon: float = 0.0
+
+    def moment(self, point, channel):
+        return self.moments[point, channel]
+
+
+class GradientBuffer:
+    """GradientBuffer (bhtree.hpp:40-49): device fp64 accumulators."""
+
+    def __init__(self, tree: "DipoleTree"):
+        h = C.c_void_p()
+        check(lib().dpl_gradbuf_create(tree._h, C.byref(h)))
+        self._h = h.value
+        self.tree = tree
+        self.dirty = False
+
+    def reset(self):
+        check(lib().dpl_gradbuf_zero(self._h))
+        self.dirty = False
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().dpl_gradbuf_destroy(self._h)
+            self._h = None
+
+
+class DipoleTree:
+    kDefaultMaxLeafSize = 8
+    kDefaultMaxDepth = 20
+
+    def __init__(self, device: int = 0, stream=None):
+        h = C.c_void_p()
+        s = None
+        if stream is not None:
+            s = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+        check(lib().dpl_tree_create(int(device), s, C.byref(h)))
+        self._h = h.value
+        self.device = device
+        self._built = False
+        self._kinds = None
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().dpl_tree_destroy(self._h)
+            self._h = None
+
+    def set_stream(self, stream):
+        s = stream.cuda_stream if hasattr(stream, "cuda_stream") else stream
+        check(lib().dpl_tree_set_stream(self._h, s))
+
+    def synchronize(self):
+        check(lib().dpl_tree_sync(self._h))
+
+    # -- build / moments ---------------------------------------------------------
+    def build(self, cloud: OrientedPointCloud, max_leaf_size=kDefaultMaxLeafSize,
+              max_depth=kDefaultMaxDepth):
+        """DipoleTree::build (bhtree.cpp:158-169)."""
+        n = cloud.size
+        if n == 0:
+            raise DataError("DipoleTree::build: empty cloud")
+        Cc = cloud.channels
+        p, k1 = _in(cloud.positions, np.float64, (n, 3))
+        q, k2 = _in(cloud.normals, np.float64, (n, 3))
+        a, k3 = _in(cloud.areas, np.float64, (n,))
+        m, k4 = _in(cloud.moments, np.float64, (n, Cc))
+        check(lib().dpl_tree_build(self._h, p, q, a, m, n, Cc, int(max_leaf_size), int(max_depth)))
+        self._built = True
+        self._kinds = np.zeros(Cc, np.uint8)
+
+    def update_moments(self, cloud: OrientedPointCloud):
+        """DipoleTree::update_moments (bhtree.cpp:171-176)."""
+        n = cloud.size
+        Cc = cloud.channels
+        p, k1 = _in(cloud.positions, np.float64, (n, 3))
+        q, k2 = _in(cloud.normals, np.float64, (n, 3))
+        a, k3 = _in(cloud.areas, np.float64, (n,))
+        m, k4 = _in(cloud.moments, np.float64, (n, Cc))
+        check(lib().dpl_tree_update_moments(self._h, p, q, a, m, n, Cc))
+
+    def set_channel_kernels(self, kernels):
+        """DipoleTree::set_channel_kernels (bhtree.cpp:178-182)."""
+        k = np.ascontiguousarray(kernels, dtype=np.uint8)
+        check(lib().dpl_tree_set_channel_kernels(self._h, k.ctypes.data, len(k)))
+        self._kinds = k.copy()
+
+    def channel_kernels(self):
+        return None if self._kinds is None else self._kinds.copy()
+
+    def channels(self) -> int:
+        c = C.c_int32()
+        check(lib().dpl_tree_channels(self._h, C.byref(c)))
+        return c.value
+
+    def point_count(self) -> int:
+        c = C.c_int64()
+        check(lib().dpl_tree_point_count(self._h, C.byref(c)))
+        return c.value
+
+    def node_count(self) -> int:
+        c = C.c_int64()
+        check(lib().dpl_tree_node_count(self._h, C.byref(c)))
+        return c.value
+
+    def export(self):
+        """nodes() + point_order() + point_leaf as arrays (TreeNode, bhtree.hpp:15-24)."""
+        nn, n = self.node_count(), self.point_count()
+        geo = np.zeros((nn, 5))
+        topo = np.zeros((nn, 6), np.int32)
+        order = np.zeros(n, np.int32)
+        leaf_of = np.zeros(n, np.int32)
+        check(lib().dpl_tree_export(self._h, geo.ctypes.data, topo.ctypes.data, order.ctypes.data,
+                                    leaf_of.ctypes.data))
+        return dict(geo=geo, topo=topo, order=order, leaf_of=leaf_of)
+
+    def nodes(self):
+        e = self.export()
+        g, t = e["geo"], e["topo"]
+        return dict(centroid=g[:, :3], area=g[:, 3], radius=g[:, 4], begin=t[:, 0], end=t[:, 1],
+                    child_begin=t[:, 2], child_count=t[:, 3], parent=t[:, 4],
+                    leaf=t[:, 5].astype(bool))
+
+    def point_order(self):
+        return self.export()["order"]
+
+    def export_moments(self):
+        nn, Cc = self.node_count(), self.channels()
+        mv = np.zeros((nn, Cc, 3), np.float32)
+        ms = np.zeros((nn, Cc), np.float32)
+        check(lib().dpl_tree_export_moments(self._h, mv.ctypes.data, ms.ctypes.data))
+        return mv, ms
+
+    def dump(self, path: str):
+        """DipoleTree::dump "DPLT" v1 (bhtree.cpp:465-494)."""
+        check(lib().dpl_tree_dump(self._h, str(path).encode()))
+
+    # -- forward queries ----------------------------------------------------------
+    def primal(self, xs, params: KernelParams, beta_bh: float, out=None, visited=False):
+        """DipoleTree::primal (bhtree.cpp:188-234) for a (Q, 3) batch -> (Q, C) fp32.
+        visited=True also returns the per-query counters (Q, 5): visited, far
+        near/far, point near/far."""
+        q = int(xs.shape[0])
+        Cc = self.channels()
+        xp, xk = _in(xs, np.float64, (q, 3))
+        if out is None:
+            op, out = _out_like(xk, (q, Cc), np.float32)
+        else:
+            op = out.data_ptr() if _is_torch(out) else out.ctypes.data
+        cnt = None
+        cp = None
+        if visited:
+            cp, cnt = _out_like(xk, (q, 5), np.int64)
+        check(lib().dpl_primal(self._h, C.byref(params), float(beta_bh), xp, q, op, None, cp))
+        return (out, cnt) if visited else out
+
+    def primal_channel(self, xs, params: KernelParams, beta_bh: float, channel: int):
+        """DipoleTree::primal_channel (bhtree.cpp:236-274) -> (Q,) fp32."""
+        q = int(xs.shape[0])
+        xp, xk = _in(xs, np.float64, (q, 3))
+        op, out = _out_like(xk, (q,), np.float32)
+        check(lib().dpl_primal_channel(self._h, C.byref(params), float(beta_bh), xp, q,
+                                       int(channel), op))
+        return out
+
+    def primal_with_gradient(self, xs, params: KernelParams, beta_bh: float):
+        """DipoleTree::primal_with_gradient (bhtree.cpp:276-334) -> ((Q, C), (Q, C, 3))."""
+        q = int(xs.shape[0])
+        Cc = self.channels()
+        xp, xk = _in(xs, np.float64, (q, 3))
+        op, out = _out_like(xk, (q, Cc), np.float32)
+        gp, grad = _out_like(xk, (q, Cc, 3), np.float32)
+        check(lib().dpl_primal(self._h, C.byref(params), float(beta_bh), xp, q, op, gp, None))
+        return out, grad
+
+    def primal_grad0(self, xs, params: KernelParams, beta_bh: float):
+        """Values of all channels and the gradient of channel 0 only (render path)."""
+        q = int(xs.shape[0])
+        Cc = self.channels()
+        xp, xk = _in(xs, np.float64, (q, 3))
+        op, out = _out_like(xk, (q, Cc), np.float32)
+        gp, grad = _out_like(xk, (q, 3), np.float32)
+        check(lib().dpl_primal_grad0(self._h, C.byref(params), float(beta_bh), xp, q, op, gp))
+        return out, grad
+
+    # -- adjoint ------------------------------------------------------------------
+    def make_buffer(self) -> GradientBuffer:
+        return GradientBuffer(self)
+
+    def adjoint(self, xs, params: KernelParams, beta_bh: float, d_out, d_grad, buf: GradientBuffer):
+        """DipoleTree::adjoint (bhtree.cpp:345-417) for a (Q, 3) batch; d_out (Q, C),
+        d_grad None or (Q, C, 3)."""
+        q = int(xs.shape[0])
+        Cc = self.channels()
+        xp, k1 = _in(xs, np.float64, (q, 3))
+        dp, k2 = _in(d_out, np.float32, (q, Cc))
+        gp, k3 = _in(d_grad, np.float32, (q, Cc, 3)) if d_grad is not None else (None, None)
+        check(lib().dpl_adjoint(self._h, C.byref(params), float(beta_bh), xp, q, dp, gp, buf._h))
+        buf.dirty = True
+
+    def flush_gradients(self, buffers, device_out=None) -> PointGradients:
+        """DipoleTree::flush_gradients (bhtree.cpp:419-463); zeroes the buffers.
+        device_out: a torch device to receive the outputs (else numpy)."""
+        if isinstance(buffers, GradientBuffer):
+            buffers = [buffers]
+        n, Cc = self.point_count(), self.channels()
+        arr = (C.c_void_p * len(buffers))(*[b._h for b in buffers])
+        if device_out is not None:
+            mom = torch.empty((n, Cc), dtype=torch.float32, device=device_out)
+            nrm = torch.empty((n, 3), dtype=torch.float32, device=device_out)
+            mp, np_ = mom.data_ptr(), nrm.data_ptr()
+        else:
+            mom = np.empty((n, Cc), np.float32)
+            nrm = np.empty((n, 3), np.float32)
+            mp, np_ = mom.ctypes.data, nrm.ctypes.data
+        de = C.c_double()
+        check(lib().dpl_flush(self._h, arr, len(buffers), mp, np_, C.byref(de)))
+        for b in buffers:
+            b.dirty = False
+        return PointGradients(Cc, mom, nrm, de.value)
+
+
+def launch_count() -> int:
+    """Kernel launches issued through the engine in this process."""
+    return int(lib().dpl_launch_count())

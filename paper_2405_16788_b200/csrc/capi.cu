@@ -1,0 +1,670 @@
+// capi.cu — the extern "C" boundary (include/dipole_b200.h).
+//
+// Each entry point validates its arguments the way the reference's methods do
+// (DataError on empty clouds / size or channel mismatches, bhtree.cpp:159,173,
+// 180), stages host arrays through the handle's stream, runs the sm_100a
+// kernels, and maps exceptions to status codes + a thread-local message.
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <fstream>
+#include <string>
+#include <vector>
+
+#include "../../include/dipole_b200.h"
+#include "adjoint.cuh"
+#include "forward.cuh"
+#include "render.cuh"
+#include "tree.cuh"
+
+namespace dpl {
+static std::atomic<long long> g_launches{0};
+void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+}  // namespace dpl
+
+using namespace dpl;
+
+struct dpl_tree_s {
+  Tree t;
+  bool built = false;
+  DevBuf ws_xs, ws_perm, ws_out, ws_grad, ws_cnt, ws_morton, ws_dout, ws_dgrad, ws_flag, ws_mom,
+      ws_nrm;
+};
+
+struct dpl_gradbuf_s {
+  dpl_tree_s* tree;
+  GradBuf b;
+};
+
+struct dpl_tape_s {
+  int64_t R = 0;
+  int S = 0;
+  int C = 0;
+  double t_near = 0;
+  DevBuf rays, ts, deltas, xs, perm, vals, g0, tape, dout, dgrad, sums, morton;
+  bool has_deltas = false;
+};
+
+static thread_local std::string g_err;
+
+template <typename F>
+static int guard(F&& f) {
+  try {
+    f();
+    return DPL_OK;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_err = "host out of memory";
+    return DPL_ERR_CUDA;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return DPL_ERR_USAGE;
+  }
+}
+
+static void require(bool ok, int code, const char* msg) {
+  if (!ok) throw Error(code, msg);
+}
+
+static bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  cudaError_t e = cudaPointerGetAttributes(&a, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// device view of an input array (copied in when it lives on the host)
+template <typename T>
+static const T* stage_in(Tree& t, const T* p, size_t count, DevBuf& tmp) {
+  if (!p) return nullptr;
+  if (is_device_ptr(p)) return p;
+  tmp.reserve(std::max<size_t>(1, count) * sizeof(T));
+  if (count)
+    DPL_CUDA(cudaMemcpyAsync(tmp.p, p, count * sizeof(T), cudaMemcpyHostToDevice, t.stream));
+  return tmp.as<T>();
+}
+
+// device target for an output array; host targets get copied back by finish()
+template <typename T>
+struct Out {
+  T* user = nullptr;
+  T* dev = nullptr;
+  size_t count = 0;
+  bool host = false;
+  void bind(Tree& t, T* p, size_t n, DevBuf& tmp) {
+    user = p;
+    count = n;
+    if (!p) return;
+    host = !is_device_ptr(p);
+    if (host) {
+      tmp.reserve(std::max<size_t>(1, n) * sizeof(T));
+      dev = tmp.as<T>();
+    } else {
+      dev = p;
+    }
+  }
+  void finish(Tree& t) {
+    if (host && count)
+      DPL_CUDA(cudaMemcpyAsync(user, dev, count * sizeof(T), cudaMemcpyDeviceToHost, t.stream));
+  }
+};
+
+static void check_params(const dpl_kernel_params* p) {
+  require(p != nullptr, DPL_ERR_USAGE, "null kernel params");
+  require(!std::isnan(p->epsilon), DPL_ERR_DATA, "epsilon is NaN");
+}
+
+static void check_tree(dpl_tree_t h) {
+  require(h != nullptr, DPL_ERR_USAGE, "null tree handle");
+  require(h->built, DPL_ERR_USAGE, "tree not built");
+}
+
+static int* overflow_flag(dpl_tree_t h) {
+  if (h->ws_flag.bytes < 4) {
+    h->ws_flag.reserve(4);
+    DPL_CUDA(cudaMemsetAsync(h->ws_flag.p, 0, 4, h->t.stream));
+  }
+  return h->ws_flag.as<int>();
+}
+
+static void check_overflow(dpl_tree_t h) {
+  int v = 0;
+  DPL_CUDA(cudaMemcpyAsync(&v, h->ws_flag.p, 4, cudaMemcpyDeviceToHost, h->t.stream));
+  DPL_CUDA(cudaStreamSynchronize(h->t.stream));
+  if (v) {
+    DPL_CUDA(cudaMemsetAsync(h->ws_flag.p, 0, 4, h->t.stream));
+    throw Error(DPL_ERR_NUMERICAL, "traversal stack overflow");
+  }
+}
+
+extern "C" {
+
+const char* dpl_last_error(void) { return g_err.c_str(); }
+int dpl_version(void) { return 1; }
+int64_t dpl_launch_count(void) { return (int64_t)g_launches.load(); }
+
+int dpl_tree_create(int device, void* stream, dpl_tree_t* out) {
+  return guard([&] {
+    require(out != nullptr, DPL_ERR_USAGE, "null out");
+    DPL_CUDA(cudaSetDevice(device));
+    auto h = new dpl_tree_s();
+    h->t.device = device;
+    if (stream) {
+      h->t.stream = (cudaStream_t)stream;
+    } else {
+      cudaError_t e = cudaStreamCreateWithFlags(&h->t.stream, cudaStreamNonBlocking);
+      if (e != cudaSuccess) {
+        delete h;
+        throw Error(DPL_ERR_CUDA, cudaGetErrorString(e));
+      }
+      h->t.own_stream = true;
+    }
+    *out = h;
+  });
+}
+
+int dpl_tree_destroy(dpl_tree_t h) {
+  return guard([&] {
+    if (!h) return;
+    cudaSetDevice(h->t.device);
+    cudaStreamSynchronize(h->t.stream);
+    cudaStream_t s = h->t.stream;
+    bool own = h->t.own_stream;
+    delete h;
+    if (own) cudaStreamDestroy(s);
+  });
+}
+
+int dpl_tree_set_stream(dpl_tree_t h, void* stream) {
+  return guard([&] {
+    require(h != nullptr, DPL_ERR_USAGE, "null tree handle");
+    DPL_CUDA(cudaStreamSynchronize(h->t.stream));
+    if (h->t.own_stream) cudaStreamDestroy(h->t.stream);
+    h->t.own_stream = false;
+    h->t.stream = (cudaStream_t)stream;
+  });
+}
+
+int dpl_tree_sync(dpl_tree_t h) {
+  return guard([&] {
+    require(h != nullptr, DPL_ERR_USAGE, "null tree handle");
+    DPL_CUDA(cudaStreamSynchronize(h->t.stream));
+    if (h->ws_flag.p) check_overflow(h);
+  });
+}
+
+int dpl_tree_build(dpl_tree_t h, const double* pos, const double* nrm, const double* area,
+                   const double* mu, int64_t n, int32_t channels, int32_t max_leaf_size,
+                   int32_t max_depth) {
+  return guard([&] {
+    require(h != nullptr, DPL_ERR_USAGE, "null tree handle");
+    if (n <= 0) throw Error(DPL_ERR_DATA, "DipoleTree::build: empty cloud");
+    require(pos && nrm && area && mu, DPL_ERR_USAGE, "null cloud array");
+    DPL_CUDA(cudaSetDevice(h->t.device));
+    h->built = false;
+    tree_build(h->t, pos, nrm, area, mu, n, channels, max_leaf_size, max_depth);
+    h->built = true;
+  });
+}
+
+int dpl_tree_update_moments(dpl_tree_t h, const double* pos, const double* nrm,
+                            const double* area, const double* mu, int64_t n, int32_t channels) {
+  return guard([&] {
+    check_tree(h);
+    if (n != h->t.n || channels != h->t.C)
+      throw Error(DPL_ERR_DATA, "DipoleTree::update_moments: cloud/tree size mismatch");
+    tree_update_points(h->t, pos, nrm, area, mu);
+    // sorted fp64 positions follow the refreshed cloud (refresh_point_data, :20-34);
+    // node geometry is NOT rebuilt, as in the reference
+    tree_compute_moments(h->t);
+    tree_refresh_sorted_positions(h->t);
+    DPL_CUDA(cudaStreamSynchronize(h->t.stream));
+  });
+}
+
+int dpl_tree_set_channel_kernels(dpl_tree_t h, const uint8_t* kinds, int32_t channels) {
+  return guard([&] {
+    check_tree(h);
+    if (channels != h->t.C)
+      throw Error(DPL_ERR_DATA, "DipoleTree::set_channel_kernels: channel count mismatch");
+    for (int c = 0; c < channels; ++c)
+      require(kinds[c] == DPL_DIPOLE || kinds[c] == DPL_RADIAL, DPL_ERR_USAGE, "bad channel kind");
+    tree_set_kinds(h->t, kinds);
+    DPL_CUDA(cudaStreamSynchronize(h->t.stream));
+  });
+}
+
+int dpl_tree_channels(dpl_tree_t h, int32_t* c) {
+  return guard([&] {
+    check_tree(h);
+    *c = h->t.C;
+  });
+}
+int dpl_tree_point_count(dpl_tree_t h, int64_t* n) {
+  return guard([&] {
+    check_tree(h);
+    *n = h->t.n;
+  });
+}
+int dpl_tree_node_count(dpl_tree_t h, int64_t* n) {
+  return guard([&] {
+    check_tree(h);
+    *n = h->t.nodes;
+  });
+}
+
+int dpl_tree_export(dpl_tree_t h, double* geo, int32_t* topo, int32_t* point_order,
+                    int32_t* point_leaf) {
+  return guard([&] {
+    check_tree(h);
+    tree_export(h->t, geo, topo, point_order, point_leaf);
+  });
+}
+
+int dpl_tree_export_moments(dpl_tree_t h, float* moments_v, float* moments_s) {
+  return guard([&] {
+    check_tree(h);
+    Tree& t = h->t;
+    int64_t nn = t.nodes;
+    std::vector<float4> pd(std::max<int64_t>(1, nn * t.Cd));
+    std::vector<float> pr(nn * t.PR);
+    if (t.Cd)
+      DPL_CUDA(cudaMemcpyAsync(pd.data(), t.node_payd.p, nn * t.Cd * 16, cudaMemcpyDeviceToHost,
+                               t.stream));
+    DPL_CUDA(cudaMemcpyAsync(pr.data(), t.node_payr.p, nn * t.PR * 4, cudaMemcpyDeviceToHost,
+                             t.stream));
+    DPL_CUDA(cudaStreamSynchronize(t.stream));
+    for (int64_t i = 0; i < nn; ++i)
+      for (int c = 0; c < t.C; ++c) {
+        int k = t.slot_of[c];
+        float* v = moments_v ? moments_v + (i * t.C + c) * 3 : nullptr;
+        if (t.kinds[c] == 0) {
+          if (v) v[0] = pd[i * t.Cd + k].x, v[1] = pd[i * t.Cd + k].y, v[2] = pd[i * t.Cd + k].z;
+          if (moments_s) moments_s[i * t.C + c] = NAN;
+        } else {
+          if (v) v[0] = v[1] = v[2] = NAN;
+          if (moments_s) moments_s[i * t.C + c] = pr[i * t.PR + k];
+        }
+      }
+  });
+}
+
+int dpl_tree_dump(dpl_tree_t h, const char* path) {
+  return guard([&] {
+    check_tree(h);
+    Tree& t = h->t;
+    std::ofstream out(path, std::ios::binary);
+    if (!out) throw Error(DPL_ERR_DATA, std::string("DipoleTree::dump: cannot open ") + path);
+    int64_t nn = t.nodes;
+    std::vector<double> geo(nn * 5);
+    std::vector<int32_t> topo(nn * 6), order(t.n);
+    tree_export(t, geo.data(), topo.data(), order.data(), nullptr);
+    std::vector<double> mv, ms;
+    tree_full_moments(t, mv, ms);
+    out.write("DPLT", 4);  // bhtree.cpp:465-494
+    uint32_t version = 1, channels = (uint32_t)t.C;
+    uint64_t points = (uint64_t)t.n, node_count = (uint64_t)nn;
+    out.write((const char*)&version, 4);
+    out.write((const char*)&channels, 4);
+    out.write((const char*)&points, 8);
+    out.write((const char*)&node_count, 8);
+    for (int64_t i = 0; i < nn; ++i) {
+      out.write((const char*)&geo[5 * i], 40);
+      int32_t s5[5] = {topo[6 * i], topo[6 * i + 1], topo[6 * i + 2], topo[6 * i + 3],
+                       topo[6 * i + 4]};
+      out.write((const char*)s5, 20);
+      uint8_t leaf = (uint8_t)topo[6 * i + 5];
+      out.write((const char*)&leaf, 1);
+    }
+    out.write((const char*)order.data(), t.n * 4);
+    out.write((const char*)mv.data(), mv.size() * 8);
+    out.write((const char*)ms.data(), ms.size() * 8);
+    if (!out) throw Error(DPL_ERR_DATA, std::string("DipoleTree::dump: write failed for ") + path);
+  });
+}
+
+// ---------------------------------------------------------------- forward
+
+static int forward_common(dpl_tree_t h, const dpl_kernel_params* params, double beta,
+                          const double* xs, int64_t q, float* out, float* grad,
+                          dpl_counters* counters, int grad_mode, int channel) {
+  return guard([&] {
+    check_tree(h);
+    check_params(params);
+    require(q >= 0, DPL_ERR_USAGE, "negative query count");
+    require(q < (int64_t)INT32_MAX, DPL_ERR_USAGE, "query batch >= 2^31");
+    require(out != nullptr || q == 0, DPL_ERR_USAGE, "null output");
+    Tree& t = h->t;
+    if (q == 0) return;
+    DPL_CUDA(cudaSetDevice(t.device));
+    KParams kp = make_kparams(params->epsilon, params->desingularized, params->desing_delta);
+    tree_ensure_thresholds(t, beta);
+    const double* xs_d = stage_in(t, xs, (size_t)q * 3, h->ws_xs);
+    h->ws_perm.reserve(q * 4);
+    morton_order(t, xs_d, q, h->ws_perm.as<int32_t>(), h->ws_morton);
+    FwdArgs a;
+    a.xs = xs_d;
+    a.perm = h->ws_perm.as<int32_t>();
+    a.q = q;
+    a.overflow = overflow_flag(h);
+    Out<float> o, g;
+    Out<long long> cnt;
+    if (channel >= 0) {
+      a.single = 1;
+      a.out_stride = 1;
+      if (t.kinds[channel] == 0)
+        a.only_dip = t.slot_of[channel];
+      else
+        a.only_rad = t.slot_of[channel];
+      o.bind(t, out, q, h->ws_out);
+    } else {
+      a.out_stride = t.C;
+      o.bind(t, out, q * t.C, h->ws_out);
+      if (grad_mode == 1) g.bind(t, grad, q * t.C * 3, h->ws_grad);
+      if (grad_mode == 2) g.bind(t, grad, q * 3, h->ws_grad);
+      a.grad_mode = grad ? grad_mode : 0;
+    }
+    if (counters) cnt.bind(t, (long long*)counters, q * 5, h->ws_cnt);
+    a.out = o.dev;
+    a.grad = g.dev;
+    a.counters = cnt.dev;
+    forward_launch(t, kp, a);
+    DPL_CUDA(cudaGetLastError());
+    o.finish(t);
+    g.finish(t);
+    cnt.finish(t);
+    if (o.host || g.host || cnt.host) check_overflow(h);
+  });
+}
+
+int dpl_primal(dpl_tree_t h, const dpl_kernel_params* params, double beta_bh, const double* xs,
+               int64_t q, float* out, float* grad, dpl_counters* counters) {
+  return forward_common(h, params, beta_bh, xs, q, out, grad, counters, grad ? 1 : 0, -1);
+}
+
+int dpl_primal_channel(dpl_tree_t h, const dpl_kernel_params* params, double beta_bh,
+                       const double* xs, int64_t q, int32_t channel, float* out) {
+  if (h && h->built && (channel < 0 || channel >= h->t.C)) {
+    g_err = "primal_channel: channel out of range";
+    return DPL_ERR_USAGE;
+  }
+  return forward_common(h, params, beta_bh, xs, q, out, nullptr, nullptr, 0, channel);
+}
+
+int dpl_primal_grad0(dpl_tree_t h, const dpl_kernel_params* params, double beta_bh,
+                     const double* xs, int64_t q, float* out, float* grad0) {
+  if (h && h->built && (h->t.kinds.empty() || h->t.kinds[0] != 0)) {
+    g_err = "primal_grad0: channel 0 must be a Dipole channel";
+    return DPL_ERR_USAGE;
+  }
+  return forward_common(h, params, beta_bh, xs, q, out, grad0, nullptr, 2, -1);
+}
+
+// ---------------------------------------------------------------- adjoint
+
+int dpl_gradbuf_create(dpl_tree_t h, dpl_gradbuf_t* out) {
+  return guard([&] {
+    check_tree(h);
+    auto b = new dpl_gradbuf_s();
+    b->tree = h;
+    try {
+      gradbuf_alloc(b->b, h->t);
+      gradbuf_zero(b->b, h->t.stream);
+    } catch (...) {
+      delete b;
+      throw;
+    }
+    *out = b;
+  });
+}
+
+int dpl_gradbuf_destroy(dpl_gradbuf_t b) {
+  return guard([&] {
+    if (!b) return;
+    cudaStreamSynchronize(b->tree->t.stream);
+    delete b;
+  });
+}
+
+int dpl_gradbuf_zero(dpl_gradbuf_t b) {
+  return guard([&] {
+    require(b != nullptr, DPL_ERR_USAGE, "null buffer");
+    gradbuf_zero(b->b, b->tree->t.stream);
+  });
+}
+
+static void check_buf(dpl_tree_t h, dpl_gradbuf_t b) {
+  require(b != nullptr, DPL_ERR_USAGE, "null gradient buffer");
+  require(b->tree == h, DPL_ERR_USAGE, "gradient buffer belongs to another tree");
+  require(b->b.nodes == h->t.nodes && b->b.n == h->t.n && b->b.Cd == h->t.Cd &&
+              b->b.Cr == h->t.Cr,
+          DPL_ERR_DATA, "gradient buffer does not match the tree (rebuilt or kinds changed)");
+}
+
+int dpl_adjoint(dpl_tree_t h, const dpl_kernel_params* params, double beta_bh, const double* xs,
+                int64_t q, const float* d_out, const float* d_grad, dpl_gradbuf_t buf) {
+  return guard([&] {
+    check_tree(h);
+    check_params(params);
+    check_buf(h, buf);
+    require(q >= 0 && q < (int64_t)INT32_MAX, DPL_ERR_USAGE, "bad query count");
+    if (q == 0) return;
+    require(xs && d_out, DPL_ERR_USAGE, "null input");
+    Tree& t = h->t;
+    DPL_CUDA(cudaSetDevice(t.device));
+    KParams kp = make_kparams(params->epsilon, params->desingularized, params->desing_delta);
+    tree_ensure_thresholds(t, beta_bh);
+    const double* xs_d = stage_in(t, xs, (size_t)q * 3, h->ws_xs);
+    const float* dout_d = stage_in(t, d_out, (size_t)q * t.C, h->ws_dout);
+    const float* dg_d = d_grad ? stage_in(t, d_grad, (size_t)q * t.C * 3, h->ws_dgrad) : nullptr;
+    h->ws_perm.reserve(q * 4);
+    morton_order(t, xs_d, q, h->ws_perm.as<int32_t>(), h->ws_morton);
+    AdjArgs a;
+    a.xs = xs_d;
+    a.perm = h->ws_perm.as<int32_t>();
+    a.q = q;
+    a.d_out = dout_d;
+    a.dstride = t.C;
+    a.d_grad = dg_d;
+    a.grad_mode = dg_d ? 1 : 0;
+    a.overflow = overflow_flag(h);
+    adjoint_launch(t, kp, a, buf->b);
+    DPL_CUDA(cudaGetLastError());
+    if (!is_device_ptr(xs) || !is_device_ptr(d_out)) DPL_CUDA(cudaStreamSynchronize(t.stream));
+  });
+}
+
+int dpl_flush(dpl_tree_t h, dpl_gradbuf_t* bufs, int32_t nbuf, float* moments, float* normals,
+              double* d_epsilon) {
+  return guard([&] {
+    check_tree(h);
+    require(nbuf >= 1 && bufs, DPL_ERR_USAGE, "no gradient buffers");
+    for (int i = 0; i < nbuf; ++i) check_buf(h, bufs[i]);
+    Tree& t = h->t;
+    DPL_CUDA(cudaSetDevice(t.device));
+    GradBuf& b0 = bufs[0]->b;
+    for (int i = 1; i < nbuf; ++i) gradbuf_accumulate(b0, bufs[i]->b, t.stream);  // :429-439
+    Out<float> mo, no;
+    mo.bind(t, moments, t.n * t.C, h->ws_mom);
+    no.bind(t, normals, t.n * 3, h->ws_nrm);
+    double de = 0;
+    DPL_CUDA(cudaMemcpyAsync(&de, b0.d_eps, 8, cudaMemcpyDeviceToHost, t.stream));
+    flush_launch(t, b0, mo.dev, no.dev);
+    mo.finish(t);
+    no.finish(t);
+    for (int i = 0; i < nbuf; ++i) gradbuf_zero(bufs[i]->b, t.stream);  // reset() (:438)
+    DPL_CUDA(cudaStreamSynchronize(t.stream));
+    if (d_epsilon) *d_epsilon = de;
+  });
+}
+
+// ---------------------------------------------------------------- render
+
+int dpl_tape_create(dpl_tape_t* out) {
+  return guard([&] {
+    require(out != nullptr, DPL_ERR_USAGE, "null out");
+    *out = new dpl_tape_s();
+  });
+}
+
+int dpl_tape_destroy(dpl_tape_t tp) {
+  return guard([&] { delete tp; });
+}
+
+double dpl_uniform(uint64_t seed, uint64_t counter) { return host_uniform(seed, counter); }
+
+static void check_render_layout(Tree& t) {
+  require(t.C >= 4, DPL_ERR_DATA, "direct-rgb head needs at least 3 appearance channels");
+  require(t.kinds[0] == 0 && t.kinds[1] == 1 && t.kinds[2] == 1 && t.kinds[3] == 1, DPL_ERR_DATA,
+          "render step expects SceneModel's layout: channel 0 Dipole, 1..K Radial");
+}
+
+int dpl_render_forward(dpl_tree_t h, const dpl_kernel_params* params, const dpl_render_params* rp,
+                       const double* rays, int64_t R, int32_t S, const double* ts,
+                       const double* deltas, float* rgb, dpl_tape_t tape) {
+  return guard([&] {
+    check_tree(h);
+    check_params(params);
+    require(rp && tape && rays && rgb, DPL_ERR_USAGE, "null argument");
+    require(R >= 0 && S >= 1, DPL_ERR_USAGE, "bad ray/sample counts");
+    require(R * (int64_t)S < (int64_t)INT32_MAX, DPL_ERR_USAGE, "R*S >= 2^31");
+    require(rp->lambda_scale > 0, DPL_ERR_DATA, "lambda_scale must be positive");
+    Tree& t = h->t;
+    check_render_layout(t);
+    DPL_CUDA(cudaSetDevice(t.device));
+    if (R == 0) return;
+    int64_t Q = R * (int64_t)S;
+    KParams kp = make_kparams(params->epsilon, params->desingularized, params->desing_delta);
+    tree_ensure_thresholds(t, rp->beta_bh);
+    tape->R = R;
+    tape->S = S;
+    tape->t_near = rp->t_near;
+    tape->rays.reserve(R * 48);
+    DPL_CUDA(cudaMemcpyAsync(tape->rays.p, rays, R * 48, cudaMemcpyDefault, t.stream));
+    const double* ts_d = nullptr;
+    DevBuf ts_in;
+    if (ts) ts_d = stage_in(t, ts, (size_t)Q, ts_in);
+    tape->has_deltas = deltas != nullptr;
+    if (deltas) {
+      tape->deltas.reserve(Q * 8);
+      DPL_CUDA(cudaMemcpyAsync(tape->deltas.p, deltas, Q * 8, cudaMemcpyDefault, t.stream));
+    }
+    tape->ts.reserve(Q * 8);
+    tape->xs.reserve(Q * 24);
+    render_samples(t.stream, tape->rays.as<double>(), R, S, ts_d, rp->t_near, rp->t_far, rp->seed,
+                   tape->ts.as<double>(), tape->xs.as<double>());
+    tape->perm.reserve(Q * 4);
+    morton_order(t, tape->xs.as<double>(), Q, tape->perm.as<int32_t>(), tape->morton);
+    tape->vals.reserve(Q * 16);
+    tape->g0.reserve(Q * 12);
+    FwdArgs a;
+    a.xs = tape->xs.as<double>();
+    a.perm = tape->perm.as<int32_t>();
+    a.q = Q;
+    a.out = tape->vals.as<float>();
+    a.out_stride = 4;
+    a.grad = tape->g0.as<float>();
+    a.grad_mode = 2;
+    a.overflow = overflow_flag(h);
+    // the direct-rgb head reads channels 0..3 only (radiance.cpp:133-145):
+    // radial slots 0..2 are channels 1..3 in SceneModel's layout
+    a.nr_limit = 3;
+    forward_launch(t, kp, a);
+    Out<float> o;
+    o.bind(t, rgb, R * 3, h->ws_out);
+    tape->tape.reserve(Q * 64);
+    double bg[3] = {rp->background[0], rp->background[1], rp->background[2]};
+    render_composite(t.stream, tape->rays.as<double>(), R, S, tape->ts.as<double>(),
+                     tape->has_deltas ? tape->deltas.as<double>() : nullptr, rp->t_near,
+                     tape->vals.as<float>(), tape->g0.as<float>(), rp->lambda_scale, bg,
+                     tape->tape.as<double>(), o.dev);
+    o.finish(t);
+    DPL_CUDA(cudaGetLastError());
+    if (o.host) DPL_CUDA(cudaStreamSynchronize(t.stream));
+  });
+}
+
+int dpl_render_backward(dpl_tree_t h, const dpl_kernel_params* params, const dpl_render_params* rp,
+                        dpl_tape_t tape, const float* d_rgb, dpl_gradbuf_t buf, double* d_lambda,
+                        double* d_background) {
+  return guard([&] {
+    check_tree(h);
+    check_params(params);
+    check_buf(h, buf);
+    require(rp && tape && d_rgb, DPL_ERR_USAGE, "null argument");
+    Tree& t = h->t;
+    check_render_layout(t);
+    DPL_CUDA(cudaSetDevice(t.device));
+    int64_t R = tape->R;
+    int S = tape->S;
+    if (R == 0) return;
+    int64_t Q = R * S;
+    KParams kp = make_kparams(params->epsilon, params->desingularized, params->desing_delta);
+    tree_ensure_thresholds(t, rp->beta_bh);
+    DevBuf drgb_tmp;
+    const float* drgb_d = stage_in(t, d_rgb, (size_t)R * 3, drgb_tmp);
+    tape->dout.reserve(Q * 16);
+    tape->dgrad.reserve(Q * 12);
+    tape->sums.reserve(32);
+    DPL_CUDA(cudaMemsetAsync(tape->sums.p, 0, 32, t.stream));
+    double bg[3] = {rp->background[0], rp->background[1], rp->background[2]};
+    render_backward_rays(t.stream, tape->rays.as<double>(), R, S, tape->tape.as<double>(), drgb_d,
+                         rp->lambda_scale, bg, tape->dout.as<float>(), tape->dgrad.as<float>(),
+                         tape->sums.as<double>());
+    AdjArgs a;
+    a.xs = tape->xs.as<double>();
+    a.perm = tape->perm.as<int32_t>();
+    a.q = Q;
+    a.d_out = tape->dout.as<float>();
+    a.dstride = 4;
+    a.d_grad = tape->dgrad.as<float>();
+    a.grad_mode = 2;
+    a.nr_limit = 3;
+    a.overflow = overflow_flag(h);
+    adjoint_launch(t, kp, a, buf->b);
+    double sums[4];
+    DPL_CUDA(cudaMemcpyAsync(sums, tape->sums.p, 32, cudaMemcpyDeviceToHost, t.stream));
+    DPL_CUDA(cudaStreamSynchronize(t.stream));
+    if (d_lambda) *d_lambda = sums[0];
+    if (d_background) d_background[0] = sums[1], d_background[1] = sums[2], d_background[2] = sums[3];
+  });
+}
+
+// ---------------------------------------------------------------- Adam
+
+__global__ void k_adam(float* p, const float* g, float* m, float* v, int64_t n, float lr,
+                       float b1, float b2, float eps, float c1, float c2) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float gi = g[i];
+  float mi = b1 * m[i] + (1.f - b1) * gi;
+  float vi = b2 * v[i] + (1.f - b2) * gi * gi;
+  m[i] = mi, v[i] = vi;
+  p[i] -= lr * (mi / c1) / (sqrtf(vi / c2) + eps);
+}
+
+int dpl_adam_step(dpl_tree_t h, float* params, const float* grads, float* m, float* v, int64_t n,
+                  double lr, double beta1, double beta2, double eps, int64_t step) {
+  return guard([&] {
+    require(h != nullptr, DPL_ERR_USAGE, "null tree handle");
+    require(step >= 1, DPL_ERR_USAGE, "Adam step counter starts at 1");
+    require(is_device_ptr(params) && is_device_ptr(grads) && is_device_ptr(m) && is_device_ptr(v),
+            DPL_ERR_USAGE, "dpl_adam_step takes device arrays");
+    if (n <= 0) return;
+    double c1 = 1.0 - std::pow(beta1, (double)step), c2 = 1.0 - std::pow(beta2, (double)step);
+    k_adam<<<(unsigned)((n + 255) / 256), 256, 0, h->t.stream>>>(
+        params, grads, m, v, n, (float)lr, (float)beta1, (float)beta2, (float)eps, (float)c1,
+        (float)c2);
+    count_launch();
+    DPL_CUDA(cudaGetLastError());
+  });
+}
+
+}  // extern "C"

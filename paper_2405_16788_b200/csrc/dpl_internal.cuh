@@ -1,0 +1,80 @@
+// dpl_internal.cuh — shared device/host definitions of the B200 dipole engine.
+//
+// HBM layout of one tree (all device-resident, built by build.cu):
+//   node_dec   double4 [nodes]   {cx, cy, cz, thr}   fp64 centroid + opening threshold
+//                                thr = (beta^2 * radius) * radius for the current beta
+//   node_topo  int4    [nodes]   {child_begin, child_count, begin, end}; leaf <=> count == 0
+//   node_geo   float4  [nodes]   {cx, cy, cz, A = area/(4 pi)} fp32 copies for arithmetic
+//   node_flag  uint8   [nodes]   bit0: area > 0 (far field allowed, bhtree.cpp:205)
+//   node_pay   float   [nodes x P]  payload row: [3 x Cd dipole moments | Cr radial moments | pad]
+//   pt_pos64   double  [N x 3]   sorted (tree) order, fp64 positions (leaf distances)
+//   pt_geo     float4  [N]       {px, py, pz, A_m = a_m/(4 pi)} sorted order
+//   pt_pay     float   [N x P]   payload row: [mu_c * n (3 x Cd) | mu_c (Cr) | pad]
+//   pt_nrm/pt_mu fp32 sorted copies for the adjoint's leaf terms
+// Channel layout: dipole channels first (dip_ch[k] = reference channel id),
+// radial channels after (rad_ch[k]); P = round_up(3*Cd + Cr, 4).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+
+#define DPL_WARP 32
+#define DPL_MAX_CHANNELS 1024
+#define DPL_STACK_PER_WARP 192  // > 7 * max_depth(21) + 8, cf. bhtree.cpp:185
+
+namespace dpl {
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define DPL_CUDA(call)                                                                  \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      throw ::dpl::Error(4, std::string(#call) + ": " + cudaGetErrorString(e_));        \
+  } while (0)
+
+void count_launch(int n = 1);
+
+// kernel radial-profile mode
+enum KMode : int { KM_REGULARIZED = 0, KM_SINGULAR = 1, KM_DESING = 2 };
+
+// Launch-constant kernel parameters (fp32 powers of 1/eps precomputed in fp64).
+struct KParams {
+  int mode;
+  float eps, inv_eps, inv_eps3, inv_eps4, inv_eps5, inv_eps6;
+  float delta2;
+};
+
+// Per-launch view of a tree for the traversal kernels.
+struct TreeView {
+  const double4* node_dec;
+  const int4* node_topo;
+  const float4* node_geo;
+  const uint8_t* node_flag;
+  const float* node_pay;
+  const double* pt_pos64;
+  const float4* pt_geo;
+  const float* pt_pay;
+  const float* pt_nrm;  // N x 3 sorted
+  const float* pt_mu;   // N x C sorted (reference channel order)
+  int P;                // payload row stride (floats)
+  int Cd, Cr, C;
+  int64_t nodes, n;
+  int max_depth;
+};
+
+// Fast host->device constant table of channel mapping for kernels.
+struct ChanMap {
+  int dip_ch[64];   // dipole slot -> channel id (tiles only use the first TD)
+  int rad_ch[1024];
+};
+
+inline int round_up4(int x) { return (x + 3) & ~3; }
+
+}  // namespace dpl

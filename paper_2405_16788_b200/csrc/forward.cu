@@ -1,0 +1,328 @@
+// forward.cu — K5/K6 forward traversals and K10 query Morton sort.
+//
+// Restates DipoleTree::primal / primal_channel / primal_with_gradient
+// (proj/src/bhtree.cpp:188-334) for a batch of queries. Channels are processed
+// in tiles of TD dipole and TR radial slots (template parameters) so that all
+// accumulators live in registers; the common layouts (C = 2, 4, 49 with channel
+// 0 Dipole) run in one pass.
+//
+// Interaction (far node or leaf point), with d = source - x, A = area/(4 pi):
+//   dipole slot:  out += A W (v . d);      grad -= A (W v + Wp_r (v . d) d)
+//   radial slot:  out += A R s;            grad -= A Rp_r s d
+// where (v, s) are the node moments (bhtree.cpp:205-213, :295-310) or, for a
+// leaf point, (mu_c n_m, mu_c) (bhtree.cpp:214-229, :311-329) — one formula.
+#include <cub/cub.cuh>
+
+#include "forward.cuh"
+#include "traverse.cuh"
+
+namespace dpl {
+
+constexpr int FWD_WARPS = 4;
+
+template <int TD, int TR, int GRAD>
+struct FAcc {
+  float vd[TD > 0 ? TD : 1];
+  float vr[TR > 0 ? TR : 1];
+  float gd[(GRAD && TD > 0) ? TD : 1][3];
+  float gr[(GRAD == 1 && TR > 0) ? TR : 1][3];
+};
+
+template <int TD, int TR, int GRAD>
+__device__ __forceinline__ void f_interact(FAcc<TD, TR, GRAD>& a, double dx, double dy, double dz,
+                                           double dist2, float A, const float4* __restrict__ pd,
+                                           const float* __restrict__ pr, int nd, int nr,
+                                           const KParams& kp, bool& near) {
+  const float fx = (float)dx, fy = (float)dy, fz = (float)dz;
+  const float r2 = (float)dist2;
+  Co c = coeffs<GRAD ? 1 : 0>(r2, kp);
+  near = c.near;
+  const float aW = A * c.W, aR = A * c.R;
+#pragma unroll
+  for (int k = 0; k < TD; ++k) {
+    if (k < nd) {
+      float4 v = __ldg(pd + k);
+      float vdot = fmaf(v.x, fx, fmaf(v.y, fy, v.z * fz));
+      a.vd[k] = fmaf(aW, vdot, a.vd[k]);
+      if (GRAD == 1 || (GRAD == 2 && k == 0)) {
+        float t = A * c.Wp_r * vdot;
+        a.gd[k][0] -= fmaf(aW, v.x, t * fx);
+        a.gd[k][1] -= fmaf(aW, v.y, t * fy);
+        a.gd[k][2] -= fmaf(aW, v.z, t * fz);
+      }
+    }
+  }
+  if (TR % 4 == 0) {
+#pragma unroll
+    for (int k4 = 0; k4 < TR / 4; ++k4) {
+      if (4 * k4 < nr) {
+        float4 s = __ldg(reinterpret_cast<const float4*>(pr) + k4);
+        float sv[4] = {s.x, s.y, s.z, s.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int k = 4 * k4 + u;
+          a.vr[k] = fmaf(aR, sv[u], a.vr[k]);
+          if (GRAD == 1) {
+            float t = A * c.Rp_r * sv[u];
+            a.gr[k][0] = fmaf(-t, fx, a.gr[k][0]);
+            a.gr[k][1] = fmaf(-t, fy, a.gr[k][1]);
+            a.gr[k][2] = fmaf(-t, fz, a.gr[k][2]);
+          }
+        }
+      }
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < TR; ++k) {
+      if (k < nr) {
+        float s = __ldg(pr + k);
+        a.vr[k] = fmaf(aR, s, a.vr[k]);
+        if (GRAD == 1) {
+          float t = A * c.Rp_r * s;
+          a.gr[k][0] = fmaf(-t, fx, a.gr[k][0]);
+          a.gr[k][1] = fmaf(-t, fy, a.gr[k][1]);
+          a.gr[k][2] = fmaf(-t, fz, a.gr[k][2]);
+        }
+      }
+    }
+  }
+}
+
+// GRAD: 0 values only; 1 gradients of every channel in the tile; 2 gradient of
+// dipole slot 0 only (render step). single: write column 0 of a q x 1 output.
+template <int TD, int TR, int GRAD, bool COUNT>
+__global__ void __launch_bounds__(FWD_WARPS * 32)
+    k_forward(TreeView tv, KParams kp, const float4* __restrict__ payd_n,
+              const float* __restrict__ payr_n, const float4* __restrict__ payd_p,
+              const float* __restrict__ payr_p, const double* __restrict__ xs,
+              const int32_t* __restrict__ perm, int64_t q, int d0, int nd, int r0, int nr,
+              const int* __restrict__ chmap, float* __restrict__ out, int out_stride, int single,
+              float* __restrict__ grad, long long* __restrict__ counters, int* overflow) {
+  __shared__ int2 stk[FWD_WARPS][DPL_STACK_PER_WARP];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t sidx = ((int64_t)blockIdx.x * FWD_WARPS + w) * 32 + lane;
+  const bool valid = sidx < q;
+  const int64_t qi = valid ? (perm ? (int64_t)perm[sidx] : sidx) : 0;
+  QueryPos x;
+  if (valid) {
+    x.x = xs[3 * qi], x.y = xs[3 * qi + 1], x.z = xs[3 * qi + 2];
+  } else {
+    x.x = x.y = x.z = 0.0;
+  }
+  const unsigned active = __ballot_sync(FULL_MASK, valid);
+  if (!active) return;
+  FAcc<TD, TR, GRAD> a;
+#pragma unroll
+  for (int k = 0; k < (TD > 0 ? TD : 1); ++k) a.vd[k] = 0.f;
+#pragma unroll
+  for (int k = 0; k < ((GRAD && TD > 0) ? TD : 1); ++k) a.gd[k][0] = a.gd[k][1] = a.gd[k][2] = 0.f;
+#pragma unroll
+  for (int k = 0; k < (TR > 0 ? TR : 1); ++k) a.vr[k] = 0.f;
+#pragma unroll
+  for (int k = 0; k < ((GRAD == 1 && TR > 0) ? TR : 1); ++k) a.gr[k][0] = a.gr[k][1] = a.gr[k][2] = 0.f;
+  long long c_vis = 0, c_fn = 0, c_ff = 0, c_pn = 0, c_pf = 0;
+  const float4* pdn = payd_n + d0;
+  const float* prn = payr_n + r0;
+  const float4* pdp = payd_p + d0;
+  const float* prp = payr_p + r0;
+  const bool skip_coincident = GRAD != 0 || kp.mode == KM_SINGULAR;  // :219 vs :316
+
+  int sp = 1;
+  if (lane == 0) stk[w][0] = make_int2(0, (int)active);
+  __syncwarp();
+  while (sp > 0) {
+    --sp;
+    const int2 e = stk[w][sp];
+    __syncwarp();
+    const int node = e.x;
+    const unsigned mask = (unsigned)e.y;
+    const bool mine = (mask >> lane) & 1u;
+    const double4 dec = ld_dec(tv.node_dec + node);
+    const int4 tp = __ldg(tv.node_topo + node);
+    double dx, dy, dz;
+    const double dist2 = dist2_rn(dec.x, dec.y, dec.z, x, dx, dy, dz);
+    const bool far = mine && (dist2 > dec.w);
+    const unsigned farm = __ballot_sync(FULL_MASK, far);
+    if (COUNT && mine) ++c_vis;
+    if (far && (__ldg(tv.node_flag + node) & 1)) {
+      bool near;
+      f_interact<TD, TR, GRAD>(a, dx, dy, dz, dist2, __ldg(tv.node_geo + node).w,
+                               pdn + (int64_t)node * tv.Cd, prn + (int64_t)node * tv.P, nd, nr,
+                               kp, near);
+      if (COUNT) near ? ++c_fn : ++c_ff;
+    }
+    const unsigned openm = mask & ~farm;
+    if (openm) {
+      if (tp.y == 0) {
+        if ((openm >> lane) & 1u) {
+          for (int j = tp.z; j < tp.w; ++j) {
+            double px = __ldg(tv.pt_pos64 + 3 * (int64_t)j);
+            double py = __ldg(tv.pt_pos64 + 3 * (int64_t)j + 1);
+            double pz = __ldg(tv.pt_pos64 + 3 * (int64_t)j + 2);
+            const double r2 = dist2_rn(px, py, pz, x, dx, dy, dz);
+            if (r2 == 0.0 && skip_coincident) continue;
+            bool near;
+            f_interact<TD, TR, GRAD>(a, dx, dy, dz, r2, __ldg(tv.pt_geo + j).w,
+                                     pdp + (int64_t)j * tv.Cd, prp + (int64_t)j * tv.P, nd, nr,
+                                     kp, near);
+            if (COUNT) near ? ++c_pn : ++c_pf;
+          }
+        }
+        __syncwarp();
+      } else {
+        if (sp + tp.y > DPL_STACK_PER_WARP) {
+          if (lane == 0) atomicExch(overflow, 1);
+          break;
+        }
+        if (lane < tp.y) stk[w][sp + lane] = make_int2(tp.x + lane, (int)openm);
+        sp += tp.y;
+        __syncwarp();
+      }
+    }
+  }
+  if (!valid) return;
+  if (single) {
+    out[qi] = TD > 0 && nd > 0 ? a.vd[0] : a.vr[0];
+  } else {
+#pragma unroll
+    for (int k = 0; k < TD; ++k)
+      if (k < nd) {
+        int ch = __ldg(chmap + d0 + k);
+        out[qi * out_stride + ch] = a.vd[k];
+        if (GRAD == 1) {
+          float* g = grad + (qi * out_stride + ch) * 3;
+          g[0] = a.gd[k][0], g[1] = a.gd[k][1], g[2] = a.gd[k][2];
+        }
+      }
+    if (GRAD == 2 && TD > 0 && nd > 0 && d0 == 0) {
+      float* g = grad + qi * 3;
+      g[0] = a.gd[0][0], g[1] = a.gd[0][1], g[2] = a.gd[0][2];
+    }
+    const int cd = tv.Cd;
+#pragma unroll
+    for (int k = 0; k < TR; ++k)
+      if (k < nr) {
+        int ch = __ldg(chmap + cd + r0 + k);
+        out[qi * out_stride + ch] = a.vr[k];
+        if (GRAD == 1) {
+          float* g = grad + (qi * out_stride + ch) * 3;
+          g[0] = a.gr[k][0], g[1] = a.gr[k][1], g[2] = a.gr[k][2];
+        }
+      }
+  }
+  if (COUNT) {
+    long long* cq = counters + 5 * qi;
+    cq[0] = c_vis, cq[1] = c_fn, cq[2] = c_ff, cq[3] = c_pn, cq[4] = c_pf;
+  }
+}
+
+// ---------------------------------------------------------------- K10
+__device__ __forceinline__ uint32_t spread10(uint32_t v) {
+  v &= 0x3ff;
+  v = (v | (v << 16)) & 0x030000FF;
+  v = (v | (v << 8)) & 0x0300F00F;
+  v = (v | (v << 4)) & 0x030C30C3;
+  v = (v | (v << 2)) & 0x09249249;
+  return v;
+}
+
+__global__ void k_morton(const double* __restrict__ xs, int64_t q, double lx, double ly,
+                         double lz, double inv, uint32_t* keys, int32_t* idx) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= q) return;
+  auto qz = [&](double v, double lo) {
+    double f = (v - lo) * inv;
+    f = f < 0 ? 0 : (f > 1023 ? 1023 : f);
+    return (uint32_t)f;
+  };
+  uint32_t a = qz(xs[3 * i], lx), b = qz(xs[3 * i + 1], ly), c = qz(xs[3 * i + 2], lz);
+  keys[i] = spread10(a) | (spread10(b) << 1) | (spread10(c) << 2);
+  idx[i] = (int32_t)i;
+}
+
+void morton_order(Tree& t, const double* xs_dev, int64_t q, int32_t* perm_out, DevBuf& ws) {
+  if (q <= 0) return;
+  double ext = 0;
+  for (int a = 0; a < 3; ++a) ext = std::max(ext, t.root_hi[a] - t.root_lo[a]);
+  double pad = 0.5 * ext + 1e-12;
+  double lo[3];
+  for (int a = 0; a < 3; ++a) lo[a] = 0.5 * (t.root_lo[a] + t.root_hi[a]) - 2 * pad;
+  double inv = 1024.0 / (4 * pad);  // frame: 2x the root cell around its centre
+  size_t tb = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tb, (uint32_t*)nullptr, (uint32_t*)nullptr,
+                                  (int32_t*)nullptr, (int32_t*)nullptr, (int)q, 0, 30, t.stream);
+  size_t need = q * 4 * 3 + tb + 256;
+  ws.reserve(need);
+  char* base = ws.as<char>();
+  uint32_t* keys = (uint32_t*)base;
+  uint32_t* keys_s = keys + q;
+  int32_t* idx = (int32_t*)(keys_s + q);
+  void* tmp = (void*)(((uintptr_t)(idx + q) + 255) & ~(uintptr_t)255);
+  k_morton<<<(unsigned)((q + 255) / 256), 256, 0, t.stream>>>(xs_dev, q, lo[0], lo[1], lo[2], inv,
+                                                               keys, idx);
+  count_launch();
+  DPL_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, keys, keys_s, idx, perm_out, (int)q, 0, 30,
+                                           t.stream));
+  count_launch(3);
+}
+
+// ---------------------------------------------------------------- dispatch
+template <int TD, int TR, int GRAD>
+static void launch_one(const Tree& t, const KParams& kp, FwdArgs& a, int d0, int nd, int r0,
+                       int nr) {
+  TreeView tv = t.view();
+  unsigned blocks = (unsigned)((a.q + FWD_WARPS * 32 - 1) / (FWD_WARPS * 32));
+  auto run = [&](auto kern) {
+    kern<<<blocks, FWD_WARPS * 32, 0, t.stream>>>(
+        tv, kp, t.node_payd.as<float4>(), t.node_payr.as<float>(), t.pt_payd.as<float4>(),
+        t.pt_payr.as<float>(), a.xs, a.perm, a.q, d0, nd, r0, nr, t.chmap.as<int>(), a.out,
+        a.out_stride, a.single, a.grad, a.counters, a.overflow);
+  };
+  if (a.counters)
+    run(k_forward<TD, TR, GRAD, true>);
+  else
+    run(k_forward<TD, TR, GRAD, false>);
+  a.counters = nullptr;  // later tiles re-walk the same decisions: count once
+  count_launch();
+}
+
+// Channel-tile plan: (TD, TR) instantiations tried in order; the first that
+// covers the tile in one pass wins, otherwise tiles of the largest are used.
+void forward_launch(const Tree& t, const KParams& kp, FwdArgs a) {
+  const int Cd = a.only_dip >= 0 ? 1 : (a.only_rad >= 0 ? 0 : t.Cd);
+  const int Cr = a.only_rad >= 0 ? 1
+                 : (a.only_dip >= 0 ? 0 : (a.nr_limit >= 0 ? std::min(a.nr_limit, t.Cr) : t.Cr));
+  const int dbase = a.only_dip >= 0 ? a.only_dip : 0;
+  const int rbase = a.only_rad >= 0 ? a.only_rad : 0;
+  if (a.grad_mode == 0) {
+    if (Cd <= 1 && Cr == 0) return launch_one<1, 0, 0>(t, kp, a, dbase, Cd, 0, 0);
+    if (Cd == 0 && Cr == 1) return launch_one<0, 1, 0>(t, kp, a, 0, 0, rbase, 1);
+    if (Cd <= 1 && Cr <= 1) return launch_one<1, 1, 0>(t, kp, a, 0, Cd, 0, Cr);
+    if (Cd <= 1 && Cr <= 4) return launch_one<1, 4, 0>(t, kp, a, 0, Cd, 0, Cr);
+    if (Cd <= 1 && Cr <= 16) return launch_one<1, 16, 0>(t, kp, a, 0, Cd, 0, Cr);
+    if (Cd <= 1 && Cr <= 48) return launch_one<1, 48, 0>(t, kp, a, 0, Cd, 0, Cr);
+    // general: dipole tiles of 4, radial tiles of 48
+    for (int d = 0; d < Cd; d += 4) launch_one<4, 0, 0>(t, kp, a, d, std::min(4, Cd - d), 0, 0);
+    for (int r = 0; r < Cr; r += 48) launch_one<0, 48, 0>(t, kp, a, 0, 0, r, std::min(48, Cr - r));
+    return;
+  }
+  if (a.grad_mode == 2) {  // values of all channels + gradient of dipole slot 0
+    if (Cd < 1) throw Error(1, "grad0 requires a dipole channel 0");
+    if (Cd == 1 && Cr <= 4) return launch_one<1, 4, 2>(t, kp, a, 0, 1, 0, Cr);
+    if (Cd == 1 && Cr <= 16) return launch_one<1, 16, 2>(t, kp, a, 0, 1, 0, Cr);
+    if (Cd == 1 && Cr <= 48) return launch_one<1, 48, 2>(t, kp, a, 0, 1, 0, Cr);
+    launch_one<1, 0, 2>(t, kp, a, 0, 1, 0, 0);
+    for (int d = 1; d < Cd; d += 4) launch_one<4, 0, 0>(t, kp, a, d, std::min(4, Cd - d), 0, 0);
+    for (int r = 0; r < Cr; r += 48) launch_one<0, 48, 0>(t, kp, a, 0, 0, r, std::min(48, Cr - r));
+    return;
+  }
+  // full gradients
+  if (Cd <= 1 && Cr == 0) return launch_one<1, 0, 1>(t, kp, a, dbase, Cd, 0, 0);
+  if (Cd == 0 && Cr == 1) return launch_one<0, 1, 1>(t, kp, a, 0, 0, rbase, 1);
+  if (Cd <= 1 && Cr <= 1) return launch_one<1, 1, 1>(t, kp, a, 0, Cd, 0, Cr);
+  if (Cd <= 1 && Cr <= 4) return launch_one<1, 4, 1>(t, kp, a, 0, Cd, 0, Cr);
+  for (int d = 0; d < Cd; d += 4) launch_one<4, 0, 1>(t, kp, a, d, std::min(4, Cd - d), 0, 0);
+  for (int r = 0; r < Cr; r += 16) launch_one<0, 16, 1>(t, kp, a, 0, 0, r, std::min(16, Cr - r));
+}
+
+}  // namespace dpl

@@ -1,0 +1,26 @@
+// forward.cuh — host entry points of the forward traversals (forward.cu).
+#pragma once
+
+#include "tree.cuh"
+
+namespace dpl {
+
+struct FwdArgs {
+  const double* xs = nullptr;     // device, q x 3 (original order)
+  const int32_t* perm = nullptr;  // device, sorted position -> query index (or null)
+  int64_t q = 0;
+  float* out = nullptr;           // device, q x out_stride
+  int out_stride = 1;
+  int single = 0;                 // primal_channel: q x 1 output
+  float* grad = nullptr;          // grad_mode 1: q x C x 3; grad_mode 2: q x 3
+  int grad_mode = 0;              // 0 none, 1 all channels, 2 dipole slot 0 only
+  long long* counters = nullptr;  // q x 5 (dpl_counters)
+  int* overflow = nullptr;        // device flag
+  int only_dip = -1, only_rad = -1;  // primal_channel: the single slot
+  int nr_limit = -1;                 // only the first nr_limit radial slots (render step)
+};
+
+void forward_launch(const Tree& t, const KParams& kp, FwdArgs a);
+void morton_order(Tree& t, const double* xs_dev, int64_t q, int32_t* perm_out, DevBuf& ws);
+
+}  // namespace dpl

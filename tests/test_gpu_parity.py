@@ -1,0 +1,291 @@
+"""GPU parity against the CPU oracle (oracle/dipole_oracle.c, itself pinned
+bit-for-bit to the reference in tests/test_oracle_pins.py).
+
+Bar (BASELINE.json north_star): tree structure bit-exact; values and gradients
+within 1e-4 relative / 1e-6 absolute in fp32 at the same Barnes-Hut beta.
+These mirror the reference's own hot-path tests (proj/tests/test_bhtree.cpp),
+re-targeted at the batched GPU API with fp32 tolerances.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+RTOL, ATOL = 1e-4, 1e-6
+
+
+def close(got, want, rtol=RTOL, atol=ATOL):
+    got = np.asarray(got, np.float64)
+    want = np.asarray(want, np.float64)
+    bad = np.abs(got - want) > atol + rtol * np.abs(want)
+    return int(bad.sum()), float(np.abs(got - want).max(initial=0.0))
+
+
+def rel_scale_err(got, want):
+    got = np.asarray(got, np.float64)
+    want = np.asarray(want, np.float64)
+    s = max(np.abs(want).max(initial=0.0), 1e-300)
+    return float(np.abs(got - want).max(initial=0.0) / s)
+
+
+def random_cloud(n, seed, C, f32=True):
+    rng = np.random.default_rng(seed)
+    pos = rng.uniform(-1, 1, (n, 3))
+    nrm = rng.standard_normal((n, 3))
+    nrm /= np.linalg.norm(nrm, axis=1, keepdims=True)
+    area = 0.5 + 0.5 * np.abs(rng.uniform(-1, 1, n))
+    mu = rng.uniform(-1, 1, (n, C))
+    if f32:
+        pos = pos.astype(np.float32).astype(np.float64)
+    return pos, nrm, area / n, mu
+
+
+@pytest.fixture(scope="module")
+def eng():
+    import paper_2405_16788_b200 as P
+
+    return P
+
+
+def make(eng, O, pos, nrm, area, mu, kinds=None, max_leaf=8, max_depth=20):
+    t = eng.DipoleTree(0)
+    t.build(eng.OrientedPointCloud(pos, nrm, area, mu), max_leaf, max_depth)
+    r = O.OracleTree(O.Cloud(pos, nrm, area, mu), max_leaf, max_depth)
+    if kinds is not None:
+        t.set_channel_kernels(kinds)
+        r.set_kinds(kinds)
+    return t, r
+
+
+# ---------------------------------------------------------------- structure
+@pytest.mark.parametrize("n,seed,max_leaf,max_depth", [
+    (1, 0, 8, 20), (2, 1, 8, 20), (9, 2, 8, 20), (1000, 3, 8, 20), (20000, 4, 8, 20),
+    (5000, 5, 1, 20), (5000, 6, 32, 20), (5000, 7, 8, 4), (3000, 8, 8, 0), (3000, 9, 8, 21)])
+def test_tree_structure_bit_exact(eng, oracle_mod, n, seed, max_leaf, max_depth):
+    pos, nrm, area, mu = random_cloud(n, seed, 2)
+    t, r = make(eng, oracle_mod, pos, nrm, area, mu, max_leaf=max_leaf, max_depth=max_depth)
+    a, b = t.export(), r.export()
+    for k in ("topo", "order", "leaf_of", "geo"):
+        assert np.array_equal(a[k], b[k]), k
+
+
+def test_tree_coincident_and_clustered(eng, oracle_mod):
+    # all points coincident must terminate with a leaf (test_bhtree.cpp:48-60)
+    pos = np.full((100, 3), 0.5)
+    nrm = np.tile([0.0, 0.0, 1.0], (100, 1))
+    t, r = make(eng, oracle_mod, pos, nrm, np.ones(100), np.ones((100, 1)))
+    a, b = t.export(), r.export()
+    assert np.array_equal(a["topo"], b["topo"]) and np.array_equal(a["order"], b["order"])
+    leaves = a["topo"][a["topo"][:, 5] == 1]
+    assert int((leaves[:, 1] - leaves[:, 0]).sum()) == 100
+    # tight clusters + duplicates stress deep levels
+    rng = np.random.default_rng(11)
+    base = rng.uniform(-1, 1, (50, 3))
+    pos = np.repeat(base, 40, axis=0) + rng.normal(0, 1e-6, (2000, 3))
+    pos[::7] = pos[0]
+    pos = pos.astype(np.float32).astype(np.float64)
+    nrm = np.tile([1.0, 0.0, 0.0], (2000, 1))
+    t, r = make(eng, oracle_mod, pos, nrm, np.full(2000, 1e-3), rng.standard_normal((2000, 2)))
+    a, b = t.export(), r.export()
+    for k in ("topo", "order", "leaf_of", "geo"):
+        assert np.array_equal(a[k], b[k]), k
+
+
+# ---------------------------------------------------------------- forward
+@pytest.mark.parametrize("beta", [2.0, 4.0, np.inf])
+def test_primal_parity_mixed_kernels(eng, oracle_mod, beta):
+    O = oracle_mod
+    pos, nrm, area, mu = random_cloud(4000, 3, 3)
+    kinds = np.array([0, 1, 1], np.uint8)
+    t, r = make(eng, O, pos, nrm, area, mu, kinds)
+    rng = np.random.default_rng(4)
+    xs = rng.uniform(-1.5, 1.5, (3000, 3)).astype(np.float32).astype(np.float64)
+    xs[:5] = pos[:5]  # coincident queries
+    p = eng.KernelParams(epsilon=0.05)
+    got, cnt = t.primal(xs, p, beta, visited=True)
+    want, wcnt = r.primal(O.Params(0.05), beta, xs, counters=True)
+    nbad, mx = close(got, want)
+    assert nbad == 0, (nbad, mx)
+    # identical opening decisions: visited / far / point counts match exactly
+    assert np.array_equal(cnt[:, 0], wcnt[:, 0])
+    assert np.array_equal(cnt[:, 1] + cnt[:, 2], wcnt[:, 1] + wcnt[:, 2])
+    assert np.array_equal(cnt[:, 3] + cnt[:, 4], wcnt[:, 3] + wcnt[:, 4])
+    # primal_channel(c) == primal()[c] (test_bhtree.cpp:140)
+    for c in range(3):
+        pc = t.primal_channel(xs, p, beta, c)
+        assert np.array_equal(pc, got[:, c])
+
+
+def test_primal_with_gradient_parity(eng, oracle_mod):
+    O = oracle_mod
+    pos, nrm, area, mu = random_cloud(3000, 7, 2)
+    kinds = np.array([0, 1], np.uint8)
+    t, r = make(eng, O, pos, nrm, area, mu, kinds)
+    xs = np.random.default_rng(8).uniform(-1.5, 1.5, (2000, 3))
+    p = eng.KernelParams(epsilon=0.2)
+    v, g = t.primal_with_gradient(xs, p, 2.0)
+    wv, wg = r.primal(O.Params(0.2), 2.0, xs, mode="grad")
+    assert close(v, wv)[0] == 0
+    nbad, mx = close(g, wg)
+    assert nbad == 0, (nbad, mx)
+    # values of primal_with_gradient equal primal (test_bhtree.cpp:215-216), fp32 tolerance
+    assert close(v, t.primal(xs, p, 2.0))[0] == 0
+    v0, g0 = t.primal_grad0(xs, p, 2.0)
+    assert close(v0, wv)[0] == 0 and close(g0, wg[:, 0])[0] == 0
+
+
+def test_beta_infinity_equals_naive(eng, oracle_mod):
+    O = oracle_mod
+    pos, nrm, area, mu = random_cloud(500, 3, 3)
+    kinds = np.array([0, 1, 1], np.uint8)
+    t, r = make(eng, O, pos, nrm, area, mu, kinds)
+    xs = np.random.default_rng(4).uniform(-1.5, 1.5, (200, 3))
+    got = t.primal(xs, eng.KernelParams(epsilon=0.15), np.inf)
+    for c in range(3):
+        want = r.naive_sum(O.Params(0.15), xs, c, int(kinds[c]))
+        assert close(got[:, c], want)[0] == 0
+
+
+@pytest.mark.parametrize("eps,desing,delta", [(0.0, False, 0.0), (0.0, True, 0.05), (0.3, False, 0.0)])
+def test_kernel_variants(eng, oracle_mod, eps, desing, delta):
+    O = oracle_mod
+    pos, nrm, area, mu = random_cloud(2000, 21, 2)
+    kinds = np.array([0, 1], np.uint8)
+    t, r = make(eng, O, pos, nrm, area, mu, kinds)
+    xs = np.random.default_rng(22).uniform(-1.2, 1.2, (1000, 3))
+    p = eng.KernelParams(epsilon=eps, desingularized=desing, desing_delta=delta)
+    v, g = t.primal_with_gradient(xs, p, 2.0)
+    wv, wg = r.primal(O.Params(eps, desing, delta), 2.0, xs, mode="grad")
+    assert close(v, wv, rtol=3e-4)[0] == 0
+    assert rel_scale_err(g, wg) < 1e-4
+
+
+def test_config1_slice(eng, oracle_mod):
+    from paper_2405_16788_b200 import workloads as W
+
+    O = oracle_mod
+    w = W.config1(scale=0.05)
+    c = w["cloud"]
+    t, r = make(eng, O, c.positions, c.normals, c.areas, c.moments, w["kinds"])
+    eps = 1.5 * O.mean_knn_spacing(c.positions)
+    xs = w["xs"]
+    got = t.primal(xs, eng.KernelParams(epsilon=eps), 2.0)
+    want = r.primal(O.Params(eps), 2.0, xs)
+    nbad, mx = close(got, want)
+    assert nbad == 0, (nbad, mx)
+
+
+# ---------------------------------------------------------------- adjoint
+@pytest.mark.parametrize("with_grad", [False, True])
+def test_adjoint_flush_parity(eng, oracle_mod, with_grad):
+    O = oracle_mod
+    pos, nrm, area, mu = random_cloud(3000, 12, 3)
+    kinds = np.array([0, 1, 1], np.uint8)
+    t, r = make(eng, O, pos, nrm, area, mu, kinds)
+    rng = np.random.default_rng(13)
+    q = 2000
+    xs = rng.uniform(-1.5, 1.5, (q, 3))
+    d_out = rng.standard_normal((q, 3)).astype(np.float32)
+    d_grad = rng.standard_normal((q, 3, 3)).astype(np.float32) if with_grad else None
+    p = eng.KernelParams(epsilon=0.1)
+    buf = t.make_buffer()
+    t.adjoint(xs, p, 2.0, d_out, d_grad, buf)
+    g = t.flush_gradients(buf)
+    wm, wn, we = r.adjoint(O.Params(0.1), 2.0, xs, d_out.astype(np.float64),
+                           None if d_grad is None else d_grad.astype(np.float64))
+    assert rel_scale_err(g.moments, wm) < 1e-5
+    assert rel_scale_err(g.normals, wn) < 1e-5
+    assert abs(g.d_epsilon - we) <= 1e-4 * abs(we) + 1e-6
+    nbad, _ = close(g.moments, wm)
+    assert nbad <= 0.001 * wm.size
+    # flush zeroes the buffer: a second flush is all zeros (test_bhtree.cpp:297-299)
+    g2 = t.flush_gradients(buf)
+    assert not np.any(g2.moments) and g2.d_epsilon == 0.0
+
+
+def test_multi_buffer_flush_order_independent(eng, oracle_mod):
+    pos, nrm, area, mu = random_cloud(300, 18, 1)
+    t, _ = make(eng, oracle_mod, pos, nrm, area, mu)
+    rng = np.random.default_rng(19)
+    xs = rng.uniform(-1, 1, (12, 3))
+    ds = rng.uniform(-1, 1, (12, 1)).astype(np.float32)
+    p = eng.KernelParams(epsilon=0.1)
+    single = t.make_buffer()
+    t.adjoint(xs, p, 2.0, ds, None, single)
+    ref = t.flush_gradients(single)
+    bufs = [t.make_buffer() for _ in range(3)]
+    for w in range(3):
+        t.adjoint(xs[w::3], p, 2.0, ds[w::3], None, bufs[w])
+    got = t.flush_gradients(bufs)
+    assert rel_scale_err(got.moments, ref.moments) < 1e-6
+
+
+def test_zero_adjoint_leaves_accumulators_untouched(eng, oracle_mod):
+    pos, nrm, area, mu = random_cloud(100, 11, 2)
+    t, _ = make(eng, oracle_mod, pos, nrm, area, mu)
+    buf = t.make_buffer()
+    t.adjoint(np.array([[0.1, 0.2, 0.3]]), eng.KernelParams(epsilon=0.2), 2.0,
+              np.zeros((1, 2), np.float32), None, buf)
+    g = t.flush_gradients(buf)
+    assert not np.any(g.moments) and not np.any(g.normals) and g.d_epsilon == 0.0
+
+
+def test_single_point_adjoint_closed_form(eng, oracle_mod):
+    # test_bhtree.cpp:259-281: radius-0 leaf seen as far field
+    import math
+
+    t = eng.DipoleTree(0)
+    t.build(eng.OrientedPointCloud(np.zeros((1, 3)), np.array([[0, 0, 1.0]]), np.array([0.8]),
+                                   np.array([[0.6]])))
+    buf = t.make_buffer()
+    t.adjoint(np.array([[0, 0, -1.0]]), eng.KernelParams(epsilon=0.3), 2.0,
+              np.array([[2.5]], np.float32), None, buf)
+    g = t.flush_gradients(buf)
+    tau = oracle_mod.port_lib().ora_tau(1 / 0.3)
+    want = 0.8 * (1 / (4 * math.pi)) * tau * 2.5 * 0.8 / 0.8  # d beta = a P_eps ds
+    assert abs(g.moments[0, 0] - want) <= 1e-5 * abs(want)
+
+
+# ---------------------------------------------------------------- render step
+def test_render_step_parity(eng, oracle_mod):
+    from paper_2405_16788_b200 import renderer as Rn
+    from paper_2405_16788_b200 import workloads as W
+
+    O = oracle_mod
+    w = W.config3(scale=0.02)
+    c = w["cloud"]
+    t, r = make(eng, O, c.positions, c.normals, c.areas, c.moments, w["kinds"])
+    eps = 1.5 * O.mean_knn_spacing(c.positions)
+    rays = w["rays"][:256]
+    S = 32
+    target = w["target"][:256]
+    rs = Rn.RenderSettings(t_near=2.0, t_far=6.0, seed=3)
+    p = eng.KernelParams(epsilon=eps)
+    rgb, tape = Rn.render_forward(t, p, rs, rays, S)
+    scale = 2.0 / (3.0 * rays.shape[0])
+    d_rgb = (scale * (rgb.astype(np.float64) - target)).astype(np.float32)
+    buf = t.make_buffer()
+    dl, dbg = Rn.render_backward(t, p, rs, tape, d_rgb, buf)
+    g = t.flush_gradients(buf)
+    ts, dlt = O.stratified_samples(rays.shape[0], S, 2.0, 6.0, 3)
+    want = r.render_step(O.Params(eps), 2.0, 20.0, [0, 0, 0], rays, ts, dlt, target, scale)
+    assert close(rgb, want["rgb"])[0] == 0
+    assert rel_scale_err(g.moments, want["moments"]) < 1e-4
+    assert rel_scale_err(g.normals, want["normals"]) < 1e-4
+    assert abs(g.d_epsilon - want["d_eps"]) <= 1e-4 * abs(want["d_eps"]) + 1e-6
+    assert abs(dl - want["d_lambda"]) <= 1e-4 * abs(want["d_lambda"]) + 1e-8
+    assert np.abs(dbg - want["d_bg"]).max() <= 1e-4 * np.abs(want["d_bg"]).max() + 1e-8
+
+
+# ---------------------------------------------------------------- errors
+def test_error_behaviour(eng, oracle_mod):
+    t = eng.DipoleTree(0)
+    with pytest.raises(eng.DataError):
+        t.build(eng.OrientedPointCloud(np.zeros((0, 3)), np.zeros((0, 3)), np.zeros(0),
+                                       np.zeros((0, 1))))
+    pos, nrm, area, mu = random_cloud(10, 24, 2)
+    t.build(eng.OrientedPointCloud(pos, nrm, area, mu))
+    with pytest.raises(eng.DataError):
+        t.set_channel_kernels([0])
+    with pytest.raises(eng.DataError):
+        t.update_moments(eng.OrientedPointCloud(pos[:-1], nrm[:-1], area[:-1], mu[:-1]))
