@@ -1,0 +1,434 @@
+#!/usr/bin/env python
+"""bench.py — Barnes-Hut dipole-sum queries/sec on B200 (BASELINE.json metric).
+
+Workload (N=1 default): BASELINE config 2 — N = 1,000,000 points (95% noisy
+torus + 5% outliers), C = 49 channels (ch 0 Dipole, 1..48 Radial), Q = 4,000,000
+uniform queries in [-2,2]^3, beta = 2, leaf 8, eps = 1.5 x mean 8-NN spacing.
+One STEP = forward primal of all Q queries + adjoint of the same Q queries with
+N(0,1) upstream gradients + flush_gradients (push-down to per-point gradients);
+with N > 1 GPUs each rank owns its own Q queries (weak scaling) against a
+replicated tree and the per-point gradients are NCCL-allreduced every step.
+
+value = (N_ranks x Q) / step time  [queries/s; each query is evaluated forward
+and adjoint], max over ranks, CUDA events, inputs resident in HBM. e2e = the
+same through the public API from pinned HOST buffers (H2D of queries and
+upstream gradients, D2H of outputs and gradients inside the timed region).
+Inputs per step (~0.9 GB) exceed the 126 MB L2, so no explicit L2 flush.
+
+--impl reference: the reference's own CPU path (oracle/_ref, compiled from
+/root/reference sources unmodified) on the box's host cores, on a bounded
+query sample of the same workload; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "dipole-sum queries/sec (forward, adjoint) at 1/2/4/8 B200; % of roofline"
+UNIT = "queries/s"
+BETA = 2.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--scale", type=float, default=1.0, help="shrink N and Q (development only)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of CPU baseline work")
+    return ap.parse_args()
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu):
+        self.gpu = gpu
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                sm.append(float(p[1]))
+                mx = max(mx, float(p[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ cost model
+def flops_model(tot, Cd, Cr):
+    """SURVEY §8(d) cost model v1 (flop constants: add/mul 1, FMA 2, div/sqrt 4,
+    exp 8, erf 16). tot = summed counters (V, F_near, F_far, P_near, P_far)."""
+    V, Fn, Ff, Pn, Pf = [float(x) for x in tot]
+    K0n, K0f, K2n = 40.0, 11.0, 12.0
+    fwd = (9 * V + Fn * (K0n + 2 + 7 * Cd + 2 * Cr) + Ff * (K0f + 2 + 7 * Cd + 2 * Cr)
+           + Pn * (14 + K0n + 2 * Cd + 2 * Cr) + Pf * (14 + K0f + 2 * Cd + 2 * Cr))
+    adj = (9 * V + Fn * (K0n + K2n + 2 + 15 * Cd + 6 * Cr) + Ff * (K0f + 2 + 7 * Cd + 2 * Cr)
+           + Pn * (14 + K0n + K2n + 15 * Cd + 6 * Cr) + Pf * (14 + K0f + 11 * Cd + 3 * Cr))
+    return fwd, adj
+
+
+# ------------------------------------------------------------------ reference arm
+def reference_measure(w, eps, budget_s, steps=None, warmup=0, threads=None):
+    """Reference CPU path (oracle/_ref): DipoleTree::primal over a query sample with
+    parallel_for, adjoint with one GradientBuffer per worker, flush_gradients."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    from paper_2405_16788_b200 import workloads as W
+
+    if not O.have_ref():
+        raise RuntimeError("oracle/_ref/libdipole_ref.so missing (built by __graft_entry__.build())")
+    c = w["cloud"]
+    t0 = time.time()
+    tree = O.OracleTree(O.Cloud(c.positions, c.normals, c.areas, c.moments), backend="ref")
+    tree.set_kinds(w["kinds"])
+    build_s = time.time() - t0
+    cores = threads or O.ref_lib().ref_hardware_concurrency()
+    # adjoint buffers are ~ (nodes*C*4 + N*(C+3)) doubles per worker (bhtree.cpp:336-343)
+    nodes = tree.node_count()
+    buf_bytes = 8.0 * (nodes * c.channels * 4 + c.size * (c.channels + 3))
+    try:
+        import psutil
+
+        avail = psutil.virtual_memory().available
+    except Exception:
+        avail = 16e9
+    adj_workers = int(max(1, min(cores, 0.5 * avail // buf_bytes)))
+    p = O.Params(eps)
+    xs_all = w["xs"]
+    C = c.channels
+
+    def one(qs):
+        xs = xs_all[:qs]
+        d_out = W.upstream(qs, C, w.get("d_out_seed", [0, 2])).astype(np.float64)
+        t = time.time()
+        tree.primal(p, BETA, xs, threads=cores)
+        tf = time.time() - t
+        t = time.time()
+        tree.adjoint(p, BETA, xs, d_out, threads=adj_workers)
+        ta = time.time() - t
+        return tf, ta
+
+    # calibrate: per-query cost and the fixed (buffer + flush) cost
+    q1, q2 = 2000, 8000
+    f1, a1 = one(q1)
+    f2, a2 = one(q2)
+    per_q = max(1e-9, (f2 + a2 - f1 - a1) / (q2 - q1))
+    fixed = max(0.0, (f1 + a1) - per_q * q1)
+    n_steps = 1 if steps is None else steps + warmup
+    per_step = budget_s / max(1, n_steps)
+    sample = int(min(xs_all.shape[0], max(q2, (per_step - fixed) / per_q)))
+    sample = max(1000, sample)
+    times = []
+    for i in range(n_steps):
+        tf, ta = one(sample)
+        if steps is None or i >= warmup:
+            times.append((tf, ta))
+    tf = float(np.mean([x[0] for x in times]))
+    ta = float(np.mean([x[1] for x in times]))
+    return dict(value=sample / (tf + ta), forward_qps=sample / tf, adjoint_qps=sample / ta,
+                sample=sample, cores=cores, adjoint_workers=adj_workers, build_s=build_s,
+                ms_per_step=1e3 * (tf + ta))
+
+
+def cpu_info():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def run_reference(args):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return
+    from paper_2405_16788_b200 import workloads as W
+
+    w = W.config2(scale=args.scale)
+    eps = W.epsilon_for("config2", args.scale)
+    budget = max(30.0, min(240.0, 8.0 * (args.steps + args.warmup)))
+    r = reference_measure(w, eps, budget, steps=args.steps, warmup=args.warmup)
+    sample_desc = (f"{r['sample']} of {w['xs'].shape[0]} config-2 queries per step (forward + "
+                   f"adjoint + flush, {r['adjoint_workers']} GradientBuffers), reference sources "
+                   f"compiled -O3 without -march; CPU {cpu_info()}")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": r["value"], "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded config-2 generator)",
+        "config": {"workload": "config2: N=1e6 torus+outliers, C=49, Q=4e6, beta=2, forward+adjoint",
+                   "sample_queries": r["sample"]},
+        "forward_qps": r["forward_qps"], "adjoint_qps": r["adjoint_qps"],
+        "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": r["cores"],
+                         "kind": "reference", "sample": sample_desc},
+        "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args):
+    import torch
+
+    import paper_2405_16788_b200 as P
+    from paper_2405_16788_b200 import bhtree as B
+    from paper_2405_16788_b200 import workloads as W
+
+    rank, world, local = env_rank()
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
+
+    w = W.config2(scale=args.scale)
+    eps = W.epsilon_for("config2", args.scale)
+    c = w["cloud"]
+    xs_np = W.rank_queries(w, rank)
+    Q, N, C = xs_np.shape[0], c.size, c.channels
+    params = P.KernelParams(epsilon=eps)
+
+    tree = P.DipoleTree(local, stream=stream)
+    t0 = time.time()
+    tree.build(c)
+    tree.set_channel_kernels(w["kinds"])
+    torch.cuda.synchronize()
+    build_s = time.time() - t0
+    nodes = tree.node_count()
+
+    xs = torch.from_numpy(xs_np).to(dev)
+    d_out = torch.from_numpy(W.upstream(Q, C, w["d_out_seed"] + [rank])).to(dev)
+    out = torch.empty((Q, C), dtype=torch.float32, device=dev)
+    mom = torch.empty((N, C), dtype=torch.float32, device=dev)
+    nrm = torch.empty((N, 3), dtype=torch.float32, device=dev)
+    deps = torch.zeros(1, dtype=torch.float64, device=dev)
+    buf = tree.make_buffer()
+
+    # counting pass (untimed): replays the opening decisions -> algorithmic work
+    _, cnt = tree.primal(xs, params, BETA, out=out, visited=True)
+    tot = cnt.sum(dim=0).cpu().numpy()
+    f_fwd, f_adj = flops_model(tot, 1, C - 1)
+
+    def step():
+        tree.primal(xs, params, BETA, out=out)
+        tree.adjoint(xs, params, BETA, d_out, None, buf)
+        g = tree.flush_gradients(buf, out=(mom, nrm))
+        if dist is not None:
+            deps.fill_(g.d_epsilon)
+            dist.all_reduce(mom)
+            dist.all_reduce(nrm)
+            dist.all_reduce(deps)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    B.profile_read(tree)
+    B.profile_enable(tree, True)
+    launches0 = B.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+    launches = B.launch_count() - launches0
+    ms = e0.elapsed_time(e1) / args.steps
+    prof = B.profile_read(tree)
+    B.profile_enable(tree, False)
+    ms_t = torch.tensor([ms], device=dev)
+    if dist is not None:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    value = world * Q / (ms_max * 1e-3)
+
+    fwd_ms = prof["forward"][0] / max(1, prof["forward"][1])
+    adj_ms = prof["adjoint"][0] / max(1, prof["adjoint"][1])
+    sort_ms = prof["sort"][0] / max(1, args.steps)
+    flush_ms = prof["flush"][0] / max(1, prof["flush"][1])
+
+    # ------------------------------------------------------------ e2e (host buffers)
+    e2e = None
+    if not args.no_e2e:
+        xs_h = torch.from_numpy(xs_np).pin_memory()
+        do_h = d_out.cpu().pin_memory()
+        out_h = torch.empty((Q, C), dtype=torch.float32).pin_memory()
+        mom_h = torch.empty((N, C), dtype=torch.float32).pin_memory()
+        nrm_h = torch.empty((N, 3), dtype=torch.float32).pin_memory()
+
+        def step_host():
+            tree.primal(xs_h, params, BETA, out=out_h)
+            tree.adjoint(xs_h, params, BETA, do_h, None, buf)
+            g = tree.flush_gradients(buf, out=(mom_h, nrm_h))
+            if dist is not None:
+                m = mom_h.to(dev, non_blocking=True)
+                dist.all_reduce(m)
+                mom_h.copy_(m)
+            return g
+
+        step_host()
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        t0 = time.perf_counter()
+        k2 = max(1, min(args.steps, 5))
+        for _ in range(k2):
+            step_host()
+        torch.cuda.synchronize()
+        e2e_s = (time.perf_counter() - t0) / k2
+        t_t = torch.tensor([e2e_s], device=dev)
+        if dist is not None:
+            dist.all_reduce(t_t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t_t.item())
+        h2d = 2 * xs_np.nbytes + Q * C * 4
+        d2h = Q * C * 4 + N * C * 4 + N * 12 + 8
+        e2e = {"value": world * Q / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": 1e3 * e2e_s,
+               "timing": "wall clock around synchronous public-API calls (pinned host buffers)"}
+
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+
+    peak32 = B.peak_fp32(local)
+    peak64 = B.peak_fp64(local)
+    dom = "adjoint" if adj_ms >= fwd_ms else "forward"
+    dom_flops = f_adj if dom == "adjoint" else f_fwd
+    dom_ms = adj_ms if dom == "adjoint" else fwd_ms
+    achieved = dom_flops / (dom_ms * 1e-3) / 1e12
+    clocks = clk.summary()
+
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        try:
+            r = reference_measure(w, eps, args.cpu_budget)
+            cpu = {"value": r["value"], "unit": UNIT, "cores": r["cores"], "kind": "reference",
+                   "sample": f"{r['sample']} config-2 queries, forward + adjoint + flush "
+                             f"({r['adjoint_workers']} GradientBuffers), reference sources "
+                             f"compiled unmodified; CPU {cpu_info()}",
+                   "forward_qps": r["forward_qps"], "adjoint_qps": r["adjoint_qps"]}
+        except Exception as e:  # report, do not hide
+            cpu = {"value": None, "error": str(e)}
+
+    bytes_fwd = Q * (24 + 4 * C) + nodes * (32 + 16 + 16 + 16 + 4 * 48) + N * (24 + 16 + 16 + 4 * 48)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32 (fp64 opening tests and accumulators)",
+        "data": "synthetic (seeded config-2 generator; no dataset)",
+        "config": {"workload": "config2: N=1e6 torus+outliers, C=49 (1 Dipole + 48 Radial), "
+                               "Q=4e6 per GPU uniform in [-2,2]^3, beta=2, leaf 8, forward+adjoint+flush",
+                   "points": N, "queries_per_gpu": Q, "channels": C, "nodes": nodes,
+                   "epsilon": eps, "l2": "inputs > L2 (0.9 GB/step), no explicit flush",
+                   "parallelism": f"replicated tree, {world}-way query sharding"
+                                  + (", NCCL allreduce of point gradients" if world > 1 else "")},
+        "forward_qps": world * Q / ((fwd_ms + sort_ms / 2) * 1e-3),
+        "adjoint_qps": world * Q / ((adj_ms + sort_ms / 2 + flush_ms) * 1e-3),
+        "phase_ms": {"morton_sort_x2": sort_ms, "forward": fwd_ms, "adjoint": adj_ms,
+                     "flush": flush_ms},
+        "interactions_per_query": float((tot[1] + tot[2] + tot[3] + tot[4]) / Q),
+        "visited_per_query": float(tot[0] / Q),
+        "roofline": {"bound": "fp32", "kernel": f"k_{dom} (warp-cooperative traversal)",
+                     "achieved": achieved, "peak": peak32, "unit": "TFLOP/s",
+                     "frac": achieved / peak32,
+                     "peak_source": "measured FFMA microbenchmark in this run (dpl_peak_fp32); "
+                                    "MEASURED_PEAKS.json has no FP32 figure",
+                     "flops_per_launch": dom_flops, "flop_model": "SURVEY §8(d) cost model v1",
+                     "traffic": None,
+                     "hbm_compulsory_bytes_forward": bytes_fwd,
+                     "peak_fp64_measured": peak64},
+        "gpu_launches": int(launches),
+        "clocks": clocks,
+        "build_s": build_s,
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

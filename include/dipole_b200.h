@@ -169,6 +169,18 @@ double dpl_uniform(uint64_t seed, uint64_t counter);
 int dpl_adam_step(dpl_tree_t tree, float* params, const float* grads, float* m, float* v,
                   int64_t n, double lr, double beta1, double beta2, double eps, int64_t t);
 
+/* ---- measurement -----------------------------------------------------------
+ * Per-phase CUDA-event timing on the handle's stream (phases: 0 query Morton
+ * sort, 1 forward traversal, 2 adjoint traversal, 3 flush, 4 render per-ray
+ * kernels, 5 moment refresh). read() synchronises, returns the summed ms and
+ * call counts since the previous read, and clears. */
+int dpl_profile_enable(dpl_tree_t tree, int on);
+int dpl_profile_read(dpl_tree_t tree, double* ms /* 6 */, int64_t* counts /* 6 */);
+/* FFMA / DFMA throughput microbenchmarks (register operands, 8 chains/thread):
+ * the measured FP32 / FP64 pipe peaks used as roofline denominators. */
+int dpl_peak_fp32(int device, double* tflops);
+int dpl_peak_fp64(int device, double* tflops);
+
 #ifdef __cplusplus
 }
 #endif

@@ -284,14 +284,19 @@ class DipoleTree:
         check(lib().dpl_adjoint(self._h, C.byref(params), float(beta_bh), xp, q, dp, gp, buf._h))
         buf.dirty = True
 
-    def flush_gradients(self, buffers, device_out=None) -> PointGradients:
+    def flush_gradients(self, buffers, device_out=None, out=None) -> PointGradients:
         """DipoleTree::flush_gradients (bhtree.cpp:419-463); zeroes the buffers.
-        device_out: a torch device to receive the outputs (else numpy)."""
+        device_out: a torch device to receive the outputs (else numpy);
+        out: preallocated (moments N x C, normals N x 3) fp32 arrays/tensors."""
         if isinstance(buffers, GradientBuffer):
             buffers = [buffers]
         n, Cc = self.point_count(), self.channels()
         arr = (C.c_void_p * len(buffers))(*[b._h for b in buffers])
-        if device_out is not None:
+        if out is not None:
+            mom, nrm = out
+            mp = mom.data_ptr() if _is_torch(mom) else mom.ctypes.data
+            np_ = nrm.data_ptr() if _is_torch(nrm) else nrm.ctypes.data
+        elif device_out is not None:
             mom = torch.empty((n, Cc), dtype=torch.float32, device=device_out)
             nrm = torch.empty((n, 3), dtype=torch.float32, device=device_out)
             mp, np_ = mom.data_ptr(), nrm.data_ptr()
@@ -309,3 +314,30 @@ class DipoleTree:
 def launch_count() -> int:
     """Kernel launches issued through the engine in this process."""
     return int(lib().dpl_launch_count())
+
+
+PHASES = ("sort", "forward", "adjoint", "flush", "render", "moments")
+
+
+def profile_enable(tree: DipoleTree, on=True):
+    check(lib().dpl_profile_enable(tree._h, int(on)))
+
+
+def profile_read(tree: DipoleTree):
+    """{phase: (total_ms, launches)} since the previous read (CUDA events)."""
+    ms = (C.c_double * 6)()
+    cnt = (C.c_int64 * 6)()
+    check(lib().dpl_profile_read(tree._h, ms, cnt))
+    return {p: (ms[i], cnt[i]) for i, p in enumerate(PHASES)}
+
+
+def peak_fp32(device=0) -> float:
+    v = C.c_double()
+    check(lib().dpl_peak_fp32(int(device), C.byref(v)))
+    return v.value
+
+
+def peak_fp64(device=0) -> float:
+    v = C.c_double()
+    check(lib().dpl_peak_fp64(int(device), C.byref(v)))
+    return v.value

@@ -4,6 +4,7 @@
 // (DataError on empty clouds / size or channel mismatches, bhtree.cpp:159,173,
 // 180), stages host arrays through the handle's stream, runs the sm_100a
 // kernels, and maps exceptions to status codes + a thread-local message.
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <cstdio>
@@ -348,7 +349,10 @@ static int forward_common(dpl_tree_t h, const dpl_kernel_params* params, double 
     tree_ensure_thresholds(t, beta);
     const double* xs_d = stage_in(t, xs, (size_t)q * 3, h->ws_xs);
     h->ws_perm.reserve(q * 4);
-    morton_order(t, xs_d, q, h->ws_perm.as<int32_t>(), h->ws_morton);
+    {
+      PhaseTimer pt(t, PH_SORT);
+      morton_order(t, xs_d, q, h->ws_perm.as<int32_t>(), h->ws_morton);
+    }
     FwdArgs a;
     a.xs = xs_d;
     a.perm = h->ws_perm.as<int32_t>();
@@ -375,7 +379,10 @@ static int forward_common(dpl_tree_t h, const dpl_kernel_params* params, double 
     a.out = o.dev;
     a.grad = g.dev;
     a.counters = cnt.dev;
-    forward_launch(t, kp, a);
+    {
+      PhaseTimer pt(t, PH_FORWARD);
+      forward_launch(t, kp, a);
+    }
     DPL_CUDA(cudaGetLastError());
     o.finish(t);
     g.finish(t);
@@ -465,7 +472,10 @@ int dpl_adjoint(dpl_tree_t h, const dpl_kernel_params* params, double beta_bh, c
     const float* dout_d = stage_in(t, d_out, (size_t)q * t.C, h->ws_dout);
     const float* dg_d = d_grad ? stage_in(t, d_grad, (size_t)q * t.C * 3, h->ws_dgrad) : nullptr;
     h->ws_perm.reserve(q * 4);
-    morton_order(t, xs_d, q, h->ws_perm.as<int32_t>(), h->ws_morton);
+    {
+      PhaseTimer pt(t, PH_SORT);
+      morton_order(t, xs_d, q, h->ws_perm.as<int32_t>(), h->ws_morton);
+    }
     AdjArgs a;
     a.xs = xs_d;
     a.perm = h->ws_perm.as<int32_t>();
@@ -475,7 +485,10 @@ int dpl_adjoint(dpl_tree_t h, const dpl_kernel_params* params, double beta_bh, c
     a.d_grad = dg_d;
     a.grad_mode = dg_d ? 1 : 0;
     a.overflow = overflow_flag(h);
-    adjoint_launch(t, kp, a, buf->b);
+    {
+      PhaseTimer pt(t, PH_ADJOINT);
+      adjoint_launch(t, kp, a, buf->b);
+    }
     DPL_CUDA(cudaGetLastError());
     if (!is_device_ptr(xs) || !is_device_ptr(d_out)) DPL_CUDA(cudaStreamSynchronize(t.stream));
   });
@@ -496,7 +509,10 @@ int dpl_flush(dpl_tree_t h, dpl_gradbuf_t* bufs, int32_t nbuf, float* moments, f
     no.bind(t, normals, t.n * 3, h->ws_nrm);
     double de = 0;
     DPL_CUDA(cudaMemcpyAsync(&de, b0.d_eps, 8, cudaMemcpyDeviceToHost, t.stream));
-    flush_launch(t, b0, mo.dev, no.dev);
+    {
+      PhaseTimer pt(t, PH_FLUSH);
+      flush_launch(t, b0, mo.dev, no.dev);
+    }
     mo.finish(t);
     no.finish(t);
     for (int i = 0; i < nbuf; ++i) gradbuf_zero(bufs[i]->b, t.stream);  // reset() (:438)
@@ -561,7 +577,10 @@ int dpl_render_forward(dpl_tree_t h, const dpl_kernel_params* params, const dpl_
     render_samples(t.stream, tape->rays.as<double>(), R, S, ts_d, rp->t_near, rp->t_far, rp->seed,
                    tape->ts.as<double>(), tape->xs.as<double>());
     tape->perm.reserve(Q * 4);
-    morton_order(t, tape->xs.as<double>(), Q, tape->perm.as<int32_t>(), tape->morton);
+    {
+      PhaseTimer pt(t, PH_SORT);
+      morton_order(t, tape->xs.as<double>(), Q, tape->perm.as<int32_t>(), tape->morton);
+    }
     tape->vals.reserve(Q * 16);
     tape->g0.reserve(Q * 12);
     FwdArgs a;
@@ -576,7 +595,10 @@ int dpl_render_forward(dpl_tree_t h, const dpl_kernel_params* params, const dpl_
     // the direct-rgb head reads channels 0..3 only (radiance.cpp:133-145):
     // radial slots 0..2 are channels 1..3 in SceneModel's layout
     a.nr_limit = 3;
-    forward_launch(t, kp, a);
+    {
+      PhaseTimer pt(t, PH_FORWARD);
+      forward_launch(t, kp, a);
+    }
     Out<float> o;
     o.bind(t, rgb, R * 3, h->ws_out);
     tape->tape.reserve(Q * 64);
@@ -628,13 +650,106 @@ int dpl_render_backward(dpl_tree_t h, const dpl_kernel_params* params, const dpl
     a.grad_mode = 2;
     a.nr_limit = 3;
     a.overflow = overflow_flag(h);
-    adjoint_launch(t, kp, a, buf->b);
+    {
+      PhaseTimer pt(t, PH_ADJOINT);
+      adjoint_launch(t, kp, a, buf->b);
+    }
     double sums[4];
     DPL_CUDA(cudaMemcpyAsync(sums, tape->sums.p, 32, cudaMemcpyDeviceToHost, t.stream));
     DPL_CUDA(cudaStreamSynchronize(t.stream));
     if (d_lambda) *d_lambda = sums[0];
     if (d_background) d_background[0] = sums[1], d_background[1] = sums[2], d_background[2] = sums[3];
   });
+}
+
+
+// ---------------------------------------------------------------- profiling
+
+int dpl_profile_enable(dpl_tree_t h, int on) {
+  return guard([&] {
+    require(h != nullptr, DPL_ERR_USAGE, "null tree handle");
+    h->t.prof = on != 0;
+  });
+}
+
+int dpl_profile_read(dpl_tree_t h, double* ms, int64_t* counts) {
+  return guard([&] {
+    require(h != nullptr, DPL_ERR_USAGE, "null tree handle");
+    Tree& t = h->t;
+    DPL_CUDA(cudaStreamSynchronize(t.stream));
+    for (int p = 0; p < PH_COUNT; ++p) {
+      if (ms) ms[p] = 0;
+      if (counts) counts[p] = 0;
+    }
+    for (auto& r : t.recs) {
+      float e = 0;
+      DPL_CUDA(cudaEventElapsedTime(&e, r.a, r.b));
+      if (ms) ms[r.phase] += e;
+      if (counts) counts[r.phase] += 1;
+      t.ev_pool.push_back(r.a);
+      t.ev_pool.push_back(r.b);
+    }
+    t.recs.clear();
+  });
+}
+
+}  // extern "C"
+
+// FFMA / DFMA throughput microbenchmarks: independent chains, register operands
+template <typename T>
+__global__ void k_peak(T* out, int iters, T b, T c) {
+  T a0 = (T)threadIdx.x, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3, a4 = a0 + 4, a5 = a0 + 5,
+    a6 = a0 + 6, a7 = a0 + 7;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      a0 = a0 * b + c; a1 = a1 * b + c; a2 = a2 * b + c; a3 = a3 * b + c;
+      a4 = a4 * b + c; a5 = a5 * b + c; a6 = a6 * b + c; a7 = a7 * b + c;
+    }
+  }
+  T s = ((a0 + a1) + (a2 + a3)) + ((a4 + a5) + (a6 + a7));
+  if (s == (T)-1.2345) out[0] = s;
+}
+
+template <typename T>
+static double run_peak(int device) {
+  DPL_CUDA(cudaSetDevice(device));
+  int sms = 0;
+  DPL_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  T* out;
+  DPL_CUDA(cudaMalloc(&out, sizeof(T)));
+  const int threads = 256, blocks = sms * 8, iters = 2048;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  k_peak<T><<<blocks, threads>>>(out, 64, (T)0.999, (T)0.001);  // warm-up
+  double best = 0;
+  for (int rep = 0; rep < 3; ++rep) {
+    cudaEventRecord(a);
+    k_peak<T><<<blocks, threads>>>(out, iters, (T)0.999, (T)0.001);
+    cudaEventRecord(b);
+    DPL_CUDA(cudaEventSynchronize(b));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    double flops = 2.0 * 64.0 * iters * (double)threads * blocks;
+    best = std::max(best, flops / (ms * 1e-3) / 1e12);
+  }
+  count_launch(4);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(out);
+  DPL_CUDA(cudaGetLastError());
+  return best;
+}
+
+extern "C" {
+
+int dpl_peak_fp32(int device, double* tflops) {
+  return guard([&] { *tflops = run_peak<float>(device); });
+}
+
+int dpl_peak_fp64(int device, double* tflops) {
+  return guard([&] { *tflops = run_peak<double>(device); });
 }
 
 // ---------------------------------------------------------------- Adam

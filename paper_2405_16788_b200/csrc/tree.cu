@@ -47,6 +47,30 @@ void DevBuf::release() {
   bytes = 0;
 }
 
+cudaEvent_t Tree::take_event() {
+  if (!ev_pool.empty()) {
+    cudaEvent_t e = ev_pool.back();
+    ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  DPL_CUDA(cudaEventCreate(&e));
+  return e;
+}
+
+PhaseTimer::PhaseTimer(Tree& tr, int ph) : t(tr), phase(ph) {
+  if (!t.prof) return;
+  a = t.take_event();
+  cudaEventRecord(a, t.stream);
+}
+
+PhaseTimer::~PhaseTimer() {
+  if (!a) return;
+  cudaEvent_t b = t.take_event();
+  cudaEventRecord(b, t.stream);
+  t.recs.push_back({phase, a, b});
+}
+
 static constexpr double kInvFourPi = 0.07957747154594766788444188168625718101;
 
 static inline unsigned grid_for(int64_t n, int block) {
@@ -422,6 +446,7 @@ void tree_update_points(Tree& t, const double* pos, const double* nrm, const dou
 }
 
 void tree_compute_moments(Tree& t) {
+  PhaseTimer ptimer(t, PH_MOMENTS);
   const int B = 256;
   int W = 3 * t.Cd + t.Cr;
   t.node_sumv.reserve(sizeof(double) * std::max<int64_t>(1, t.nodes * t.Cd * 3));

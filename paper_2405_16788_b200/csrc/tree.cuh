@@ -55,6 +55,16 @@ struct Tree {
   // scratch
   DevBuf scratch[8];
 
+  // optional per-phase CUDA-event timing (dpl_profile_*)
+  bool prof = false;
+  struct Rec {
+    int phase;
+    cudaEvent_t a, b;
+  };
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> ev_pool;
+  cudaEvent_t take_event();
+
   TreeView view() const;
   void set_layout();  // from kinds: Cd, Cr, channel maps, upload
 };
@@ -72,5 +82,18 @@ void tree_export(Tree& t, double* geo, int32_t* topo, int32_t* order, int32_t* l
 void tree_full_moments(Tree& t, std::vector<double>& mv, std::vector<double>& ms);
 
 KParams make_kparams(const double epsilon, int desingularized, double delta);
+
+// profiling phases
+enum Phase : int { PH_SORT = 0, PH_FORWARD = 1, PH_ADJOINT = 2, PH_FLUSH = 3, PH_RENDER = 4,
+                   PH_MOMENTS = 5, PH_COUNT = 6 };
+
+// RAII: records an event pair on the tree's stream around a phase when profiling
+struct PhaseTimer {
+  Tree& t;
+  int phase;
+  cudaEvent_t a = nullptr;
+  PhaseTimer(Tree& tr, int ph);
+  ~PhaseTimer();
+};
 
 }  // namespace dpl

@@ -209,7 +209,26 @@ def config3(scale=1.0, seed=0):
 
 
 # Regularisation widths eps = 1.5 x mean 8-NN spacing (SceneModel::prepare,
-# fields.cpp:10-11), computed ONCE by the CPU oracle on the full-size clouds and
-# recorded here (tests/test_workloads.py re-derives them); queries use them as
-# KernelParams.epsilon.
-EPSILON = {}
+# fields.cpp:10-11), computed ONCE by the CPU oracle on the full-size clouds
+# (bit-identical to the reference's kd-tree result; tests/test_workloads.py
+# re-derives config 1) and recorded here; queries use them as KernelParams.epsilon.
+EPSILON = {
+    "config1": 0.018716529322515815,
+    "config2": 0.016877094843460314,
+    "config3": 0.018716529322515815,  # config-1 cloud
+}
+
+
+def epsilon_for(name, scale=1.0):
+    """Recorded eps at full size; for shrunken development runs the surface
+    spacing scales like N^(-1/2)."""
+    return EPSILON[name] / math.sqrt(scale)
+
+
+def rank_queries(w, rank, seed=0):
+    """Weak scaling: rank r > 0 draws its own queries from the same distribution."""
+    if rank == 0:
+        return w["xs"]
+    lo, hi = {"config1": (-1.5, 1.5), "config2": (-2, 2), "config4": (-2, 2)}[w["name"]]
+    q = w["xs"].shape[0]
+    return _f32(np.random.default_rng([seed, 1000 + rank]).uniform(lo, hi, (q, 3)))
