@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32)
   }
   const unsigned active = __ballot_sync(FULL_MASK, valid);
   if (!active) return;
-  const int Cd = tv.Cd, Cr = tv.Cr, PR = tv.P;
+  const int Cd = tv.Cd, Cr = tv.Cr, F4 = tv.F4;
 
   // own-query dipole upstream gradients
   DipLane<TD> dl;
@@ -273,8 +273,9 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32)
     const unsigned farm = __ballot_sync(FULL_MASK, far);
     if (farm && (__ldg(tv.node_flag + node) & 1)) {
       source(far, dx, dy, dz, dist2, __ldg(tv.node_geo + node).w,
-             node_payd + (int64_t)node * Cd + d0,
-             node_payr + (int64_t)node * PR + r0, node, false);
+             node_payd + (int64_t)node * F4 + d0,
+             reinterpret_cast<const float*>(node_payd + (int64_t)node * F4 + Cd) + r0, node,
+             false);
     }
     const unsigned openm = mask & ~farm;
     if (openm) {
@@ -287,8 +288,8 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32)
           const double r2 = dist2_rn(px, py, pz, x, dx, dy, dz);
           const bool me = me_open && !(r2 == 0.0 && skip_coincident);
           if (__any_sync(FULL_MASK, me))
-            source(me, dx, dy, dz, r2, __ldg(tv.pt_geo + j).w, pt_payd + (int64_t)j * Cd + d0,
-                   pt_payr + (int64_t)j * PR + r0, j, true);
+            source(me, dx, dy, dz, r2, __ldg(tv.pt_geo + j).w, pt_payd + (int64_t)j * F4 + d0,
+                   reinterpret_cast<const float*>(pt_payd + (int64_t)j * F4 + Cd) + r0, j, true);
         }
       } else {
         if (sp + tp.y > DPL_STACK_PER_WARP) {
@@ -398,8 +399,7 @@ static void adj_launch(const Tree& t, const KParams& kp, const AdjArgs& a, GradB
   AdjPtrs p{b.node_v, b.node_s, b.pt_mud, b.pt_mur, b.pt_n, b.d_eps};
   unsigned blocks = (unsigned)((a.q + ADJ_WARPS * 32 - 1) / (ADJ_WARPS * 32));
   k_adjoint<TD, NCOL, GM><<<blocks, ADJ_WARPS * 32, 0, t.stream>>>(
-      tv, kp, t.node_payd.as<float4>(), t.node_payr.as<float>(), t.pt_payd.as<float4>(),
-      t.pt_payr.as<float>(), a.xs, a.perm, a.q, a.d_out, a.dstride, a.d_grad, d0, nd, r0, nr,
+      tv, kp, t.node_row.as<float4>(), nullptr, t.pt_row.as<float4>(), nullptr, a.xs, a.perm, a.q, a.d_out, a.dstride, a.d_grad, d0, nd, r0, nr,
       t.chmap.as<int>(), p, a.overflow);
   count_launch();
 }
@@ -425,6 +425,8 @@ static void adj_plan(const Tree& t, const KParams& kp, const AdjArgs& a, GradBuf
 }
 
 void adjoint_launch(const Tree& t, const KParams& kp, const AdjArgs& a, GradBuf& b) {
+  static const bool single_phase = getenv("DPL_ADJOINT_SINGLE_PHASE") != nullptr;
+  if (!single_phase && adjoint2_launch(t, kp, a, b)) return;
   if (a.grad_mode == 0) return adj_plan<0>(t, kp, a, b);
   if (a.grad_mode == 1) return adj_plan<1>(t, kp, a, b);
   return adj_plan<2>(t, kp, a, b);

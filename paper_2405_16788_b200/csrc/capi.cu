@@ -274,26 +274,25 @@ int dpl_tree_export_moments(dpl_tree_t h, float* moments_v, float* moments_s) {
     check_tree(h);
     Tree& t = h->t;
     int64_t nn = t.nodes;
-    std::vector<float4> pd(std::max<int64_t>(1, nn * t.Cd));
-    std::vector<float> pr(nn * t.PR);
-    if (t.Cd)
-      DPL_CUDA(cudaMemcpyAsync(pd.data(), t.node_payd.p, nn * t.Cd * 16, cudaMemcpyDeviceToHost,
-                               t.stream));
-    DPL_CUDA(cudaMemcpyAsync(pr.data(), t.node_payr.p, nn * t.PR * 4, cudaMemcpyDeviceToHost,
+    std::vector<float4> rows(std::max<int64_t>(1, nn * t.F4));
+    DPL_CUDA(cudaMemcpyAsync(rows.data(), t.node_row.p, nn * t.F4 * 16, cudaMemcpyDeviceToHost,
                              t.stream));
     DPL_CUDA(cudaStreamSynchronize(t.stream));
-    for (int64_t i = 0; i < nn; ++i)
+    for (int64_t i = 0; i < nn; ++i) {
+      const float4* row = rows.data() + i * t.F4;
+      const float* rad = reinterpret_cast<const float*>(row + t.Cd);
       for (int c = 0; c < t.C; ++c) {
         int k = t.slot_of[c];
         float* v = moments_v ? moments_v + (i * t.C + c) * 3 : nullptr;
         if (t.kinds[c] == 0) {
-          if (v) v[0] = pd[i * t.Cd + k].x, v[1] = pd[i * t.Cd + k].y, v[2] = pd[i * t.Cd + k].z;
+          if (v) v[0] = row[k].x, v[1] = row[k].y, v[2] = row[k].z;
           if (moments_s) moments_s[i * t.C + c] = NAN;
         } else {
           if (v) v[0] = v[1] = v[2] = NAN;
-          if (moments_s) moments_s[i * t.C + c] = pr[i * t.PR + k];
+          if (moments_s) moments_s[i * t.C + c] = rad[k];
         }
       }
+    }
   });
 }
 

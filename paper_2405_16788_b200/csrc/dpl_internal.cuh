@@ -51,19 +51,29 @@ struct KParams {
   float delta2;
 };
 
+// Packed 64-byte node record for the two-phase kernels: fp64 centroid and
+// opening threshold, topology {child_begin, child_count, begin, end}, A.
+struct alignas(16) NodeRec {
+  double4 c;     // cx, cy, cz, thr
+  int4 topo;     // child_begin, child_count (0 = leaf), begin, end
+  float4 A;      // x: area / (4 pi); yzw unused
+};
+
 // Per-launch view of a tree for the traversal kernels.
 struct TreeView {
   const double4* node_dec;
   const int4* node_topo;
   const float4* node_geo;
   const uint8_t* node_flag;
-  const float* node_pay;
+  const NodeRec* node_rec;
+  const float4* node_row;   // nodes x F4: [dipole float4 x Cd | radial floats | pad]
   const double* pt_pos64;
   const float4* pt_geo;
-  const float* pt_pay;
+  const float4* pt_row;     // N x F4 (sorted order)
   const float* pt_nrm;  // N x 3 sorted
   const float* pt_mu;   // N x C sorted (reference channel order)
-  int P;                // payload row stride (floats)
+  int P;                // radial pad (floats, multiple of 4)
+  int F4;               // payload row stride (float4)
   int Cd, Cr, C;
   int64_t nodes, n;
   int max_depth;

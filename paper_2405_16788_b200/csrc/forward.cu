@@ -121,10 +121,11 @@ __global__ void __launch_bounds__(FWD_WARPS * 32)
 #pragma unroll
   for (int k = 0; k < ((GRAD == 1 && TR > 0) ? TR : 1); ++k) a.gr[k][0] = a.gr[k][1] = a.gr[k][2] = 0.f;
   long long c_vis = 0, c_fn = 0, c_ff = 0, c_pn = 0, c_pf = 0;
+  // payload rows: [dipole float4 x Cd | radial floats]; row stride F4 float4
   const float4* pdn = payd_n + d0;
-  const float* prn = payr_n + r0;
+  const float* prn = reinterpret_cast<const float*>(payd_n + tv.Cd) + r0;
   const float4* pdp = payd_p + d0;
-  const float* prp = payr_p + r0;
+  const float* prp = reinterpret_cast<const float*>(payd_p + tv.Cd) + r0;
   const bool skip_coincident = GRAD != 0 || kp.mode == KM_SINGULAR;  // :219 vs :316
 
   int sp = 1;
@@ -147,7 +148,8 @@ __global__ void __launch_bounds__(FWD_WARPS * 32)
     if (far && (__ldg(tv.node_flag + node) & 1)) {
       bool near;
       f_interact<TD, TR, GRAD>(a, dx, dy, dz, dist2, __ldg(tv.node_geo + node).w,
-                               pdn + (int64_t)node * tv.Cd, prn + (int64_t)node * tv.P, nd, nr,
+                               pdn + (int64_t)node * tv.F4, prn + (int64_t)node * 4 * tv.F4,
+                               nd, nr,
                                kp, near);
       if (COUNT) near ? ++c_fn : ++c_ff;
     }
@@ -163,7 +165,8 @@ __global__ void __launch_bounds__(FWD_WARPS * 32)
             if (r2 == 0.0 && skip_coincident) continue;
             bool near;
             f_interact<TD, TR, GRAD>(a, dx, dy, dz, r2, __ldg(tv.pt_geo + j).w,
-                                     pdp + (int64_t)j * tv.Cd, prp + (int64_t)j * tv.P, nd, nr,
+                                     pdp + (int64_t)j * tv.F4, prp + (int64_t)j * 4 * tv.F4,
+                                     nd, nr,
                                      kp, near);
             if (COUNT) near ? ++c_pn : ++c_pf;
           }
@@ -274,8 +277,7 @@ static void launch_one(const Tree& t, const KParams& kp, FwdArgs& a, int d0, int
   unsigned blocks = (unsigned)((a.q + FWD_WARPS * 32 - 1) / (FWD_WARPS * 32));
   auto run = [&](auto kern) {
     kern<<<blocks, FWD_WARPS * 32, 0, t.stream>>>(
-        tv, kp, t.node_payd.as<float4>(), t.node_payr.as<float>(), t.pt_payd.as<float4>(),
-        t.pt_payr.as<float>(), a.xs, a.perm, a.q, d0, nd, r0, nr, t.chmap.as<int>(), a.out,
+        tv, kp, t.node_row.as<float4>(), nullptr, t.pt_row.as<float4>(), nullptr, a.xs, a.perm, a.q, d0, nd, r0, nr, t.chmap.as<int>(), a.out,
         a.out_stride, a.single, a.grad, a.counters, a.overflow);
   };
   if (a.counters)
@@ -289,6 +291,8 @@ static void launch_one(const Tree& t, const KParams& kp, FwdArgs& a, int d0, int
 // Channel-tile plan: (TD, TR) instantiations tried in order; the first that
 // covers the tile in one pass wins, otherwise tiles of the largest are used.
 void forward_launch(const Tree& t, const KParams& kp, FwdArgs a) {
+  static const bool single_phase = getenv("DPL_FORWARD_SINGLE_PHASE") != nullptr;
+  if (!single_phase && forward2_launch(t, kp, a)) return;
   const int Cd = a.only_dip >= 0 ? 1 : (a.only_rad >= 0 ? 0 : t.Cd);
   const int Cr = a.only_rad >= 0 ? 1
                  : (a.only_dip >= 0 ? 0 : (a.nr_limit >= 0 ? std::min(a.nr_limit, t.Cr) : t.Cr));

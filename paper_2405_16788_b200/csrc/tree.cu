@@ -102,13 +102,15 @@ TreeView Tree::view() const {
   v.node_topo = node_topo.as<int4>();
   v.node_geo = node_geo.as<float4>();
   v.node_flag = node_flag.as<uint8_t>();
-  v.node_pay = nullptr;
+  v.node_rec = node_rec.as<NodeRec>();
+  v.node_row = node_row.as<float4>();
   v.pt_pos64 = pt_pos64.as<double>();
   v.pt_geo = pt_geo.as<float4>();
-  v.pt_pay = nullptr;
+  v.pt_row = pt_row.as<float4>();
   v.pt_nrm = pt_nrm.as<float>();
   v.pt_mu = pt_mud.as<float>();
   v.P = PR;
+  v.F4 = F4;
   v.Cd = Cd;
   v.Cr = Cr;
   v.C = C;
@@ -134,6 +136,7 @@ void Tree::set_layout() {
   Cd = (int)dip_ch.size();
   Cr = (int)rad_ch.size();
   PR = round_up4(std::max(Cr, 1));
+  F4 = Cd + PR / 4;
   std::vector<int> m(dip_ch);
   m.insert(m.end(), rad_ch.begin(), rad_ch.end());
   chmap.reserve(sizeof(int) * std::max(1, C));
@@ -342,33 +345,44 @@ __global__ void k_topo(const int32_t* __restrict__ beg, const int32_t* __restric
 }
 
 // opening thresholds thr = (beta^2 * r) * r (bhtree.cpp:193,204); IEEE keeps
-// inf * 0 = NaN so radius-0 nodes never pass at beta = inf.
+// inf * 0 = NaN so radius-0 nodes never pass at beta = inf. Also writes the
+// packed 64-byte node records the two-phase kernels read.
 __global__ void k_thresholds(const double* __restrict__ ctr, const double* __restrict__ rad,
-                             int64_t nodes, double beta2, double4* dec) {
+                             const int4* __restrict__ topo, const float4* __restrict__ geo,
+                             int64_t nodes, double beta2, double4* dec, NodeRec* rec) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= nodes) return;
   double r = rad[i];
-  dec[i] = make_double4(ctr[3 * i], ctr[3 * i + 1], ctr[3 * i + 2],
-                        __dmul_rn(__dmul_rn(beta2, r), r));
+  double thr = __dmul_rn(__dmul_rn(beta2, r), r);
+  dec[i] = make_double4(ctr[3 * i], ctr[3 * i + 1], ctr[3 * i + 2], thr);
+  NodeRec nr;
+  nr.c = make_double4(ctr[3 * i], ctr[3 * i + 1], ctr[3 * i + 2], thr);
+  nr.topo = topo[i];
+  float4 g = geo[i];
+  nr.A = make_float4(g.w, 0.f, 0.f, 0.f);
+  rec[i] = nr;
 }
 
-// K4a: per sorted point payload (mu_c * n for dipole slots, mu_c for radial)
-// and fp32 normal / dipole-mu copies for the adjoint's leaf terms.
+// K4a: per sorted point payload row [mu_c * n (dipole slots, float4 each) |
+// mu_c (radial slots) | pad] and fp32 normal / dipole-mu copies for the
+// adjoint's leaf terms.
 __global__ void k_point_payload(const int32_t* __restrict__ order, const double* __restrict__ nrm,
                                 const double* __restrict__ mu, int64_t n, int C, int Cd, int Cr,
-                                int PR, const int* __restrict__ chmap, float4* payd, float* payr,
-                                float* pnrm, float* pmud) {
+                                int F4, const int* __restrict__ chmap, float4* rows, float* pnrm,
+                                float* pmud) {
   int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (j >= n) return;
   int64_t m = order[j];
   double nx = nrm[3 * m], ny = nrm[3 * m + 1], nz = nrm[3 * m + 2];
   pnrm[3 * j] = (float)nx, pnrm[3 * j + 1] = (float)ny, pnrm[3 * j + 2] = (float)nz;
+  float4* row = rows + j * F4;
   for (int k = 0; k < Cd; ++k) {
     double u = mu[m * C + chmap[k]];
-    payd[j * Cd + k] = make_float4((float)(u * nx), (float)(u * ny), (float)(u * nz), 0.f);
+    row[k] = make_float4((float)(u * nx), (float)(u * ny), (float)(u * nz), 0.f);
     pmud[j * Cd + k] = (float)u;
   }
-  for (int k = 0; k < PR; ++k) payr[j * PR + k] = k < Cr ? (float)mu[m * C + chmap[Cd + k]] : 0.f;
+  float* r = reinterpret_cast<float*>(row + Cd);
+  for (int k = 0; k < 4 * (F4 - Cd); ++k) r[k] = k < Cr ? (float)mu[m * C + chmap[Cd + k]] : 0.f;
 }
 
 // K4b: fp64 unnormalised sums, one thread per (node, component) of a level.
@@ -411,21 +425,23 @@ __global__ void k_moments_level(int64_t off, int64_t cnt, int W, int C, int Cd,
   }
 }
 
-__global__ void k_moments_normalise(int64_t nodes, int Cd, int Cr, int PR,
+__global__ void k_moments_normalise(int64_t nodes, int Cd, int Cr, int F4,
                                     const double* __restrict__ narea,
                                     const double* __restrict__ sumv,
-                                    const double* __restrict__ sums, float4* payd, float* payr) {
+                                    const double* __restrict__ sums, float4* rows) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= nodes) return;
   double a = narea[i];
   bool ok = a > 0;  // nodes with area <= 0 keep zero moments (:142)
+  float4* row = rows + i * F4;
   for (int k = 0; k < Cd; ++k) {
     const double* s = sumv + (i * Cd + k) * 3;
-    payd[i * Cd + k] = ok ? make_float4((float)(s[0] / a), (float)(s[1] / a), (float)(s[2] / a), 0.f)
-                          : make_float4(0.f, 0.f, 0.f, 0.f);
+    row[k] = ok ? make_float4((float)(s[0] / a), (float)(s[1] / a), (float)(s[2] / a), 0.f)
+                : make_float4(0.f, 0.f, 0.f, 0.f);
   }
-  for (int k = 0; k < PR; ++k)
-    payr[i * PR + k] = (ok && k < Cr) ? (float)(sums[i * Cr + k] / a) : 0.f;
+  float* r = reinterpret_cast<float*>(row + Cd);
+  for (int k = 0; k < 4 * (F4 - Cd); ++k)
+    r[k] = (ok && k < Cr) ? (float)(sums[i * Cr + k] / a) : 0.f;
 }
 
 // ---------------------------------------------------------------- host
@@ -451,16 +467,13 @@ void tree_compute_moments(Tree& t) {
   int W = 3 * t.Cd + t.Cr;
   t.node_sumv.reserve(sizeof(double) * std::max<int64_t>(1, t.nodes * t.Cd * 3));
   t.node_sums.reserve(sizeof(double) * std::max<int64_t>(1, t.nodes * t.Cr));
-  t.node_payd.reserve(sizeof(float4) * std::max<int64_t>(1, (t.nodes + 1) * t.Cd));
-  t.node_payr.reserve(sizeof(float) * (t.nodes + 1) * t.PR);
-  t.pt_payd.reserve(sizeof(float4) * std::max<int64_t>(1, (t.n + 1) * t.Cd));
-  t.pt_payr.reserve(sizeof(float) * (t.n + 1) * t.PR);
+  t.node_row.reserve(sizeof(float4) * (t.nodes + 1) * t.F4);
+  t.pt_row.reserve(sizeof(float4) * (t.n + 1) * t.F4);
   t.pt_nrm.reserve(sizeof(float) * t.n * 3);
   t.pt_mud.reserve(sizeof(float) * std::max<int64_t>(1, t.n * t.Cd));
   k_point_payload<<<grid_for(t.n, B), B, 0, t.stream>>>(
       t.order.as<int32_t>(), t.nrm64.as<double>(), t.mu64.as<double>(), t.n, t.C, t.Cd, t.Cr,
-      t.PR, t.chmap.as<int>(), t.pt_payd.as<float4>(), t.pt_payr.as<float>(),
-      t.pt_nrm.as<float>(), t.pt_mud.as<float>());
+      t.F4, t.chmap.as<int>(), t.pt_row.as<float4>(), t.pt_nrm.as<float>(), t.pt_mud.as<float>());
   count_launch();
   int levels = (int)t.level_off.size() - 1;
   for (int d = levels - 1; d >= 0; --d) {
@@ -473,8 +486,8 @@ void tree_compute_moments(Tree& t) {
     count_launch();
   }
   k_moments_normalise<<<grid_for(t.nodes, B), B, 0, t.stream>>>(
-      t.nodes, t.Cd, t.Cr, t.PR, t.node_area64.as<double>(), t.node_sumv.as<double>(),
-      t.node_sums.as<double>(), t.node_payd.as<float4>(), t.node_payr.as<float>());
+      t.nodes, t.Cd, t.Cr, t.F4, t.node_area64.as<double>(), t.node_sumv.as<double>(),
+      t.node_sums.as<double>(), t.node_row.as<float4>());
   count_launch();
   DPL_CUDA(cudaGetLastError());
 }
@@ -488,8 +501,10 @@ void tree_set_kinds(Tree& t, const uint8_t* kinds) {
 void tree_ensure_thresholds(Tree& t, double beta) {
   if (t.thr_valid && (t.thr_beta == beta)) return;
   double beta2 = beta * beta;
+  t.node_rec.reserve(sizeof(NodeRec) * std::max<int64_t>(1, t.nodes));
   k_thresholds<<<grid_for(t.nodes, 256), 256, 0, t.stream>>>(
-      t.node_ctr64.as<double>(), t.node_rad64.as<double>(), t.nodes, beta2, t.node_dec.as<double4>());
+      t.node_ctr64.as<double>(), t.node_rad64.as<double>(), t.node_topo.as<int4>(),
+      t.node_geo.as<float4>(), t.nodes, beta2, t.node_dec.as<double4>(), t.node_rec.as<NodeRec>());
   count_launch();
   DPL_CUDA(cudaGetLastError());
   t.thr_beta = beta;

@@ -35,7 +35,7 @@ struct Tree {
   int C = 0, max_leaf = 8, max_depth = 20;
   std::vector<int64_t> level_off;  // BFS level offsets, size levels + 1
   std::vector<uint8_t> kinds;      // per channel, 0 Dipole, 1 Radial
-  int Cd = 0, Cr = 0, PR = 0;      // dipole / radial channel counts, radial row stride
+  int Cd = 0, Cr = 0, PR = 0, F4 = 1;  // dipole / radial channel counts, radial pad, row float4s
   std::vector<int> dip_ch, rad_ch, slot_of;
   double root_lo[3] = {0, 0, 0}, root_hi[3] = {0, 0, 0};
   double thr_beta = -1.0;  // beta the thresholds were computed for (NaN-safe compare)
@@ -48,9 +48,9 @@ struct Tree {
   DevBuf node_ctr64, node_area64, node_rad64;  // double3 / double / double
   DevBuf node_dec, node_topo, node_parent, node_geo, node_flag;
   DevBuf node_sumv, node_sums;  // fp64 unnormalised moment sums (nodes x Cd x 3, nodes x Cr)
-  DevBuf node_payd, node_payr;  // fp32 payload
+  DevBuf node_row, node_rec;  // fp32 payload rows (nodes x F4 float4), packed node records
   // sorted point data
-  DevBuf pt_pos64, pt_geo, pt_payd, pt_payr, pt_nrm, pt_mud;
+  DevBuf pt_pos64, pt_geo, pt_row, pt_nrm, pt_mud;
   DevBuf chmap;  // int32 [Cd dip ids | Cr rad ids]
   // scratch
   DevBuf scratch[8];

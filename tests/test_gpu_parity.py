@@ -277,6 +277,35 @@ def test_render_step_parity(eng, oracle_mod):
     assert np.abs(dbg - want["d_bg"]).max() <= 1e-4 * np.abs(want["d_bg"]).max() + 1e-8
 
 
+@pytest.mark.parametrize("C", [2, 17, 33, 49, 65, 70])
+def test_many_channel_forward_adjoint(eng, oracle_mod, C):
+    """Config-2 channel layouts (1 Dipole + C-1 Radial, N(0,1) moments and
+    upstream gradients): covers the two-phase kernels' column splits (<=32,
+    <=48, <=64 radial) and the multi-tile fallback beyond."""
+    O = oracle_mod
+    rng = np.random.default_rng(C)
+    pos, nrm, area, _ = random_cloud(3000, 30 + C, 1)
+    mu = rng.standard_normal((3000, C))
+    kinds = np.ones(C, np.uint8)
+    kinds[0] = 0
+    t, r = make(eng, O, pos, nrm, area, mu, kinds)
+    q = 1500
+    xs = rng.uniform(-1.5, 1.5, (q, 3)).astype(np.float32).astype(np.float64)
+    p = eng.KernelParams(epsilon=0.06)
+    got = t.primal(xs, p, 2.0)
+    want = r.primal(O.Params(0.06), 2.0, xs)
+    nbad, mx = close(got, want)
+    assert nbad == 0, (nbad, mx)
+    d_out = rng.standard_normal((q, C)).astype(np.float32)
+    buf = t.make_buffer()
+    t.adjoint(xs, p, 2.0, d_out, None, buf)
+    g = t.flush_gradients(buf)
+    wm, wn, we = r.adjoint(O.Params(0.06), 2.0, xs, d_out.astype(np.float64))
+    assert rel_scale_err(g.moments, wm) < 1e-5
+    assert rel_scale_err(g.normals, wn) < 1e-5
+    assert abs(g.d_epsilon - we) <= 1e-4 * abs(we) + 1e-6
+
+
 # ---------------------------------------------------------------- errors
 def test_error_behaviour(eng, oracle_mod):
     t = eng.DipoleTree(0)
