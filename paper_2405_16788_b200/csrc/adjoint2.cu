@@ -38,6 +38,25 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 }
 }  // namespace
 
+// Coefficients for the adjoint: beyond 6.5 eps (and for the singular kernel)
+// tau = 1, tau' = tau'' = 0 (kernels.cpp:50-55), so only W, R (and Wp_r when
+// query-gradient adjoints are present) are non-zero.
+template <int GM>
+__device__ __forceinline__ Co adj_coeffs(float r2, const KParams& kp) {
+  if (kp.mode == KM_SINGULAR || (kp.mode == KM_REGULARIZED && r2 >= kp.near2)) {
+    Co c;
+    const float inv_r = rsqrtf(r2);
+    c.R = inv_r * inv_r;
+    c.W = c.R * inv_r;
+    c.Wp_r = GM ? -3.0f * c.W * c.R : 0.f;
+    c.Rp_r = 0.f;
+    c.dW_de = c.dWp_r_de = c.dR_de = 0.f;
+    c.near = false;
+    return c;
+  }
+  return coeffs<2>(r2, kp);
+}
+
 struct Adj2Ptrs {
   double* node_v;  // nodes x Cd(=1) x 3
   double* node_s;  // nodes x Cr
@@ -49,8 +68,9 @@ struct Adj2Ptrs {
 
 // NB: 0 -> Cr <= 32; 1 -> 32 < Cr <= 48 (split); 2 -> Cr <= 64.
 // GM: 0 no d_grad; 1 d_grad q x dstride x 3; 2 d_grad q x 3 (channel 0).
-template <int NB, int GM, int WARPS, int ENT, int RR>
-__global__ void __launch_bounds__(WARPS * 32)
+// MAXR: register cap (occupancy vs. spills; chosen by measurement)
+template <int NB, int GM, int WARPS, int ENT, int RR, int MAXR = 128>
+__global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
     k_adjoint2(TreeView tv, KParams kp, const double* __restrict__ xs,
                const int32_t* __restrict__ perm, int64_t q, const float* __restrict__ d_out,
                int dstride, const float* __restrict__ d_grad, int nr,
@@ -83,6 +103,7 @@ __global__ void __launch_bounds__(WARPS * 32)
   const unsigned active = __ballot_sync(FULL_MASK, valid);
   if (!active) return;
   const int Cr = tv.Cr;
+  const QueryDF qx = make_qdf(x);
 
   // own-query dipole upstream gradients (channel slot 0)
   const int ch0 = __ldg(chmap);
@@ -213,21 +234,20 @@ __global__ void __launch_bounds__(WARPS * 32)
     const unsigned mask = (unsigned)en.y;
     const bool mine = (mask >> lane) & 1u;
     const NodeRec* rec = tv.node_rec + node;
-    const double2 c01 = __ldg(reinterpret_cast<const double2*>(&rec->c));
-    const double2 c23 = __ldg(reinterpret_cast<const double2*>(&rec->c) + 1);
+    const float4 hi = __ldg(&rec->hi);
+    const float4 lo = __ldg(&rec->lo);
     const int4 tp = __ldg(&rec->topo);
-    const float A = __ldg(&rec->A.x);
-    double dx, dy, dz;
-    const double dist2 = dist2_rn(c01.x, c01.y, c23.x, x, dx, dy, dz);
-    const bool far = mine && (dist2 > c23.y);
+    const float A = lo.w;
+    float fx, fy, fz;
+    const float s = dist2_df(hi, lo, qx, fx, fy, fz);
+    const bool far = mine && far_test(s, hi, qx, x, tv.node_dec + node);
     const unsigned farm = __ballot_sync(FULL_MASK, far);
     if (farm && A > 0.f) {
       begin_entry();
       float r_ = 0.f, e_ = 0.f, u0 = 0.f, u1 = 0.f, u2 = 0.f;
       bool nr_ = false;
       if (far) {
-        const float fx = (float)dx, fy = (float)dy, fz = (float)dz;
-        const Co c = coeffs<2>((float)dist2, kp);
+        const Co c = adj_coeffs<GM>(s, kp);
         nr_ = c.near;
         r_ = A * c.R;
         e_ = A * c.dR_de;
@@ -269,12 +289,14 @@ __global__ void __launch_bounds__(WARPS * 32)
           float r_ = 0.f, e_ = 0.f, n0 = 0.f, n1 = 0.f, n2 = 0.f, dmu = 0.f;
           bool nr_ = false;
           if (me_open) {
-            const double* pp = tv.pt_pos64 + 3 * (size_t)j;
-            const double r2 = dist2_rn(__ldg(pp), __ldg(pp + 1), __ldg(pp + 2), x, dx, dy, dz);
-            if (r2 != 0.0) {  // :387
-              const float fx = (float)dx, fy = (float)dy, fz = (float)dz;
-              const Co c = coeffs<2>((float)r2, kp);
-              const float Am = __ldg(&tv.pt_geo[j].w);
+            const PtRec* pr = tv.pt_rec + j;
+            const float4 ph = __ldg(&pr->hi);
+            float fx, fy, fz;
+            const float r2 = dist2_df(ph, __ldg(&pr->lo), qx, fx, fy, fz);
+            // :387 skips exact coincidence (fp64); fp32 r2 == 0 triggers the exact check
+            if (!(r2 == 0.f && coincident_exact(tv.pt_pos64 + 3 * (size_t)j, x))) {
+              const Co c = adj_coeffs<GM>(r2, kp);
+              const float Am = ph.w;
               nr_ = c.near;
               r_ = Am * c.R;
               e_ = Am * c.dR_de;
@@ -327,21 +349,20 @@ __global__ void __launch_bounds__(WARPS * 32)
   if (lane == 0 && eps_acc != 0.0) atomicAdd(acc.d_eps, eps_acc);
 }
 
-template <int NB, int GM, int RR>
+template <int NB, int GM, int RR, int WARPS = 4, int ENT = 8, int MINB = 128>
 static void launch_adj2(const Tree& t, const KParams& kp, const AdjArgs& a, GradBuf& b, int nr) {
-  constexpr int WARPS = 4, ENT = 8;
   constexpr int F4 = 1 + RR;
   constexpr int WARP_FLOATS = ENT * 32 * 6 + ENT * F4 * 4 + ENT + 2 * DPL_STACK_PER_WARP;
   const size_t smem = (size_t)WARPS * ((WARP_FLOATS + 3) & ~3) * 4;
   static bool attr = false;
   if (!attr) {
-    DPL_CUDA(cudaFuncSetAttribute(k_adjoint2<NB, GM, WARPS, ENT, RR>,
+    DPL_CUDA(cudaFuncSetAttribute(k_adjoint2<NB, GM, WARPS, ENT, RR, MINB>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
   Adj2Ptrs p{b.node_v, b.node_s, b.pt_mud, b.pt_mur, b.pt_n, b.d_eps};
   unsigned blocks = (unsigned)((a.q + WARPS * 32 - 1) / (WARPS * 32));
-  k_adjoint2<NB, GM, WARPS, ENT, RR><<<blocks, WARPS * 32, smem, t.stream>>>(
+  k_adjoint2<NB, GM, WARPS, ENT, RR, MINB><<<blocks, WARPS * 32, smem, t.stream>>>(
       t.view(), kp, a.xs, a.perm, a.q, a.d_out, a.dstride, a.d_grad, nr, t.chmap.as<int>(), p,
       a.overflow);
   count_launch();
@@ -352,6 +373,17 @@ static bool adj2_plan(const Tree& t, const KParams& kp, const AdjArgs& a, GradBu
   const int nr = a.nr_limit >= 0 ? std::min(a.nr_limit, t.Cr) : t.Cr;
   if (t.F4 - 1 > 16) return false;
   if (nr <= 32) return launch_adj2<0, GM, 16>(t, kp, a, b, nr), true;
+  if (nr <= 48 && GM == 0) {
+    const char* v = getenv("DPL_TUNE_ADJ");
+    switch (v ? atoi(v) : 0) {  // occupancy / batch experiments
+      case 1: return launch_adj2<1, GM, 16, 4, 8, 112>(t, kp, a, b, nr), true;
+      case 2: return launch_adj2<1, GM, 16, 4, 8, 104>(t, kp, a, b, nr), true;
+      case 3: return launch_adj2<1, GM, 16, 4, 4, 112>(t, kp, a, b, nr), true;
+      case 4: return launch_adj2<1, GM, 16, 4, 4, 96>(t, kp, a, b, nr), true;
+      case 5: return launch_adj2<1, GM, 16, 4, 6, 112>(t, kp, a, b, nr), true;
+      default: break;
+    }
+  }
   if (nr <= 48) return launch_adj2<1, GM, 16>(t, kp, a, b, nr), true;
   if (nr <= 64) return launch_adj2<2, GM, 16>(t, kp, a, b, nr), true;
   return false;

@@ -49,14 +49,24 @@ struct KParams {
   int mode;
   float eps, inv_eps, inv_eps3, inv_eps4, inv_eps5, inv_eps6;
   float delta2;
+  float near2;  // (6.5 eps)^2: beyond it tau = 1 (kernels.cpp:50-55)
 };
 
-// Packed 64-byte node record for the two-phase kernels: fp64 centroid and
-// opening threshold, topology {child_begin, child_count, begin, end}, A.
+// Packed 48-byte node record for the two-phase kernels. The fp64 centroid c
+// is stored as a double-float pair (hi = fl32(c), lo = fl32(c - hi)), so
+// d = (c_hi - x_hi) + (c_lo - x_lo) carries ~2^-23 relative error and the
+// opening test can run in fp32 with a rigorous ambiguity band; only inside
+// the band is the reference's exact fp64 test re-evaluated (node_dec).
 struct alignas(16) NodeRec {
-  double4 c;     // cx, cy, cz, thr
+  float4 hi;     // c_hi.xyz, thr32 = fl32((beta^2 r) r)
+  float4 lo;     // c_lo.xyz, A = area / (4 pi)
   int4 topo;     // child_begin, child_count (0 = leaf), begin, end
-  float4 A;      // x: area / (4 pi); yzw unused
+};
+
+// Double-float point record (tree order): p_hi.xyz + A, p_lo.xyz.
+struct alignas(16) PtRec {
+  float4 hi;
+  float4 lo;
 };
 
 // Per-launch view of a tree for the traversal kernels.
@@ -66,6 +76,7 @@ struct TreeView {
   const float4* node_geo;
   const uint8_t* node_flag;
   const NodeRec* node_rec;
+  const PtRec* pt_rec;
   const float4* node_row;   // nodes x F4: [dipole float4 x Cd | radial floats | pad]
   const double* pt_pos64;
   const float4* pt_geo;

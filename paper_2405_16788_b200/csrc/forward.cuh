@@ -23,6 +23,8 @@ struct FwdArgs {
 void forward_launch(const Tree& t, const KParams& kp, FwdArgs a);
 // two-phase values-only kernel (forward2.cu); false if the layout is not covered
 bool forward2_launch(const Tree& t, const KParams& kp, const FwdArgs& a);
+// tensor-core (3xTF32 mma.sync) values-only kernel (forward_tc.cu)
+bool forward_tc_launch(const Tree& t, const KParams& kp, const FwdArgs& a);
 void morton_order(Tree& t, const double* xs_dev, int64_t q, int32_t* perm_out, DevBuf& ws);
 
 }  // namespace dpl

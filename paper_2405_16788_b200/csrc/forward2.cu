@@ -31,14 +31,11 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 }
 
 // lane weights of one source: (A W dx, A W dy, A W dz, A R)
-__device__ __forceinline__ float4 fwd_weights(double dx, double dy, double dz, double dist2,
-                                              float A, const KParams& kp) {
-  const float fx = (float)dx, fy = (float)dy, fz = (float)dz;
-  const float r2 = (float)dist2;
+__device__ __forceinline__ float4 fwd_weights(float fx, float fy, float fz, float r2, float A,
+                                              const KParams& kp) {
   const float inv_r = rsqrtf(r2);
-  const float t = r2 * inv_r * kp.inv_eps;
   float W, R;
-  if (kp.mode == KM_SINGULAR || (kp.mode == KM_REGULARIZED && t >= 6.5f)) {
+  if (kp.mode == KM_SINGULAR || (kp.mode == KM_REGULARIZED && r2 >= kp.near2)) {
     R = inv_r * inv_r;  // tau = 1 beyond t = 6.5 (kernels.cpp:50-55)
     W = R * inv_r;
   } else {
@@ -50,8 +47,9 @@ __device__ __forceinline__ float4 fwd_weights(double dx, double dy, double dz, d
   return make_float4(aW * fx, aW * fy, aW * fz, A * R);
 }
 
-template <int TD, int TR, int WARPS, int ENT>
-__global__ void __launch_bounds__(WARPS * 32)
+// MAXR: register cap (occupancy vs. spills; chosen by measurement)
+template <int TD, int TR, int WARPS, int ENT, int MAXR = 128>
+__global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
     k_forward2(TreeView tv, KParams kp, const double* __restrict__ xs,
                const int32_t* __restrict__ perm, int64_t q, int nd, int nr,
                const int* __restrict__ chmap, float* __restrict__ out, int out_stride,
@@ -78,6 +76,7 @@ __global__ void __launch_bounds__(WARPS * 32)
   }
   const unsigned active = __ballot_sync(FULL_MASK, valid);
   if (!active) return;
+  const QueryDF qx = make_qdf(x);
 
   float accd[TD > 0 ? TD : 1], accr[TR > 0 ? TR : 1];
 #pragma unroll
@@ -133,17 +132,16 @@ __global__ void __launch_bounds__(WARPS * 32)
     const unsigned mask = (unsigned)e.y;
     const bool mine = (mask >> lane) & 1u;
     const NodeRec* rec = tv.node_rec + node;
-    const double2 c01 = __ldg(reinterpret_cast<const double2*>(&rec->c));
-    const double2 c23 = __ldg(reinterpret_cast<const double2*>(&rec->c) + 1);
+    const float4 hi = __ldg(&rec->hi);
+    const float4 lo = __ldg(&rec->lo);
     const int4 tp = __ldg(&rec->topo);
-    const float A = __ldg(&rec->A.x);
-    double dx, dy, dz;
-    const double dist2 = dist2_rn(c01.x, c01.y, c23.x, x, dx, dy, dz);
-    const bool far = mine && (dist2 > c23.y);
+    const float A = lo.w;
+    float dx, dy, dz;
+    const float s = dist2_df(hi, lo, qx, dx, dy, dz);
+    const bool far = mine && far_test(s, hi, qx, x, tv.node_dec + node);
     const unsigned farm = __ballot_sync(FULL_MASK, far);
     if (farm && A > 0.f) {  // area > 0 (bhtree.cpp:205)
-      const float4 wv = far ? fwd_weights(dx, dy, dz, dist2, A, kp)
-                            : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 wv = far ? fwd_weights(dx, dy, dz, s, A, kp) : make_float4(0.f, 0.f, 0.f, 0.f);
       append(wv, node_row + (size_t)node * F4);
     }
     const unsigned openm = mask & ~farm;
@@ -153,10 +151,13 @@ __global__ void __launch_bounds__(WARPS * 32)
         for (int j = tp.z; j < tp.w; ++j) {
           float4 wv = make_float4(0.f, 0.f, 0.f, 0.f);
           if (me_open) {
-            const double* pp = tv.pt_pos64 + 3 * (size_t)j;
-            const double r2 = dist2_rn(__ldg(pp), __ldg(pp + 1), __ldg(pp + 2), x, dx, dy, dz);
-            if (!(r2 == 0.0 && singular))  // bhtree.cpp:219
-              wv = fwd_weights(dx, dy, dz, r2, __ldg(&tv.pt_geo[j].w), kp);
+            const PtRec* pr = tv.pt_rec + j;
+            const float4 ph = __ldg(&pr->hi);
+            const float r2 = dist2_df(ph, __ldg(&pr->lo), qx, dx, dy, dz);
+            // exact coincidence only matters for the singular kernel (bhtree.cpp:219);
+            // the regularized kernel's r = 0 contribution is identically zero
+            if (!(singular && r2 == 0.f && coincident_exact(tv.pt_pos64 + 3 * (size_t)j, x)))
+              wv = fwd_weights(dx, dy, dz, r2, ph.w, kp);
           }
           append(wv, pt_row + (size_t)j * F4);
         }
@@ -182,21 +183,26 @@ __global__ void __launch_bounds__(WARPS * 32)
     if (k < nr) o[__ldg(chmap + TD + k)] = accr[k];
 }
 
-template <int TD, int TR, int WARPS, int ENT>
+template <int TD, int TR, int WARPS, int ENT, int MINB = 128>
 static void launch2(const Tree& t, const KParams& kp, const FwdArgs& a, int nd, int nr) {
   constexpr int F4 = TD + TR / 4;
   const size_t smem = (size_t)WARPS * (ENT * 32 + ENT * F4 + DPL_STACK_PER_WARP / 2) * 16;
   static bool attr = false;
   if (!attr) {
-    DPL_CUDA(cudaFuncSetAttribute(k_forward2<TD, TR, WARPS, ENT>,
+    DPL_CUDA(cudaFuncSetAttribute(k_forward2<TD, TR, WARPS, ENT, MINB>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
   unsigned blocks = (unsigned)((a.q + WARPS * 32 - 1) / (WARPS * 32));
-  k_forward2<TD, TR, WARPS, ENT><<<blocks, WARPS * 32, smem, t.stream>>>(
+  k_forward2<TD, TR, WARPS, ENT, MINB><<<blocks, WARPS * 32, smem, t.stream>>>(
       t.view(), kp, a.xs, a.perm, a.q, nd, nr, t.chmap.as<int>(), a.out, a.out_stride,
       a.overflow);
   count_launch();
+}
+
+static int tune_choice(const char* env) {
+  const char* v = getenv(env);
+  return v ? atoi(v) : 0;
 }
 
 // Values-only plan for the two-phase kernel: the compile-time row shape must
@@ -210,7 +216,16 @@ bool forward2_launch(const Tree& t, const KParams& kp, const FwdArgs& a) {
   switch (t.PR) {
     case 4: return launch2<1, 4, W, E>(t, kp, a, 1, nr), true;
     case 16: return launch2<1, 16, W, E>(t, kp, a, 1, nr), true;
-    case 48: return launch2<1, 48, W, E>(t, kp, a, 1, nr), true;
+    case 48:
+      switch (tune_choice("DPL_TUNE_FWD")) {  // (batch, register cap) experiments
+        case 1: return launch2<1, 48, W, 8, 128>(t, kp, a, 1, nr), true;
+        case 2: return launch2<1, 48, W, 8, 112>(t, kp, a, 1, nr), true;
+        case 3: return launch2<1, 48, W, 8, 104>(t, kp, a, 1, nr), true;
+        case 4: return launch2<1, 48, W, 8, 96>(t, kp, a, 1, nr), true;
+        case 5: return launch2<1, 48, W, 12, 112>(t, kp, a, 1, nr), true;
+        case 6: return launch2<1, 48, W, 16, 128>(t, kp, a, 1, nr), true;
+        default: return launch2<1, 48, W, 8, 128>(t, kp, a, 1, nr), true;  // measured best
+      }
     default: return false;
   }
 }

@@ -1,0 +1,284 @@
+// forward_tc.cu — two-phase forward with the radial-channel contraction on
+// tensor cores (mma.sync m16n8k8 TF32, 3xTF32 split for fp32 accuracy).
+//
+// Phase A is forward2.cu's (exact opening decisions, per-lane weights into
+// shared memory, cp.async-staged payload rows). Phase B is a dense product
+// per batch of ENT entries:
+//     out[32 queries x TR radial] += Wr[32 x ENT] . Rows[ENT x TR]
+// with Wr[l][e] = A R of lane l for entry e (0 when lane l does not take e).
+// Each operand is split a = hi + lo (hi = tf32(a), lo = tf32(a - hi)) and
+// hi.hi + hi.lo + lo.hi is accumulated in fp32 (error ~2^-21 relative per
+// product, i.e. fp32-class; the dropped lo.lo term is < 2^-22). The dipole
+// slot (3 FMA per entry) stays on the FP32 pipe.
+// Shared-memory strides are padded so every fragment load is bank-conflict
+// free: weights Wr[ENT][40], rows [ENT][RSF] with RSF = 8 or 24 mod 32 floats.
+#include "forward.cuh"
+#include "traverse.cuh"
+
+namespace dpl {
+
+namespace {
+__device__ __forceinline__ void cp_async16(uint32_t smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(smem), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+}
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ uint32_t to_tf32(float a) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(r) : "f"(a));
+  return r;
+}
+__device__ __forceinline__ void split_tf32(float a, uint32_t& hi, uint32_t& lo) {
+  hi = to_tf32(a);
+  lo = to_tf32(a - __uint_as_float(hi));
+}
+__device__ __forceinline__ void mma_tf32(float (&c)[4], const uint32_t (&a)[4], uint32_t b0,
+                                         uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};\n"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ float4 fwd_w(float fx, float fy, float fz, float r2, float A,
+                                        const KParams& kp) {
+  const float inv_r = rsqrtf(r2);
+  float W, R;
+  if (kp.mode == KM_SINGULAR || (kp.mode == KM_REGULARIZED && r2 >= kp.near2)) {
+    R = inv_r * inv_r;
+    W = R * inv_r;
+  } else {
+    Co c = coeffs<0>(r2, kp);
+    W = c.W;
+    R = c.R;
+  }
+  const float aW = A * W;
+  return make_float4(aW * fx, aW * fy, aW * fz, A * R);
+}
+
+constexpr int row_stride_floats(int f4) {
+  int r = 4 * f4;
+  while (r % 32 != 8 && r % 32 != 24) r += 4;
+  return r;
+}
+}  // namespace
+
+// NT: radial n-tiles of 8 channels (TR = 8 NT); one dipole slot.
+template <int NT, int WARPS, int ENT, int MAXR>
+__global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
+    k_forward_tc(TreeView tv, KParams kp, const double* __restrict__ xs,
+                 const int32_t* __restrict__ perm, int64_t q, int nr,
+                 const int* __restrict__ chmap, float* __restrict__ out, int out_stride,
+                 int* overflow) {
+  static_assert(ENT % 8 == 0, "ENT must be a multiple of the mma K (8)");
+  constexpr int TR = 8 * NT;
+  constexpr int F4 = 1 + TR / 4;               // global row float4 (dipole + radial)
+  constexpr int RSF = row_stride_floats(F4);   // padded smem row stride (floats)
+  constexpr int WSTR = 40;                     // padded Wr row stride (floats)
+  constexpr int WARP_FLOATS = ENT * 32 * 4 + ENT * WSTR + ENT * RSF + 2 * DPL_STACK_PER_WARP;
+  extern __shared__ float4 smem_f4[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int g = lane >> 2, tq = lane & 3;  // mma fragment coordinates
+  float* base = reinterpret_cast<float*>(smem_f4) + (size_t)w * WARP_FLOATS;
+  float4* wd = reinterpret_cast<float4*>(base);  // [ENT][32] (A W d, -)
+  float* wr = base + ENT * 128;                  // [ENT][WSTR]  A R
+  float* rows = wr + ENT * WSTR;                 // [ENT][RSF]
+  int2* stk = reinterpret_cast<int2*>(rows + ENT * RSF);
+  const uint32_t s_rows = smem_u32(rows) + 16u * lane;
+
+  const int64_t sidx = ((int64_t)blockIdx.x * WARPS + w) * 32 + lane;
+  const bool valid = sidx < q;
+  const int64_t qi = valid ? (perm ? (int64_t)perm[sidx] : sidx) : 0;
+  QueryPos x;
+  if (valid) {
+    x.x = xs[3 * qi], x.y = xs[3 * qi + 1], x.z = xs[3 * qi + 2];
+  } else {
+    x.x = x.y = x.z = 0.0;
+  }
+  const unsigned active = __ballot_sync(FULL_MASK, valid);
+  if (!active) return;
+  const QueryDF qx = make_qdf(x);
+
+  float accd = 0.f;
+  float acc[2][NT][4];
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = acc[mt][nt][2] = acc[mt][nt][3] = 0.f;
+
+  const bool singular = kp.mode == KM_SINGULAR;
+  const float4* __restrict__ node_row = tv.node_row;
+  const float4* __restrict__ pt_row = tv.pt_row;
+  int nent = 0;
+
+  auto evaluate = [&]() {
+    // zero-fill the batch tail so the K=8 steps read zeros
+    for (int e = nent; e < ((nent + 7) & ~7); ++e) {
+      wr[e * WSTR + lane] = 0.f;
+      wd[e * 32 + lane] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    cp_async_wait_all();
+    __syncwarp();
+    // dipole slot on the FP32 pipe
+    for (int e = 0; e < nent; ++e) {
+      const float4 wv = wd[e * 32 + lane];
+      const float4 v = *reinterpret_cast<const float4*>(rows + e * RSF);
+      accd = fmaf(wv.x, v.x, fmaf(wv.y, v.y, fmaf(wv.z, v.z, accd)));
+    }
+    // radial channels on the tensor cores
+    const int ksteps = (nent + 7) >> 3;
+    for (int ks = 0; ks < ksteps; ++ks) {
+      const int e0 = 8 * ks;
+      uint32_t ah[2][4], al[2][4];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        const float* wcol = wr + 16 * mt + g;
+        split_tf32(wcol[(e0 + tq) * WSTR], ah[mt][0], al[mt][0]);
+        split_tf32(wcol[(e0 + tq) * WSTR + 8], ah[mt][1], al[mt][1]);
+        split_tf32(wcol[(e0 + tq + 4) * WSTR], ah[mt][2], al[mt][2]);
+        split_tf32(wcol[(e0 + tq + 4) * WSTR + 8], ah[mt][3], al[mt][3]);
+      }
+      // rows of this k-step: entry e0 + tq (b0) and e0 + tq + 4 (b1), radial col 8 nt + g
+      const float* r0 = rows + (e0 + tq) * RSF + 4 + g;
+      const float* r1 = rows + (e0 + tq + 4) * RSF + 4 + g;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        uint32_t bh0, bl0, bh1, bl1;
+        const float v0 = (e0 + tq < nent) ? r0[8 * nt] : 0.f;
+        const float v1 = (e0 + tq + 4 < nent) ? r1[8 * nt] : 0.f;
+        split_tf32(v0, bh0, bl0);
+        split_tf32(v1, bh1, bl1);
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+          mma_tf32(acc[mt][nt], ah[mt], bh0, bh1);
+          mma_tf32(acc[mt][nt], ah[mt], bl0, bl1);
+          mma_tf32(acc[mt][nt], al[mt], bh0, bh1);
+        }
+      }
+    }
+    __syncwarp();
+    nent = 0;
+  };
+
+  auto append = [&](float4 wv, const float4* rowsrc) {
+    if (nent == ENT) evaluate();
+    wd[nent * 32 + lane] = make_float4(wv.x, wv.y, wv.z, 0.f);
+    wr[nent * WSTR + lane] = wv.w;
+    if (lane < F4) cp_async16(s_rows + 4u * RSF * nent, rowsrc + lane);
+    ++nent;
+  };
+
+  int sp = 1;
+  if (lane == 0) stk[0] = make_int2(0, (int)active);
+  __syncwarp();
+  while (sp > 0) {
+    --sp;
+    const int2 e = stk[sp];
+    __syncwarp();
+    const int node = e.x;
+    const unsigned mask = (unsigned)e.y;
+    const bool mine = (mask >> lane) & 1u;
+    const NodeRec* rec = tv.node_rec + node;
+    const float4 hi = __ldg(&rec->hi);
+    const float4 lo = __ldg(&rec->lo);
+    const int4 tp = __ldg(&rec->topo);
+    const float A = lo.w;
+    float dx, dy, dz;
+    const float s = dist2_df(hi, lo, qx, dx, dy, dz);
+    const bool far = mine && far_test(s, hi, qx, x, tv.node_dec + node);
+    const unsigned farm = __ballot_sync(FULL_MASK, far);
+    if (farm && A > 0.f) {  // area > 0 (bhtree.cpp:205)
+      const float4 wv = far ? fwd_w(dx, dy, dz, s, A, kp) : make_float4(0.f, 0.f, 0.f, 0.f);
+      append(wv, node_row + (size_t)node * F4);
+    }
+    const unsigned openm = mask & ~farm;
+    if (openm) {
+      if (tp.y == 0) {
+        const bool me_open = (openm >> lane) & 1u;
+        for (int j = tp.z; j < tp.w; ++j) {
+          float4 wv = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (me_open) {
+            const PtRec* pr = tv.pt_rec + j;
+            const float4 ph = __ldg(&pr->hi);
+            const float r2 = dist2_df(ph, __ldg(&pr->lo), qx, dx, dy, dz);
+            if (!(singular && r2 == 0.f && coincident_exact(tv.pt_pos64 + 3 * (size_t)j, x)))
+              wv = fwd_w(dx, dy, dz, r2, ph.w, kp);
+          }
+          append(wv, pt_row + (size_t)j * F4);
+        }
+      } else {
+        if (sp + tp.y > DPL_STACK_PER_WARP) {
+          if (lane == 0) atomicExch(overflow, 1);
+          break;
+        }
+        if (lane < tp.y) stk[sp + lane] = make_int2(tp.x + lane, (int)openm);
+        sp += tp.y;
+        __syncwarp();
+      }
+    }
+  }
+  if (nent) evaluate();
+  // outputs: the dipole value is lane-local; radial values live in mma C fragments
+  if (valid) out[qi * out_stride + __ldg(chmap)] = accd;
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int row = 16 * mt + 8 * h + g;  // lane whose query this row is
+      const int64_t qr = __shfl_sync(FULL_MASK, qi, row);
+      const bool vr = (active >> row) & 1u;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int col = 8 * nt + 2 * tq + u;
+          if (vr && col < nr) out[qr * out_stride + __ldg(chmap + 1 + col)] = acc[mt][nt][2 * h + u];
+        }
+    }
+}
+
+template <int NT, int WARPS, int ENT, int MAXR>
+static void launch_tc(const Tree& t, const KParams& kp, const FwdArgs& a, int nr) {
+  constexpr int F4 = 1 + 2 * NT;
+  constexpr int RSF = row_stride_floats(F4);
+  constexpr int WARP_FLOATS = ENT * 32 * 4 + ENT * 40 + ENT * RSF + 2 * DPL_STACK_PER_WARP;
+  const size_t smem = (size_t)WARPS * WARP_FLOATS * 4;
+  static bool attr = false;
+  if (!attr) {
+    DPL_CUDA(cudaFuncSetAttribute(k_forward_tc<NT, WARPS, ENT, MAXR>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  unsigned blocks = (unsigned)((a.q + WARPS * 32 - 1) / (WARPS * 32));
+  k_forward_tc<NT, WARPS, ENT, MAXR><<<blocks, WARPS * 32, smem, t.stream>>>(
+      t.view(), kp, a.xs, a.perm, a.q, nr, t.chmap.as<int>(), a.out, a.out_stride, a.overflow);
+  count_launch();
+}
+
+// Tensor-core plan: one dipole slot and PR a multiple of 8 (8..64 radial).
+bool forward_tc_launch(const Tree& t, const KParams& kp, const FwdArgs& a) {
+  if (a.grad_mode != 0 || a.counters || a.single) return false;
+  if (t.Cd != 1 || t.PR % 8 != 0) return false;
+  const int nr = a.nr_limit >= 0 ? std::min(a.nr_limit, t.Cr) : t.Cr;
+  const char* v = getenv("DPL_TUNE_TC");
+  const int choice = v ? atoi(v) : 0;
+  switch (t.PR) {
+    case 16: return launch_tc<2, 4, 8, 128>(t, kp, a, nr), true;
+    case 48:
+      switch (choice) {
+        case 1: return launch_tc<6, 4, 16, 128>(t, kp, a, nr), true;
+        case 2: return launch_tc<6, 4, 8, 112>(t, kp, a, nr), true;
+        case 3: return launch_tc<6, 8, 8, 128>(t, kp, a, nr), true;
+        default: return launch_tc<6, 4, 8, 128>(t, kp, a, nr), true;  // measured best
+      }
+    case 64: return launch_tc<8, 4, 8, 128>(t, kp, a, nr), true;
+    default: return false;
+  }
+}
+
+}  // namespace dpl

@@ -34,6 +34,54 @@ __device__ __forceinline__ double dist2_rn(double cx, double cy, double cz, cons
   return __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
 }
 
+// Query in double-float form (x = hi + lo to ~2^-48) plus its fp64 original.
+struct QueryDF {
+  float hx, hy, hz, lx, ly, lz, m;  // m = max |x_hi|
+};
+
+__device__ __forceinline__ QueryDF make_qdf(const QueryPos& x) {
+  QueryDF q;
+  q.hx = (float)x.x, q.hy = (float)x.y, q.hz = (float)x.z;
+  q.lx = (float)(x.x - (double)q.hx), q.ly = (float)(x.y - (double)q.hy),
+  q.lz = (float)(x.z - (double)q.hz);
+  q.m = fmaxf(fmaxf(fabsf(q.hx), fabsf(q.hy)), fabsf(q.hz));
+  return q;
+}
+
+// d = source - x from double-float operands: |d - d_exact| <= 2^-23 |d| + 2^-46 (|c| + |x|).
+__device__ __forceinline__ float dist2_df(const float4& hi, const float4& lo, const QueryDF& q,
+                                          float& dx, float& dy, float& dz) {
+  dx = (hi.x - q.hx) + (lo.x - q.lx);
+  dy = (hi.y - q.hy) + (lo.y - q.ly);
+  dz = (hi.z - q.hz) + (lo.z - q.lz);
+  return fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+}
+
+// The reference's opening test dist2 > (beta^2 r) r (bhtree.cpp:204), decided
+// in fp32 when the margin exceeds a rigorous error bound (dist2 error
+// <= 2^-21 s + 2^-46 M^2, threshold rounding 2^-24 thr; the band below is 2x
+// that), else re-evaluated exactly in fp64 with the reference's operation
+// order. NaN / inf thresholds (beta = inf) always take the exact path.
+__device__ __forceinline__ bool far_test(float s, const float4& hi, const QueryDF& q,
+                                         const QueryPos& x, const double4* __restrict__ dec) {
+  const float thr = hi.w;
+  const float M = fmaxf(fmaxf(fabsf(hi.x), fabsf(hi.y)), fabsf(hi.z)) + q.m;
+  const float band = 2e-6f * (s + thr) + 1e-13f * M * M;
+  const float diff = s - thr;
+  if (diff > band) return true;
+  if (-diff > band) return false;
+  const double2 a = __ldg(reinterpret_cast<const double2*>(dec));
+  const double2 b = __ldg(reinterpret_cast<const double2*>(dec) + 1);
+  double ex, ey, ez;
+  return dist2_rn(a.x, a.y, b.x, x, ex, ey, ez) > b.y;
+}
+
+// exact fp64 coincidence check for a leaf point (bhtree.cpp:219,316,387)
+__device__ __forceinline__ bool coincident_exact(const double* __restrict__ p, const QueryPos& x) {
+  double ex, ey, ez;
+  return dist2_rn(__ldg(p), __ldg(p + 1), __ldg(p + 2), x, ex, ey, ez) == 0.0;
+}
+
 __device__ __forceinline__ double4 ld_dec(const double4* p) {
   const double2* q = reinterpret_cast<const double2*>(p);
   double2 a = __ldg(q), b = __ldg(q + 1);

@@ -92,6 +92,7 @@ KParams make_kparams(double eps, int desing, double delta) {
     k.inv_eps4 = (float)(1.0 / (eps * eps * eps * eps));
     k.inv_eps5 = (float)(1.0 / (eps * eps * eps * eps * eps));
     k.inv_eps6 = (float)(1.0 / (eps * eps * eps * eps * eps * eps));
+    k.near2 = (float)((6.5 * eps) * (6.5 * eps));
   }
   return k;
 }
@@ -107,6 +108,7 @@ TreeView Tree::view() const {
   v.pt_pos64 = pt_pos64.as<double>();
   v.pt_geo = pt_geo.as<float4>();
   v.pt_row = pt_row.as<float4>();
+  v.pt_rec = pt_rec.as<PtRec>();
   v.pt_nrm = pt_nrm.as<float>();
   v.pt_mu = pt_mud.as<float>();
   v.P = PR;
@@ -275,13 +277,19 @@ __global__ void k_finish_points(const uint64_t* __restrict__ key2, int64_t n, in
 // sorted fp64 / fp32 point copies
 __global__ void k_gather_points(const int32_t* __restrict__ order, const double* __restrict__ pos,
                                 const double* __restrict__ area, int64_t n, double* pt_pos64,
-                                float4* pt_geo) {
+                                float4* pt_geo, PtRec* pt_rec) {
   int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (j >= n) return;
   int64_t m = order[j];
   double x = pos[3 * m], y = pos[3 * m + 1], z = pos[3 * m + 2];
   pt_pos64[3 * j] = x, pt_pos64[3 * j + 1] = y, pt_pos64[3 * j + 2] = z;
-  pt_geo[j] = make_float4((float)x, (float)y, (float)z, (float)(area[m] * kInvFourPi));
+  float A = (float)(area[m] * kInvFourPi);
+  float hx = (float)x, hy = (float)y, hz = (float)z;
+  pt_geo[j] = make_float4(hx, hy, hz, A);
+  PtRec r;
+  r.hi = make_float4(hx, hy, hz, A);
+  r.lo = make_float4((float)(x - (double)hx), (float)(y - (double)hy), (float)(z - (double)hz), 0.f);
+  pt_rec[j] = r;
 }
 
 // K3: geometry, one thread per node, sequential in point_order (bit-exact).
@@ -356,10 +364,11 @@ __global__ void k_thresholds(const double* __restrict__ ctr, const double* __res
   double thr = __dmul_rn(__dmul_rn(beta2, r), r);
   dec[i] = make_double4(ctr[3 * i], ctr[3 * i + 1], ctr[3 * i + 2], thr);
   NodeRec nr;
-  nr.c = make_double4(ctr[3 * i], ctr[3 * i + 1], ctr[3 * i + 2], thr);
+  float hx = (float)ctr[3 * i], hy = (float)ctr[3 * i + 1], hz = (float)ctr[3 * i + 2];
+  nr.hi = make_float4(hx, hy, hz, (float)thr);
+  nr.lo = make_float4((float)(ctr[3 * i] - (double)hx), (float)(ctr[3 * i + 1] - (double)hy),
+                      (float)(ctr[3 * i + 2] - (double)hz), geo[i].w);
   nr.topo = topo[i];
-  float4 g = geo[i];
-  nr.A = make_float4(g.w, 0.f, 0.f, 0.f);
   rec[i] = nr;
 }
 
@@ -683,9 +692,10 @@ void tree_build(Tree& t, const double* pos, const double* nrm, const double* are
   count_launch();
   t.pt_pos64.reserve(n * 24);
   t.pt_geo.reserve((n + 1) * sizeof(float4));
+  t.pt_rec.reserve((n + 1) * sizeof(PtRec));
   k_gather_points<<<grid_for(n, B), B, 0, s>>>(t.order.as<int32_t>(), t.pos64.as<double>(),
                                                 t.area64.as<double>(), n, t.pt_pos64.as<double>(),
-                                                t.pt_geo.as<float4>());
+                                                t.pt_geo.as<float4>(), t.pt_rec.as<PtRec>());
   count_launch();
   t.node_ctr64.reserve(nodes * 24);
   t.node_area64.reserve(nodes * 8);
@@ -707,7 +717,7 @@ void tree_build(Tree& t, const double* pos, const double* nrm, const double* are
 void tree_refresh_sorted_positions(Tree& t) {
   k_gather_points<<<grid_for(t.n, 256), 256, 0, t.stream>>>(
       t.order.as<int32_t>(), t.pos64.as<double>(), t.area64.as<double>(), t.n,
-      t.pt_pos64.as<double>(), t.pt_geo.as<float4>());
+      t.pt_pos64.as<double>(), t.pt_geo.as<float4>(), t.pt_rec.as<PtRec>());
   count_launch();
   DPL_CUDA(cudaGetLastError());
 }

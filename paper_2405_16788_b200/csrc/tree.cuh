@@ -50,7 +50,7 @@ struct Tree {
   DevBuf node_sumv, node_sums;  // fp64 unnormalised moment sums (nodes x Cd x 3, nodes x Cr)
   DevBuf node_row, node_rec;  // fp32 payload rows (nodes x F4 float4), packed node records
   // sorted point data
-  DevBuf pt_pos64, pt_geo, pt_row, pt_nrm, pt_mud;
+  DevBuf pt_pos64, pt_geo, pt_row, pt_nrm, pt_mud, pt_rec;
   DevBuf chmap;  // int32 [Cd dip ids | Cr rad ids]
   // scratch
   DevBuf scratch[8];
