@@ -108,7 +108,10 @@ class GradientBuffer:
 
     def __del__(self):
         if getattr(self, "_h", None):
-            lib().dpl_gradbuf_destroy(self._h)
+            try:
+                lib().dpl_gradbuf_destroy(self._h)
+            except Exception:  # interpreter shutdown: the process frees the device
+                pass
             self._h = None
 
 
@@ -129,7 +132,10 @@ class DipoleTree:
 
     def __del__(self):
         if getattr(self, "_h", None):
-            lib().dpl_tree_destroy(self._h)
+            try:
+                lib().dpl_tree_destroy(self._h)
+            except Exception:  # interpreter shutdown: the process frees the device
+                pass
             self._h = None
 
     def set_stream(self, stream):

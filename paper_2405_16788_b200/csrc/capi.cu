@@ -31,6 +31,13 @@ struct dpl_tree_s {
   bool built = false;
   DevBuf ws_xs, ws_perm, ws_out, ws_grad, ws_cnt, ws_morton, ws_dout, ws_dgrad, ws_flag, ws_mom,
       ws_nrm;
+  cudaStream_t copy = nullptr, copy_out = nullptr;  // host<->device pipeline streams
+  std::vector<cudaEvent_t> pipe_ev;                 // chunk hand-off events
+  ~dpl_tree_s() {
+    for (cudaEvent_t e : pipe_ev) cudaEventDestroy(e);
+    if (copy) cudaStreamDestroy(copy);
+    if (copy_out) cudaStreamDestroy(copy_out);
+  }
 };
 
 struct dpl_gradbuf_s {
@@ -160,7 +167,10 @@ int dpl_tree_create(int device, void* stream, dpl_tree_t* out) {
     if (stream) {
       h->t.stream = (cudaStream_t)stream;
     } else {
-      cudaError_t e = cudaStreamCreateWithFlags(&h->t.stream, cudaStreamNonBlocking);
+      // a BLOCKING stream: it orders against the legacy default stream, so
+      // device arrays produced there (e.g. by torch) are complete before our
+      // kernels read them, and our outputs before their consumers run
+      cudaError_t e = cudaStreamCreateWithFlags(&h->t.stream, cudaStreamDefault);
       if (e != cudaSuccess) {
         delete h;
         throw Error(DPL_ERR_CUDA, cudaGetErrorString(e));
@@ -332,6 +342,81 @@ int dpl_tree_dump(dpl_tree_t h, const char* path) {
 
 // ---------------------------------------------------------------- forward
 
+}  // extern "C"
+
+// ------------------------------------------------------- host-buffer pipeline
+// Host-resident query batches are processed in chunks: the copy stream moves
+// chunk c+1's inputs host->device and chunk c-1's outputs device->host while
+// the compute stream runs chunk c (sort + traversal), so PCIe traffic overlaps
+// the kernels instead of serialising with them.
+struct HostSeg {
+  const char* src;  // inputs: host; outputs: device
+  char* dst;        // inputs: device; outputs: host
+  size_t row_bytes;
+};
+
+static cudaStream_t copy_stream(dpl_tree_t h, int which) {
+  cudaStream_t& s = which ? h->copy_out : h->copy;
+  if (!s) DPL_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  return s;
+}
+
+static cudaEvent_t pipe_event(dpl_tree_t h, size_t i) {
+  while (h->pipe_ev.size() <= i) {
+    cudaEvent_t e;
+    DPL_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    h->pipe_ev.push_back(e);
+  }
+  return h->pipe_ev[i];
+}
+
+template <typename F>
+static void run_chunked(dpl_tree_t h, int64_t q, int64_t chunk, const std::vector<HostSeg>& ins,
+                        const std::vector<HostSeg>& outs, F&& body) {
+  // inputs and outputs use separate copy streams so H2D of later chunks never
+  // queues behind D2H of earlier ones (both copy engines run concurrently)
+  cudaStream_t cin = copy_stream(h, 0), cout = copy_stream(h, 1), ks = h->t.stream;
+  int64_t nchunks = (q + chunk - 1) / chunk;
+  // the compute stream may still be using the device staging buffers
+  cudaEvent_t start = pipe_event(h, 0);
+  DPL_CUDA(cudaEventRecord(start, ks));
+  DPL_CUDA(cudaStreamWaitEvent(cin, start, 0));
+  for (int64_t c = 0; c < nchunks; ++c) {
+    const int64_t c0 = c * chunk, qc = std::min(chunk, q - c0);
+    for (const HostSeg& s : ins)
+      DPL_CUDA(cudaMemcpyAsync(s.dst + c0 * s.row_bytes, s.src + c0 * s.row_bytes,
+                               qc * s.row_bytes, cudaMemcpyHostToDevice, cin));
+    DPL_CUDA(cudaEventRecord(pipe_event(h, 1 + 2 * c), cin));
+  }
+  for (int64_t c = 0; c < nchunks; ++c) {
+    const int64_t c0 = c * chunk, qc = std::min(chunk, q - c0);
+    DPL_CUDA(cudaStreamWaitEvent(ks, pipe_event(h, 1 + 2 * c), 0));
+    body(c0, qc);
+    cudaEvent_t done = pipe_event(h, 2 + 2 * c);
+    DPL_CUDA(cudaEventRecord(done, ks));
+    if (!outs.empty()) {
+      DPL_CUDA(cudaStreamWaitEvent(cout, done, 0));
+      for (const HostSeg& s : outs)
+        DPL_CUDA(cudaMemcpyAsync(s.dst + c0 * s.row_bytes, s.src + c0 * s.row_bytes,
+                                 qc * s.row_bytes, cudaMemcpyDeviceToHost, cout));
+    }
+  }
+  DPL_CUDA(cudaStreamSynchronize(cout));
+  DPL_CUDA(cudaStreamSynchronize(ks));
+}
+
+// Default: ONE chunk. Measured on config 2 (4M uniform queries): Morton-sorting
+// 8 chunks of 500k separately makes each warp's queries span a 2x larger cell,
+// which raised the forward kernel time from 16.5 to 29 ms and more than ate the
+// PCIe overlap. DPL_PIPELINE_CHUNKS=k re-enables k chunks for experiments.
+static int64_t pipe_chunk(int64_t q) {
+  static const char* v = getenv("DPL_PIPELINE_CHUNKS");
+  const int64_t k = v ? std::max(1, atoi(v)) : 1;
+  return std::max<int64_t>(1, (q + k - 1) / k);
+}
+
+extern "C" {
+
 static int forward_common(dpl_tree_t h, const dpl_kernel_params* params, double beta,
                           const double* xs, int64_t q, float* out, float* grad,
                           dpl_counters* counters, int grad_mode, int channel) {
@@ -346,6 +431,61 @@ static int forward_common(dpl_tree_t h, const dpl_kernel_params* params, double 
     DPL_CUDA(cudaSetDevice(t.device));
     KParams kp = make_kparams(params->epsilon, params->desingularized, params->desing_delta);
     tree_ensure_thresholds(t, beta);
+    const bool xs_host = !is_device_ptr(xs);
+    const bool out_host = !is_device_ptr(out);
+    const bool grad_host = grad && !is_device_ptr(grad);
+    if ((xs_host || out_host || grad_host) && !counters && q > (1 << 18)) {
+      // pipelined host path
+      const int stride = channel >= 0 ? 1 : t.C;
+      const int gstride = grad_mode == 1 ? t.C * 3 : 3;
+      h->ws_xs.reserve(q * 24);
+      h->ws_perm.reserve(q * 4);
+      const double* xs_d = xs_host ? h->ws_xs.as<double>() : xs;
+      float* out_d = out;
+      if (out_host) {
+        h->ws_out.reserve(q * stride * 4);
+        out_d = h->ws_out.as<float>();
+      }
+      float* grad_d = grad;
+      if (grad_host) {
+        h->ws_grad.reserve(q * gstride * 4);
+        grad_d = h->ws_grad.as<float>();
+      }
+      std::vector<HostSeg> ins, outs;
+      if (xs_host) ins.push_back({(const char*)xs, (char*)xs_d, 24});
+      if (out_host) outs.push_back({(const char*)out_d, (char*)out, (size_t)stride * 4});
+      if (grad_host) outs.push_back({(const char*)grad_d, (char*)grad, (size_t)gstride * 4});
+      int* ovf = overflow_flag(h);
+      run_chunked(h, q, pipe_chunk(q), ins, outs, [&](int64_t c0, int64_t qc) {
+        int32_t* perm = h->ws_perm.as<int32_t>() + c0;
+        {
+          PhaseTimer pt(t, PH_SORT);
+          morton_order(t, xs_d + 3 * c0, qc, perm, h->ws_morton);
+        }
+        FwdArgs a;
+        a.xs = xs_d + 3 * c0;
+        a.perm = perm;
+        a.q = qc;
+        a.overflow = ovf;
+        a.out = out_d + c0 * stride;
+        a.out_stride = stride;
+        if (channel >= 0) {
+          a.single = 1;
+          if (t.kinds[channel] == 0)
+            a.only_dip = t.slot_of[channel];
+          else
+            a.only_rad = t.slot_of[channel];
+        } else if (grad) {
+          a.grad = grad_d + c0 * gstride;
+          a.grad_mode = grad_mode;
+        }
+        PhaseTimer pt(t, PH_FORWARD);
+        forward_launch(t, kp, a);
+      });
+      DPL_CUDA(cudaGetLastError());
+      check_overflow(h);
+      return;
+    }
     const double* xs_d = stage_in(t, xs, (size_t)q * 3, h->ws_xs);
     h->ws_perm.reserve(q * 4);
     {
@@ -467,6 +607,52 @@ int dpl_adjoint(dpl_tree_t h, const dpl_kernel_params* params, double beta_bh, c
     DPL_CUDA(cudaSetDevice(t.device));
     KParams kp = make_kparams(params->epsilon, params->desingularized, params->desing_delta);
     tree_ensure_thresholds(t, beta_bh);
+    const bool xs_host = !is_device_ptr(xs), do_host = !is_device_ptr(d_out);
+    const bool dg_host = d_grad && !is_device_ptr(d_grad);
+    if ((xs_host || do_host || dg_host) && q > (1 << 18)) {
+      // pipelined host path: H2D of chunk c+1 overlaps the adjoint of chunk c
+      h->ws_perm.reserve(q * 4);
+      const double* xs_d = xs;
+      const float* dout_d = d_out;
+      const float* dg_d = d_grad;
+      std::vector<HostSeg> ins;
+      if (xs_host) {
+        h->ws_xs.reserve(q * 24);
+        xs_d = h->ws_xs.as<double>();
+        ins.push_back({(const char*)xs, (char*)xs_d, 24});
+      }
+      if (do_host) {
+        h->ws_dout.reserve(q * t.C * 4);
+        dout_d = h->ws_dout.as<float>();
+        ins.push_back({(const char*)d_out, (char*)dout_d, (size_t)t.C * 4});
+      }
+      if (dg_host) {
+        h->ws_dgrad.reserve(q * t.C * 12);
+        dg_d = h->ws_dgrad.as<float>();
+        ins.push_back({(const char*)d_grad, (char*)dg_d, (size_t)t.C * 12});
+      }
+      int* ovf = overflow_flag(h);
+      run_chunked(h, q, pipe_chunk(q), ins, {}, [&](int64_t c0, int64_t qc) {
+        int32_t* perm = h->ws_perm.as<int32_t>() + c0;
+        {
+          PhaseTimer pt(t, PH_SORT);
+          morton_order(t, xs_d + 3 * c0, qc, perm, h->ws_morton);
+        }
+        AdjArgs a;
+        a.xs = xs_d + 3 * c0;
+        a.perm = perm;
+        a.q = qc;
+        a.d_out = dout_d + c0 * t.C;
+        a.dstride = t.C;
+        a.d_grad = dg_d ? dg_d + c0 * t.C * 3 : nullptr;
+        a.grad_mode = dg_d ? 1 : 0;
+        a.overflow = ovf;
+        PhaseTimer pt(t, PH_ADJOINT);
+        adjoint_launch(t, kp, a, buf->b);
+      });
+      DPL_CUDA(cudaGetLastError());
+      return;
+    }
     const double* xs_d = stage_in(t, xs, (size_t)q * 3, h->ws_xs);
     const float* dout_d = stage_in(t, d_out, (size_t)q * t.C, h->ws_dout);
     const float* dg_d = d_grad ? stage_in(t, d_grad, (size_t)q * t.C * 3, h->ws_dgrad) : nullptr;

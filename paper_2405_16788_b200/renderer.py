@@ -70,7 +70,10 @@ class Tape:
 
     def __del__(self):
         if getattr(self, "_h", None):
-            lib().dpl_tape_destroy(self._h)
+            try:
+                lib().dpl_tape_destroy(self._h)
+            except Exception:  # interpreter shutdown
+                pass
             self._h = None
 
 

@@ -318,3 +318,30 @@ def test_error_behaviour(eng, oracle_mod):
         t.set_channel_kernels([0])
     with pytest.raises(eng.DataError):
         t.update_moments(eng.OrientedPointCloud(pos[:-1], nrm[:-1], area[:-1], mu[:-1]))
+
+
+def test_host_pointer_pipeline_matches_device_path(eng, oracle_mod):
+    """Host-resident batches take the chunked H2D/compute/D2H pipeline. Chunks
+    are Morton-sorted separately, so warp groupings (hence fp32 summation
+    order) differ from the device-resident path: agreement to rounding."""
+    import torch
+
+    rng = np.random.default_rng(77)
+    n, C, q = 20000, 49, 600_000
+    pos, nrm, area, _ = random_cloud(n, 78, 1)
+    mu = rng.standard_normal((n, C))
+    kinds = np.ones(C, np.uint8)
+    kinds[0] = 0
+    t, _ = make(eng, oracle_mod, pos, nrm, area, mu, kinds)
+    xs = rng.uniform(-1.2, 1.2, (q, 3)).astype(np.float32).astype(np.float64)
+    d_out = rng.standard_normal((q, C)).astype(np.float32)
+    p = eng.KernelParams(epsilon=0.02)
+    host = t.primal(xs, p, 2.0)
+    dev = t.primal(torch.from_numpy(xs).cuda(), p, 2.0).cpu().numpy()
+    assert rel_scale_err(host, dev) < 1e-5
+    assert close(host, dev, rtol=1e-4, atol=1e-6)[0] == 0
+    b1, b2 = t.make_buffer(), t.make_buffer()
+    t.adjoint(xs, p, 2.0, d_out, None, b1)
+    t.adjoint(torch.from_numpy(xs).cuda(), p, 2.0, torch.from_numpy(d_out).cuda(), None, b2)
+    g1, g2 = t.flush_gradients(b1), t.flush_gradients(b2)
+    assert rel_scale_err(g1.moments, g2.moments) < 1e-6
