@@ -163,6 +163,28 @@ int dpl_render_backward(dpl_tree_t tree, const dpl_kernel_params* params,
 /* The sampler's uniform draw, exported so host code can reproduce it. */
 double dpl_uniform(uint64_t seed, uint64_t counter);
 
+/* ---- SceneModel::prepare's eps default (fields.cpp:10-11) -------------------
+ * OrientedPointCloud::mean_knn_spacing(k) (pointcloud.cpp:51-65): mean over
+ * points of the distances to their k nearest other points; exact kNN on a GPU
+ * uniform grid, fp64 distances as the reference computes them. pos: n x 3
+ * (host or device). eps = 1.5 * result. */
+int dpl_mean_knn_spacing(int device, const double* pos, int64_t n, int32_t k, double* out);
+
+/* ---- Trainer::step point update (optimizer.cpp:161-205) ---------------------
+ * Adam (fp64 state, optimizer.cpp:65-81) on the geometry moments, appearance
+ * moments and raw normals with flushed gradients g_moments (N x C) and
+ * g_normals (N x 3) (fp32, original point order, host or device); normals
+ * renormalised when changed (:196-200); then update_moments (bhtree.cpp:171-176).
+ * Positions and areas stay fixed, as in the reference trainer. */
+typedef struct dpl_point_adam_s* dpl_point_adam_t;
+int dpl_point_adam_create(dpl_tree_t tree, dpl_point_adam_t* out);
+int dpl_point_adam_destroy(dpl_point_adam_t opt);
+int dpl_point_adam_step(dpl_tree_t tree, dpl_point_adam_t opt, const float* g_moments,
+                        const float* g_normals, double lr, double beta1, double beta2,
+                        double eps);
+/* Current cloud parameters (original order, fp64): normals N x 3, moments N x C. */
+int dpl_tree_get_points(dpl_tree_t tree, double* normals, double* moments);
+
 /* ---- Adam (optimizer.cpp:65-81) on device parameter groups ------------------ */
 /* In-place Adam on n fp32 params with fp32 grads and fp32 m/v state; step t is
  * the 1-based iteration after increment. */

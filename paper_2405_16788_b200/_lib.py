@@ -96,6 +96,13 @@ _sig = {
     "dpl_profile_read": (C.c_int, [_vp, _vp, _vp]),
     "dpl_peak_fp32": (C.c_int, [C.c_int, C.POINTER(C.c_double)]),
     "dpl_peak_fp64": (C.c_int, [C.c_int, C.POINTER(C.c_double)]),
+    "dpl_mean_knn_spacing": (C.c_int, [C.c_int, _vp, C.c_int64, C.c_int32,
+                                       C.POINTER(C.c_double)]),
+    "dpl_point_adam_create": (C.c_int, [_vp, C.POINTER(_vp)]),
+    "dpl_point_adam_destroy": (C.c_int, [_vp]),
+    "dpl_point_adam_step": (C.c_int, [_vp, _vp, _vp, _vp, C.c_double, C.c_double, C.c_double,
+                                      C.c_double]),
+    "dpl_tree_get_points": (C.c_int, [_vp, _vp, _vp]),
     "dpl_adam_step": (C.c_int, [_vp, _vp, _vp, _vp, _vp, C.c_int64, C.c_double, C.c_double,
                                 C.c_double, C.c_double, C.c_int64]),
 }

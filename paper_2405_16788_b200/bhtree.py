@@ -322,6 +322,57 @@ def launch_count() -> int:
     return int(lib().dpl_launch_count())
 
 
+def mean_knn_spacing(positions, k: int = 8, device: int = 0) -> float:
+    """OrientedPointCloud::mean_knn_spacing (pointcloud.cpp:51-65) on the GPU."""
+    n = int(positions.shape[0])
+    p, keep = _in(positions, np.float64, (n, 3))
+    out = C.c_double()
+    check(lib().dpl_mean_knn_spacing(int(device), p, n, int(k), C.byref(out)))
+    return out.value
+
+
+def default_epsilon(cloud: OrientedPointCloud, device: int = 0) -> float:
+    """SceneModel::prepare's eps when unset: 1.5 x mean 8-NN spacing (fields.cpp:10-11)."""
+    return 1.5 * mean_knn_spacing(cloud.positions, 8, device)
+
+
+class PointAdam:
+    """Trainer::step's point-parameter update (optimizer.cpp:161-205): Adam on
+    geometry moments, appearance moments and normals, then update_moments."""
+
+    def __init__(self, tree: DipoleTree, lr=1e-2, beta1=0.9, beta2=0.999, eps=1e-8):
+        h = C.c_void_p()
+        check(lib().dpl_point_adam_create(tree._h, C.byref(h)))
+        self._h = h.value
+        self.tree = tree
+        self.lr, self.beta1, self.beta2, self.eps = lr, beta1, beta2, eps
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            try:
+                lib().dpl_point_adam_destroy(self._h)
+            except Exception:
+                pass
+            self._h = None
+
+    def step(self, grads: PointGradients, lr=None):
+        n, Cc = self.tree.point_count(), self.tree.channels()
+        gm, k1 = _in(grads.moments, np.float32, (n, Cc))
+        gn, k2 = _in(grads.normals, np.float32, (n, 3))
+        check(lib().dpl_point_adam_step(self.tree._h, self._h, gm, gn,
+                                        float(self.lr if lr is None else lr), self.beta1,
+                                        self.beta2, self.eps))
+
+
+def get_points(tree: DipoleTree):
+    """(normals N x 3, moments N x C) fp64 of the tree's current cloud."""
+    n, Cc = tree.point_count(), tree.channels()
+    nrm = np.zeros((n, 3))
+    mu = np.zeros((n, Cc))
+    check(lib().dpl_tree_get_points(tree._h, nrm.ctypes.data, mu.ctypes.data))
+    return nrm, mu
+
+
 PHASES = ("sort", "forward", "adjoint", "flush", "render", "moments")
 
 

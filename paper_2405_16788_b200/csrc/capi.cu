@@ -16,6 +16,8 @@
 #include "../../include/dipole_b200.h"
 #include "adjoint.cuh"
 #include "forward.cuh"
+#include "knn.cuh"
+#include "train.cuh"
 #include "render.cuh"
 #include "tree.cuh"
 
@@ -43,6 +45,11 @@ struct dpl_tree_s {
 struct dpl_gradbuf_s {
   dpl_tree_s* tree;
   GradBuf b;
+};
+
+struct dpl_point_adam_s {
+  dpl_tree_s* tree;
+  PointAdam a;
 };
 
 struct dpl_tape_s {
@@ -928,6 +935,86 @@ static double run_peak(int device) {
 }
 
 extern "C" {
+
+int dpl_point_adam_create(dpl_tree_t h, dpl_point_adam_t* out) {
+  return guard([&] {
+    check_tree(h);
+    require(out != nullptr, DPL_ERR_USAGE, "null out");
+    auto o = new dpl_point_adam_s();
+    o->tree = h;
+    try {
+      point_adam_alloc(o->a, h->t);
+    } catch (...) {
+      delete o;
+      throw;
+    }
+    *out = o;
+  });
+}
+
+int dpl_point_adam_destroy(dpl_point_adam_t o) {
+  return guard([&] { delete o; });
+}
+
+int dpl_point_adam_step(dpl_tree_t h, dpl_point_adam_t o, const float* g_moments,
+                        const float* g_normals, double lr, double beta1, double beta2,
+                        double eps) {
+  return guard([&] {
+    check_tree(h);
+    require(o != nullptr && o->tree == h, DPL_ERR_USAGE, "optimizer belongs to another tree");
+    require(o->a.n == h->t.n && o->a.C == h->t.C, DPL_ERR_DATA, "optimizer / tree size mismatch");
+    require(g_moments && g_normals, DPL_ERR_USAGE, "null gradient");
+    Tree& t = h->t;
+    DPL_CUDA(cudaSetDevice(t.device));
+    DevBuf tm, tn;
+    const float* gm = stage_in(t, g_moments, (size_t)t.n * t.C, tm);
+    const float* gn = stage_in(t, g_normals, (size_t)t.n * 3, tn);
+    point_adam_step(t, o->a, gm, gn, lr, beta1, beta2, eps);
+    DPL_CUDA(cudaStreamSynchronize(t.stream));
+  });
+}
+
+int dpl_tree_get_points(dpl_tree_t h, double* nrm, double* mu) {
+  return guard([&] {
+    check_tree(h);
+    Tree& t = h->t;
+    if (nrm)
+      DPL_CUDA(cudaMemcpyAsync(nrm, t.nrm64.p, t.n * 24, cudaMemcpyDefault, t.stream));
+    if (mu)
+      DPL_CUDA(cudaMemcpyAsync(mu, t.mu64.p, t.n * (size_t)t.C * 8, cudaMemcpyDefault, t.stream));
+    DPL_CUDA(cudaStreamSynchronize(t.stream));
+  });
+}
+
+int dpl_mean_knn_spacing(int device, const double* pos, int64_t n, int32_t k, double* out) {
+  return guard([&] {
+    require(out != nullptr, DPL_ERR_USAGE, "null out");
+    require(k >= 1, DPL_ERR_USAGE, "k must be >= 1");
+    if (n < 2) {  // pointcloud.cpp:52
+      *out = 0.0;
+      return;
+    }
+    require(pos != nullptr, DPL_ERR_USAGE, "null positions");
+    DPL_CUDA(cudaSetDevice(device));
+    cudaStream_t st;
+    DPL_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamDefault));
+    DevBuf ws[4];
+    try {
+      const double* p = pos;
+      if (!is_device_ptr(pos)) {
+        ws[3].reserve(n * 24);
+        DPL_CUDA(cudaMemcpyAsync(ws[3].p, pos, n * 24, cudaMemcpyHostToDevice, st));
+        p = ws[3].as<double>();
+      }
+      *out = mean_knn_spacing(st, p, n, k, ws);
+    } catch (...) {
+      cudaStreamDestroy(st);
+      throw;
+    }
+    cudaStreamSynchronize(st);
+    cudaStreamDestroy(st);
+  });
+}
 
 int dpl_peak_fp32(int device, double* tflops) {
   return guard([&] { *tflops = run_peak<float>(device); });

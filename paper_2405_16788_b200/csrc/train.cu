@@ -1,0 +1,80 @@
+// train.cu — the point-parameter half of Trainer::step on the device.
+//
+// Restates proj/src/optimizer.cpp:161-205 for the point groups: Adam
+// (optimizer.cpp:65-81) on the geometry moments beta, the appearance moments
+// alpha and the raw normals n, one step counter shared by the three groups
+// (they are stepped together every iteration), then the write-back: moments
+// copied, normals renormalised only when the update changed them (:196-200),
+// and finally update_moments (bhtree.cpp:171-176) refreshes the tree's node
+// moments and payload rows. fp64 with the reference's operation order and no
+// FMA, so given identical gradients the parameters match the reference's bits.
+#include <cmath>
+
+#include "train.cuh"
+
+namespace dpl {
+
+__device__ __forceinline__ double adam1(double p, double g, double& m, double& v, double lr,
+                                        double b1, double b2, double eps, double c1, double c2) {
+  m = __dadd_rn(__dmul_rn(b1, m), __dmul_rn(__dsub_rn(1.0, b1), g));
+  v = __dadd_rn(__dmul_rn(b2, v), __dmul_rn(__dmul_rn(__dsub_rn(1.0, b2), g), g));
+  const double step = __ddiv_rn(__dmul_rn(lr, __ddiv_rn(m, c1)),
+                                __dadd_rn(__dsqrt_rn(__ddiv_rn(v, c2)), eps));
+  return __dsub_rn(p, step);
+}
+
+// one thread per point (original order)
+__global__ void k_point_adam(int64_t n, int C, double* __restrict__ mu, double* __restrict__ nrm,
+                             const float* __restrict__ g_mu, const float* __restrict__ g_n,
+                             double* __restrict__ m_mu, double* __restrict__ v_mu,
+                             double* __restrict__ m_n, double* __restrict__ v_n, double lr,
+                             double b1, double b2, double eps, double c1, double c2) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  for (int c = 0; c < C; ++c) {
+    const int64_t k = i * C + c;
+    double m = m_mu[k], v = v_mu[k];
+    mu[k] = adam1(mu[k], (double)g_mu[k], m, v, lr, b1, b2, eps, c1, c2);
+    m_mu[k] = m, v_mu[k] = v;
+  }
+  double old[3], nw[3];
+  for (int a = 0; a < 3; ++a) {
+    const int64_t k = 3 * i + a;
+    old[a] = nrm[k];
+    double m = m_n[k], v = v_n[k];
+    nw[a] = adam1(old[a], (double)g_n[k], m, v, lr, b1, b2, eps, c1, c2);
+    m_n[k] = m, v_n[k] = v;
+  }
+  if (nw[0] != old[0] || nw[1] != old[1] || nw[2] != old[2]) {  // n != p.normal (:197)
+    const double len = __dsqrt_rn(
+        __dadd_rn(__dadd_rn(__dmul_rn(nw[0], nw[0]), __dmul_rn(nw[1], nw[1])), __dmul_rn(nw[2], nw[2])));
+    if (len > 1e-12)
+      for (int a = 0; a < 3; ++a) nrm[3 * i + a] = __ddiv_rn(nw[a], len);
+  }
+}
+
+void point_adam_alloc(PointAdam& o, const Tree& t) {
+  o.n = t.n;
+  o.C = t.C;
+  o.t = 0;
+  size_t nm = (size_t)t.n * t.C, nn = (size_t)t.n * 3;
+  o.state.reserve((2 * nm + 2 * nn) * sizeof(double));
+  DPL_CUDA(cudaMemsetAsync(o.state.p, 0, (2 * nm + 2 * nn) * sizeof(double), t.stream));
+}
+
+void point_adam_step(Tree& t, PointAdam& o, const float* g_mu, const float* g_n, double lr,
+                     double b1, double b2, double eps) {
+  ++o.t;  // Adam::step increments before use (:73)
+  const double c1 = 1.0 - std::pow(b1, (double)o.t);
+  const double c2 = 1.0 - std::pow(b2, (double)o.t);
+  size_t nm = (size_t)t.n * t.C, nn = (size_t)t.n * 3;
+  double* s = o.state.as<double>();
+  k_point_adam<<<(unsigned)((t.n + 255) / 256), 256, 0, t.stream>>>(
+      t.n, t.C, t.mu64.as<double>(), t.nrm64.as<double>(), g_mu, g_n, s, s + nm, s + 2 * nm,
+      s + 2 * nm + nn, lr, b1, b2, eps, c1, c2);
+  count_launch();
+  DPL_CUDA(cudaGetLastError());
+  tree_compute_moments(t);  // update_moments (bhtree.cpp:171-176)
+}
+
+}  // namespace dpl

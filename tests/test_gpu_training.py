@@ -1,0 +1,96 @@
+"""GPU parity for the rows around the query engine: SceneModel's eps default
+(mean k-NN spacing, pointcloud.cpp:51-65) and the trainer's point update
+(Adam + renormalisation + update_moments, optimizer.cpp:65-81,161-205)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def cloud(n, seed, C):
+    rng = np.random.default_rng(seed)
+    pos = rng.uniform(-1, 1, (n, 3)).astype(np.float32).astype(np.float64)
+    nrm = rng.standard_normal((n, 3))
+    nrm /= np.linalg.norm(nrm, axis=1, keepdims=True)
+    area = rng.uniform(0.5, 1, n) / n
+    mu = rng.standard_normal((n, C))
+    return pos, nrm, area, mu
+
+
+@pytest.mark.parametrize("n,k", [(2, 8), (9, 8), (5000, 8), (20000, 4)])
+def test_mean_knn_spacing_matches_reference(oracle_mod, n, k):
+    from paper_2405_16788_b200.bhtree import mean_knn_spacing
+
+    pos, _, _, _ = cloud(n, 3 + n, 1)
+    pos[1] = pos[0]  # a duplicate point
+    got = mean_knn_spacing(pos, k)
+    want = oracle_mod.mean_knn_spacing(pos, k)
+    assert abs(got - want) <= 1e-12 * abs(want)
+
+
+def test_knn_on_surface_cloud(oracle_mod):
+    from paper_2405_16788_b200 import workloads as W
+    from paper_2405_16788_b200.bhtree import mean_knn_spacing
+
+    w = W.config1(scale=0.1)
+    p = w["cloud"].positions
+    assert abs(mean_knn_spacing(p) - oracle_mod.mean_knn_spacing(p)) <= 1e-12
+
+
+def test_point_adam_step_matches_oracle(oracle_mod):
+    """One trainer update with identical gradients: Adam (fp64, reference op
+    order) + normal renormalisation must reproduce the oracle's parameters to
+    the bit; the refreshed tree then answers queries like the oracle's
+    update_moments."""
+    import paper_2405_16788_b200 as P
+    from paper_2405_16788_b200.bhtree import PointAdam, get_points
+
+    O = oracle_mod
+    n, C = 3000, 4
+    pos, nrm, area, mu = cloud(n, 41, C)
+    kinds = np.array([0, 1, 1, 1], np.uint8)
+    t = P.DipoleTree(0)
+    t.build(P.OrientedPointCloud(pos, nrm, area, mu))
+    t.set_channel_kernels(kinds)
+    rng = np.random.default_rng(42)
+    xs = rng.uniform(-1.2, 1.2, (800, 3))
+    p = P.KernelParams(epsilon=0.05)
+    opt = PointAdam(t, lr=1e-2)
+    m_mu, v_mu = np.zeros((n, C)), np.zeros((n, C))
+    m_n, v_n = np.zeros((n, 3)), np.zeros((n, 3))
+    cur_mu, cur_n = mu.copy(), nrm.copy()
+    for step in range(1, 3):
+        d_out = rng.standard_normal((800, C)).astype(np.float32)
+        buf = t.make_buffer()
+        t.adjoint(xs, p, 2.0, d_out, None, buf)
+        g = t.flush_gradients(buf)
+        opt.step(g)
+        # oracle: the same update on the same (fp32) gradients
+        gm = np.ascontiguousarray(g.moments, np.float64)
+        gn = np.ascontiguousarray(g.normals, np.float64)
+        lib = O.port_lib()
+        pm = cur_mu.ravel().copy()
+        lib.ora_adam_step(pm.ctypes.data_as(O._dp), gm.ravel().ctypes.data_as(O._dp),
+                          m_mu.ctypes.data_as(O._dp), v_mu.ctypes.data_as(O._dp), n * C, 1e-2, 0.9,
+                          0.999, 1e-8, step)
+        pn = cur_n.ravel().copy()
+        lib.ora_adam_step(pn.ctypes.data_as(O._dp), gn.ravel().ctypes.data_as(O._dp),
+                          m_n.ctypes.data_as(O._dp), v_n.ctypes.data_as(O._dp), n * 3, 1e-2, 0.9,
+                          0.999, 1e-8, step)
+        cur_mu = pm.reshape(n, C)
+        newn = pn.reshape(n, 3)
+        changed = np.any(newn != cur_n, axis=1)
+        lens = np.sqrt((newn[:, 0] ** 2 + newn[:, 1] ** 2) + newn[:, 2] ** 2)
+        ok = changed & (lens > 1e-12)
+        newn[ok] = newn[ok] / lens[ok, None]
+        newn[~ok] = cur_n[~ok]
+        cur_n = newn
+        gn_, gmu_ = get_points(t)
+        assert np.array_equal(gmu_, cur_mu)
+        assert np.abs(gn_ - cur_n).max() <= 1e-15
+    r = O.OracleTree(O.Cloud(pos, nrm, area, mu))
+    r.set_kinds(kinds)
+    r.update_moments(O.Cloud(pos, cur_n, area, cur_mu))
+    got = t.primal(xs, p, 2.0)
+    want = r.primal(O.Params(0.05), 2.0, xs)
+    assert np.all(np.abs(got - want) <= 1e-6 + 1e-4 * np.abs(want))
