@@ -1,0 +1,144 @@
+#!/usr/bin/env python
+"""Per-configuration timings beyond bench.py's headline (config 2).
+
+    python tools/bench_configs.py --config 1|3|4|5 [--steps K] [--scale s]
+
+Config 1: forward primal, N=1e5 sphere, C=2, Q=1e6 (+ primal_channel).
+Config 3: render step (65,536 rays x 128 samples) on the config-1 cloud, C=4:
+          render_forward -> L2 d_rgb -> render_backward (adjoint) -> flush.
+Config 4: N=8e6 shapes cloud, C=49, Q=6.4e7 forward + adjoint + flush.
+Config 5: full differentiable step, N=4e6, 1,048,576 rays x 192 samples:
+          render fwd/bwd, flush, Adam(beta, alpha, n; lr 1e-2) + update_moments.
+eps = 1.5 x mean 8-NN spacing from the GPU kNN (dpl_mean_knn_spacing). Times
+are CUDA-event per-phase means (dpl_profile_*) and wall clock per step, after
+a warm-up step; prints one JSON line.
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import paper_2405_16788_b200 as P  # noqa: E402
+from paper_2405_16788_b200 import bhtree as B  # noqa: E402
+from paper_2405_16788_b200 import renderer as Rn  # noqa: E402
+from paper_2405_16788_b200 import workloads as W  # noqa: E402
+
+
+def timed(fn, steps, tree):
+    fn()
+    torch.cuda.synchronize()
+    B.profile_read(tree)
+    B.profile_enable(tree, True)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        fn()
+    torch.cuda.synchronize()
+    wall = (time.perf_counter() - t0) / steps
+    prof = B.profile_read(tree)
+    B.profile_enable(tree, False)
+    return 1e3 * wall, {k: v[0] / steps for k, v in prof.items() if v[1]}
+
+
+def build(cloud, kinds, dev):
+    t = P.DipoleTree(0, stream=torch.cuda.current_stream())
+    t0 = time.perf_counter()
+    t.build(cloud)
+    t.set_channel_kernels(kinds)
+    torch.cuda.synchronize()
+    return t, time.perf_counter() - t0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", type=int, required=True)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--scale", type=float, default=1.0)
+    args = ap.parse_args()
+    dev = torch.device("cuda", 0)
+    res = {"config": args.config, "scale": args.scale}
+    if args.config in (1, 2, 4):
+        w = {1: W.config1, 2: W.config2, 4: W.config4}[args.config](scale=args.scale)
+        c = w["cloud"]
+        t0 = time.perf_counter()
+        eps = B.default_epsilon(c)
+        res["eps"], res["knn_s"] = eps, time.perf_counter() - t0
+        tree, res["build_s"] = build(c, w["kinds"], dev)
+        Q, C = w["xs"].shape[0], c.channels
+        xs = torch.from_numpy(w["xs"]).to(dev)
+        out = torch.empty((Q, C), device=dev)
+        p = P.KernelParams(epsilon=eps)
+        ms, ph = timed(lambda: tree.primal(xs, p, 2.0, out=out), args.steps, tree)
+        res.update(points=c.size, nodes=tree.node_count(), queries=Q, channels=C,
+                   forward_ms=ms, forward_phases=ph, forward_qps=Q / (ms * 1e-3))
+        if args.config == 1:
+            ms, _ = timed(lambda: tree.primal_channel(xs, p, 2.0, 0), args.steps, tree)
+            res["primal_channel_ms"] = ms
+        else:
+            g = torch.Generator(device=dev).manual_seed(7)
+            d_out = torch.randn((Q, C), device=dev, generator=g)
+            buf = tree.make_buffer()
+            mom = torch.empty((c.size, C), device=dev)
+            nrm = torch.empty((c.size, 3), device=dev)
+
+            def adj():
+                tree.adjoint(xs, p, 2.0, d_out, None, buf)
+                tree.flush_gradients(buf, out=(mom, nrm))
+
+            ms, ph = timed(adj, args.steps, tree)
+            res.update(adjoint_flush_ms=ms, adjoint_phases=ph, adjoint_qps=Q / (ms * 1e-3),
+                       step_qps=Q / ((ms + res["forward_ms"]) * 1e-3))
+    elif args.config in (3, 5):
+        if args.config == 3:
+            w = W.config3(scale=args.scale)
+            c, rays, S = w["cloud"], w["rays"], w["S"]
+            kinds = w["kinds"]
+        else:
+            n = max(64, int(4_000_000 * args.scale))
+            pos, nrm_, area, rng = W.shapes_cloud(n, 5)
+            mu = rng.standard_normal((n, 49))
+            c = W.cloud(pos, nrm_, area, mu)
+            kinds = np.ones(49, np.uint8)
+            kinds[0] = 0
+            px = max(1, int(16384 * args.scale))
+            rays = W.camera_rays(64, 1024, px, seed=2)
+            S = 192
+        t0 = time.perf_counter()
+        eps = B.default_epsilon(c)
+        res["eps"], res["knn_s"] = eps, time.perf_counter() - t0
+        tree, res["build_s"] = build(c, kinds, dev)
+        R = rays.shape[0]
+        rays_d = torch.from_numpy(rays).to(dev)
+        target = torch.rand((R, 3), device=dev, generator=torch.Generator(device=dev).manual_seed(4))
+        p = P.KernelParams(epsilon=eps)
+        rs = Rn.RenderSettings(t_near=2.0, t_far=6.0, seed=3)
+        buf = tree.make_buffer()
+        mom = torch.empty((c.size, c.channels), device=dev)
+        nrm = torch.empty((c.size, 3), device=dev)
+        opt = B.PointAdam(tree, lr=1e-2) if args.config == 5 else None
+        tape = Rn.Tape()
+        scale = 2.0 / (3.0 * R)
+
+        def step():
+            rgb, _ = Rn.render_forward(tree, p, rs, rays_d, S, tape=tape)
+            d_rgb = (scale * (rgb - target)).float()
+            Rn.render_backward(tree, p, rs, tape, d_rgb, buf)
+            g = tree.flush_gradients(buf, out=(mom, nrm))
+            if opt is not None:
+                opt.step(g)
+
+        ms, ph = timed(step, args.steps, tree)
+        Q = R * S
+        res.update(points=c.size, nodes=tree.node_count(), rays=R, samples=S, queries=Q,
+                   channels=c.channels, step_ms=ms, phases=ph, samples_per_s=Q / (ms * 1e-3))
+    print(json.dumps(res), flush=True)
+
+
+if __name__ == "__main__":
+    main()
