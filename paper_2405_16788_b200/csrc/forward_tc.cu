@@ -69,12 +69,12 @@ constexpr int row_stride_floats(int f4) {
 }  // namespace
 
 // NT: radial n-tiles of 8 channels (TR = 8 NT); one dipole slot.
-template <int NT, int WARPS, int ENT, int MAXR>
+template <int NT, int WARPS, int ENT, int MAXR, bool COUNT>
 __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
     k_forward_tc(TreeView tv, KParams kp, const double* __restrict__ xs,
                  const int32_t* __restrict__ perm, int64_t q, int nr,
                  const int* __restrict__ chmap, float* __restrict__ out, int out_stride,
-                 int* overflow) {
+                 long long* __restrict__ counters, int* overflow) {
   static_assert(ENT % 8 == 0, "ENT must be a multiple of the mma K (8)");
   constexpr int TR = 8 * NT;
   constexpr int F4 = 1 + TR / 4;               // global row float4 (dipole + radial)
@@ -173,6 +173,10 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
     ++nent;
   };
 
+  // COUNT: per-query replay counters (visited, far near/far, point near/far)
+  long long c_vis = 0, c_fn = 0, c_ff = 0, c_pn = 0, c_pf = 0;
+  const bool reg = kp.mode == KM_REGULARIZED;
+
   int sp = 1;
   if (lane == 0) stk[0] = make_int2(0, (int)active);
   __syncwarp();
@@ -192,8 +196,10 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
     const float s = dist2_df(hi, lo, qx, dx, dy, dz);
     const bool far = mine && far_test(s, hi, qx, x, tv.node_dec + node);
     const unsigned farm = __ballot_sync(FULL_MASK, far);
+    if (COUNT && mine) ++c_vis;
     if (farm && A > 0.f) {  // area > 0 (bhtree.cpp:205)
       const float4 wv = far ? fwd_w(dx, dy, dz, s, A, kp) : make_float4(0.f, 0.f, 0.f, 0.f);
+      if (COUNT && far) (reg && s < kp.near2) ? ++c_fn : ++c_ff;
       append(wv, node_row + (size_t)node * F4);
     }
     const unsigned openm = mask & ~farm;
@@ -206,8 +212,10 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
             const PtRec* pr = tv.pt_rec + j;
             const float4 ph = __ldg(&pr->hi);
             const float r2 = dist2_df(ph, __ldg(&pr->lo), qx, dx, dy, dz);
-            if (!(singular && r2 == 0.f && coincident_exact(tv.pt_pos64 + 3 * (size_t)j, x)))
+            if (!(singular && r2 == 0.f && coincident_exact(tv.pt_pos64 + 3 * (size_t)j, x))) {
               wv = fwd_w(dx, dy, dz, r2, ph.w, kp);
+              if (COUNT) (reg && r2 < kp.near2) ? ++c_pn : ++c_pf;
+            }
           }
           append(wv, pt_row + (size_t)j * F4);
         }
@@ -221,6 +229,10 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
         __syncwarp();
       }
     }
+  }
+  if (COUNT && valid) {
+    long long* cq = counters + 5 * qi;
+    cq[0] = c_vis, cq[1] = c_fn, cq[2] = c_ff, cq[3] = c_pn, cq[4] = c_pf;
   }
   if (nent) evaluate();
   // outputs: the dipole value is lane-local; radial values live in mma C fragments
@@ -242,27 +254,36 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
     }
 }
 
-template <int NT, int WARPS, int ENT, int MAXR>
-static void launch_tc(const Tree& t, const KParams& kp, const FwdArgs& a, int nr) {
+template <int NT, int WARPS, int ENT, int MAXR, bool COUNT>
+static void launch_tc1(const Tree& t, const KParams& kp, const FwdArgs& a, int nr) {
   constexpr int F4 = 1 + 2 * NT;
   constexpr int RSF = row_stride_floats(F4);
   constexpr int WARP_FLOATS = ENT * 32 * 4 + ENT * 40 + ENT * RSF + 2 * DPL_STACK_PER_WARP;
   const size_t smem = (size_t)WARPS * WARP_FLOATS * 4;
   static bool attr = false;
   if (!attr) {
-    DPL_CUDA(cudaFuncSetAttribute(k_forward_tc<NT, WARPS, ENT, MAXR>,
+    DPL_CUDA(cudaFuncSetAttribute(k_forward_tc<NT, WARPS, ENT, MAXR, COUNT>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
   unsigned blocks = (unsigned)((a.q + WARPS * 32 - 1) / (WARPS * 32));
-  k_forward_tc<NT, WARPS, ENT, MAXR><<<blocks, WARPS * 32, smem, t.stream>>>(
-      t.view(), kp, a.xs, a.perm, a.q, nr, t.chmap.as<int>(), a.out, a.out_stride, a.overflow);
+  k_forward_tc<NT, WARPS, ENT, MAXR, COUNT><<<blocks, WARPS * 32, smem, t.stream>>>(
+      t.view(), kp, a.xs, a.perm, a.q, nr, t.chmap.as<int>(), a.out, a.out_stride, a.counters,
+      a.overflow);
   count_launch();
+}
+
+template <int NT, int WARPS, int ENT, int MAXR>
+static void launch_tc(const Tree& t, const KParams& kp, const FwdArgs& a, int nr) {
+  if (a.counters)
+    launch_tc1<NT, WARPS, ENT, MAXR, true>(t, kp, a, nr);
+  else
+    launch_tc1<NT, WARPS, ENT, MAXR, false>(t, kp, a, nr);
 }
 
 // Tensor-core plan: one dipole slot and PR a multiple of 8 (8..64 radial).
 bool forward_tc_launch(const Tree& t, const KParams& kp, const FwdArgs& a) {
-  if (a.grad_mode != 0 || a.counters || a.single) return false;
+  if (a.grad_mode != 0 || a.single) return false;
   if (t.Cd != 1 || t.PR % 8 != 0) return false;
   const int nr = a.nr_limit >= 0 ? std::min(a.nr_limit, t.Cr) : t.Cr;
   const char* v = getenv("DPL_TUNE_TC");

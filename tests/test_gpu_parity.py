@@ -293,9 +293,15 @@ def test_many_channel_forward_adjoint(eng, oracle_mod, C):
     xs = rng.uniform(-1.5, 1.5, (q, 3)).astype(np.float32).astype(np.float64)
     p = eng.KernelParams(epsilon=0.06)
     got = t.primal(xs, p, 2.0)
-    want = r.primal(O.Params(0.06), 2.0, xs)
+    want, wcnt = r.primal(O.Params(0.06), 2.0, xs, counters=True)
     nbad, mx = close(got, want)
     assert nbad == 0, (nbad, mx)
+    # the production (two-phase / tensor-core) path replays the reference's
+    # opening decisions exactly: identical visited / far / leaf-point counts
+    _, cnt = t.primal(xs, p, 2.0, visited=True)
+    assert np.array_equal(cnt[:, 0], wcnt[:, 0])
+    assert np.array_equal(cnt[:, 1] + cnt[:, 2], wcnt[:, 1] + wcnt[:, 2])
+    assert np.array_equal(cnt[:, 3] + cnt[:, 4], wcnt[:, 3] + wcnt[:, 4])
     d_out = rng.standard_normal((q, C)).astype(np.float32)
     buf = t.make_buffer()
     t.adjoint(xs, p, 2.0, d_out, None, buf)
