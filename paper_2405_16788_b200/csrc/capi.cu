@@ -478,6 +478,7 @@ static int forward_common(dpl_tree_t h, const dpl_kernel_params* params, double 
         a.out_stride = stride;
         if (channel >= 0) {
           a.single = 1;
+          a.only_ch = channel;
           if (t.kinds[channel] == 0)
             a.only_dip = t.slot_of[channel];
           else
@@ -508,6 +509,7 @@ static int forward_common(dpl_tree_t h, const dpl_kernel_params* params, double 
     Out<long long> cnt;
     if (channel >= 0) {
       a.single = 1;
+      a.only_ch = channel;
       a.out_stride = 1;
       if (t.kinds[channel] == 0)
         a.only_dip = t.slot_of[channel];

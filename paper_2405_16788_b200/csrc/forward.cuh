@@ -17,6 +17,9 @@ struct FwdArgs {
   long long* counters = nullptr;  // q x 5 (dpl_counters)
   int* overflow = nullptr;        // device flag
   int only_dip = -1, only_rad = -1;  // primal_channel: the single slot
+  int only_ch = -1;  // primal_channel on the two-phase kernels: same kernel as
+                     // primal, only channel only_ch stored (q x 1) -> bitwise
+                     // primal_channel(c) == primal()[c] (test_bhtree.cpp:140)
   int nr_limit = -1;                 // only the first nr_limit radial slots (render step)
 };
 

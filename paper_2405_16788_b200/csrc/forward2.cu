@@ -48,12 +48,12 @@ __device__ __forceinline__ float4 fwd_weights(float fx, float fy, float fz, floa
 }
 
 // MAXR: register cap (occupancy vs. spills; chosen by measurement)
-template <int TD, int TR, int WARPS, int ENT, int MAXR = 128>
+template <int TD, int TR, int WARPS, int ENT, int MAXR = 128, bool COUNT = false>
 __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
     k_forward2(TreeView tv, KParams kp, const double* __restrict__ xs,
                const int32_t* __restrict__ perm, int64_t q, int nd, int nr,
                const int* __restrict__ chmap, float* __restrict__ out, int out_stride,
-               int* overflow) {
+               int only_ch, long long* __restrict__ counters, int* overflow) {
   constexpr int RR = TR / 4;          // radial float4 per row
   constexpr int F4 = TD + RR;         // float4 per row (== tree F4)
   constexpr int WARP_F4 = ENT * 32 + ENT * F4 + DPL_STACK_PER_WARP / 2;
@@ -121,6 +121,11 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
     ++nent;
   };
 
+  // COUNT: per-query replay counters (visited, far near/far, point near/far);
+  // same kernel as the values-only launch so primal(visited) == primal()
+  long long c_vis = 0, c_fn = 0, c_ff = 0, c_pn = 0, c_pf = 0;
+  const bool reg = kp.mode == KM_REGULARIZED;
+
   int sp = 1;
   if (lane == 0) stk[0] = make_int2(0, (int)active);
   __syncwarp();
@@ -139,6 +144,8 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
     float dx, dy, dz;
     const float s = dist2_df(hi, lo, qx, dx, dy, dz);
     const bool far = mine && far_test(s, hi, qx, x, tv.node_dec + node);
+    if (COUNT && mine) ++c_vis;
+    if (COUNT && far) (reg && s < kp.near2) ? ++c_fn : ++c_ff;
     const unsigned farm = __ballot_sync(FULL_MASK, far);
     if (farm && A > 0.f) {  // area > 0 (bhtree.cpp:205)
       const float4 wv = far ? fwd_weights(dx, dy, dz, s, A, kp) : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -156,8 +163,10 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
             const float r2 = dist2_df(ph, __ldg(&pr->lo), qx, dx, dy, dz);
             // exact coincidence only matters for the singular kernel (bhtree.cpp:219);
             // the regularized kernel's r = 0 contribution is identically zero
-            if (!(singular && r2 == 0.f && coincident_exact(tv.pt_pos64 + 3 * (size_t)j, x)))
+            if (!(singular && r2 == 0.f && coincident_exact(tv.pt_pos64 + 3 * (size_t)j, x))) {
               wv = fwd_weights(dx, dy, dz, r2, ph.w, kp);
+              if (COUNT) (reg && r2 < kp.near2) ? ++c_pn : ++c_pf;
+            }
           }
           append(wv, pt_row + (size_t)j * F4);
         }
@@ -174,6 +183,19 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
   }
   if (nent) evaluate();
   if (!valid) return;
+  if (COUNT) {
+    long long* cq = counters + 5 * qi;
+    cq[0] = c_vis, cq[1] = c_fn, cq[2] = c_ff, cq[3] = c_pn, cq[4] = c_pf;
+  }
+  if (only_ch >= 0) {  // primal_channel: same arithmetic, one column stored
+#pragma unroll
+    for (int k = 0; k < TD; ++k)
+      if (k < nd && __ldg(chmap + k) == only_ch) out[qi] = accd[k];
+#pragma unroll
+    for (int k = 0; k < TR; ++k)
+      if (k < nr && __ldg(chmap + TD + k) == only_ch) out[qi] = accr[k];
+    return;
+  }
   float* o = out + qi * out_stride;
 #pragma unroll
   for (int k = 0; k < TD; ++k)
@@ -183,21 +205,29 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
     if (k < nr) o[__ldg(chmap + TD + k)] = accr[k];
 }
 
-template <int TD, int TR, int WARPS, int ENT, int MINB = 128>
-static void launch2(const Tree& t, const KParams& kp, const FwdArgs& a, int nd, int nr) {
+template <int TD, int TR, int WARPS, int ENT, int MAXR, bool COUNT>
+static void launch2c(const Tree& t, const KParams& kp, const FwdArgs& a, int nd, int nr) {
   constexpr int F4 = TD + TR / 4;
   const size_t smem = (size_t)WARPS * (ENT * 32 + ENT * F4 + DPL_STACK_PER_WARP / 2) * 16;
   static bool attr = false;
   if (!attr) {
-    DPL_CUDA(cudaFuncSetAttribute(k_forward2<TD, TR, WARPS, ENT, MINB>,
+    DPL_CUDA(cudaFuncSetAttribute(k_forward2<TD, TR, WARPS, ENT, MAXR, COUNT>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
   unsigned blocks = (unsigned)((a.q + WARPS * 32 - 1) / (WARPS * 32));
-  k_forward2<TD, TR, WARPS, ENT, MINB><<<blocks, WARPS * 32, smem, t.stream>>>(
-      t.view(), kp, a.xs, a.perm, a.q, nd, nr, t.chmap.as<int>(), a.out, a.out_stride,
-      a.overflow);
+  k_forward2<TD, TR, WARPS, ENT, MAXR, COUNT><<<blocks, WARPS * 32, smem, t.stream>>>(
+      t.view(), kp, a.xs, a.perm, a.q, nd, nr, t.chmap.as<int>(), a.out, a.out_stride, a.only_ch,
+      a.counters, a.overflow);
   count_launch();
+}
+
+template <int TD, int TR, int WARPS, int ENT, int MAXR = 128>
+static void launch2(const Tree& t, const KParams& kp, const FwdArgs& a, int nd, int nr) {
+  if (a.counters)
+    launch2c<TD, TR, WARPS, ENT, MAXR, true>(t, kp, a, nd, nr);
+  else
+    launch2c<TD, TR, WARPS, ENT, MAXR, false>(t, kp, a, nd, nr);
 }
 
 static int tune_choice(const char* env) {
@@ -209,7 +239,7 @@ static int tune_choice(const char* env) {
 // equal the tree's (one dipole slot + PR radial floats). Returns false when
 // not covered (the caller falls back to the single-phase kernels).
 bool forward2_launch(const Tree& t, const KParams& kp, const FwdArgs& a) {
-  if (a.grad_mode != 0 || a.counters || a.single) return false;
+  if (a.grad_mode != 0 || (a.single && a.only_ch < 0)) return false;
   if (t.Cd != 1) return false;
   const int nr = a.nr_limit >= 0 ? std::min(a.nr_limit, t.Cr) : t.Cr;
   constexpr int W = 4, E = 16;

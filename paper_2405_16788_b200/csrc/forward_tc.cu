@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
     k_forward_tc(TreeView tv, KParams kp, const double* __restrict__ xs,
                  const int32_t* __restrict__ perm, int64_t q, int nr,
                  const int* __restrict__ chmap, float* __restrict__ out, int out_stride,
-                 long long* __restrict__ counters, int* overflow) {
+                 int only_ch, long long* __restrict__ counters, int* overflow) {
   static_assert(ENT % 8 == 0, "ENT must be a multiple of the mma K (8)");
   constexpr int TR = 8 * NT;
   constexpr int F4 = 1 + TR / 4;               // global row float4 (dipole + radial)
@@ -236,7 +236,11 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
   }
   if (nent) evaluate();
   // outputs: the dipole value is lane-local; radial values live in mma C fragments
-  if (valid) out[qi * out_stride + __ldg(chmap)] = accd;
+  if (only_ch >= 0) {  // primal_channel: same kernel as primal, one column stored
+    if (valid && __ldg(chmap) == only_ch) out[qi] = accd;
+  } else if (valid) {
+    out[qi * out_stride + __ldg(chmap)] = accd;
+  }
 #pragma unroll
   for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
@@ -249,7 +253,13 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
           const int col = 8 * nt + 2 * tq + u;
-          if (vr && col < nr) out[qr * out_stride + __ldg(chmap + 1 + col)] = acc[mt][nt][2 * h + u];
+          if (vr && col < nr) {
+            const int ch = __ldg(chmap + 1 + col);
+            if (only_ch < 0)
+              out[qr * out_stride + ch] = acc[mt][nt][2 * h + u];
+            else if (ch == only_ch)
+              out[qr] = acc[mt][nt][2 * h + u];
+          }
         }
     }
 }
@@ -268,8 +278,8 @@ static void launch_tc1(const Tree& t, const KParams& kp, const FwdArgs& a, int n
   }
   unsigned blocks = (unsigned)((a.q + WARPS * 32 - 1) / (WARPS * 32));
   k_forward_tc<NT, WARPS, ENT, MAXR, COUNT><<<blocks, WARPS * 32, smem, t.stream>>>(
-      t.view(), kp, a.xs, a.perm, a.q, nr, t.chmap.as<int>(), a.out, a.out_stride, a.counters,
-      a.overflow);
+      t.view(), kp, a.xs, a.perm, a.q, nr, t.chmap.as<int>(), a.out, a.out_stride, a.only_ch,
+      a.counters, a.overflow);
   count_launch();
 }
 
@@ -283,7 +293,7 @@ static void launch_tc(const Tree& t, const KParams& kp, const FwdArgs& a, int nr
 
 // Tensor-core plan: one dipole slot and PR a multiple of 8 (8..64 radial).
 bool forward_tc_launch(const Tree& t, const KParams& kp, const FwdArgs& a) {
-  if (a.grad_mode != 0 || a.single) return false;
+  if (a.grad_mode != 0 || (a.single && a.only_ch < 0)) return false;
   if (t.Cd != 1 || t.PR % 8 != 0) return false;
   const int nr = a.nr_limit >= 0 ? std::min(a.nr_limit, t.Cr) : t.Cr;
   const char* v = getenv("DPL_TUNE_TC");
