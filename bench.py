@@ -48,7 +48,8 @@ def parse():
     ap.add_argument("--scale", type=float, default=1.0, help="shrink N and Q (development only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--cpu-budget", type=float, default=30.0, help="seconds of CPU baseline work")
+    ap.add_argument("--cpu-sample", type=int, default=400_000,
+                    help="queries per reference CPU sample (bounded: ~20 s on 16 cores)")
     return ap.parse_args()
 
 
@@ -129,7 +130,7 @@ def flops_model(tot, Cd, Cr):
 
 
 # ------------------------------------------------------------------ reference arm
-def reference_measure(w, eps, budget_s, steps=None, warmup=0, threads=None):
+def reference_measure(w, eps, sample, steps=None, warmup=0, threads=None):
     """Reference CPU path (oracle/_ref): DipoleTree::primal over a query sample with
     parallel_for, adjoint with one GradientBuffer per worker, flush_gradients."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
@@ -174,16 +175,13 @@ def reference_measure(w, eps, budget_s, steps=None, warmup=0, threads=None):
     # single-threaded flush_gradients (bhtree.cpp:419-459). Calibrate it with a
     # tiny batch, then time bounded samples and extrapolate the FULL workload's
     # step (Q forward + Q adjoint + one flush) — amortising the fixed cost over
-    # Q queries, i.e. the reference's best case.
+    # Q queries, i.e. the reference's best case. The sample is a fixed-size
+    # prefix of the workload's queries (bounded CPU time, not the whole step).
     Q = xs_all.shape[0]
     q0 = 256
     _, fixed = one(q0)
     n_steps = 1 if steps is None else steps + warmup
-    per_step = budget_s / max(1, n_steps)
-    qc = 4000
-    tf_c, ta_c = one(qc)
-    per_q = max(1e-9, (tf_c + max(0.0, ta_c - fixed)) / qc)
-    sample = int(min(Q, max(qc, (per_step - fixed) / per_q)))
+    sample = int(min(Q, max(q0 * 4, sample)))
     times = []
     for i in range(n_steps):
         tf, ta = one(sample)
@@ -222,8 +220,11 @@ def run_reference(args):
     eps = W.epsilon_for("config2", args.scale)
     # >= 25 s per step: the adjoint's fixed cost (~14 s of GradientBuffer
     # allocation + flush on 16 workers) must not dominate the per-query fit
-    budget = 25.0 * (args.steps + args.warmup)
-    r = reference_measure(w, eps, budget, steps=args.steps, warmup=args.warmup)
+    # each reference step pays ~14 s of per-call GradientBuffer setup + flush on
+    # config 2; shrink the per-step sample for long runs so the arm stays bounded
+    n = args.steps + args.warmup
+    sample = args.cpu_sample if n <= 8 else max(50_000, args.cpu_sample * 8 // n)
+    r = reference_measure(w, eps, sample, steps=args.steps, warmup=args.warmup)
     sample_desc = (f"{r['sample']} of {w['xs'].shape[0]} config-2 queries timed per step (forward + "
                    f"adjoint + flush, {r['adjoint_workers']} GradientBuffers); full-workload step "
                    f"extrapolated as Q*t_query + fixed flush cost; reference sources compiled -O3 "
@@ -343,6 +344,11 @@ def run_ours(args):
         mom_h = torch.empty((N, C), dtype=torch.float32).pin_memory()
         nrm_h = torch.empty((N, 3), dtype=torch.float32).pin_memory()
 
+        # host-async mode: primal/adjoint return once queued, so the d_out H2D
+        # overlaps the forward kernel and the out D2H overlaps the adjoint;
+        # flush_gradients synchronizes every stream (all host results complete)
+        tree.set_host_async(True)
+
         def step_host():
             tree.primal(xs_h, params, BETA, out=out_h)
             tree.adjoint(xs_h, params, BETA, do_h, None, buf)
@@ -363,6 +369,7 @@ def run_ours(args):
             step_host()
         torch.cuda.synchronize()
         e2e_s = (time.perf_counter() - t0) / k2
+        tree.set_host_async(False)
         t_t = torch.tensor([e2e_s], device=dev)
         if dist is not None:
             dist.all_reduce(t_t, op=dist.ReduceOp.MAX)
@@ -371,7 +378,8 @@ def run_ours(args):
         d2h = Q * C * 4 + N * C * 4 + N * 12 + 8
         e2e = {"value": world * Q / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": 1e3 * e2e_s,
-               "timing": "wall clock around synchronous public-API calls (pinned host buffers)"}
+               "timing": "wall clock around public-API calls on pinned host buffers (host-async "
+                         "mode; flush_gradients synchronizes, all results on the host)"}
 
     if rank != 0:
         if dist is not None:
@@ -389,7 +397,7 @@ def run_ours(args):
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         try:
-            r = reference_measure(w, eps, args.cpu_budget)
+            r = reference_measure(w, eps, args.cpu_sample)
             cpu = {"value": r["value"], "unit": UNIT, "cores": r["cores"], "kind": "reference",
                    "sample": f"{r['sample']} config-2 queries timed (forward + adjoint + "
                              f"flush, {r['adjoint_workers']} GradientBuffers), full 4M-query "

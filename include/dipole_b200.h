@@ -72,6 +72,14 @@ int dpl_tree_create(int device, void* stream, dpl_tree_t* out);
 int dpl_tree_destroy(dpl_tree_t tree);
 int dpl_tree_set_stream(dpl_tree_t tree, void* stream);
 int dpl_tree_sync(dpl_tree_t tree);
+/* Host-async mode (default off). When on, dpl_primal / dpl_primal_channel /
+ * dpl_adjoint calls on large HOST batches return as soon as their work is
+ * queued: inputs are copied host->device on a copy stream (the next call's
+ * H2D overlaps the current kernels) and host outputs device->host on a second
+ * copy stream. Host inputs must stay unchanged and host outputs unread until
+ * dpl_tree_sync() or dpl_flush() (which synchronizes everything) returns; use
+ * pinned host memory for real overlap. Off: every call is synchronous. */
+int dpl_tree_set_host_async(dpl_tree_t tree, int on);
 
 /* DipoleTree::build (bhtree.cpp:158-169): GPU Morton-digit sort + level-by-level
  * BFS numbering reproduces build_structure (:36-105) bit-exactly; geometry

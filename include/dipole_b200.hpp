@@ -197,6 +197,9 @@ class DipoleTree {
   PointGradients flush_gradients(GradientBuffer& b) const { return flush_gradients({&b}); }
 
   void dump(const std::string& path) const { check(dpl_tree_dump(h_, path.c_str())); }
+  // host-async mode: see dpl_tree_set_host_async
+  void set_host_async(bool on) { check(dpl_tree_set_host_async(h_, on ? 1 : 0)); }
+  void synchronize() const { check(dpl_tree_sync(h_)); }
   dpl_tree_t handle() const { return h_; }
 
  private:

@@ -63,6 +63,7 @@ _sig = {
     "dpl_tree_destroy": (C.c_int, [_vp]),
     "dpl_tree_set_stream": (C.c_int, [_vp, _vp]),
     "dpl_tree_sync": (C.c_int, [_vp]),
+    "dpl_tree_set_host_async": (C.c_int, [_vp, C.c_int]),
     "dpl_tree_build": (C.c_int, [_vp, _vp, _vp, _vp, _vp, C.c_int64, C.c_int32, C.c_int32,
                                  C.c_int32]),
     "dpl_tree_update_moments": (C.c_int, [_vp, _vp, _vp, _vp, _vp, C.c_int64, C.c_int32]),

@@ -129,6 +129,8 @@ class DipoleTree:
         self.device = device
         self._built = False
         self._kinds = None
+        self._async = False
+        self._keep = []  # host arrays in flight (host-async mode)
 
     def __del__(self):
         if getattr(self, "_h", None):
@@ -144,6 +146,20 @@ class DipoleTree:
 
     def synchronize(self):
         check(lib().dpl_tree_sync(self._h))
+        self._keep.clear()
+
+    def set_host_async(self, on: bool):
+        """Host-async mode (dpl_tree_set_host_async): primal / adjoint on host
+        batches return once queued; results are valid after synchronize() or
+        flush_gradients(). Inputs must not be modified before then."""
+        check(lib().dpl_tree_set_host_async(self._h, 1 if on else 0))
+        self._async = bool(on)
+        if not on:
+            self._keep.clear()
+
+    def _hold(self, *objs):
+        if self._async:
+            self._keep.append(objs)
 
     # -- build / moments ---------------------------------------------------------
     def build(self, cloud: OrientedPointCloud, max_leaf_size=kDefaultMaxLeafSize,
@@ -244,6 +260,7 @@ class DipoleTree:
         if visited:
             cp, cnt = _out_like(xk, (q, 5), np.int64)
         check(lib().dpl_primal(self._h, C.byref(params), float(beta_bh), xp, q, op, None, cp))
+        self._hold(xk, out)
         return (out, cnt) if visited else out
 
     def primal_channel(self, xs, params: KernelParams, beta_bh: float, channel: int):
@@ -253,6 +270,7 @@ class DipoleTree:
         op, out = _out_like(xk, (q,), np.float32)
         check(lib().dpl_primal_channel(self._h, C.byref(params), float(beta_bh), xp, q,
                                        int(channel), op))
+        self._hold(xk, out)
         return out
 
     def primal_with_gradient(self, xs, params: KernelParams, beta_bh: float):
@@ -288,6 +306,7 @@ class DipoleTree:
         dp, k2 = _in(d_out, np.float32, (q, Cc))
         gp, k3 = _in(d_grad, np.float32, (q, Cc, 3)) if d_grad is not None else (None, None)
         check(lib().dpl_adjoint(self._h, C.byref(params), float(beta_bh), xp, q, dp, gp, buf._h))
+        self._hold(k1, k2, k3)
         buf.dirty = True
 
     def flush_gradients(self, buffers, device_out=None, out=None) -> PointGradients:
@@ -312,6 +331,7 @@ class DipoleTree:
             mp, np_ = mom.ctypes.data, nrm.ctypes.data
         de = C.c_double()
         check(lib().dpl_flush(self._h, arr, len(buffers), mp, np_, C.byref(de)))
+        self._keep.clear()  # dpl_flush synchronizes every stream of the handle
         for b in buffers:
             b.dirty = False
         return PointGradients(Cc, mom, nrm, de.value)

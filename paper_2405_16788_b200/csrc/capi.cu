@@ -32,10 +32,23 @@ struct dpl_tree_s {
   Tree t;
   bool built = false;
   DevBuf ws_xs, ws_perm, ws_out, ws_grad, ws_cnt, ws_morton, ws_dout, ws_dgrad, ws_flag, ws_mom,
-      ws_nrm;
+      ws_nrm, ws_xs_adj;
   cudaStream_t copy = nullptr, copy_out = nullptr;  // host<->device pipeline streams
   std::vector<cudaEvent_t> pipe_ev;                 // chunk hand-off events
+  // host-async mode (dpl_tree_set_host_async): staging-buffer hazards between
+  // calls are tracked with events instead of a synchronize per call
+  bool host_async = false;
+  cudaEvent_t ev_fwd_in = nullptr, ev_fwd_out = nullptr, ev_adj_in = nullptr;
+  void sync_all() {
+    if (copy) DPL_CUDA(cudaStreamSynchronize(copy));
+    if (copy_out) DPL_CUDA(cudaStreamSynchronize(copy_out));
+    DPL_CUDA(cudaStreamSynchronize(t.stream));
+  }
   ~dpl_tree_s() {
+    if (copy) cudaStreamSynchronize(copy);
+    if (copy_out) cudaStreamSynchronize(copy_out);
+    for (cudaEvent_t e : {ev_fwd_in, ev_fwd_out, ev_adj_in})
+      if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : pipe_ev) cudaEventDestroy(e);
     if (copy) cudaStreamDestroy(copy);
     if (copy_out) cudaStreamDestroy(copy_out);
@@ -200,10 +213,18 @@ int dpl_tree_destroy(dpl_tree_t h) {
   });
 }
 
+int dpl_tree_set_host_async(dpl_tree_t h, int on) {
+  return guard([&] {
+    require(h != nullptr, DPL_ERR_USAGE, "null tree handle");
+    if (!on) h->sync_all();
+    h->host_async = on != 0;
+  });
+}
+
 int dpl_tree_set_stream(dpl_tree_t h, void* stream) {
   return guard([&] {
     require(h != nullptr, DPL_ERR_USAGE, "null tree handle");
-    DPL_CUDA(cudaStreamSynchronize(h->t.stream));
+    h->sync_all();
     if (h->t.own_stream) cudaStreamDestroy(h->t.stream);
     h->t.own_stream = false;
     h->t.stream = (cudaStream_t)stream;
@@ -213,7 +234,7 @@ int dpl_tree_set_stream(dpl_tree_t h, void* stream) {
 int dpl_tree_sync(dpl_tree_t h) {
   return guard([&] {
     require(h != nullptr, DPL_ERR_USAGE, "null tree handle");
-    DPL_CUDA(cudaStreamSynchronize(h->t.stream));
+    h->sync_all();
     if (h->ws_flag.p) check_overflow(h);
   });
 }
@@ -377,17 +398,29 @@ static cudaEvent_t pipe_event(dpl_tree_t h, size_t i) {
   return h->pipe_ev[i];
 }
 
+static cudaEvent_t& hazard_event(cudaEvent_t& e) {
+  if (!e) DPL_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  return e;
+}
+
+// in_free: recorded on the compute stream after the last kernel that read this
+// call kind's input staging buffers; out_free: recorded on the D2H stream after
+// the last copy out of its output staging buffers. Waiting on them (instead of
+// on the whole compute stream) lets the H2D of the next call's inputs overlap
+// the current kernels. Synchronous unless the handle is in host-async mode.
 template <typename F>
 static void run_chunked(dpl_tree_t h, int64_t q, int64_t chunk, const std::vector<HostSeg>& ins,
-                        const std::vector<HostSeg>& outs, F&& body) {
+                        const std::vector<HostSeg>& outs, cudaEvent_t& in_free,
+                        cudaEvent_t* out_free, F&& body) {
   // inputs and outputs use separate copy streams so H2D of later chunks never
   // queues behind D2H of earlier ones (both copy engines run concurrently)
   cudaStream_t cin = copy_stream(h, 0), cout = copy_stream(h, 1), ks = h->t.stream;
   int64_t nchunks = (q + chunk - 1) / chunk;
-  // the compute stream may still be using the device staging buffers
-  cudaEvent_t start = pipe_event(h, 0);
-  DPL_CUDA(cudaEventRecord(start, ks));
-  DPL_CUDA(cudaStreamWaitEvent(cin, start, 0));
+  // previous readers of the input staging buffers must be done
+  DPL_CUDA(cudaStreamWaitEvent(cin, hazard_event(in_free), 0));
+  // device-resident inputs (and everything else queued before this call on the
+  // compute stream) stay ordered: the kernels run on the compute stream itself
+  if (out_free && !outs.empty()) DPL_CUDA(cudaStreamWaitEvent(ks, hazard_event(*out_free), 0));
   for (int64_t c = 0; c < nchunks; ++c) {
     const int64_t c0 = c * chunk, qc = std::min(chunk, q - c0);
     for (const HostSeg& s : ins)
@@ -408,8 +441,12 @@ static void run_chunked(dpl_tree_t h, int64_t q, int64_t chunk, const std::vecto
                                  qc * s.row_bytes, cudaMemcpyDeviceToHost, cout));
     }
   }
-  DPL_CUDA(cudaStreamSynchronize(cout));
-  DPL_CUDA(cudaStreamSynchronize(ks));
+  DPL_CUDA(cudaEventRecord(in_free, ks));
+  if (out_free && !outs.empty()) DPL_CUDA(cudaEventRecord(*out_free, cout));
+  if (!h->host_async) {
+    DPL_CUDA(cudaStreamSynchronize(cout));
+    DPL_CUDA(cudaStreamSynchronize(ks));
+  }
 }
 
 // Default: ONE chunk. Measured on config 2 (4M uniform queries): Morton-sorting
@@ -463,7 +500,8 @@ static int forward_common(dpl_tree_t h, const dpl_kernel_params* params, double 
       if (out_host) outs.push_back({(const char*)out_d, (char*)out, (size_t)stride * 4});
       if (grad_host) outs.push_back({(const char*)grad_d, (char*)grad, (size_t)gstride * 4});
       int* ovf = overflow_flag(h);
-      run_chunked(h, q, pipe_chunk(q), ins, outs, [&](int64_t c0, int64_t qc) {
+      run_chunked(h, q, pipe_chunk(q), ins, outs, h->ev_fwd_in, &h->ev_fwd_out,
+                  [&](int64_t c0, int64_t qc) {
         int32_t* perm = h->ws_perm.as<int32_t>() + c0;
         {
           PhaseTimer pt(t, PH_SORT);
@@ -491,9 +529,10 @@ static int forward_common(dpl_tree_t h, const dpl_kernel_params* params, double 
         forward_launch(t, kp, a);
       });
       DPL_CUDA(cudaGetLastError());
-      check_overflow(h);
+      if (!h->host_async) check_overflow(h);  // async: reported by dpl_tree_sync
       return;
     }
+    if (h->host_async) h->sync_all();  // the staged path below is synchronous
     const double* xs_d = stage_in(t, xs, (size_t)q * 3, h->ws_xs);
     h->ws_perm.reserve(q * 4);
     {
@@ -625,9 +664,9 @@ int dpl_adjoint(dpl_tree_t h, const dpl_kernel_params* params, double beta_bh, c
       const float* dout_d = d_out;
       const float* dg_d = d_grad;
       std::vector<HostSeg> ins;
-      if (xs_host) {
-        h->ws_xs.reserve(q * 24);
-        xs_d = h->ws_xs.as<double>();
+      if (xs_host) {  // own staging buffer: may fill while the forward still runs
+        h->ws_xs_adj.reserve(q * 24);
+        xs_d = h->ws_xs_adj.as<double>();
         ins.push_back({(const char*)xs, (char*)xs_d, 24});
       }
       if (do_host) {
@@ -641,7 +680,8 @@ int dpl_adjoint(dpl_tree_t h, const dpl_kernel_params* params, double beta_bh, c
         ins.push_back({(const char*)d_grad, (char*)dg_d, (size_t)t.C * 12});
       }
       int* ovf = overflow_flag(h);
-      run_chunked(h, q, pipe_chunk(q), ins, {}, [&](int64_t c0, int64_t qc) {
+      run_chunked(h, q, pipe_chunk(q), ins, {}, h->ev_adj_in, nullptr,
+                  [&](int64_t c0, int64_t qc) {
         int32_t* perm = h->ws_perm.as<int32_t>() + c0;
         {
           PhaseTimer pt(t, PH_SORT);
@@ -662,6 +702,7 @@ int dpl_adjoint(dpl_tree_t h, const dpl_kernel_params* params, double beta_bh, c
       DPL_CUDA(cudaGetLastError());
       return;
     }
+    if (h->host_async) h->sync_all();
     const double* xs_d = stage_in(t, xs, (size_t)q * 3, h->ws_xs);
     const float* dout_d = stage_in(t, d_out, (size_t)q * t.C, h->ws_dout);
     const float* dg_d = d_grad ? stage_in(t, d_grad, (size_t)q * t.C * 3, h->ws_dgrad) : nullptr;
@@ -710,7 +751,7 @@ int dpl_flush(dpl_tree_t h, dpl_gradbuf_t* bufs, int32_t nbuf, float* moments, f
     mo.finish(t);
     no.finish(t);
     for (int i = 0; i < nbuf; ++i) gradbuf_zero(bufs[i]->b, t.stream);  // reset() (:438)
-    DPL_CUDA(cudaStreamSynchronize(t.stream));
+    h->sync_all();  // also completes host-async outputs of earlier calls
     if (d_epsilon) *d_epsilon = de;
   });
 }

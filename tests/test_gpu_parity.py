@@ -351,3 +351,26 @@ def test_host_pointer_pipeline_matches_device_path(eng, oracle_mod):
     t.adjoint(torch.from_numpy(xs).cuda(), p, 2.0, torch.from_numpy(d_out).cuda(), None, b2)
     g1, g2 = t.flush_gradients(b1), t.flush_gradients(b2)
     assert rel_scale_err(g1.moments, g2.moments) < 1e-6
+
+    # host-async mode: same kernels, results complete at flush / synchronize;
+    # pinned and pageable host buffers, back-to-back steps reusing the staging
+    pin_x = torch.from_numpy(xs).pin_memory()
+    pin_d = torch.from_numpy(d_out).pin_memory()
+    pin_o = torch.empty((q, C), dtype=torch.float32).pin_memory()
+    t.set_host_async(True)
+    try:
+        for xs_in, do_in, out_in in ((pin_x, pin_d, pin_o), (xs, d_out, None)):
+            for _ in range(2):
+                o = t.primal(xs_in, p, 2.0, out=out_in)
+                b3 = t.make_buffer()
+                t.adjoint(xs_in, p, 2.0, do_in, None, b3)
+                g3 = t.flush_gradients(b3)
+                o = o.numpy() if hasattr(o, "numpy") else o
+                assert np.array_equal(o, host)
+                assert np.array_equal(g3.moments, g1.moments)
+                assert np.array_equal(g3.normals, g1.normals)
+        o = t.primal(xs, p, 2.0)
+        t.synchronize()
+        assert np.array_equal(o, host)
+    finally:
+        t.set_host_async(False)
