@@ -21,12 +21,53 @@
 //     channel. The 4 per-lane vector quantities are reduced with one LDS.128,
 //     3 FADD and 3 shuffles and land in node_v / point_n / point_mu_0 with at
 //     most 4 REDs. Accumulators are fp64 (SURVEY §7 hard part 4).
+//   tensor-core phase B (MT > 0, the default for Cr <= 64): the radial product
+//     D[channel][entry] = sum_l dsT[channel][l] wR[entry][l] (and its epsilon
+//     twin with wE) runs on mma.sync: A = the warp's transposed d_out tile,
+//     held as TF32 fragments in registers for the whole traversal (16 MT
+//     registers, the same budget as the FFMA tile) with its low part as BF16
+//     fragments in shared memory; B = the batch's weights. Three-term split
+//     A_hi B_hi + A_hi B_lo (TF32) + A_lo B_hi (BF16): per-product error
+//     ~2^-19 relative, fp32-class. The epilogue REDs 8 consecutive channels of
+//     4 entries per instruction (8 sectors per 32 lanes, as the FFMA path).
 #include "adjoint.cuh"
 #include "traverse.cuh"
 
 namespace dpl {
 
 namespace {
+__device__ __forceinline__ uint32_t to_tf32(float a) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(r) : "f"(a));
+  return r;
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo_col, float hi_col) {
+  uint32_t r;  // lower 16 bits: the smaller k index
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;\n" : "=r"(r) : "f"(hi_col), "f"(lo_col));
+  return r;
+}
+__device__ __forceinline__ void mma_tf32(float (&c)[4], const uint32_t (&a)[4], uint32_t b0,
+                                         uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};\n"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ void mma_bf16(float (&c)[4], const uint4& a, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};\n"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b0), "r"(b1));
+}
+// smallest stride >= n floats with stride = 8 or 24 (mod 32): conflict-free
+// fragment gathers from a [32][stride] tile
+constexpr int tile_stride(int n) {
+  int r = n;
+  while (r % 32 != 8 && r % 32 != 24) ++r;
+  return r;
+}
 __device__ __forceinline__ void cp_async16(uint32_t smem, const void* gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(smem), "l"(gmem));
 }
@@ -66,30 +107,48 @@ struct Adj2Ptrs {
   double* d_eps;
 };
 
-// NB: 0 -> Cr <= 32; 1 -> 32 < Cr <= 48 (split); 2 -> Cr <= 64.
+// Per-warp shared-memory layout. The d_out tile staged by the tensor-core
+// prologue aliases the batch arrays (it is consumed before the first entry).
+template <int MT, int ENT, int RR>
+struct AdjLayout {
+  static constexpr int WS = MT ? 36 : 32;  // weight row stride: conflict-free B gathers
+  static constexpr int F4 = 1 + RR;        // smem row capacity (float4)
+  static constexpr int S = tile_stride(16 * (MT ? MT : 1));
+  static constexpr int BATCH = ENT * WS * 2 + ENT * 128 + ENT * F4 * 4;
+  static constexpr int TILE = MT ? 32 * S : 0;
+  static constexpr int UNION = BATCH > TILE ? BATCH : TILE;
+  static constexpr int ALO = MT * 2 * 32 * 4;  // BF16 A_lo fragments (uint32 words)
+  static constexpr int WARP_FLOATS = (UNION + ALO + ENT + (ENT & 1) + 2 * DPL_STACK_PER_WARP + 3) & ~3;
+};
+
+// NB: 0 -> Cr <= 32; 1 -> 32 < Cr <= 48 (split); 2 -> Cr <= 64 (FFMA phase B).
+// MT: > 0 selects the tensor-core phase B with MT m-tiles (Cr <= 16 MT); NB unused.
 // GM: 0 no d_grad; 1 d_grad q x dstride x 3; 2 d_grad q x 3 (channel 0).
 // MAXR: register cap (occupancy vs. spills; chosen by measurement)
-template <int NB, int GM, int WARPS, int ENT, int RR, int MAXR = 128>
+template <int NB, int GM, int WARPS, int ENT, int RR, int MAXR = 128, int MT = 0>
 __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
     k_adjoint2(TreeView tv, KParams kp, const double* __restrict__ xs,
                const int32_t* __restrict__ perm, int64_t q, const float* __restrict__ d_out,
                int dstride, const float* __restrict__ d_grad, int nr,
                const int* __restrict__ chmap, Adj2Ptrs acc, int* overflow) {
-  constexpr int F4 = 1 + RR;  // smem row capacity: [dipole float4 | up to RR radial float4]
-  // per-warp shared layout (floats): wR[ENT][32] wE[ENT][32] vq[ENT][4][32]
-  //                                  rows[ENT][F4*4] meta[ENT] stack[2*STACK]
-  constexpr int WARP_FLOATS = ENT * 32 * 6 + ENT * F4 * 4 + ENT + 2 * DPL_STACK_PER_WARP;
+  using L = AdjLayout<MT, ENT, RR>;
+  constexpr int F4 = L::F4;
+  constexpr int WS = L::WS;
+  static_assert(MT == 0 || ENT == 8, "tensor-core phase B uses one n-tile of 8 entries");
   extern __shared__ float4 smem_f4[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  float* base = reinterpret_cast<float*>(smem_f4) + (size_t)w * ((WARP_FLOATS + 3) & ~3);
+  const int g = lane >> 2, tq = lane & 3;  // mma fragment coordinates
+  float* base = reinterpret_cast<float*>(smem_f4) + (size_t)w * L::WARP_FLOATS;
   float* wR = base;
-  float* wE = wR + ENT * 32;
-  float* vq = wE + ENT * 32;
+  float* wE = wR + ENT * WS;
+  float* vq = wE + ENT * WS;
   float4* rows = reinterpret_cast<float4*>(vq + ENT * 128);
-  int* meta = reinterpret_cast<int*>(rows + ENT * F4);
+  const uint4* alo = reinterpret_cast<const uint4*>(base + L::UNION);
+  int* meta = reinterpret_cast<int*>(base + L::UNION + L::ALO);
   int2* stk = reinterpret_cast<int2*>(meta + ENT + (ENT & 1));
   const uint32_t s_rows = smem_u32(rows) + 16u * lane;
-  const int F4g = tv.F4;  // global row stride (<= F4)
+  const int F4g = tv.F4;               // global row stride
+  const int F4c = F4g < F4 ? F4g : F4;  // float4 staged per row (dipole + radial slots used)
 
   const int64_t sidx = ((int64_t)blockIdx.x * WARPS + w) * 32 + lane;
   const bool valid = sidx < q;
@@ -104,6 +163,8 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
   if (!active) return;
   const int Cr = tv.Cr;
   const QueryDF qx = make_qdf(x);
+  // fp64 position for the exact fallbacks, re-read there (invalid lanes never test)
+  const double* xq = xs + 3 * qi;
 
   // own-query dipole upstream gradients (channel slot 0)
   const int ch0 = __ldg(chmap);
@@ -113,94 +174,207 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
     const float* g = GM == 1 ? d_grad + (qi * dstride + ch0) * 3 : d_grad + qi * 3;
     dg0 = g[0], dg1 = g[1], dg2 = g[2];
   }
-  // transposed radial tile
-  float colA[32];
-  float colB[NB == 2 ? 32 : (NB == 1 ? 16 : 1)];
+  // FFMA phase B: transposed radial tile in registers (lanes = channels)
+  constexpr bool FF = MT == 0;
+  float colA[FF ? 32 : 1];
+  float colB[FF ? (NB == 2 ? 32 : (NB == 1 ? 16 : 1)) : 1];
   const bool okA = lane < nr;
-  const int chA = okA ? __ldg(chmap + 1 + lane) : 0;
   const int slotB = NB == 1 ? 32 + (lane & 15) : 32 + lane;
-  const bool okB = NB > 0 && slotB < nr;
-  const int chB = okB ? __ldg(chmap + 1 + slotB) : 0;
+  const bool okB = FF && NB > 0 && slotB < nr;
+  // tensor-core phase B: A = d_out tile^T [channel][query] as TF32 fragments
+  uint32_t ahi[MT ? MT : 1][4][4];
+  if constexpr (FF) {
+    const int chA = okA ? __ldg(chmap + 1 + lane) : 0;
+    const int chB = okB ? __ldg(chmap + 1 + slotB) : 0;
 #pragma unroll
-  for (int l = 0; l < 32; ++l) {
-    const int64_t ql = __shfl_sync(FULL_MASK, qi, l);
-    const bool vl = (active >> l) & 1u;
-    colA[l] = (okA && vl) ? __ldg(d_out + ql * dstride + chA) : 0.f;
-    if (NB == 2) colB[l] = (okB && vl) ? __ldg(d_out + ql * dstride + chB) : 0.f;
-  }
-  if (NB == 1) {
-    const int h = lane >> 4;
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const int l = 16 * h + i;
-      const int64_t ql = __shfl_sync(FULL_MASK, qi, l);  // all lanes participate
+    for (int l = 0; l < 32; ++l) {
+      const int64_t ql = __shfl_sync(FULL_MASK, qi, l);
       const bool vl = (active >> l) & 1u;
-      colB[i] = (okB && vl) ? __ldg(d_out + ql * dstride + chB) : 0.f;
+      colA[l] = (okA && vl) ? __ldg(d_out + ql * dstride + chA) : 0.f;
+      if (NB == 2) colB[l] = (okB && vl) ? __ldg(d_out + ql * dstride + chB) : 0.f;
     }
+    if (NB == 1) {
+      const int h = lane >> 4;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int l = 16 * h + i;
+        const int64_t ql = __shfl_sync(FULL_MASK, qi, l);  // all lanes participate
+        const bool vl = (active >> l) & 1u;
+        colB[i] = (okB && vl) ? __ldg(d_out + ql * dstride + chB) : 0.f;
+      }
+    }
+  } else {
+    // coalesced staging of the tile T[query l][slot c] (c < 16 MT), then
+    // fragment gathers (stride S = 8 or 24 mod 32: conflict-free)
+    constexpr int S = L::S;
+    float* T = base;
+    const int c1 = lane + 32;
+    const int chm0 = lane < nr ? __ldg(chmap + 1 + lane) : 0;
+    const int chm1 = (16 * MT > 32 && c1 < nr) ? __ldg(chmap + 1 + c1) : 0;
+    for (int l = 0; l < 32; ++l) {
+      const int64_t ql = __shfl_sync(FULL_MASK, qi, l);
+      const bool vl = (active >> l) & 1u;
+      if (lane < 16 * MT)
+        T[l * S + lane] = (vl && lane < nr) ? __ldg(d_out + ql * dstride + chm0) : 0.f;
+      if (16 * MT > 32 && c1 < 16 * MT)
+        T[l * S + c1] = (vl && c1 < nr) ? __ldg(d_out + ql * dstride + chm1) : 0.f;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int mt = 0; mt < (MT ? MT : 1); ++mt)
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) {
+        const float* t0 = T + (8 * ks + tq) * S + 16 * mt + g;  // A[g][tq] = T[q][ch]
+        ahi[mt][ks][0] = to_tf32(t0[0]);
+        ahi[mt][ks][1] = to_tf32(t0[8]);
+        ahi[mt][ks][2] = to_tf32(t0[4 * S]);
+        ahi[mt][ks][3] = to_tf32(t0[4 * S + 8]);
+      }
+    auto lo = [](float v) { return v - __uint_as_float(to_tf32(v)); };
+    uint4* alo_w = reinterpret_cast<uint4*>(base + L::UNION);
+#pragma unroll
+    for (int mt = 0; mt < (MT ? MT : 1); ++mt)
+#pragma unroll
+      for (int ks2 = 0; ks2 < 2; ++ks2) {
+        const float* u0 = T + (16 * ks2 + 2 * tq) * S + 16 * mt + g;
+        uint4 a;
+        a.x = pack_bf16(lo(u0[0]), lo(u0[S]));               // (g,   2tq | 2tq+1)
+        a.y = pack_bf16(lo(u0[8]), lo(u0[S + 8]));           // (g+8, 2tq | 2tq+1)
+        a.z = pack_bf16(lo(u0[8 * S]), lo(u0[9 * S]));       // (g,   2tq+8 | +9)
+        a.w = pack_bf16(lo(u0[8 * S + 8]), lo(u0[9 * S + 8]));
+        alo_w[(mt * 2 + ks2) * 32 + lane] = a;
+      }
+    __syncwarp();  // the tile region becomes the batch arrays
   }
   double eps_acc = 0.0;
   int nent = 0;
 
+  // D[slot][entry] += A . W^T over the 32 queries for a batch of <= 8 entries
+  // (columns >= nent hold stale weights; they only reach columns never read)
+  auto tc_product = [&](const float* wbase, float (&d)[MT ? MT : 1][4]) {
+#pragma unroll
+    for (int mt = 0; mt < (MT ? MT : 1); ++mt) d[mt][0] = d[mt][1] = d[mt][2] = d[mt][3] = 0.f;
+    const float* wrow = wbase + g * WS;
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {
+      const float b0 = wrow[8 * ks + tq], b1 = wrow[8 * ks + tq + 4];
+      const uint32_t h0 = to_tf32(b0), h1 = to_tf32(b1);
+      const uint32_t l0 = to_tf32(b0 - __uint_as_float(h0)), l1 = to_tf32(b1 - __uint_as_float(h1));
+#pragma unroll
+      for (int mt = 0; mt < (MT ? MT : 1); ++mt) {
+        mma_tf32(d[mt], ahi[mt][ks], h0, h1);
+        mma_tf32(d[mt], ahi[mt][ks], l0, l1);
+      }
+    }
+#pragma unroll
+    for (int ks2 = 0; ks2 < 2; ++ks2) {
+      const float2 p0 = *reinterpret_cast<const float2*>(wrow + 16 * ks2 + 2 * tq);
+      const float2 p1 = *reinterpret_cast<const float2*>(wrow + 16 * ks2 + 2 * tq + 8);
+      const uint32_t b0 = pack_bf16(p0.x, p0.y), b1 = pack_bf16(p1.x, p1.y);
+#pragma unroll
+      for (int mt = 0; mt < (MT ? MT : 1); ++mt) mma_bf16(d[mt], alo[(mt * 2 + ks2) * 32 + lane], b0, b1);
+    }
+  };
+
   auto evaluate = [&]() {
     cp_async_wait_all();
     __syncwarp();
+    if constexpr (!FF) {
+      float d[MT ? MT : 1][4];
+      tc_product(wR, d);
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int e = 2 * tq + j;
+        if (e < nent) {
+          const int m = meta[e];
+          const int64_t src = m & ((1 << 29) - 1);
+          double* dst = (m & (1 << 30)) ? acc.pt_mur + src * Cr : acc.node_s + src * Cr;
+#pragma unroll
+          for (int mt = 0; mt < (MT ? MT : 1); ++mt) {
+            const int c = 16 * mt + g;
+            if (c < nr && d[mt][j] != 0.f) atomicAdd(dst + c, (double)d[mt][j]);
+            if (c + 8 < nr && d[mt][2 + j] != 0.f) atomicAdd(dst + c + 8, (double)d[mt][2 + j]);
+          }
+        }
+      }
+      // radial epsilon terms (:379, :409) for entries with a lane within 6.5 eps
+      const unsigned nb = __ballot_sync(FULL_MASK, lane < nent && ((meta[lane & 7] >> 29) & 1));
+      if (nb) {
+        tc_product(wE, d);
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int e = 2 * tq + j;
+          if ((nb >> e) & 1u) {
+            const float* rad = reinterpret_cast<const float*>(rows + e * F4 + 1);
+#pragma unroll
+            for (int mt = 0; mt < (MT ? MT : 1); ++mt) {
+              const int c = 16 * mt + g;
+              if (c < nr) eps_acc += (double)(d[mt][j] * rad[c]);
+              if (c + 8 < nr) eps_acc += (double)(d[mt][2 + j] * rad[c + 8]);
+            }
+          }
+        }
+      }
+    }
     for (int e = 0; e < nent; ++e) {
       const int m = meta[e];
       const bool is_point = m & (1 << 30);
-      const bool near = m & (1 << 29);
       const int64_t src = m & ((1 << 29) - 1);
-      const float4* wr4 = reinterpret_cast<const float4*>(wR + e * 32);
-      float sA = 0.f, sB = 0.f;
-#pragma unroll
-      for (int l4 = 0; l4 < 8; ++l4) {
-        const float4 ww = wr4[l4];
-        const float wv[4] = {ww.x, ww.y, ww.z, ww.w};
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int l = 4 * l4 + u;
-          sA = fmaf(wv[u], colA[l], sA);
-          if (NB == 2) sB = fmaf(wv[u], colB[l], sB);
-        }
-      }
-      if (NB == 1) {
-        // half-warp split: lanes 0-15 cover queries 0-15, lanes 16-31 queries 16-31
-        const float* wh = wR + e * 32 + 16 * (lane >> 4);
-#pragma unroll
-        for (int i4 = 0; i4 < 4; ++i4) {
-          const float4 ww = reinterpret_cast<const float4*>(wh)[i4];
-          sB = fmaf(ww.x, colB[4 * i4 + 0], sB);
-          sB = fmaf(ww.y, colB[4 * i4 + 1], sB);
-          sB = fmaf(ww.z, colB[4 * i4 + 2], sB);
-          sB = fmaf(ww.w, colB[4 * i4 + 3], sB);
-        }
-        sB += __shfl_xor_sync(FULL_MASK, sB, 16);
-      }
-      double* dst_s = is_point ? acc.pt_mur + src * Cr : acc.node_s + src * Cr;
-      if (okA && sA != 0.f) atomicAdd(dst_s + lane, (double)sA);
-      const bool ownB = NB == 2 ? okB : (NB == 1 ? (okB && lane < 16) : false);
-      if (ownB && sB != 0.f) atomicAdd(dst_s + slotB, (double)sB);
-      if (near) {  // radial epsilon terms (:379, :409)
-        const float4* we4 = reinterpret_cast<const float4*>(wE + e * 32);
-        float eA = 0.f, eB = 0.f;
+      if constexpr (FF) {
+        const bool near = m & (1 << 29);
+        const float4* wr4 = reinterpret_cast<const float4*>(wR + e * WS);
+        float sA = 0.f, sB = 0.f;
 #pragma unroll
         for (int l4 = 0; l4 < 8; ++l4) {
-          const float4 ww = we4[l4];
+          const float4 ww = wr4[l4];
           const float wv[4] = {ww.x, ww.y, ww.z, ww.w};
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            eA = fmaf(wv[u], colA[4 * l4 + u], eA);
-            if (NB == 2) eB = fmaf(wv[u], colB[4 * l4 + u], eB);
+            const int l = 4 * l4 + u;
+            sA = fmaf(wv[u], colA[l], sA);
+            if (NB == 2) sB = fmaf(wv[u], colB[l], sB);
           }
         }
         if (NB == 1) {
-          const float* wh = wE + e * 32 + 16 * (lane >> 4);
+          // half-warp split: lanes 0-15 cover queries 0-15, lanes 16-31 queries 16-31
+          const float* wh = wR + e * WS + 16 * (lane >> 4);
 #pragma unroll
-          for (int i = 0; i < 16; ++i) eB = fmaf(wh[i], colB[i], eB);
-          eB += __shfl_xor_sync(FULL_MASK, eB, 16);
+          for (int i4 = 0; i4 < 4; ++i4) {
+            const float4 ww = reinterpret_cast<const float4*>(wh)[i4];
+            sB = fmaf(ww.x, colB[4 * i4 + 0], sB);
+            sB = fmaf(ww.y, colB[4 * i4 + 1], sB);
+            sB = fmaf(ww.z, colB[4 * i4 + 2], sB);
+            sB = fmaf(ww.w, colB[4 * i4 + 3], sB);
+          }
+          sB += __shfl_xor_sync(FULL_MASK, sB, 16);
         }
-        const float* rad = reinterpret_cast<const float*>(rows + e * F4 + 1);
-        if (okA) eps_acc += (double)(eA * rad[lane]);
-        if (ownB) eps_acc += (double)(eB * rad[slotB]);
+        double* dst_s = is_point ? acc.pt_mur + src * Cr : acc.node_s + src * Cr;
+        if (okA && sA != 0.f) atomicAdd(dst_s + lane, (double)sA);
+        const bool ownB = NB == 2 ? okB : (NB == 1 ? (okB && lane < 16) : false);
+        if (ownB && sB != 0.f) atomicAdd(dst_s + slotB, (double)sB);
+        if (near) {  // radial epsilon terms (:379, :409)
+          const float4* we4 = reinterpret_cast<const float4*>(wE + e * WS);
+          float eA = 0.f, eB = 0.f;
+#pragma unroll
+          for (int l4 = 0; l4 < 8; ++l4) {
+            const float4 ww = we4[l4];
+            const float wv[4] = {ww.x, ww.y, ww.z, ww.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              eA = fmaf(wv[u], colA[4 * l4 + u], eA);
+              if (NB == 2) eB = fmaf(wv[u], colB[4 * l4 + u], eB);
+            }
+          }
+          if (NB == 1) {
+            const float* wh = wE + e * WS + 16 * (lane >> 4);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) eB = fmaf(wh[i], colB[i], eB);
+            eB += __shfl_xor_sync(FULL_MASK, eB, 16);
+          }
+          const float* rad = reinterpret_cast<const float*>(rows + e * F4 + 1);
+          if (okA) eps_acc += (double)(eA * rad[lane]);
+          if (ownB) eps_acc += (double)(eB * rad[slotB]);
+        }
       }
       // vector quantities: transposed sum of vq[e][k][l] over l
       const float4 v4 = reinterpret_cast<const float4*>(vq + e * 128)[lane];
@@ -240,13 +414,41 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
     const float A = lo.w;
     float fx, fy, fz;
     const float s = dist2_df(hi, lo, qx, fx, fy, fz);
-    const bool far = mine && far_test(s, hi, qx, x, tv.node_dec + node);
+    const bool far = mine && far_test(s, hi, qx, xq, tv.node_dec + node);
     const unsigned farm = __ballot_sync(FULL_MASK, far);
     if (farm && A > 0.f) {
       begin_entry();
       float r_ = 0.f, e_ = 0.f, u0 = 0.f, u1 = 0.f, u2 = 0.f;
       bool nr_ = false;
-      if (far) {
+      if (GM == 0) {
+        // far lanes beyond 6.5 eps (or singular): tau = 1, no epsilon terms
+        // (kernels.cpp:50-55); the coefficient series only under a warp-uniform
+        // branch, so a batch without near lanes never issues it
+        const bool slow = far && !(kp.mode == KM_SINGULAR ||
+                                   (kp.mode == KM_REGULARIZED && s >= kp.near2));
+        if (far) {
+          const float inv_r = rsqrtf(s);
+          const float R = inv_r * inv_r;
+          r_ = A * R;
+          const float aWds = A * (R * inv_r) * ds0;
+          u0 = aWds * fx, u1 = aWds * fy, u2 = aWds * fz;
+        }
+        if (__any_sync(FULL_MASK, slow)) {
+          if (slow) {
+            const Co c = coeffs<2>(s, kp);
+            nr_ = c.near;
+            r_ = A * c.R;
+            e_ = A * c.dR_de;
+            const float aWds = A * c.W * ds0;
+            u0 = aWds * fx, u1 = aWds * fy, u2 = aWds * fz;
+            if (c.near) {
+              const float4 v = __ldg(tv.node_row + (size_t)node * F4g);
+              const float vd = fmaf(v.x, fx, fmaf(v.y, fy, v.z * fz));
+              eps_acc += (double)(ds0 * A * c.dW_de * vd);  // :370
+            }
+          }
+        }
+      } else if (far) {
         const Co c = adj_coeffs<GM>(s, kp);
         nr_ = c.near;
         r_ = A * c.R;
@@ -270,12 +472,12 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
           eps_acc += (double)e;
         }
       }
-      wR[nent * 32 + lane] = r_;
-      wE[nent * 32 + lane] = e_;
+      wR[nent * WS + lane] = r_;
+      wE[nent * WS + lane] = e_;
       float* vqe = vq + nent * 128;
       vqe[lane] = u0, vqe[32 + lane] = u1, vqe[64 + lane] = u2, vqe[96 + lane] = 0.f;
       const bool any_near = __any_sync(FULL_MASK, nr_);
-      if (any_near && lane < F4g)
+      if (any_near && lane < F4c)
         cp_async16(s_rows + 16u * F4 * nent, tv.node_row + (size_t)node * F4g + lane);
       if (lane == 0) meta[nent] = node | (any_near ? (1 << 29) : 0);
       ++nent;
@@ -294,7 +496,7 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
             float fx, fy, fz;
             const float r2 = dist2_df(ph, __ldg(&pr->lo), qx, fx, fy, fz);
             // :387 skips exact coincidence (fp64); fp32 r2 == 0 triggers the exact check
-            if (!(r2 == 0.f && coincident_exact(tv.pt_pos64 + 3 * (size_t)j, x))) {
+            if (!(r2 == 0.f && coincident_exact(tv.pt_pos64 + 3 * (size_t)j, xq))) {
               const Co c = adj_coeffs<GM>(r2, kp);
               const float Am = ph.w;
               nr_ = c.near;
@@ -322,12 +524,12 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
               eps_acc += (double)e;
             }
           }
-          wR[nent * 32 + lane] = r_;
-          wE[nent * 32 + lane] = e_;
+          wR[nent * WS + lane] = r_;
+          wE[nent * WS + lane] = e_;
           float* vqe = vq + nent * 128;
           vqe[lane] = n0, vqe[32 + lane] = n1, vqe[64 + lane] = n2, vqe[96 + lane] = dmu;
           const bool any_near = __any_sync(FULL_MASK, nr_);
-          if (any_near && lane < F4g)
+          if (any_near && lane < F4c)
             cp_async16(s_rows + 16u * F4 * nent, tv.pt_row + (size_t)j * F4g + lane);
           if (lane == 0) meta[nent] = j | (1 << 30) | (any_near ? (1 << 29) : 0);
           ++nent;
@@ -349,20 +551,18 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
   if (lane == 0 && eps_acc != 0.0) atomicAdd(acc.d_eps, eps_acc);
 }
 
-template <int NB, int GM, int RR, int WARPS = 4, int ENT = 8, int MINB = 128>
+template <int NB, int GM, int RR, int WARPS = 4, int ENT = 8, int MAXR = 128, int MT = 0>
 static void launch_adj2(const Tree& t, const KParams& kp, const AdjArgs& a, GradBuf& b, int nr) {
-  constexpr int F4 = 1 + RR;
-  constexpr int WARP_FLOATS = ENT * 32 * 6 + ENT * F4 * 4 + ENT + 2 * DPL_STACK_PER_WARP;
-  const size_t smem = (size_t)WARPS * ((WARP_FLOATS + 3) & ~3) * 4;
+  const size_t smem = (size_t)WARPS * AdjLayout<MT, ENT, RR>::WARP_FLOATS * 4;
   static bool attr = false;
   if (!attr) {
-    DPL_CUDA(cudaFuncSetAttribute(k_adjoint2<NB, GM, WARPS, ENT, RR, MINB>,
+    DPL_CUDA(cudaFuncSetAttribute(k_adjoint2<NB, GM, WARPS, ENT, RR, MAXR, MT>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
   Adj2Ptrs p{b.node_v, b.node_s, b.pt_mud, b.pt_mur, b.pt_n, b.d_eps};
   unsigned blocks = (unsigned)((a.q + WARPS * 32 - 1) / (WARPS * 32));
-  k_adjoint2<NB, GM, WARPS, ENT, RR, MINB><<<blocks, WARPS * 32, smem, t.stream>>>(
+  k_adjoint2<NB, GM, WARPS, ENT, RR, MAXR, MT><<<blocks, WARPS * 32, smem, t.stream>>>(
       t.view(), kp, a.xs, a.perm, a.q, a.d_out, a.dstride, a.d_grad, nr, t.chmap.as<int>(), p,
       a.overflow);
   count_launch();
@@ -371,19 +571,26 @@ static void launch_adj2(const Tree& t, const KParams& kp, const AdjArgs& a, Grad
 template <int GM>
 static bool adj2_plan(const Tree& t, const KParams& kp, const AdjArgs& a, GradBuf& b) {
   const int nr = a.nr_limit >= 0 ? std::min(a.nr_limit, t.Cr) : t.Cr;
-  if (t.F4 - 1 > 16) return false;
-  if (nr <= 32) return launch_adj2<0, GM, 16>(t, kp, a, b, nr), true;
-  if (nr <= 48 && GM == 0) {
-    const char* v = getenv("DPL_TUNE_ADJ");
-    switch (v ? atoi(v) : 0) {  // occupancy / batch experiments
-      case 1: return launch_adj2<1, GM, 16, 4, 8, 112>(t, kp, a, b, nr), true;
-      case 2: return launch_adj2<1, GM, 16, 4, 8, 104>(t, kp, a, b, nr), true;
-      case 3: return launch_adj2<1, GM, 16, 4, 4, 112>(t, kp, a, b, nr), true;
-      case 4: return launch_adj2<1, GM, 16, 4, 4, 96>(t, kp, a, b, nr), true;
-      case 5: return launch_adj2<1, GM, 16, 4, 6, 112>(t, kp, a, b, nr), true;
-      default: break;
+  // Tensor-core phase B: correct (parity-tested) but measured SLOWER on config 2
+  // (34.9-36.6 ms vs 29.2 ms FFMA: the 48 A_hi registers push the traversal
+  // into spills or lower occupancy) -> opt-in experiment.
+  static const bool tc = getenv("DPL_ADJOINT_TC") != nullptr;
+  if (tc) {  // rows staged up to the slots used
+    if (nr <= 16) return launch_adj2<0, GM, 4, 4, 8, 128, 1>(t, kp, a, b, nr), true;
+    if (nr <= 32) return launch_adj2<0, GM, 8, 4, 8, 128, 2>(t, kp, a, b, nr), true;
+    if (nr <= 48) {
+      const char* v = getenv("DPL_TUNE_ADJ");
+      switch (v ? atoi(v) : 0) {  // (warps, register cap) experiments
+        case 1: return launch_adj2<0, GM, 12, 4, 8, 168, 3>(t, kp, a, b, nr), true;
+        case 2: return launch_adj2<0, GM, 12, 3, 8, 168, 3>(t, kp, a, b, nr), true;
+        case 3: return launch_adj2<0, GM, 12, 2, 8, 160, 3>(t, kp, a, b, nr), true;
+        case 4: return launch_adj2<0, GM, 12, 4, 8, 144, 3>(t, kp, a, b, nr), true;
+        default: return launch_adj2<0, GM, 12, 4, 8, 128, 3>(t, kp, a, b, nr), true;
+      }
     }
   }
+  if (t.F4 - 1 > 16) return false;
+  if (nr <= 32) return launch_adj2<0, GM, 16>(t, kp, a, b, nr), true;
   if (nr <= 48) return launch_adj2<1, GM, 16>(t, kp, a, b, nr), true;
   if (nr <= 64) return launch_adj2<2, GM, 16>(t, kp, a, b, nr), true;
   return false;

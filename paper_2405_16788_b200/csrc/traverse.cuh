@@ -39,12 +39,20 @@ struct QueryDF {
   float hx, hy, hz, lx, ly, lz, m;  // m = max |x_hi|
 };
 
+// the empty asm makes each value opaque, so the compiler keeps the 7 floats
+// instead of re-deriving them from a live fp64 position inside the loops
+__device__ __forceinline__ float opaque(float v) {
+  asm volatile("" : "+f"(v));
+  return v;
+}
+
 __device__ __forceinline__ QueryDF make_qdf(const QueryPos& x) {
   QueryDF q;
   q.hx = (float)x.x, q.hy = (float)x.y, q.hz = (float)x.z;
-  q.lx = (float)(x.x - (double)q.hx), q.ly = (float)(x.y - (double)q.hy),
-  q.lz = (float)(x.z - (double)q.hz);
-  q.m = fmaxf(fmaxf(fabsf(q.hx), fabsf(q.hy)), fabsf(q.hz));
+  q.lx = opaque((float)(x.x - (double)q.hx)), q.ly = opaque((float)(x.y - (double)q.hy)),
+  q.lz = opaque((float)(x.z - (double)q.hz));
+  q.m = opaque(fmaxf(fmaxf(fabsf(q.hx), fabsf(q.hy)), fabsf(q.hz)));
+  q.hx = opaque(q.hx), q.hy = opaque(q.hy), q.hz = opaque(q.hz);
   return q;
 }
 
@@ -74,6 +82,32 @@ __device__ __forceinline__ bool far_test(float s, const float4& hi, const QueryD
   const double2 b = __ldg(reinterpret_cast<const double2*>(dec) + 1);
   double ex, ey, ez;
   return dist2_rn(a.x, a.y, b.x, x, ex, ey, ez) > b.y;
+}
+
+// Same test with the fp64 query re-read from memory on the (rare) exact path:
+// keeps the 6 registers of the fp64 position out of the traversal loop.
+__device__ __forceinline__ bool far_test(float s, const float4& hi, const QueryDF& q,
+                                         const double* __restrict__ xq,
+                                         const double4* __restrict__ dec) {
+  const float thr = hi.w;
+  const float M = fmaxf(fmaxf(fabsf(hi.x), fabsf(hi.y)), fabsf(hi.z)) + q.m;
+  const float band = 2e-6f * (s + thr) + 1e-13f * M * M;
+  const float diff = s - thr;
+  if (diff > band) return true;
+  if (-diff > band) return false;
+  const double2 a = __ldg(reinterpret_cast<const double2*>(dec));
+  const double2 b = __ldg(reinterpret_cast<const double2*>(dec) + 1);
+  const QueryPos x{xq[0], xq[1], xq[2]};
+  double ex, ey, ez;
+  return dist2_rn(a.x, a.y, b.x, x, ex, ey, ez) > b.y;
+}
+
+// exact fp64 coincidence check for a leaf point (bhtree.cpp:219,316,387)
+__device__ __forceinline__ bool coincident_exact(const double* __restrict__ p,
+                                                 const double* __restrict__ xq) {
+  const QueryPos x{xq[0], xq[1], xq[2]};
+  double ex, ey, ez;
+  return dist2_rn(__ldg(p), __ldg(p + 1), __ldg(p + 2), x, ex, ey, ez) == 0.0;
 }
 
 // exact fp64 coincidence check for a leaf point (bhtree.cpp:219,316,387)

@@ -374,3 +374,20 @@ def test_host_pointer_pipeline_matches_device_path(eng, oracle_mod):
         assert np.array_equal(o, host)
     finally:
         t.set_host_async(False)
+
+
+@pytest.mark.parametrize("env", ["DPL_ADJOINT_TC", "DPL_ADJOINT_SINGLE_PHASE",
+                                 "DPL_FORWARD_NO_TC", "DPL_FORWARD_SINGLE_PHASE"])
+def test_alternate_kernel_paths(env):
+    """The opt-in / fallback kernels (selected once per process from the
+    environment) pass the same forward / adjoint / render parity tests."""
+    import os
+    import subprocess
+    import sys
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    r = subprocess.run(
+        [sys.executable, "-m", "pytest", os.path.join(here, "test_gpu_parity.py"), "-q", "-x",
+         "-m", "gpu", "-k", "(adjoint or render or many_channel or primal) and not alternate"],
+        env=dict(os.environ, **{env: "1"}), capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
