@@ -1,6 +1,7 @@
 // adjoint.cuh — GradientBuffer on device and the adjoint / flush entry points.
 #pragma once
 
+#include "ilist.cuh"
 #include "tree.cuh"
 
 namespace dpl {
@@ -26,6 +27,9 @@ struct AdjArgs {
   int grad_mode = 0;   // 0 none, 1 q x dstride x 3, 2 q x 3 for channel 0
   int nr_limit = -1;   // only the first nr_limit radial slots carry non-zero d_out
   int* overflow = nullptr;
+  double beta = 0;         // opening parameter (interaction-list reuse key)
+  IList* ilist = nullptr;  // interaction lists (ilist.cuh); reused when the previous
+                           // call built them for the same queries / beta / tree
 };
 
 void gradbuf_alloc(GradBuf& b, const Tree& t);

@@ -125,12 +125,14 @@ struct AdjLayout {
 // MT: > 0 selects the tensor-core phase B with MT m-tiles (Cr <= 16 MT); NB unused.
 // GM: 0 no d_grad; 1 d_grad q x dstride x 3; 2 d_grad q x 3 (channel 0).
 // MAXR: register cap (occupancy vs. spills; chosen by measurement)
-template <int NB, int GM, int WARPS, int ENT, int RR, int MAXR = 128, int MT = 0>
+// LIST: replay the batch's interaction lists (ilist.cuh); warps whose list is
+// incomplete walk the tree as the fused kernel does (same entry order).
+template <int NB, int GM, int WARPS, int ENT, int RR, int MAXR = 128, int MT = 0, bool LIST = false>
 __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
     k_adjoint2(TreeView tv, KParams kp, const double* __restrict__ xs,
                const int32_t* __restrict__ perm, int64_t q, const float* __restrict__ d_out,
                int dstride, const float* __restrict__ d_grad, int nr,
-               const int* __restrict__ chmap, Adj2Ptrs acc, int* overflow) {
+               const int* __restrict__ chmap, Adj2Ptrs acc, IListView lv, int* overflow) {
   using L = AdjLayout<MT, ENT, RR>;
   constexpr int F4 = L::F4;
   constexpr int WS = L::WS;
@@ -397,8 +399,162 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
     if (nent == ENT) evaluate();
   };
 
-  int sp = 1;
-  if (lane == 0) stk[0] = make_int2(0, (int)active);
+  // one far source (node) for the lanes in `far` (bhtree.cpp:361-381)
+  auto far_entry = [&](int node, float A, float s, float fx, float fy, float fz, bool far) {
+    begin_entry();
+    float r_ = 0.f, e_ = 0.f, u0 = 0.f, u1 = 0.f, u2 = 0.f;
+    bool nr_ = false;
+    if (GM == 0) {
+      // far lanes beyond 6.5 eps (or singular): tau = 1, no epsilon terms
+      // (kernels.cpp:50-55); the coefficient series only under a warp-uniform
+      // branch, so a batch without near lanes never issues it
+      const bool slow = far && !(kp.mode == KM_SINGULAR ||
+                                 (kp.mode == KM_REGULARIZED && s >= kp.near2));
+      if (far) {
+        const float inv_r = rsqrtf(s);
+        const float R = inv_r * inv_r;
+        r_ = A * R;
+        const float aWds = A * (R * inv_r) * ds0;
+        u0 = aWds * fx, u1 = aWds * fy, u2 = aWds * fz;
+      }
+      if (__any_sync(FULL_MASK, slow)) {
+        if (slow) {
+          const Co c = coeffs<2>(s, kp);
+          nr_ = c.near;
+          r_ = A * c.R;
+          e_ = A * c.dR_de;
+          const float aWds = A * c.W * ds0;
+          u0 = aWds * fx, u1 = aWds * fy, u2 = aWds * fz;
+          if (c.near) {
+            const float4 v = __ldg(tv.node_row + (size_t)node * F4g);
+            const float vd = fmaf(v.x, fx, fmaf(v.y, fy, v.z * fz));
+            eps_acc += (double)(ds0 * A * c.dW_de * vd);  // :370
+          }
+        }
+      }
+    } else if (far) {
+      const Co c = adj_coeffs<GM>(s, kp);
+      nr_ = c.near;
+      r_ = A * c.R;
+      e_ = A * c.dR_de;
+      const float aWds = A * c.W * ds0;
+      u0 = aWds * fx, u1 = aWds * fy, u2 = aWds * fz;
+      if (c.near || GM) {
+        const float4 v = __ldg(tv.node_row + (size_t)node * F4g);
+        const float vd = fmaf(v.x, fx, fmaf(v.y, fy, v.z * fz));
+        float e = ds0 * A * c.dW_de * vd;  // :370
+        if (GM) {                          // :372-374
+          const float gd = fmaf(dg0, fx, fmaf(dg1, fy, dg2 * fz));
+          const float t = c.Wp_r * gd;
+          u0 -= A * fmaf(c.W, dg0, t * fx);
+          u1 -= A * fmaf(c.W, dg1, t * fy);
+          u2 -= A * fmaf(c.W, dg2, t * fz);
+          const float k2 = c.dWp_r_de * vd;
+          e -= A * fmaf(dg0, fmaf(c.dW_de, v.x, k2 * fx),
+                        fmaf(dg1, fmaf(c.dW_de, v.y, k2 * fy), dg2 * fmaf(c.dW_de, v.z, k2 * fz)));
+        }
+        eps_acc += (double)e;
+      }
+    }
+    wR[nent * WS + lane] = r_;
+    wE[nent * WS + lane] = e_;
+    float* vqe = vq + nent * 128;
+    vqe[lane] = u0, vqe[32 + lane] = u1, vqe[64 + lane] = u2, vqe[96 + lane] = 0.f;
+    const bool any_near = __any_sync(FULL_MASK, nr_);
+    if (any_near && lane < F4c)
+      cp_async16(s_rows + 16u * F4 * nent, tv.node_row + (size_t)node * F4g + lane);
+    if (lane == 0) meta[nent] = node | (any_near ? (1 << 29) : 0);
+    ++nent;
+  };
+  // the points of an opened leaf for the lanes in `me_open` (:382-412)
+  auto leaf_points = [&](const int4 tp, bool me_open) {
+    for (int j = tp.z; j < tp.w; ++j) {
+      begin_entry();
+      float r_ = 0.f, e_ = 0.f, n0 = 0.f, n1 = 0.f, n2 = 0.f, dmu = 0.f;
+      bool nr_ = false;
+      if (me_open) {
+        const PtRec* pr = tv.pt_rec + j;
+        const float4 ph = __ldg(&pr->hi);
+        float fx, fy, fz;
+        const float r2 = dist2_df(ph, __ldg(&pr->lo), qx, fx, fy, fz);
+        // :387 skips exact coincidence (fp64); fp32 r2 == 0 triggers the exact check
+        if (!(r2 == 0.f && coincident_exact(tv.pt_pos64 + 3 * (size_t)j, xq))) {
+          const Co c = adj_coeffs<GM>(r2, kp);
+          const float Am = ph.w;
+          nr_ = c.near;
+          r_ = Am * c.R;
+          e_ = Am * c.dR_de;
+          const float mu = __ldg(tv.pt_mu + j);
+          const float nx = __ldg(tv.pt_nrm + 3 * (size_t)j), ny = __ldg(tv.pt_nrm + 3 * (size_t)j + 1),
+                      nz = __ldg(tv.pt_nrm + 3 * (size_t)j + 2);
+          const float nu = fmaf(nx, fx, fmaf(ny, fy, nz * fz));
+          const float aW = Am * c.W;
+          dmu = ds0 * aW * nu;
+          const float sc = ds0 * aW * mu;
+          n0 = sc * fx, n1 = sc * fy, n2 = sc * fz;
+          float e = ds0 * Am * mu * c.dW_de * nu;
+          if (GM) {
+            const float gd = fmaf(dg0, fx, fmaf(dg1, fy, dg2 * fz));
+            const float gn = fmaf(dg0, nx, fmaf(dg1, ny, dg2 * nz));
+            dmu -= Am * fmaf(c.W, gn, c.Wp_r * nu * gd);
+            const float am = Am * mu, t = c.Wp_r * gd;
+            n0 -= am * fmaf(c.W, dg0, t * fx);
+            n1 -= am * fmaf(c.W, dg1, t * fy);
+            n2 -= am * fmaf(c.W, dg2, t * fz);
+            e -= am * fmaf(c.dW_de, gn, c.dWp_r_de * nu * gd);
+          }
+          eps_acc += (double)e;
+        }
+      }
+      wR[nent * WS + lane] = r_;
+      wE[nent * WS + lane] = e_;
+      float* vqe = vq + nent * 128;
+      vqe[lane] = n0, vqe[32 + lane] = n1, vqe[64 + lane] = n2, vqe[96 + lane] = dmu;
+      const bool any_near = __any_sync(FULL_MASK, nr_);
+      if (any_near && lane < F4c)
+        cp_async16(s_rows + 16u * F4 * nent, tv.pt_row + (size_t)j * F4g + lane);
+      if (lane == 0) meta[nent] = j | (1 << 30) | (any_near ? (1 << 29) : 0);
+      ++nent;
+    }
+  };
+  const int64_t wg = (int64_t)blockIdx.x * WARPS + w;
+  const int total = LIST ? __ldg(lv.count + wg) : -1;
+  if (LIST && total >= 0) {
+    // replay the interaction list (ilist.cuh): 32 entries at a time, their node
+    // records prefetched into the (unused) stack region with cp.async
+    const NodeRec* rb = reinterpret_cast<const NodeRec*>(stk);
+    const uint32_t s_rb = smem_u32(stk) + 48u * lane;
+    int chunk = (int)wg;
+    for (int base = 0; base < total; base += 32) {
+      if (base > 0 && base % IL_CHUNK == 0) chunk = __ldg(lv.next + chunk);
+      const uint2 my = il_load(lv, chunk, base, total, lane);
+      const int n = min(32, total - base);
+      __syncwarp();  // the previous window's records are consumed
+      if (lane < n) {
+        const NodeRec* r = tv.node_rec + (my.x & IL_NODE);
+        cp_async16(s_rb, &r->hi);
+        cp_async16(s_rb + 16u, &r->lo);
+        cp_async16(s_rb + 32u, &r->topo);
+      }
+      cp_async_wait_all();
+      __syncwarp();
+      for (int i = 0; i < n; ++i) {
+        const uint32_t src = __shfl_sync(FULL_MASK, my.x, i);
+        const unsigned m = __shfl_sync(FULL_MASK, my.y, i);
+        const bool mine = (m >> lane) & 1u;
+        if (!(src & IL_LEAF)) {
+          const float4 hi = rb[i].hi, lo = rb[i].lo;
+          float fx, fy, fz;
+          const float s = dist2_df(hi, lo, qx, fx, fy, fz);
+          far_entry((int)(src & IL_NODE), lo.w, s, fx, fy, fz, mine);
+        } else {
+          leaf_points(rb[i].topo, mine);
+        }
+      }
+    }
+  }
+  int sp = (LIST && total >= 0) ? 0 : 1;
+  if (sp && lane == 0) stk[0] = make_int2(0, (int)active);
   __syncwarp();
   while (sp > 0) {
     --sp;
@@ -417,123 +573,12 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
     const bool far = mine && far_test(s, hi, qx, xq, tv.node_dec + node);
     const unsigned farm = __ballot_sync(FULL_MASK, far);
     if (farm && A > 0.f) {
-      begin_entry();
-      float r_ = 0.f, e_ = 0.f, u0 = 0.f, u1 = 0.f, u2 = 0.f;
-      bool nr_ = false;
-      if (GM == 0) {
-        // far lanes beyond 6.5 eps (or singular): tau = 1, no epsilon terms
-        // (kernels.cpp:50-55); the coefficient series only under a warp-uniform
-        // branch, so a batch without near lanes never issues it
-        const bool slow = far && !(kp.mode == KM_SINGULAR ||
-                                   (kp.mode == KM_REGULARIZED && s >= kp.near2));
-        if (far) {
-          const float inv_r = rsqrtf(s);
-          const float R = inv_r * inv_r;
-          r_ = A * R;
-          const float aWds = A * (R * inv_r) * ds0;
-          u0 = aWds * fx, u1 = aWds * fy, u2 = aWds * fz;
-        }
-        if (__any_sync(FULL_MASK, slow)) {
-          if (slow) {
-            const Co c = coeffs<2>(s, kp);
-            nr_ = c.near;
-            r_ = A * c.R;
-            e_ = A * c.dR_de;
-            const float aWds = A * c.W * ds0;
-            u0 = aWds * fx, u1 = aWds * fy, u2 = aWds * fz;
-            if (c.near) {
-              const float4 v = __ldg(tv.node_row + (size_t)node * F4g);
-              const float vd = fmaf(v.x, fx, fmaf(v.y, fy, v.z * fz));
-              eps_acc += (double)(ds0 * A * c.dW_de * vd);  // :370
-            }
-          }
-        }
-      } else if (far) {
-        const Co c = adj_coeffs<GM>(s, kp);
-        nr_ = c.near;
-        r_ = A * c.R;
-        e_ = A * c.dR_de;
-        const float aWds = A * c.W * ds0;
-        u0 = aWds * fx, u1 = aWds * fy, u2 = aWds * fz;
-        if (c.near || GM) {
-          const float4 v = __ldg(tv.node_row + (size_t)node * F4g);
-          const float vd = fmaf(v.x, fx, fmaf(v.y, fy, v.z * fz));
-          float e = ds0 * A * c.dW_de * vd;  // :370
-          if (GM) {                          // :372-374
-            const float gd = fmaf(dg0, fx, fmaf(dg1, fy, dg2 * fz));
-            const float t = c.Wp_r * gd;
-            u0 -= A * fmaf(c.W, dg0, t * fx);
-            u1 -= A * fmaf(c.W, dg1, t * fy);
-            u2 -= A * fmaf(c.W, dg2, t * fz);
-            const float k2 = c.dWp_r_de * vd;
-            e -= A * fmaf(dg0, fmaf(c.dW_de, v.x, k2 * fx),
-                          fmaf(dg1, fmaf(c.dW_de, v.y, k2 * fy), dg2 * fmaf(c.dW_de, v.z, k2 * fz)));
-          }
-          eps_acc += (double)e;
-        }
-      }
-      wR[nent * WS + lane] = r_;
-      wE[nent * WS + lane] = e_;
-      float* vqe = vq + nent * 128;
-      vqe[lane] = u0, vqe[32 + lane] = u1, vqe[64 + lane] = u2, vqe[96 + lane] = 0.f;
-      const bool any_near = __any_sync(FULL_MASK, nr_);
-      if (any_near && lane < F4c)
-        cp_async16(s_rows + 16u * F4 * nent, tv.node_row + (size_t)node * F4g + lane);
-      if (lane == 0) meta[nent] = node | (any_near ? (1 << 29) : 0);
-      ++nent;
+      far_entry(node, A, s, fx, fy, fz, far);
     }
     const unsigned openm = mask & ~farm;
     if (openm) {
       if (tp.y == 0) {
-        const bool me_open = (openm >> lane) & 1u;
-        for (int j = tp.z; j < tp.w; ++j) {
-          begin_entry();
-          float r_ = 0.f, e_ = 0.f, n0 = 0.f, n1 = 0.f, n2 = 0.f, dmu = 0.f;
-          bool nr_ = false;
-          if (me_open) {
-            const PtRec* pr = tv.pt_rec + j;
-            const float4 ph = __ldg(&pr->hi);
-            float fx, fy, fz;
-            const float r2 = dist2_df(ph, __ldg(&pr->lo), qx, fx, fy, fz);
-            // :387 skips exact coincidence (fp64); fp32 r2 == 0 triggers the exact check
-            if (!(r2 == 0.f && coincident_exact(tv.pt_pos64 + 3 * (size_t)j, xq))) {
-              const Co c = adj_coeffs<GM>(r2, kp);
-              const float Am = ph.w;
-              nr_ = c.near;
-              r_ = Am * c.R;
-              e_ = Am * c.dR_de;
-              const float mu = __ldg(tv.pt_mu + j);
-              const float nx = __ldg(tv.pt_nrm + 3 * (size_t)j), ny = __ldg(tv.pt_nrm + 3 * (size_t)j + 1),
-                          nz = __ldg(tv.pt_nrm + 3 * (size_t)j + 2);
-              const float nu = fmaf(nx, fx, fmaf(ny, fy, nz * fz));
-              const float aW = Am * c.W;
-              dmu = ds0 * aW * nu;
-              const float sc = ds0 * aW * mu;
-              n0 = sc * fx, n1 = sc * fy, n2 = sc * fz;
-              float e = ds0 * Am * mu * c.dW_de * nu;
-              if (GM) {
-                const float gd = fmaf(dg0, fx, fmaf(dg1, fy, dg2 * fz));
-                const float gn = fmaf(dg0, nx, fmaf(dg1, ny, dg2 * nz));
-                dmu -= Am * fmaf(c.W, gn, c.Wp_r * nu * gd);
-                const float am = Am * mu, t = c.Wp_r * gd;
-                n0 -= am * fmaf(c.W, dg0, t * fx);
-                n1 -= am * fmaf(c.W, dg1, t * fy);
-                n2 -= am * fmaf(c.W, dg2, t * fz);
-                e -= am * fmaf(c.dW_de, gn, c.dWp_r_de * nu * gd);
-              }
-              eps_acc += (double)e;
-            }
-          }
-          wR[nent * WS + lane] = r_;
-          wE[nent * WS + lane] = e_;
-          float* vqe = vq + nent * 128;
-          vqe[lane] = n0, vqe[32 + lane] = n1, vqe[64 + lane] = n2, vqe[96 + lane] = dmu;
-          const bool any_near = __any_sync(FULL_MASK, nr_);
-          if (any_near && lane < F4c)
-            cp_async16(s_rows + 16u * F4 * nent, tv.pt_row + (size_t)j * F4g + lane);
-          if (lane == 0) meta[nent] = j | (1 << 30) | (any_near ? (1 << 29) : 0);
-          ++nent;
-        }
+        leaf_points(tp, (openm >> lane) & 1u);
       } else {
         if (sp + tp.y > DPL_STACK_PER_WARP) {
           if (lane == 0) atomicExch(overflow, 1);
@@ -551,21 +596,33 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
   if (lane == 0 && eps_acc != 0.0) atomicAdd(acc.d_eps, eps_acc);
 }
 
-template <int NB, int GM, int RR, int WARPS = 4, int ENT = 8, int MAXR = 128, int MT = 0>
-static void launch_adj2(const Tree& t, const KParams& kp, const AdjArgs& a, GradBuf& b, int nr) {
+template <int NB, int GM, int RR, int WARPS, int ENT, int MAXR, int MT, bool LIST>
+static void launch_adj2c(const Tree& t, const KParams& kp, const AdjArgs& a, GradBuf& b, int nr,
+                         IListView lv) {
   const size_t smem = (size_t)WARPS * AdjLayout<MT, ENT, RR>::WARP_FLOATS * 4;
   static bool attr = false;
   if (!attr) {
-    DPL_CUDA(cudaFuncSetAttribute(k_adjoint2<NB, GM, WARPS, ENT, RR, MAXR, MT>,
+    DPL_CUDA(cudaFuncSetAttribute(k_adjoint2<NB, GM, WARPS, ENT, RR, MAXR, MT, LIST>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
   Adj2Ptrs p{b.node_v, b.node_s, b.pt_mud, b.pt_mur, b.pt_n, b.d_eps};
   unsigned blocks = (unsigned)((a.q + WARPS * 32 - 1) / (WARPS * 32));
-  k_adjoint2<NB, GM, WARPS, ENT, RR, MAXR, MT><<<blocks, WARPS * 32, smem, t.stream>>>(
-      t.view(), kp, a.xs, a.perm, a.q, a.d_out, a.dstride, a.d_grad, nr, t.chmap.as<int>(), p,
+  k_adjoint2<NB, GM, WARPS, ENT, RR, MAXR, MT, LIST><<<blocks, WARPS * 32, smem, t.stream>>>(
+      t.view(), kp, a.xs, a.perm, a.q, a.d_out, a.dstride, a.d_grad, nr, t.chmap.as<int>(), p, lv,
       a.overflow);
   count_launch();
+}
+
+// builds (or reuses) the interaction lists when the caller provides the workspace
+template <int NB, int GM, int RR, int WARPS = 4, int ENT = 8, int MAXR = 128, int MT = 0>
+static void launch_adj2(const Tree& t, const KParams& kp, const AdjArgs& a, GradBuf& b, int nr) {
+  if (a.ilist && !no_ilist()) {
+    ilist_build(t, *a.ilist, a.xs, a.perm, a.q, a.beta, a.overflow);
+    launch_adj2c<NB, GM, RR, WARPS, ENT, MAXR, MT, true>(t, kp, a, b, nr, a.ilist->view());
+  } else {
+    launch_adj2c<NB, GM, RR, WARPS, ENT, MAXR, MT, false>(t, kp, a, b, nr, IListView{});
+  }
 }
 
 template <int GM>

@@ -38,6 +38,7 @@ struct dpl_tree_s {
   // host-async mode (dpl_tree_set_host_async): staging-buffer hazards between
   // calls are tracked with events instead of a synchronize per call
   bool host_async = false;
+  IList il;  // interaction lists of the last batch (ilist.cuh)
   cudaEvent_t ev_fwd_in = nullptr, ev_fwd_out = nullptr, ev_adj_in = nullptr;
   void sync_all() {
     if (copy) DPL_CUDA(cudaStreamSynchronize(copy));
@@ -512,6 +513,8 @@ static int forward_common(dpl_tree_t h, const dpl_kernel_params* params, double 
         a.perm = perm;
         a.q = qc;
         a.overflow = ovf;
+        a.ilist = &h->il;
+        a.beta = beta;
         a.out = out_d + c0 * stride;
         a.out_stride = stride;
         if (channel >= 0) {
@@ -544,6 +547,8 @@ static int forward_common(dpl_tree_t h, const dpl_kernel_params* params, double 
     a.perm = h->ws_perm.as<int32_t>();
     a.q = q;
     a.overflow = overflow_flag(h);
+    a.ilist = &h->il;
+    a.beta = beta;
     Out<float> o, g;
     Out<long long> cnt;
     if (channel >= 0) {
@@ -696,6 +701,8 @@ int dpl_adjoint(dpl_tree_t h, const dpl_kernel_params* params, double beta_bh, c
         a.d_grad = dg_d ? dg_d + c0 * t.C * 3 : nullptr;
         a.grad_mode = dg_d ? 1 : 0;
         a.overflow = ovf;
+        a.ilist = &h->il;
+        a.beta = beta_bh;
         PhaseTimer pt(t, PH_ADJOINT);
         adjoint_launch(t, kp, a, buf->b);
       });
@@ -720,6 +727,8 @@ int dpl_adjoint(dpl_tree_t h, const dpl_kernel_params* params, double beta_bh, c
     a.d_grad = dg_d;
     a.grad_mode = dg_d ? 1 : 0;
     a.overflow = overflow_flag(h);
+    a.ilist = &h->il;
+    a.beta = beta_bh;
     {
       PhaseTimer pt(t, PH_ADJOINT);
       adjoint_launch(t, kp, a, buf->b);

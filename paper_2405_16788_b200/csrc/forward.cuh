@@ -1,6 +1,7 @@
 // forward.cuh — host entry points of the forward traversals (forward.cu).
 #pragma once
 
+#include "ilist.cuh"
 #include "tree.cuh"
 
 namespace dpl {
@@ -21,6 +22,9 @@ struct FwdArgs {
                      // primal, only channel only_ch stored (q x 1) -> bitwise
                      // primal_channel(c) == primal()[c] (test_bhtree.cpp:140)
   int nr_limit = -1;                 // only the first nr_limit radial slots (render step)
+  double beta = 0;         // opening parameter (interaction-list reuse key)
+  IList* ilist = nullptr;  // interaction-list workspace (ilist.cuh): built and replayed by the
+                           // kernels that support it, unless DPL_NO_ILIST is set
 };
 
 void forward_launch(const Tree& t, const KParams& kp, FwdArgs a);

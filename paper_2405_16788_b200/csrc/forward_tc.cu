@@ -69,12 +69,15 @@ constexpr int row_stride_floats(int f4) {
 }  // namespace
 
 // NT: radial n-tiles of 8 channels (TR = 8 NT); one dipole slot.
-template <int NT, int WARPS, int ENT, int MAXR, bool COUNT>
+// LIST: replay the batch's interaction lists (ilist.cuh) instead of walking the
+// tree; warps whose list is incomplete walk it as in the fused kernel. Both
+// paths run the same arithmetic in the same entry order -> identical results.
+template <int NT, int WARPS, int ENT, int MAXR, bool COUNT, bool LIST>
 __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
     k_forward_tc(TreeView tv, KParams kp, const double* __restrict__ xs,
                  const int32_t* __restrict__ perm, int64_t q, int nr,
                  const int* __restrict__ chmap, float* __restrict__ out, int out_stride,
-                 int only_ch, long long* __restrict__ counters, int* overflow) {
+                 int only_ch, long long* __restrict__ counters, IListView lv, int* overflow) {
   static_assert(ENT % 8 == 0, "ENT must be a multiple of the mma K (8)");
   constexpr int TR = 8 * NT;
   constexpr int F4 = 1 + TR / 4;               // global row float4 (dipole + radial)
@@ -177,8 +180,59 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
   long long c_vis = 0, c_fn = 0, c_ff = 0, c_pn = 0, c_pf = 0;
   const bool reg = kp.mode == KM_REGULARIZED;
 
-  int sp = 1;
-  if (lane == 0) stk[0] = make_int2(0, (int)active);
+  const int64_t wg = (int64_t)blockIdx.x * WARPS + w;
+  const int total = LIST ? __ldg(lv.count + wg) : -1;
+  if (LIST && total >= 0) {
+    // 32 entries at a time; their node records are prefetched into the
+    // (unused) stack region with cp.async, read back as broadcast LDS.128
+    const NodeRec* rb = reinterpret_cast<const NodeRec*>(stk);
+    const uint32_t s_rb = smem_u32(stk) + 48u * lane;
+    const double* xq = xs + 3 * qi;
+    int chunk = (int)wg;
+    for (int base = 0; base < total; base += 32) {
+      if (base > 0 && base % IL_CHUNK == 0) chunk = __ldg(lv.next + chunk);
+      const uint2 my = il_load(lv, chunk, base, total, lane);
+      const int n = min(32, total - base);
+      __syncwarp();  // the previous window's records are consumed
+      if (lane < n) {
+        const NodeRec* r = tv.node_rec + (my.x & IL_NODE);
+        cp_async16(s_rb, &r->hi);
+        cp_async16(s_rb + 16u, &r->lo);
+        cp_async16(s_rb + 32u, &r->topo);
+      }
+      cp_async_wait_all();
+      __syncwarp();
+      for (int i = 0; i < n; ++i) {
+        const uint32_t src = __shfl_sync(FULL_MASK, my.x, i);
+        const unsigned m = __shfl_sync(FULL_MASK, my.y, i);
+        const int node = (int)(src & IL_NODE);
+        const bool mine = (m >> lane) & 1u;
+        if (!(src & IL_LEAF)) {
+          const float4 hi = rb[i].hi, lo = rb[i].lo;
+          float dx, dy, dz;
+          const float s = dist2_df(hi, lo, qx, dx, dy, dz);
+          const float4 wv = mine ? fwd_w(dx, dy, dz, s, lo.w, kp) : make_float4(0.f, 0.f, 0.f, 0.f);
+          append(wv, node_row + (size_t)node * F4);
+        } else {
+          const int4 tp = rb[i].topo;
+          for (int j = tp.z; j < tp.w; ++j) {
+            float4 wv = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (mine) {
+              const PtRec* pr = tv.pt_rec + j;
+              const float4 ph = __ldg(&pr->hi);
+              float dx, dy, dz;
+              const float r2 = dist2_df(ph, __ldg(&pr->lo), qx, dx, dy, dz);
+              if (!(singular && r2 == 0.f && coincident_exact(tv.pt_pos64 + 3 * (size_t)j, xq)))
+                wv = fwd_w(dx, dy, dz, r2, ph.w, kp);
+            }
+            append(wv, pt_row + (size_t)j * F4);
+          }
+        }
+      }
+    }
+  }
+  int sp = (LIST && total >= 0) ? 0 : 1;
+  if (sp && lane == 0) stk[0] = make_int2(0, (int)active);
   __syncwarp();
   while (sp > 0) {
     --sp;
@@ -264,31 +318,36 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
     }
 }
 
-template <int NT, int WARPS, int ENT, int MAXR, bool COUNT>
-static void launch_tc1(const Tree& t, const KParams& kp, const FwdArgs& a, int nr) {
+template <int NT, int WARPS, int ENT, int MAXR, bool COUNT, bool LIST>
+static void launch_tc1(const Tree& t, const KParams& kp, const FwdArgs& a, int nr,
+                       IListView lv = {}) {
   constexpr int F4 = 1 + 2 * NT;
   constexpr int RSF = row_stride_floats(F4);
   constexpr int WARP_FLOATS = ENT * 32 * 4 + ENT * 40 + ENT * RSF + 2 * DPL_STACK_PER_WARP;
   const size_t smem = (size_t)WARPS * WARP_FLOATS * 4;
   static bool attr = false;
   if (!attr) {
-    DPL_CUDA(cudaFuncSetAttribute(k_forward_tc<NT, WARPS, ENT, MAXR, COUNT>,
+    DPL_CUDA(cudaFuncSetAttribute(k_forward_tc<NT, WARPS, ENT, MAXR, COUNT, LIST>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
   unsigned blocks = (unsigned)((a.q + WARPS * 32 - 1) / (WARPS * 32));
-  k_forward_tc<NT, WARPS, ENT, MAXR, COUNT><<<blocks, WARPS * 32, smem, t.stream>>>(
+  k_forward_tc<NT, WARPS, ENT, MAXR, COUNT, LIST><<<blocks, WARPS * 32, smem, t.stream>>>(
       t.view(), kp, a.xs, a.perm, a.q, nr, t.chmap.as<int>(), a.out, a.out_stride, a.only_ch,
-      a.counters, a.overflow);
+      a.counters, lv, a.overflow);
   count_launch();
 }
 
 template <int NT, int WARPS, int ENT, int MAXR>
 static void launch_tc(const Tree& t, const KParams& kp, const FwdArgs& a, int nr) {
   if (a.counters)
-    launch_tc1<NT, WARPS, ENT, MAXR, true>(t, kp, a, nr);
+    launch_tc1<NT, WARPS, ENT, MAXR, true, false>(t, kp, a, nr);
+  else if (a.ilist && !no_ilist()) {
+    ilist_build(t, *a.ilist, a.xs, a.perm, a.q, a.beta, a.overflow);
+    launch_tc1<NT, WARPS, ENT, MAXR, false, true>(t, kp, a, nr, a.ilist->view());
+  }
   else
-    launch_tc1<NT, WARPS, ENT, MAXR, false>(t, kp, a, nr);
+    launch_tc1<NT, WARPS, ENT, MAXR, false, false>(t, kp, a, nr);
 }
 
 // Tensor-core plan: one dipole slot and PR a multiple of 8 (8..64 radial).

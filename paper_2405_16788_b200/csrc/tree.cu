@@ -463,6 +463,7 @@ static T* sbuf(Tree& t, int slot, size_t count) {
 
 void tree_update_points(Tree& t, const double* pos, const double* nrm, const double* area,
                         const double* mu) {
+  ++t.version;
   size_t n = (size_t)t.n;
   DPL_CUDA(cudaMemcpyAsync(t.pos64.p, pos, n * 3 * 8, cudaMemcpyDefault, t.stream));
   DPL_CUDA(cudaMemcpyAsync(t.nrm64.p, nrm, n * 3 * 8, cudaMemcpyDefault, t.stream));
@@ -523,6 +524,7 @@ void tree_ensure_thresholds(Tree& t, double beta) {
 void tree_build(Tree& t, const double* pos, const double* nrm, const double* area,
                 const double* mu, int64_t n, int C, int max_leaf, int max_depth) {
   if (n <= 0) throw Error(2, "DipoleTree::build: empty cloud");
+  ++t.version;
   if (n >= (int64_t)INT32_MAX) throw Error(1, "dpl_tree_build: more than 2^31-1 points");
   if (C < 1 || C > DPL_MAX_CHANNELS) throw Error(1, "dpl_tree_build: channel count out of range");
   max_leaf = std::max(1, max_leaf);   // :162

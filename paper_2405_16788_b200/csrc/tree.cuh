@@ -38,6 +38,7 @@ struct Tree {
   int Cd = 0, Cr = 0, PR = 0, F4 = 1;  // dipole / radial channel counts, radial pad, row float4s
   std::vector<int> dip_ch, rad_ch, slot_of;
   double root_lo[3] = {0, 0, 0}, root_hi[3] = {0, 0, 0};
+  uint64_t version = 0;    // bumped by build / update_points (invalidates interaction lists)
   double thr_beta = -1.0;  // beta the thresholds were computed for (NaN-safe compare)
   bool thr_valid = false;
 

@@ -225,6 +225,17 @@ def epsilon_for(name, scale=1.0):
     return EPSILON[name] / math.sqrt(scale)
 
 
+def step_queries(w, rank, k):
+    """Query batch k of a rank: k = 0 is rank_queries(); k > 0 are fresh draws
+    from the same distribution (benchmarks alternate batches so that no step
+    can reuse the previous step's traversal)."""
+    if k == 0:
+        return rank_queries(w, rank)
+    lo, hi = {"config1": (-1.5, 1.5), "config2": (-2, 2), "config4": (-2, 2)}[w["name"]]
+    q = w["xs"].shape[0]
+    return _f32(np.random.default_rng([7919, rank, k]).uniform(lo, hi, (q, 3)))
+
+
 def rank_queries(w, rank, seed=0):
     """Weak scaling: rank r > 0 draws its own queries from the same distribution."""
     if rank == 0:

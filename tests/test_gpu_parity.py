@@ -377,7 +377,8 @@ def test_host_pointer_pipeline_matches_device_path(eng, oracle_mod):
 
 
 @pytest.mark.parametrize("env", ["DPL_ADJOINT_TC", "DPL_ADJOINT_SINGLE_PHASE",
-                                 "DPL_FORWARD_NO_TC", "DPL_FORWARD_SINGLE_PHASE"])
+                                 "DPL_FORWARD_NO_TC", "DPL_FORWARD_SINGLE_PHASE",
+                                 "DPL_NO_ILIST", "DPL_ILIST_POOL"])
 def test_alternate_kernel_paths(env):
     """The opt-in / fallback kernels (selected once per process from the
     environment) pass the same forward / adjoint / render parity tests."""
@@ -391,3 +392,45 @@ def test_alternate_kernel_paths(env):
          "-m", "gpu", "-k", "(adjoint or render or many_channel or primal) and not alternate"],
         env=dict(os.environ, **{env: "1"}), capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+def test_interaction_list_reuse_is_keyed_on_the_batch(eng, oracle_mod):
+    """The adjoint reuses the primal's interaction lists only for bit-identical
+    queries (same tree, beta, count): queries edited in place in the same
+    device buffer, a different beta, or a rebuilt tree all re-traverse."""
+    import torch
+
+    O = oracle_mod
+    pos, nrm, area, mu = random_cloud(3000, 31, 49)
+    kinds = np.ones(49, np.uint8)
+    kinds[0] = 0
+    t, r = make(eng, O, pos, nrm, area, mu, kinds)
+    rng = np.random.default_rng(32)
+    q = 4096
+    xs1 = rng.uniform(-1.2, 1.2, (q, 3))
+    xs2 = rng.uniform(-1.2, 1.2, (q, 3))
+    d_out = rng.standard_normal((q, 49)).astype(np.float32)
+    p = eng.KernelParams(epsilon=0.05)
+    dev = torch.from_numpy(xs1).cuda()
+    ddo = torch.from_numpy(d_out).cuda()
+    for beta_f, beta_a in ((2.0, 2.0), (2.0, 3.0)):
+        dev.copy_(torch.from_numpy(xs1))
+        t.primal(dev, p, beta_f)  # lists for xs1 at beta_f
+        dev.copy_(torch.from_numpy(xs2))  # same pointer, new content
+        b = t.make_buffer()
+        t.adjoint(dev, p, beta_a, ddo, None, b)
+        g = t.flush_gradients(b)
+        wm, wn, we = r.adjoint(O.Params(0.05), beta_a, xs2, d_out.astype(np.float64))
+        assert rel_scale_err(g.moments, wm) < 1e-5
+        assert rel_scale_err(g.normals, wn) < 1e-5
+        # and a primal on the edited buffer matches the oracle too
+        got = t.primal(dev, p, beta_a).cpu().numpy()
+        assert close(got, r.primal(O.Params(0.05), beta_a, xs2))[0] == 0
+    # rebuilt tree (same queries): lists are rebuilt as well
+    pos2 = pos + 0.01
+    t.build(eng.OrientedPointCloud(pos2, nrm, area, mu))
+    t.set_channel_kernels(kinds)
+    r2 = O.OracleTree(O.Cloud(pos2, nrm, area, mu))
+    r2.set_kinds(kinds)
+    got = t.primal(dev, p, 2.0).cpu().numpy()
+    assert close(got, r2.primal(O.Params(0.05), 2.0, xs2))[0] == 0
