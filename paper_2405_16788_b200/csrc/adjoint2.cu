@@ -164,7 +164,7 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
   const unsigned active = __ballot_sync(FULL_MASK, valid);
   if (!active) return;
   const int Cr = tv.Cr;
-  const QueryDF qx = make_qdf(x);
+  const QueryDF qx = make_qdf(x, tv.cmax);
   // fp64 position for the exact fallbacks, re-read there (invalid lanes never test)
   const double* xq = xs + 3 * qi;
 

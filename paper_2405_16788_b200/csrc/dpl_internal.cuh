@@ -88,6 +88,7 @@ struct TreeView {
   int Cd, Cr, C;
   int64_t nodes, n;
   int max_depth;
+  float cmax;  // >= max |centroid coordinate| (root bounding box, with margin)
 };
 
 // Fast host->device constant table of channel mapping for kernels.

@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
   }
   const unsigned active = __ballot_sync(FULL_MASK, valid);
   if (!active) return;
-  const QueryDF qx = make_qdf(x);
+  const QueryDF qx = make_qdf(x, tv.cmax);
 
   float accd[TD > 0 ? TD : 1], accr[TR > 0 ? TR : 1];
 #pragma unroll

@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
   }
   const unsigned active = __ballot_sync(FULL_MASK, valid);
   if (!active) return;
-  const QueryDF qx = make_qdf(x);
+  const QueryDF qx = make_qdf(x, tv.cmax);
 
   float accd = 0.f;
   float acc[2][NT][4];

@@ -41,10 +41,8 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
                  const int* skip, int* overflow) {
   if (skip && *skip) return;  // lists of this exact batch are already in place
   __shared__ int2 stk_all[WARPS][DPL_STACK_PER_WARP];
-  __shared__ uint2 buf_all[WARPS][32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   int2* stk = stk_all[w];
-  uint2* buf = buf_all[w];
   const int64_t wg = (int64_t)blockIdx.x * WARPS + w;
   const int64_t sidx = wg * 32 + lane;
   const bool valid = sidx < q;
@@ -57,37 +55,28 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
   }
   const unsigned active = __ballot_sync(FULL_MASK, valid);
   if (!active) return;  // evaluation kernels return for such warps too
-  const QueryDF qx = make_qdf(x);
+  const QueryDF qx = make_qdf(x, tv.cmax);
   const double* xq = xs + 3 * qi;
 
   int cur = (int)wg;  // chunk being filled (warp w owns chunk w)
   int total = 0;      // entries written
-  int nb = 0;         // entries buffered in shared memory
   bool ok = true;
-
-  auto flush = [&]() {
-    __syncwarp();
-    if (total > 0 && total % IL_CHUNK == 0) {  // chunk full: link a fresh one
+  // lane 0 appends each entry with one 8-byte store (a warp's entries are
+  // contiguous within a chunk, so L2 merges them into full sectors)
+  auto emit = [&](uint32_t src, uint32_t m) {
+    if (total > 0 && (total & (IL_CHUNK - 1)) == 0) {  // chunk full: link a fresh one
       unsigned long long c = 0;
       if (lane == 0) c = atomicAdd(ctr, 1ull);
       c = __shfl_sync(FULL_MASK, c, 0);
       if (c >= (unsigned long long)chunks) {  // pool exhausted: this warp traverses itself
         ok = false;
-        nb = 0;
         return;
       }
       if (lane == 0) next[cur] = (int)c;
       cur = (int)c;
     }
-    if (lane < nb) pool[(size_t)cur * IL_CHUNK + total % IL_CHUNK + lane] = buf[lane];
-    total += nb;
-    nb = 0;
-    __syncwarp();
-  };
-  auto emit = [&](uint32_t src, uint32_t m) {
-    if (!ok) return;
-    if (lane == 0) buf[nb] = make_uint2(src, m);
-    if (++nb == 32) flush();
+    if (lane == 0) pool[(size_t)cur * IL_CHUNK + (total & (IL_CHUNK - 1))] = make_uint2(src, m);
+    ++total;
   };
 
   int sp = 1;
@@ -110,7 +99,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
     const unsigned farm = __ballot_sync(FULL_MASK, far);
     if (farm && lo.w > 0.f) emit((uint32_t)node, farm);
     const unsigned openm = mask & ~farm;
-    if (openm) {
+    if (openm && ok) {
       if (tp.y == 0) {
         emit((uint32_t)node | IL_LEAF, openm);
       } else {
@@ -124,13 +113,12 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
       }
     }
   }
-  if (ok && nb) flush();
   if (lane == 0) count[wg] = ok ? total : -1;
 }
 
 void ilist_build(const Tree& t, IList& il, const double* xs, const int32_t* perm, int64_t q,
                  double beta, int* overflow) {
-  constexpr int WARPS = 4, MINB = 10;
+  constexpr int WARPS = 4, MINB = 12;
   const int64_t nwarps = (q + 31) / 32;
   static const char* pool_env = getenv("DPL_ILIST_POOL");  // chunks per warp (tests: 1 forces
   if (pool_env && il.nwarps == 0) il.per_warp = atof(pool_env);  // incomplete lists)

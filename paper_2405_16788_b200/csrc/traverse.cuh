@@ -36,7 +36,8 @@ __device__ __forceinline__ double dist2_rn(double cx, double cy, double cz, cons
 
 // Query in double-float form (x = hi + lo to ~2^-48) plus its fp64 original.
 struct QueryDF {
-  float hx, hy, hz, lx, ly, lz, m;  // m = max |x_hi|
+  float hx, hy, hz, lx, ly, lz;
+  float m;  // absolute part of the opening-test error band, 1e-13 (cmax + max|x|)^2
 };
 
 // the empty asm makes each value opaque, so the compiler keeps the 7 floats
@@ -46,12 +47,14 @@ __device__ __forceinline__ float opaque(float v) {
   return v;
 }
 
-__device__ __forceinline__ QueryDF make_qdf(const QueryPos& x) {
+// cmax >= max |centroid coordinate| over the tree (TreeView::cmax)
+__device__ __forceinline__ QueryDF make_qdf(const QueryPos& x, float cmax) {
   QueryDF q;
   q.hx = (float)x.x, q.hy = (float)x.y, q.hz = (float)x.z;
   q.lx = opaque((float)(x.x - (double)q.hx)), q.ly = opaque((float)(x.y - (double)q.hy)),
   q.lz = opaque((float)(x.z - (double)q.hz));
-  q.m = opaque(fmaxf(fmaxf(fabsf(q.hx), fabsf(q.hy)), fabsf(q.hz)));
+  const float M = cmax + fmaxf(fmaxf(fabsf(q.hx), fabsf(q.hy)), fabsf(q.hz));
+  q.m = opaque(1e-13f * M * M);
   q.hx = opaque(q.hx), q.hy = opaque(q.hy), q.hz = opaque(q.hz);
   return q;
 }
@@ -67,14 +70,15 @@ __device__ __forceinline__ float dist2_df(const float4& hi, const float4& lo, co
 
 // The reference's opening test dist2 > (beta^2 r) r (bhtree.cpp:204), decided
 // in fp32 when the margin exceeds a rigorous error bound (dist2 error
-// <= 2^-21 s + 2^-46 M^2, threshold rounding 2^-24 thr; the band below is 2x
-// that), else re-evaluated exactly in fp64 with the reference's operation
-// order. NaN / inf thresholds (beta = inf) always take the exact path.
+// <= 2^-21 s + 2^-46 M^2 with M = |c| + |x| <= cmax + max|x|, threshold
+// rounding 2^-24 thr; the band below is 2x that, its absolute part precomputed
+// per query in QueryDF::m), else re-evaluated exactly in fp64 with the
+// reference's operation order. NaN / inf thresholds (beta = inf) always take
+// the exact path.
 __device__ __forceinline__ bool far_test(float s, const float4& hi, const QueryDF& q,
                                          const QueryPos& x, const double4* __restrict__ dec) {
   const float thr = hi.w;
-  const float M = fmaxf(fmaxf(fabsf(hi.x), fabsf(hi.y)), fabsf(hi.z)) + q.m;
-  const float band = 2e-6f * (s + thr) + 1e-13f * M * M;
+  const float band = 2e-6f * (s + thr) + q.m;
   const float diff = s - thr;
   if (diff > band) return true;
   if (-diff > band) return false;
@@ -90,8 +94,7 @@ __device__ __forceinline__ bool far_test(float s, const float4& hi, const QueryD
                                          const double* __restrict__ xq,
                                          const double4* __restrict__ dec) {
   const float thr = hi.w;
-  const float M = fmaxf(fmaxf(fabsf(hi.x), fabsf(hi.y)), fabsf(hi.z)) + q.m;
-  const float band = 2e-6f * (s + thr) + 1e-13f * M * M;
+  const float band = 2e-6f * (s + thr) + q.m;
   const float diff = s - thr;
   if (diff > band) return true;
   if (-diff > band) return false;

@@ -119,6 +119,9 @@ TreeView Tree::view() const {
   v.nodes = nodes;
   v.n = n;
   v.max_depth = max_depth;
+  double cm = 0.0;  // centroids lie in the root bounding box
+  for (int a = 0; a < 3; ++a) cm = std::max(cm, std::max(std::fabs(root_lo[a]), std::fabs(root_hi[a])));
+  v.cmax = (float)(cm * 1.001) + 1e-30f;
   return v;
 }
 
