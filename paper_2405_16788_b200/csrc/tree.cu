@@ -295,7 +295,10 @@ __global__ void k_gather_points(const int32_t* __restrict__ order, const double*
   pt_rec[j] = r;
 }
 
-// K3: geometry, one thread per node, sequential in point_order (bit-exact).
+// K3: geometry, sequential in point_order (bit-exact). Nodes of up to
+// GEO_BIG points: one thread per node. Larger nodes: k_geometry_warp.
+constexpr int GEO_BIG = 64;
+
 __global__ void k_geometry(const int32_t* __restrict__ beg, const int32_t* __restrict__ end,
                            int64_t nodes, const double* __restrict__ pt_pos64,
                            const int32_t* __restrict__ order, const double* __restrict__ area,
@@ -304,6 +307,7 @@ __global__ void k_geometry(const int32_t* __restrict__ beg, const int32_t* __res
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= nodes) return;
   int32_t b = beg[i], e = end[i];
+  if (e - b > GEO_BIG) return;
   double cx, cy, cz, asum, rad;
   if (e - b == 1) {  // bitwise copies for single-point nodes (:109-116)
     asum = area[order[b]];
@@ -344,6 +348,78 @@ __global__ void k_geometry(const int32_t* __restrict__ beg, const int32_t* __res
   nrad[i] = rad;
   flag[i] = asum > 0 ? 1 : 0;
   geo[i] = make_float4((float)cx, (float)cy, (float)cz, (float)(asum * kInvFourPi));
+}
+
+// Large nodes, one warp each. The sums stay sequential in point_order (the
+// reference's rounding, bhtree.cpp:117-124): the warp stages 32 points in
+// shared memory with coalesced loads and lane 0 runs the fp64 chains, so the
+// load latency is off the dependency chain. The radius is a max (order-free:
+// the same `r < s ? s : r` comparator in a lane-parallel reduction).
+template <int WARPS>
+__global__ void __launch_bounds__(WARPS * 32)
+    k_geometry_warp(const int32_t* __restrict__ beg, const int32_t* __restrict__ end,
+                    int64_t nodes, const double* __restrict__ pt_pos64,
+                    const int32_t* __restrict__ order, const double* __restrict__ area,
+                    double* ctr, double* narea, double* nrad, uint8_t* flag, float4* geo) {
+  __shared__ double4 stage[WARPS][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t i = (int64_t)blockIdx.x * WARPS + w;
+  if (i >= nodes) return;
+  const int32_t b = beg[i], e = end[i];
+  if (e - b <= GEO_BIG) return;
+  double asum = 0, px = 0, py = 0, pz = 0, mx = 0, my = 0, mz = 0;
+  for (int32_t base = b; base < e; base += 32) {
+    const int32_t j = base + lane;
+    if (j < e)
+      stage[w][lane] = make_double4(area[order[j]], pt_pos64[3 * (size_t)j],
+                                    pt_pos64[3 * (size_t)j + 1], pt_pos64[3 * (size_t)j + 2]);
+    __syncwarp();
+    if (lane == 0) {
+      const int n = min(32, e - base);
+      for (int k = 0; k < n; ++k) {
+        const double4 v = stage[w][k];
+        asum = __dadd_rn(asum, v.x);
+        px = __dadd_rn(px, __dmul_rn(v.x, v.y));
+        py = __dadd_rn(py, __dmul_rn(v.x, v.z));
+        pz = __dadd_rn(pz, __dmul_rn(v.x, v.w));
+        mx = __dadd_rn(mx, v.y);
+        my = __dadd_rn(my, v.z);
+        mz = __dadd_rn(mz, v.w);
+      }
+    }
+    __syncwarp();
+  }
+  double cx = 0, cy = 0, cz = 0;
+  if (lane == 0) {
+    if (asum > 0) {
+      cx = __ddiv_rn(px, asum), cy = __ddiv_rn(py, asum), cz = __ddiv_rn(pz, asum);
+    } else {
+      const double cnt = (double)(e - b);
+      cx = __ddiv_rn(mx, cnt), cy = __ddiv_rn(my, cnt), cz = __ddiv_rn(mz, cnt);
+    }
+  }
+  cx = __shfl_sync(0xffffffffu, cx, 0);
+  cy = __shfl_sync(0xffffffffu, cy, 0);
+  cz = __shfl_sync(0xffffffffu, cz, 0);
+  double r2max = 0;
+  for (int32_t j = b + lane; j < e; j += 32) {
+    const double dx = __dsub_rn(pt_pos64[3 * (size_t)j], cx);
+    const double dy = __dsub_rn(pt_pos64[3 * (size_t)j + 1], cy);
+    const double dz = __dsub_rn(pt_pos64[3 * (size_t)j + 2], cz);
+    const double s = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+    r2max = r2max < s ? s : r2max;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const double other = __shfl_xor_sync(0xffffffffu, r2max, o);
+    r2max = r2max < other ? other : r2max;
+  }
+  if (lane == 0) {
+    ctr[3 * i] = cx, ctr[3 * i + 1] = cy, ctr[3 * i + 2] = cz;
+    narea[i] = asum;
+    nrad[i] = __dsqrt_rn(r2max);
+    flag[i] = asum > 0 ? 1 : 0;
+    geo[i] = make_float4((float)cx, (float)cy, (float)cz, (float)(asum * kInvFourPi));
+  }
 }
 
 __global__ void k_topo(const int32_t* __restrict__ beg, const int32_t* __restrict__ end,
@@ -712,7 +788,11 @@ void tree_build(Tree& t, const double* pos, const double* nrm, const double* are
       beg.as<int32_t>(), end.as<int32_t>(), nodes, t.pt_pos64.as<double>(), t.order.as<int32_t>(),
       t.area64.as<double>(), t.node_ctr64.as<double>(), t.node_area64.as<double>(),
       t.node_rad64.as<double>(), t.node_flag.as<uint8_t>(), t.node_geo.as<float4>());
-  count_launch();
+  k_geometry_warp<4><<<(unsigned)((nodes + 3) / 4), 128, 0, s>>>(
+      beg.as<int32_t>(), end.as<int32_t>(), nodes, t.pt_pos64.as<double>(), t.order.as<int32_t>(),
+      t.area64.as<double>(), t.node_ctr64.as<double>(), t.node_area64.as<double>(),
+      t.node_rad64.as<double>(), t.node_flag.as<uint8_t>(), t.node_geo.as<float4>());
+  count_launch(2);
   DPL_CUDA(cudaGetLastError());
   t.set_layout();
   tree_compute_moments(t);
