@@ -397,6 +397,16 @@ def run_ours(args):
             dist.destroy_process_group()
         return
 
+    # DRAM bytes per launch of the dominant kernel from the committed ncu capture
+    traffic = {}
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as f:
+            tj = json.load(f)
+        traffic["_source"] = tj["_source"]
+        for k in ("adjoint", "forward"):
+            traffic[k] = {"bytes": tj[k]["dram_read"] + tj[k]["dram_write"]}
+    except (OSError, KeyError, ValueError):
+        pass
     peak32 = B.peak_fp32(local)
     peak64 = B.peak_fp64(local)
     dom = "adjoint" if adj_ms >= fwd_ms else "forward"
@@ -439,13 +449,15 @@ def run_ours(args):
                      "flush": flush_ms},
         "interactions_per_query": float((tot[1] + tot[2] + tot[3] + tot[4]) / Q),
         "visited_per_query": float(tot[0] / Q),
-        "roofline": {"bound": "fp32", "kernel": f"k_{dom} (warp-cooperative traversal)",
+        "roofline": {"bound": "fp32", "kernel": {"adjoint": "k_adjoint2 (interaction-list replay)",
+                                                 "forward": "k_build_list + k_forward_tc"}[dom],
                      "achieved": achieved, "peak": peak32, "unit": "TFLOP/s",
                      "frac": achieved / peak32,
                      "peak_source": "measured FFMA microbenchmark in this run (dpl_peak_fp32); "
                                     "MEASURED_PEAKS.json has no FP32 figure",
                      "flops_per_launch": dom_flops, "flop_model": "SURVEY §8(d) cost model v1",
-                     "traffic": None,
+                     "traffic": traffic.get(dom, {}).get("bytes"),
+                     "traffic_source": traffic.get("_source"),
                      "hbm_compulsory_bytes_forward": bytes_fwd,
                      "peak_fp64_measured": peak64},
         "gpu_launches": int(launches),

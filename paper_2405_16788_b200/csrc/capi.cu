@@ -39,6 +39,20 @@ struct dpl_tree_s {
   // calls are tracked with events instead of a synchronize per call
   bool host_async = false;
   IList il;  // interaction lists of the last batch (ilist.cuh)
+  // List policy. Building lists costs one extra pass (~5 ms per 4M queries),
+  // repaid only when an adjoint follows a primal on the same batch. The
+  // handle watches the call pattern: after a primal -> adjoint pair on the
+  // same queries it builds lists in the next primal for that adjoint to reuse;
+  // a primal whose lists no adjoint consumed switches back to the fused
+  // kernels. (Policy only: reuse itself is verified on the device.)
+  struct {
+    const void* xs = nullptr;
+    int64_t q = 0;
+    double beta = 0;
+    bool listed = false;
+  } last_fwd;
+  bool last_was_fwd = false;
+  bool want_lists = false;
   cudaEvent_t ev_fwd_in = nullptr, ev_fwd_out = nullptr, ev_adj_in = nullptr;
   void sync_all() {
     if (copy) DPL_CUDA(cudaStreamSynchronize(copy));
@@ -476,6 +490,11 @@ static int forward_common(dpl_tree_t h, const dpl_kernel_params* params, double 
     DPL_CUDA(cudaSetDevice(t.device));
     KParams kp = make_kparams(params->epsilon, params->desingularized, params->desing_delta);
     tree_ensure_thresholds(t, beta);
+    // list policy (see dpl_tree_s): lists only for plain value batches
+    if (h->last_was_fwd && h->last_fwd.listed) h->want_lists = false;  // unconsumed
+    const bool lists = (h->want_lists || ilist_always()) && grad_mode == 0 && !counters;
+    h->last_fwd = {xs, q, beta, lists};
+    h->last_was_fwd = true;
     const bool xs_host = !is_device_ptr(xs);
     const bool out_host = !is_device_ptr(out);
     const bool grad_host = grad && !is_device_ptr(grad);
@@ -513,7 +532,7 @@ static int forward_common(dpl_tree_t h, const dpl_kernel_params* params, double 
         a.perm = perm;
         a.q = qc;
         a.overflow = ovf;
-        a.ilist = &h->il;
+        a.ilist = lists ? &h->il : nullptr;
         a.beta = beta;
         a.out = out_d + c0 * stride;
         a.out_stride = stride;
@@ -547,7 +566,7 @@ static int forward_common(dpl_tree_t h, const dpl_kernel_params* params, double 
     a.perm = h->ws_perm.as<int32_t>();
     a.q = q;
     a.overflow = overflow_flag(h);
-    a.ilist = &h->il;
+    a.ilist = lists ? &h->il : nullptr;
     a.beta = beta;
     Out<float> o, g;
     Out<long long> cnt;
@@ -660,6 +679,12 @@ int dpl_adjoint(dpl_tree_t h, const dpl_kernel_params* params, double beta_bh, c
     DPL_CUDA(cudaSetDevice(t.device));
     KParams kp = make_kparams(params->epsilon, params->desingularized, params->desing_delta);
     tree_ensure_thresholds(t, beta_bh);
+    // list policy (see dpl_tree_s)
+    const bool pair = h->last_was_fwd && h->last_fwd.xs == (const void*)xs &&
+                      h->last_fwd.q == q && h->last_fwd.beta == beta_bh;
+    const bool lists = (pair && h->last_fwd.listed) || ilist_always();
+    h->want_lists = pair;
+    h->last_was_fwd = false;
     const bool xs_host = !is_device_ptr(xs), do_host = !is_device_ptr(d_out);
     const bool dg_host = d_grad && !is_device_ptr(d_grad);
     if ((xs_host || do_host || dg_host) && q > (1 << 18)) {
@@ -701,7 +726,7 @@ int dpl_adjoint(dpl_tree_t h, const dpl_kernel_params* params, double beta_bh, c
         a.d_grad = dg_d ? dg_d + c0 * t.C * 3 : nullptr;
         a.grad_mode = dg_d ? 1 : 0;
         a.overflow = ovf;
-        a.ilist = &h->il;
+        a.ilist = lists ? &h->il : nullptr;
         a.beta = beta_bh;
         PhaseTimer pt(t, PH_ADJOINT);
         adjoint_launch(t, kp, a, buf->b);
@@ -727,7 +752,7 @@ int dpl_adjoint(dpl_tree_t h, const dpl_kernel_params* params, double beta_bh, c
     a.d_grad = dg_d;
     a.grad_mode = dg_d ? 1 : 0;
     a.overflow = overflow_flag(h);
-    a.ilist = &h->il;
+    a.ilist = lists ? &h->il : nullptr;
     a.beta = beta_bh;
     {
       PhaseTimer pt(t, PH_ADJOINT);

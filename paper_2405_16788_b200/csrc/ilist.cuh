@@ -55,6 +55,12 @@ inline bool no_ilist() {
   static const bool v = getenv("DPL_NO_ILIST") != nullptr;
   return v;
 }
+// DPL_ILIST_ALWAYS set: every primal / adjoint builds or reuses lists,
+// whatever the call pattern (tests of the replay kernels)
+inline bool ilist_always() {
+  static const bool v = getenv("DPL_ILIST_ALWAYS") != nullptr && !no_ilist();
+  return v;
+}
 
 // Lists for q queries (device xs, Morton permutation perm) at opening
 // parameter beta. When the previous lists were built for the same tree

@@ -48,8 +48,11 @@ def summarize(path, dst, title):
             try:
                 fv = float(v.replace(",", ""))
                 u = units[hdr.index(k)] if k in hdr else ""
-                if k == "gpu__time_duration.sum" and u == "ms":
-                    sc = 1
+                if k == "gpu__time_duration.sum":
+                    sc = {"ms": 1, "us": 1e-3, "ns": 1e-6, "s": 1e3}.get(u, sc)
+                if k.startswith("dram__bytes"):  # report MB whatever unit ncu chose
+                    sc = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1, "Gbyte": 1e3,
+                          "Tbyte": 1e6}.get(u, sc)
                 v = f"{fv * sc:.4g}"
             except (ValueError, AttributeError):
                 pass

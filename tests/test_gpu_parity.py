@@ -378,7 +378,7 @@ def test_host_pointer_pipeline_matches_device_path(eng, oracle_mod):
 
 @pytest.mark.parametrize("env", ["DPL_ADJOINT_TC", "DPL_ADJOINT_SINGLE_PHASE",
                                  "DPL_FORWARD_NO_TC", "DPL_FORWARD_SINGLE_PHASE",
-                                 "DPL_NO_ILIST", "DPL_ILIST_POOL"])
+                                 "DPL_NO_ILIST", "DPL_ILIST_POOL", "DPL_ILIST_ALWAYS"])
 def test_alternate_kernel_paths(env):
     """The opt-in / fallback kernels (selected once per process from the
     environment) pass the same forward / adjoint / render parity tests."""
@@ -389,7 +389,8 @@ def test_alternate_kernel_paths(env):
     here = os.path.dirname(os.path.abspath(__file__))
     r = subprocess.run(
         [sys.executable, "-m", "pytest", os.path.join(here, "test_gpu_parity.py"), "-q", "-x",
-         "-m", "gpu", "-k", "(adjoint or render or many_channel or primal) and not alternate"],
+         "-m", "gpu", "-k",
+         "(adjoint or render or many_channel or primal or interaction_list) and not alternate"],
         env=dict(os.environ, **{env: "1"}), capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
 
@@ -413,8 +414,13 @@ def test_interaction_list_reuse_is_keyed_on_the_batch(eng, oracle_mod):
     p = eng.KernelParams(epsilon=0.05)
     dev = torch.from_numpy(xs1).cuda()
     ddo = torch.from_numpy(d_out).cuda()
+    b0 = t.make_buffer()
     for beta_f, beta_a in ((2.0, 2.0), (2.0, 3.0)):
         dev.copy_(torch.from_numpy(xs1))
+        # a primal -> adjoint pair on this buffer makes the next primal build lists
+        t.primal(dev, p, beta_f)
+        t.adjoint(dev, p, beta_f, ddo, None, b0)
+        b0.reset()
         t.primal(dev, p, beta_f)  # lists for xs1 at beta_f
         dev.copy_(torch.from_numpy(xs2))  # same pointer, new content
         b = t.make_buffer()
