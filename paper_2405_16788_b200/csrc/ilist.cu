@@ -20,6 +20,21 @@ __global__ void k_set_u64(unsigned long long* p, unsigned long long v, const int
   *p = v;
 }
 __global__ void k_set_int(int* p, int v) { *p = v; }
+// chunk usage to mapped pinned memory: a kernel store, not a D2H copy that
+// would wait behind a host-async download on the copy engine
+__global__ void k_publish_u64(volatile unsigned long long* host, const unsigned long long* v) {
+  *host = *v;
+}
+// SM copy (not cudaMemcpy: a D2D copy-engine transfer would queue behind a
+// host-async D2H in flight on the same engine); skipped when the batch is unchanged
+__global__ void k_copy_u64(unsigned long long* __restrict__ dst,
+                           const unsigned long long* __restrict__ src, int64_t n,
+                           const int* skip) {
+  if (skip && *skip) return;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = __ldg(src + i);
+}
 // same = 0 if any coordinate differs bitwise (NaN payloads included)
 __global__ void k_compare(const unsigned long long* __restrict__ a,
                           const unsigned long long* __restrict__ b, int64_t n, int* same) {
@@ -128,7 +143,7 @@ void ilist_build(const Tree& t, IList& il, const double* xs, const int32_t* perm
     if (used > 0.8 * il.per_warp && !pool_env) il.per_warp = std::min(64.0, used * 1.5);
   }
   if (!il.used_host) {
-    DPL_CUDA(cudaMallocHost(&il.used_host, sizeof(unsigned long long)));
+    DPL_CUDA(cudaHostAlloc(&il.used_host, sizeof(unsigned long long), cudaHostAllocMapped));
     *il.used_host = 0;
   }
   il.same.reserve(sizeof(int));
@@ -161,12 +176,17 @@ void ilist_build(const Tree& t, IList& il, const double* xs, const int32_t* perm
       il.ctr.as<unsigned long long>(), chunks, skip, overflow);
   count_launch();
   // chunks actually used, read back without a sync (sizes the next build)
-  DPL_CUDA(cudaMemcpyAsync(il.used_host, il.ctr.p, sizeof(unsigned long long),
-                           cudaMemcpyDeviceToHost, t.stream));
+  unsigned long long* used_dev = nullptr;
+  DPL_CUDA(cudaHostGetDevicePointer((void**)&used_dev, il.used_host, 0));
+  k_publish_u64<<<1, 1, 0, t.stream>>>(used_dev, il.ctr.as<unsigned long long>());
+  count_launch();
   // remember the batch the lists now describe (whether rebuilt or reused; the
   // host cannot tell without a sync, and the copy is ~0.03 ms per 4M queries)
   il.xs_copy.reserve((size_t)q * 24);
-  DPL_CUDA(cudaMemcpyAsync(il.xs_copy.p, xs, (size_t)q * 24, cudaMemcpyDeviceToDevice, t.stream));
+  k_copy_u64<<<8 * 148, 256, 0, t.stream>>>(il.xs_copy.as<unsigned long long>(),
+                                             reinterpret_cast<const unsigned long long*>(xs),
+                                             3 * q, skip);
+  count_launch();
   il.valid = true;
   il.q = q;
   il.beta = beta;
