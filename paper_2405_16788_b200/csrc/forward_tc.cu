@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
   const QueryDF qx = make_qdf(x, tv.cmax);
 
   float accd = 0.f;
-  float acc[2][NT][4];
+  float acc[2][NT ? NT : 1][4];  // NT = 0: dipole-only variant (primal_channel of the dipole)
 #pragma unroll
   for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
@@ -117,6 +117,7 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
   const bool singular = kp.mode == KM_SINGULAR;
   const float4* __restrict__ node_row = tv.node_row;
   const float4* __restrict__ pt_row = tv.pt_row;
+  const int F4g = tv.F4;  // row stride in HBM (== F4 unless NT = 0)
   int nent = 0;
 
   auto evaluate = [&]() {
@@ -134,7 +135,7 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
       accd = fmaf(wv.x, v.x, fmaf(wv.y, v.y, fmaf(wv.z, v.z, accd)));
     }
     // radial channels on the tensor cores
-    const int ksteps = (nent + 7) >> 3;
+    const int ksteps = NT > 0 ? (nent + 7) >> 3 : 0;
     for (int ks = 0; ks < ksteps; ++ks) {
       const int e0 = 8 * ks;
       uint32_t ah[2][4], al[2][4];
@@ -212,7 +213,7 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
           float dx, dy, dz;
           const float s = dist2_df(hi, lo, qx, dx, dy, dz);
           const float4 wv = mine ? fwd_w(dx, dy, dz, s, lo.w, kp) : make_float4(0.f, 0.f, 0.f, 0.f);
-          append(wv, node_row + (size_t)node * F4);
+          append(wv, node_row + (size_t)node * F4g);
         } else {
           const int4 tp = rb[i].topo;
           for (int j = tp.z; j < tp.w; ++j) {
@@ -225,7 +226,7 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
               if (!(singular && r2 == 0.f && coincident_exact(tv.pt_pos64 + 3 * (size_t)j, xq)))
                 wv = fwd_w(dx, dy, dz, r2, ph.w, kp);
             }
-            append(wv, pt_row + (size_t)j * F4);
+            append(wv, pt_row + (size_t)j * F4g);
           }
         }
       }
@@ -254,7 +255,7 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
     if (farm && A > 0.f) {  // area > 0 (bhtree.cpp:205)
       const float4 wv = far ? fwd_w(dx, dy, dz, s, A, kp) : make_float4(0.f, 0.f, 0.f, 0.f);
       if (COUNT && far) (reg && s < kp.near2) ? ++c_fn : ++c_ff;
-      append(wv, node_row + (size_t)node * F4);
+      append(wv, node_row + (size_t)node * F4g);
     }
     const unsigned openm = mask & ~farm;
     if (openm) {
@@ -271,7 +272,7 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
               if (COUNT) (reg && r2 < kp.near2) ? ++c_pn : ++c_pf;
             }
           }
-          append(wv, pt_row + (size_t)j * F4);
+          append(wv, pt_row + (size_t)j * F4g);
         }
       } else {
         if (sp + tp.y > DPL_STACK_PER_WARP) {
@@ -296,7 +297,7 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
     out[qi * out_stride + __ldg(chmap)] = accd;
   }
 #pragma unroll
-  for (int mt = 0; mt < 2; ++mt)
+  for (int mt = 0; mt < (NT > 0 ? 2 : 0); ++mt)
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int row = 16 * mt + 8 * h + g;  // lane whose query this row is
@@ -353,11 +354,18 @@ static void launch_tc(const Tree& t, const KParams& kp, const FwdArgs& a, int nr
 // Tensor-core plan: one dipole slot and PR a multiple of 8 (8..64 radial).
 bool forward_tc_launch(const Tree& t, const KParams& kp, const FwdArgs& a) {
   if (a.grad_mode != 0 || (a.single && a.only_ch < 0)) return false;
+  // primal_channel of the dipole channel: the dipole-only variant runs the same
+  // entry sequence and the same dipole arithmetic as every values kernel
+  // (forward_tc / forward2), so it is bitwise primal()[c] at a fraction of the work
+  const bool two_phase_values = t.PR == 0 || t.PR == 4 || t.PR == 16 || t.PR == 48 || t.PR == 64;
+  if (a.only_ch >= 0 && t.Cd == 1 && t.kinds[a.only_ch] == 0 && two_phase_values)
+    return launch_tc<0, 4, 8, 128>(t, kp, a, 0), true;
   if (t.Cd != 1 || t.PR % 8 != 0) return false;
   const int nr = a.nr_limit >= 0 ? std::min(a.nr_limit, t.Cr) : t.Cr;
   const char* v = getenv("DPL_TUNE_TC");
   const int choice = v ? atoi(v) : 0;
   switch (t.PR) {
+    case 0: return launch_tc<0, 4, 8, 128>(t, kp, a, 0), true;  // dipole only (C = 1)
     case 16: return launch_tc<2, 4, 8, 128>(t, kp, a, nr), true;
     case 48:
       switch (choice) {

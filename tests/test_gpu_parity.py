@@ -440,3 +440,21 @@ def test_interaction_list_reuse_is_keyed_on_the_batch(eng, oracle_mod):
     r2.set_kinds(kinds)
     got = t.primal(dev, p, 2.0).cpu().numpy()
     assert close(got, r2.primal(O.Params(0.05), 2.0, xs2))[0] == 0
+
+
+@pytest.mark.parametrize("C", [1, 2, 3, 17, 33, 49])
+def test_primal_channel_bitwise_equals_primal(eng, oracle_mod, C):
+    """primal_channel(c) == primal()[c] bitwise (test_bhtree.cpp:140) for every
+    layout, including the dipole-only kernel primal_channel(0) uses."""
+    O = oracle_mod
+    pos, nrm, area, mu = random_cloud(3000, 40 + C, C)
+    kinds = np.ones(C, np.uint8)
+    kinds[0] = 0
+    t, r = make(eng, O, pos, nrm, area, mu, kinds)
+    xs = np.random.default_rng(41).uniform(-1.3, 1.3, (2500, 3))
+    p = eng.KernelParams(epsilon=0.04)
+    full = t.primal(xs, p, 2.0)
+    for c in sorted({0, C // 2, C - 1}):
+        assert np.array_equal(t.primal_channel(xs, p, 2.0, c), full[:, c]), c
+    want = r.primal(O.Params(0.04), 2.0, xs)
+    assert close(full, want)[0] == 0
