@@ -124,6 +124,33 @@ int dpl_primal_channel(dpl_tree_t tree, const dpl_kernel_params* params, double 
 int dpl_primal_grad0(dpl_tree_t tree, const dpl_kernel_params* params, double beta_bh,
                      const double* xs, int64_t q, float* out, float* grad0);
 
+/* ---- query generators -------------------------------------- */
+/* sample_grid (meshing.cpp:33-59) with geometry_field(x) = 0.5 -
+ * primal_channel(x, 0) (fields.cpp:27-29): res[3] >= 2 per axis (DataError
+ * otherwise); node (i, j, k) = lo + (i/(r0-1), j/(r1-1), k/(r2-1)) * (hi - lo)
+ * in fp64 (FieldGrid::node, :25-30); values[(k * r1 + j) * r0 + i]. When
+ * |hi - lo| == 0 the box is the cloud's bounding box padded by 5%; lo_out /
+ * hi_out (may be NULL) receive the box used. */
+int dpl_sample_grid(dpl_tree_t tree, const dpl_kernel_params* params, double beta_bh,
+                    const int32_t* res, const double* lo, const double* hi, float* values,
+                    double* lo_out, double* hi_out);
+
+/* The sampler fields of RenderConfig (renderer.hpp:33-41). */
+typedef struct {
+  double t_near, t_far;
+  int32_t probe_count, sparse_before, dense_at, sparse_after, uniform_count, reserved;
+} dpl_ray_sampler;
+
+/* sample_ray (renderer.cpp:46-86) for R rays (origin xyz, dir xyz: R x 6 fp64):
+ * value-only probes f = 0.5 - primal_channel(o + t dir, 0) at t_near + span i /
+ * (n - 1), the first sign change brackets the surface, then sparse / dense /
+ * sparse samples around it (or uniform samples). Outputs per ray: t and delta
+ * (R x max_samples, first count[r] valid, ascending), count, bracketed.
+ * DataError when t_near >= t_far. */
+int dpl_sample_rays(dpl_tree_t tree, const dpl_kernel_params* params, double beta_bh,
+                    const double* rays, int64_t R, const dpl_ray_sampler* cfg, int32_t max_samples,
+                    double* t, double* delta, int32_t* count, uint8_t* bracketed);
+
 /* ---- adjoint (two-stage) ---------------------------------------------------
  * GradientBuffer (bhtree.hpp:40-49): device fp64 accumulators node_v, node_s,
  * point_mu, point_n, d_epsilon. */

@@ -171,6 +171,24 @@ class DipoleTree {
     check(dpl_primal(h_, &kp, beta_bh, xs, q, out, grad, nullptr));
   }
 
+  // sample_grid (meshing.cpp:33-59): values[(k * r1 + j) * r0 + i] = 0.5 - D0(node)
+  std::vector<float> sample_grid(const KernelParams& p, double beta_bh, const int32_t res[3],
+                                 const double lo[3], const double hi[3], double lo_out[3] = nullptr,
+                                 double hi_out[3] = nullptr) const {
+    dpl_kernel_params kp = p.c();
+    std::vector<float> v((size_t)res[0] * res[1] * res[2]);
+    check(dpl_sample_grid(h_, &kp, beta_bh, res, lo, hi, v.data(), lo_out, hi_out));
+    return v;
+  }
+  // sample_ray (renderer.cpp:46-86) for R rays (origin, dir): t / delta R x max_samples
+  void sample_rays(const KernelParams& p, double beta_bh, const double* rays, int64_t R,
+                   const dpl_ray_sampler& cfg, int32_t max_samples, double* t, double* delta,
+                   int32_t* count, uint8_t* bracketed) const {
+    dpl_kernel_params kp = p.c();
+    check(dpl_sample_rays(h_, &kp, beta_bh, rays, R, &cfg, max_samples, t, delta, count,
+                          bracketed));
+  }
+
   GradientBuffer make_buffer() const {
     dpl_gradbuf_t b = nullptr;
     check(dpl_gradbuf_create(h_, &b));

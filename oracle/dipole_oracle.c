@@ -1098,3 +1098,120 @@ void ora_adam_step(double* params, const double* grads, double* m, double* v, in
     params[i] -= lr * (m[i] / c1) / (sqrt(v[i] / c2) + eps);
   }
 }
+
+/* ------------------------------------------------------- query generators */
+/* sample_grid: meshing.cpp:33-59. geometry_field(x) = 0.5 - primal_channel(x,
+ * 0) (fields.cpp:27-29); node (i, j, k) = lo + f .* (hi - lo) with f = i /
+ * (dims - 1) (FieldGrid::node, meshing.cpp:25-30). If |hi - lo| == 0 the box
+ * is the bounding box of pos (pointcloud.cpp:22-29) padded by 5% (:38-43). */
+int ora_sample_grid(const ora_tree* t, const ora_params* p, double beta, const int32_t* res,
+                    const double* lo_in, const double* hi_in, const double* pos, int64_t n,
+                    int threads, double* values, double* lo_out, double* hi_out) {
+  for (int a = 0; a < 3; ++a)
+    if (res[a] < 2) return 2; /* DataError */
+  double lo[3] = {lo_in[0], lo_in[1], lo_in[2]}, hi[3] = {hi_in[0], hi_in[1], hi_in[2]};
+  double d[3] = {hi[0] - lo[0], hi[1] - lo[1], hi[2] - lo[2]};
+  if (sqrt(dot3(d, d)) == 0.0) {
+    for (int a = 0; a < 3; ++a) lo[a] = INFINITY, hi[a] = -INFINITY;
+    for (int64_t i = 0; i < n; ++i)
+      for (int a = 0; a < 3; ++a) {
+        double v = pos[3 * i + a];
+        lo[a] = v < lo[a] ? v : lo[a]; /* cwiseMin */
+        hi[a] = hi[a] < v ? v : hi[a]; /* cwiseMax */
+      }
+    for (int a = 0; a < 3; ++a) {
+      double pad = 0.05 * (hi[a] - lo[a]);
+      lo[a] -= pad;
+      hi[a] += pad;
+    }
+  }
+  int64_t total = (int64_t)res[0] * res[1] * res[2];
+  double* xs = malloc((size_t)total * 3 * sizeof(double));
+  for (int64_t g = 0; g < total; ++g) {
+    int64_t i = g % res[0], j = (g / res[0]) % res[1], k = g / ((int64_t)res[0] * res[1]);
+    double f[3] = {(double)i / (res[0] - 1), (double)j / (res[1] - 1), (double)k / (res[2] - 1)};
+    for (int a = 0; a < 3; ++a) xs[3 * g + a] = lo[a] + f[a] * (hi[a] - lo[a]);
+  }
+  ora_primal(t, p, beta, xs, total, 2, 0, values, NULL, NULL, threads);
+  for (int64_t g = 0; g < total; ++g) values[g] = 0.5 - values[g];
+  free(xs);
+  for (int a = 0; a < 3; ++a) lo_out[a] = lo[a], hi_out[a] = hi[a];
+  return 0;
+}
+
+/* sample_ray: renderer.cpp:46-86 (probe pass, first sign change of f, then
+ * sparse / dense / sparse or uniform samples; delta[j] = t[j] - t[j-1]). */
+typedef struct {
+  const ora_tree* t;
+  const ora_params* p;
+  double beta;
+  const double* rays;
+  double t_near, t_far;
+  const int32_t* cnt5; /* probe, sparse_before, dense_at, sparse_after, uniform */
+  int32_t max_s;
+  double *ts, *delta;
+  int32_t* count;
+  uint8_t* bracketed;
+} ray_ctx;
+
+static void ray_body(void* v, int64_t lo_r, int64_t hi_r, int w) {
+  (void)w;
+  ray_ctx* c = v;
+  for (int64_t r = lo_r; r < hi_r; ++r) {
+    const double* ray = c->rays + 6 * r;
+    double* t = c->ts + r * c->max_s;
+    double* dl = c->delta + r * c->max_s;
+    double span = c->t_far - c->t_near;
+    int m = 0, br = 0;
+    if (span < 1e-9) {
+      t[0] = 0.5 * (c->t_near + c->t_far);
+      dl[0] = t[0] - c->t_near;
+      c->count[r] = 1;
+      c->bracketed[r] = 0;
+      continue;
+    }
+    int n = c->cnt5[0] < 2 ? 2 : c->cnt5[0];
+    double prev_f = 0, prev_t = 0, blo = 0, bhi = 0;
+    for (int i = 0; i < n; ++i) {
+      double tt = c->t_near + span * i / (n - 1);
+      double x[3] = {ray[0] + tt * ray[3], ray[1] + tt * ray[4], ray[2] + tt * ray[5]};
+      double v0;
+      primal_one(c->t, c->p, c->beta, x, 2, 0, &v0, NULL, NULL);
+      double f = 0.5 - v0;
+      if (i > 0 && ((prev_f > 0 && f <= 0) || (prev_f <= 0 && f > 0))) {
+        br = 1;
+        blo = prev_t;
+        bhi = tt;
+        break;
+      }
+      prev_f = f;
+      prev_t = tt;
+    }
+#define EMIT(L, H, K)                                                     \
+  do {                                                                    \
+    double lo_ = (L), hi_ = (H);                                          \
+    int k_ = (K);                                                         \
+    for (int i_ = 0; i_ < k_ && m < c->max_s; ++i_)                       \
+      t[m++] = lo_ + (hi_ - lo_) * (i_ + 0.5) / k_;                        \
+  } while (0)
+    if (!br) {
+      EMIT(c->t_near, c->t_far, c->cnt5[4] > 1 ? c->cnt5[4] : 1);
+    } else {
+      EMIT(c->t_near, blo, c->cnt5[1]);
+      EMIT(blo, bhi, c->cnt5[2] > 1 ? c->cnt5[2] : 1);
+      EMIT(bhi, c->t_far, c->cnt5[3]);
+    }
+#undef EMIT
+    for (int j = 0; j < m; ++j) dl[j] = t[j] - (j == 0 ? c->t_near : t[j - 1]);
+    c->count[r] = m;
+    c->bracketed[r] = (uint8_t)br;
+  }
+}
+
+void ora_sample_rays(const ora_tree* t, const ora_params* p, double beta, const double* rays,
+                     int64_t R, double t_near, double t_far, const int32_t* counts5,
+                     int32_t max_s, int threads, double* ts, double* delta, int32_t* count,
+                     uint8_t* bracketed) {
+  ray_ctx c = {t, p, beta, rays, t_near, t_far, counts5, max_s, ts, delta, count, bracketed};
+  parallel_for(R, threads, ray_body, &c);
+}

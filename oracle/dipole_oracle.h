@@ -81,6 +81,18 @@ void ora_render_step(const ora_tree* t, const ora_params* p, double beta, double
 
 double ora_mean_knn_spacing(const double* pos, int64_t n, int k);
 
+/* sample_grid (meshing.cpp:33-59): values r2 x r1 x r0 of 0.5 - primal_channel(x, 0);
+ * returns 2 (DataError) for a resolution below 2. pos: the cloud (bounding box). */
+int ora_sample_grid(const ora_tree* t, const ora_params* p, double beta, const int32_t* res,
+                    const double* lo, const double* hi, const double* pos, int64_t n,
+                    int threads, double* values, double* lo_out, double* hi_out);
+/* sample_ray (renderer.cpp:46-86) for R rays (origin, dir); counts5 = {probe_count,
+ * sparse_before, dense_at, sparse_after, uniform_count}; t / delta R x max_s. */
+void ora_sample_rays(const ora_tree* t, const ora_params* p, double beta, const double* rays,
+                     int64_t R, double t_near, double t_far, const int32_t* counts5,
+                     int32_t max_s, int threads, double* ts, double* delta, int32_t* count,
+                     uint8_t* bracketed);
+
 void ora_adam_step(double* params, const double* grads, double* m, double* v, int64_t n,
                    double lr, double beta1, double beta2, double eps, int64_t t);
 

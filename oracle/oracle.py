@@ -107,6 +107,12 @@ def port_lib():
         lib.ora_mean_knn_spacing.argtypes = [_dp, C.c_int64, C.c_int]
         lib.ora_adam_step.argtypes = [_dp, _dp, _dp, _dp, C.c_int64, C.c_double, C.c_double,
                                       C.c_double, C.c_double, C.c_int64]
+        lib.ora_sample_grid.restype = C.c_int
+        lib.ora_sample_grid.argtypes = [C.c_void_p, C.POINTER(Params), C.c_double, _ip, _dp, _dp,
+                                        _dp, C.c_int64, C.c_int, _dp, _dp, _dp]
+        lib.ora_sample_rays.argtypes = [C.c_void_p, C.POINTER(Params), C.c_double, _dp, C.c_int64,
+                                        C.c_double, C.c_double, _ip, C.c_int32, C.c_int, _dp, _dp,
+                                        _ip, _up]
         _port = lib
     return _port
 
@@ -125,6 +131,9 @@ def ref_lib():
         lib.ref_erf_approx.argtypes = [C.c_double]
         lib.ref_normal_hazard.restype = C.c_double
         lib.ref_normal_hazard.argtypes = [C.c_double]
+        lib.ref_sample_grid.argtypes = [vp, _ip, _dp, _dp, C.c_int, _dp, _dp, _dp]
+        lib.ref_sample_rays.argtypes = [vp, _dp, C.c_int64, C.c_double, C.c_double, _ip, C.c_int32,
+                                        _dp, _dp, _ip, _up]
         lib.ref_mean_knn_spacing.restype = C.c_double
         lib.ref_mean_knn_spacing.argtypes = [_dp, C.c_int64, C.c_int]
         lib.ref_tree_build.argtypes = [_dp, _dp, _dp, _dp, C.c_int64, C.c_int32, C.c_int32,
@@ -229,6 +238,32 @@ class OracleTree:
         if rc:
             raise ValueError("DataError: cloud/tree size mismatch")
         self.cloud = c
+
+    def sample_grid(self, params, beta, res, lo=(0, 0, 0), hi=(0, 0, 0), threads=0):
+        """sample_grid (meshing.cpp:33-59), port backend: (values r2 x r1 x r0, lo, hi)."""
+        assert self.backend == "port"
+        res = np.ascontiguousarray(res, dtype=np.int32)
+        vals = np.zeros((int(res[2]), int(res[1]), int(res[0])))
+        lo_o, hi_o = np.zeros(3), np.zeros(3)
+        rc = self._lib.ora_sample_grid(self._h, C.byref(params), beta, _ptr(res, _ip),
+                                       _ptr(_d(lo)), _ptr(_d(hi)), _ptr(self.cloud.pos), self.n,
+                                       threads, _ptr(vals), _ptr(lo_o), _ptr(hi_o))
+        if rc:
+            raise ValueError("DataError: sample_grid resolution")
+        return vals, lo_o, hi_o
+
+    def sample_rays(self, params, beta, rays, t_near, t_far, counts5, max_s, threads=0):
+        """sample_ray (renderer.cpp:46-86), port backend."""
+        assert self.backend == "port"
+        rays = _d(rays).reshape(-1, 6)
+        R = rays.shape[0]
+        k = np.ascontiguousarray(counts5, dtype=np.int32)
+        t, d = np.zeros((R, max_s)), np.zeros((R, max_s))
+        cnt, br = np.zeros(R, np.int32), np.zeros(R, np.uint8)
+        self._lib.ora_sample_rays(self._h, C.byref(params), beta, _ptr(rays), R, t_near, t_far,
+                                  _ptr(k, _ip), max_s, threads, _ptr(t), _ptr(d), _ptr(cnt, _ip),
+                                  _ptr(br, _up))
+        return t, d, cnt, br.astype(bool)
 
     def node_count(self):
         f = self._lib.ora_tree_node_count if self.backend == "port" else self._lib.ref_tree_node_count
@@ -375,6 +410,27 @@ class RefModel:
         if getattr(self, "_h", None):
             self._lib.ref_model_free(self._h)
             self._h = None
+
+    def sample_grid(self, res, lo=(0, 0, 0), hi=(0, 0, 0), threads=0):
+        """The reference's own sample_grid (meshing.cpp:33-59) on this model."""
+        res = np.ascontiguousarray(res, dtype=np.int32)
+        vals = np.zeros((int(res[2]), int(res[1]), int(res[0])))
+        lo_o, hi_o = np.zeros(3), np.zeros(3)
+        _check_ref(self._lib.ref_sample_grid(self._h, _ptr(res, _ip), _ptr(_d(lo)), _ptr(_d(hi)),
+                                             threads, _ptr(vals), _ptr(lo_o), _ptr(hi_o)))
+        return vals, lo_o, hi_o
+
+    def sample_rays(self, rays, t_near, t_far, counts5, max_s):
+        """The reference's own sample_ray (renderer.cpp:46-86) per ray."""
+        rays = _d(rays).reshape(-1, 6)
+        R = rays.shape[0]
+        k = np.ascontiguousarray(counts5, dtype=np.int32)
+        t, d = np.zeros((R, max_s)), np.zeros((R, max_s))
+        cnt, br = np.zeros(R, np.int32), np.zeros(R, np.uint8)
+        _check_ref(self._lib.ref_sample_rays(self._h, _ptr(rays), R, t_near, t_far, _ptr(k, _ip),
+                                             max_s, _ptr(t), _ptr(d), _ptr(cnt, _ip),
+                                             _ptr(br, _up)))
+        return t, d, cnt, br.astype(bool)
 
     def render_step(self, rays, ts, deltas, target, scale, threads=None):
         rays = _d(rays).reshape(-1, 6)

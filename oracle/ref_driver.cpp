@@ -27,6 +27,7 @@
 #include "dipole/bhtree.hpp"
 #include "dipole/fields.hpp"
 #include "dipole/kernels.hpp"
+#include "dipole/meshing.hpp"
 #include "dipole/optimizer.hpp"
 #include "dipole/oracles.hpp"
 #include "dipole/renderer.hpp"
@@ -315,6 +316,50 @@ int ref_model_create(const double* pos, const double* nrm, const double* area, c
 }
 
 void ref_model_free(ref_model* m) { delete m; }
+
+// ---- query generators ----------------------------------------
+// sample_grid (meshing.cpp:33-59) on the model: values (r2 x r1 x r0), box used
+int ref_sample_grid(ref_model* m, const int32_t* res, const double* lo, const double* hi,
+                    int workers, double* values, double* lo_out, double* hi_out) {
+  return guard([&] {
+    FieldGrid g = sample_grid(m->model, {res[0], res[1], res[2]}, Vec3(lo[0], lo[1], lo[2]),
+                              Vec3(hi[0], hi[1], hi[2]), workers > 0 ? workers : default_workers());
+    std::memcpy(values, g.values.data(), g.values.size() * sizeof(double));
+    for (int a = 0; a < 3; ++a) lo_out[a] = g.lo[a], hi_out[a] = g.hi[a];
+  });
+}
+
+// sample_ray (renderer.cpp:46-86) per ray; t / delta R x max_s
+int ref_sample_rays(ref_model* m, const double* rays, int64_t R, double t_near, double t_far,
+                    const int32_t* counts5, int32_t max_s, double* t, double* delta,
+                    int32_t* count, uint8_t* bracketed) {
+  return guard([&] {
+    RenderConfig cfg;
+    cfg.t_near = t_near;
+    cfg.t_far = t_far;
+    cfg.probe_count = counts5[0];
+    cfg.sparse_before = counts5[1];
+    cfg.dense_at = counts5[2];
+    cfg.sparse_after = counts5[3];
+    cfg.uniform_count = counts5[4];
+    parallel_for(
+        R,
+        [&](std::int64_t r0, std::int64_t r1, int) {
+          for (std::int64_t r = r0; r < r1; ++r) {
+            Ray ray;
+            ray.origin = Vec3(rays[6 * r], rays[6 * r + 1], rays[6 * r + 2]);
+            ray.dir = Vec3(rays[6 * r + 3], rays[6 * r + 4], rays[6 * r + 5]);
+            RaySamples s = sample_ray(m->model, ray, cfg);
+            if ((int)s.t.size() > max_s) throw DataError("ref_sample_rays: max_s too small");
+            for (std::size_t j = 0; j < s.t.size(); ++j)
+              t[r * max_s + j] = s.t[j], delta[r * max_s + j] = s.delta[j];
+            count[r] = (int32_t)s.t.size();
+            bracketed[r] = s.bracketed ? 1 : 0;
+          }
+        },
+        default_workers());
+  });
+}
 
 double ref_model_epsilon(const ref_model* m) { return m->model.kernel.epsilon; }
 

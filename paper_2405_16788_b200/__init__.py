@@ -7,9 +7,9 @@ this package is its host-side mirror of the reference API:
   * workloads              — seeded synthetic inputs for BASELINE.json configs
 """
 from ._lib import (DataError, KernelParams, NumericalError, UsageError, CudaError,  # noqa: F401
-                   DPL_DIPOLE, DPL_RADIAL)
+                   DPL_DIPOLE, DPL_RADIAL, RaySampler)
 from .bhtree import (DipoleTree, GradientBuffer, OrientedPointCloud, PointGradients,  # noqa: F401
                      launch_count)
 
 __all__ = ["DipoleTree", "GradientBuffer", "OrientedPointCloud", "PointGradients", "KernelParams",
-           "DataError", "NumericalError", "UsageError", "CudaError", "launch_count"]
+           "DataError", "NumericalError", "UsageError", "CudaError", "launch_count", "RaySampler"]

@@ -52,6 +52,24 @@ class RenderParams(C.Structure):
                 ("seed", C.c_uint64)]
 
 
+class RaySampler(C.Structure):
+    """RenderConfig sampler fields (renderer.hpp:33-41) == dpl_ray_sampler."""
+
+    _fields_ = [("t_near", C.c_double), ("t_far", C.c_double), ("probe_count", C.c_int32),
+                ("sparse_before", C.c_int32), ("dense_at", C.c_int32),
+                ("sparse_after", C.c_int32), ("uniform_count", C.c_int32),
+                ("reserved", C.c_int32)]
+
+    def __init__(self, t_near=0.05, t_far=6.0, probe_count=1024, sparse_before=24, dense_at=48,
+                 sparse_after=8, uniform_count=80):
+        super().__init__(float(t_near), float(t_far), int(probe_count), int(sparse_before),
+                         int(dense_at), int(sparse_after), int(uniform_count), 0)
+
+    def max_samples(self):
+        return max(max(1, self.uniform_count),
+                   self.sparse_before + max(1, self.dense_at) + self.sparse_after)
+
+
 _lib = None
 
 _vp = C.c_void_p
@@ -80,6 +98,10 @@ _sig = {
                                      C.c_int32, _vp]),
     "dpl_primal_grad0": (C.c_int, [_vp, C.POINTER(KernelParams), C.c_double, _vp, C.c_int64,
                                    _vp, _vp]),
+    "dpl_sample_grid": (C.c_int, [_vp, C.POINTER(KernelParams), C.c_double, _vp, _vp, _vp, _vp,
+                                  _vp, _vp]),
+    "dpl_sample_rays": (C.c_int, [_vp, C.POINTER(KernelParams), C.c_double, _vp, C.c_int64,
+                                  C.POINTER(RaySampler), C.c_int32, _vp, _vp, _vp, _vp]),
     "dpl_gradbuf_create": (C.c_int, [_vp, C.POINTER(_vp)]),
     "dpl_gradbuf_destroy": (C.c_int, [_vp]),
     "dpl_gradbuf_zero": (C.c_int, [_vp]),

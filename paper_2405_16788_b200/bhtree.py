@@ -283,6 +283,41 @@ class DipoleTree:
         check(lib().dpl_primal(self._h, C.byref(params), float(beta_bh), xp, q, op, gp, None))
         return out, grad
 
+    # -- query generators ----------------------------------------
+    def sample_grid(self, params: KernelParams, beta_bh: float, resolution, lo=(0, 0, 0),
+                    hi=(0, 0, 0)):
+        """sample_grid (meshing.cpp:33-59): geometry_field = 0.5 - primal_channel(x, 0)
+        on a res0 x res1 x res2 grid. Returns (values (r2, r1, r0) fp32, lo, hi);
+        lo == hi selects the cloud's bounding box padded by 5%."""
+        res = np.ascontiguousarray(resolution, dtype=np.int32).reshape(3)
+        lo_ = np.ascontiguousarray(lo, dtype=np.float64).reshape(3)
+        hi_ = np.ascontiguousarray(hi, dtype=np.float64).reshape(3)
+        vals = np.empty((int(res[2]), int(res[1]), int(res[0])), np.float32)
+        lo_o, hi_o = np.empty(3), np.empty(3)
+        check(lib().dpl_sample_grid(self._h, C.byref(params), float(beta_bh), res.ctypes.data,
+                                    lo_.ctypes.data, hi_.ctypes.data, vals.ctypes.data,
+                                    lo_o.ctypes.data, hi_o.ctypes.data))
+        return vals, lo_o, hi_o
+
+    def sample_rays(self, params: KernelParams, beta_bh: float, rays, sampler=None):
+        """sample_ray (renderer.cpp:46-86) for a (R, 6) batch of rays (origin, dir).
+        Returns (t (R, M), delta (R, M), count (R,), bracketed (R,)); row r holds
+        count[r] ascending samples."""
+        from ._lib import RaySampler
+
+        cfg = sampler or RaySampler()
+        rp, rk = _in(rays, np.float64)
+        R = int(rays.shape[0])
+        M = cfg.max_samples()
+        t = np.zeros((R, M))
+        d = np.zeros((R, M))
+        cnt = np.zeros(R, np.int32)
+        br = np.zeros(R, np.uint8)
+        check(lib().dpl_sample_rays(self._h, C.byref(params), float(beta_bh), rp, R, C.byref(cfg),
+                                    M, t.ctypes.data, d.ctypes.data, cnt.ctypes.data,
+                                    br.ctypes.data))
+        return t, d, cnt, br.astype(bool)
+
     def primal_grad0(self, xs, params: KernelParams, beta_bh: float):
         """Values of all channels and the gradient of channel 0 only (render path)."""
         q = int(xs.shape[0])

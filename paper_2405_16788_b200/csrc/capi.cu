@@ -19,6 +19,7 @@
 #include "knn.cuh"
 #include "train.cuh"
 #include "render.cuh"
+#include "sampling.cuh"
 #include "tree.cuh"
 
 namespace dpl {
@@ -614,6 +615,135 @@ int dpl_primal_channel(dpl_tree_t h, const dpl_kernel_params* params, double bet
     return DPL_ERR_USAGE;
   }
   return forward_common(h, params, beta_bh, xs, q, out, nullptr, nullptr, 0, channel);
+}
+
+// ---------------------------------------------------------------- sampling
+
+static void check_rc(int rc) {
+  if (rc != DPL_OK) throw Error(rc, g_err);
+}
+
+int dpl_sample_grid(dpl_tree_t h, const dpl_kernel_params* params, double beta_bh,
+                    const int32_t* res, const double* lo_in, const double* hi_in, float* values,
+                    double* lo_out, double* hi_out) {
+  return guard([&] {
+    check_tree(h);
+    check_params(params);
+    require(res && lo_in && hi_in && values, DPL_ERR_USAGE, "null argument");
+    for (int a = 0; a < 3; ++a)
+      if (res[a] < 2) throw Error(DPL_ERR_DATA, "sample_grid: resolution must be at least 2 per axis");
+    Tree& t = h->t;
+    DPL_CUDA(cudaSetDevice(t.device));
+    double lo[3] = {lo_in[0], lo_in[1], lo_in[2]}, hi[3] = {hi_in[0], hi_in[1], hi_in[2]};
+    const double d0 = hi[0] - lo[0], d1 = hi[1] - lo[1], d2 = hi[2] - lo[2];
+    if (std::sqrt((d0 * d0 + d1 * d1) + d2 * d2) == 0.0) {  // (hi - lo).norm() == 0 (:38-43)
+      tree_point_bbox(t, lo, hi);
+      for (int a = 0; a < 3; ++a) {
+        const double pad = 0.05 * (hi[a] - lo[a]);
+        lo[a] -= pad;
+        hi[a] += pad;
+      }
+    }
+    if (lo_out)
+      for (int a = 0; a < 3; ++a) lo_out[a] = lo[a];
+    if (hi_out)
+      for (int a = 0; a < 3; ++a) hi_out[a] = hi[a];
+    const int r[3] = {res[0], res[1], res[2]};
+    const int64_t total = (int64_t)r[0] * r[1] * r[2];
+    const int64_t slab = std::min<int64_t>(total, 1 << 24);
+    DevBuf xs, vals;
+    xs.reserve((size_t)slab * 24);
+    vals.reserve((size_t)slab * 4);
+    Out<float> o;
+    o.bind(t, values, total, h->ws_out);
+    for (int64_t s0 = 0; s0 < total; s0 += slab) {
+      const int64_t n = std::min(slab, total - s0);
+      grid_nodes(lo, hi, r, s0, n, xs.as<double>(), t.stream);
+      // geometry_field = 0.5 - primal_channel(x, 0) (fields.cpp:27-29)
+      check_rc(forward_common(h, params, beta_bh, xs.as<double>(), n, vals.as<float>(), nullptr,
+                              nullptr, 0, 0));
+      half_minus(vals.as<float>(), n, o.dev + s0, t.stream);
+    }
+    o.finish(t);
+    DPL_CUDA(cudaStreamSynchronize(t.stream));
+  });
+}
+
+int dpl_sample_rays(dpl_tree_t h, const dpl_kernel_params* params, double beta_bh,
+                    const double* rays, int64_t R, const dpl_ray_sampler* cfg, int32_t max_samples,
+                    double* t_out, double* delta_out, int32_t* count_out, uint8_t* bracketed_out) {
+  return guard([&] {
+    check_tree(h);
+    check_params(params);
+    require(cfg && rays && t_out && delta_out && count_out && bracketed_out, DPL_ERR_USAGE,
+            "null argument");
+    if (!(cfg->t_near < cfg->t_far))
+      throw Error(DPL_ERR_DATA, "sample_ray: t_near must precede t_far");
+    const int need = std::max(std::max(1, cfg->uniform_count),
+                              cfg->sparse_before + std::max(1, cfg->dense_at) + cfg->sparse_after);
+    require(max_samples >= need, DPL_ERR_USAGE, "sample_rays: max_samples below the schedule");
+    if (R == 0) return;
+    Tree& t = h->t;
+    DPL_CUDA(cudaSetDevice(t.device));
+    RaySampler c{cfg->t_near, cfg->t_far, cfg->probe_count, cfg->sparse_before, cfg->dense_at,
+                 cfg->sparse_after, cfg->uniform_count};
+    const int n = std::max(2, c.probe_count);
+    const bool probe = cfg->t_far - cfg->t_near >= 1e-9;
+    DevBuf rays_tmp, prev, brk, act0, act1, nnext, xs, vals;
+    const double* rays_d = stage_in(t, rays, (size_t)R * 6, rays_tmp);
+    prev.reserve((size_t)R * 4);
+    brk.reserve((size_t)R * 4);
+    DPL_CUDA(cudaMemsetAsync(prev.p, 0, (size_t)R * 4, t.stream));  // prev_f = 0 (:57)
+    DPL_CUDA(cudaMemsetAsync(brk.p, 0xff, (size_t)R * 4, t.stream));
+    if (probe) {
+      // probe rounds of K probes over the rays still without a bracket; each
+      // round is one batched value-only primal_channel(0) (Morton-sorted)
+      constexpr int K = 64;
+      const int64_t chunk = std::min<int64_t>(R, (int64_t)(1 << 24) / K);
+      act0.reserve((size_t)R * 4);
+      act1.reserve((size_t)R * 4);
+      nnext.reserve(sizeof(int));
+      xs.reserve((size_t)chunk * K * 24);
+      vals.reserve((size_t)chunk * K * 4);
+      std::vector<int32_t> all(R);
+      for (int64_t i = 0; i < R; ++i) all[i] = (int32_t)i;
+      DPL_CUDA(cudaMemcpyAsync(act0.p, all.data(), (size_t)R * 4, cudaMemcpyHostToDevice, t.stream));
+      int64_t n_act = R;
+      int32_t* cur = act0.as<int32_t>();
+      int32_t* nxt = act1.as<int32_t>();
+      for (int i0 = 0; i0 < n && n_act > 0; i0 += K) {
+        const int kc = std::min(K, n - i0);
+        DPL_CUDA(cudaMemsetAsync(nnext.p, 0, sizeof(int), t.stream));
+        for (int64_t a0 = 0; a0 < n_act; a0 += chunk) {
+          const int64_t na = std::min(chunk, n_act - a0);
+          probe_points(rays_d, cur + a0, na, i0, kc, c, xs.as<double>(), t.stream);
+          check_rc(forward_common(h, params, beta_bh, xs.as<double>(), na * kc, vals.as<float>(),
+                                  nullptr, nullptr, 0, 0));
+          probe_scan(vals.as<float>(), cur + a0, na, i0, kc, c, prev.as<float>(), brk.as<int32_t>(),
+                     nxt, nnext.as<int>(), t.stream);
+        }
+        int nn = 0;
+        DPL_CUDA(cudaMemcpyAsync(&nn, nnext.p, sizeof(int), cudaMemcpyDeviceToHost, t.stream));
+        DPL_CUDA(cudaStreamSynchronize(t.stream));
+        n_act = nn;
+        std::swap(cur, nxt);
+      }
+    }
+    Out<double> to, dout;
+    Out<int32_t> co;
+    Out<uint8_t> bo;
+    DevBuf t_tmp, d_tmp, c_tmp, b_tmp;
+    to.bind(t, t_out, (size_t)R * max_samples, t_tmp);
+    dout.bind(t, delta_out, (size_t)R * max_samples, d_tmp);
+    co.bind(t, count_out, (size_t)R, c_tmp);
+    bo.bind(t, bracketed_out, (size_t)R, b_tmp);
+    emit_samples(brk.as<int32_t>(), R, c, max_samples, to.dev, dout.dev, co.dev, bo.dev, t.stream);
+    to.finish(t);
+    dout.finish(t);
+    co.finish(t);
+    bo.finish(t);
+    DPL_CUDA(cudaStreamSynchronize(t.stream));
+  });
 }
 
 int dpl_primal_grad0(dpl_tree_t h, const dpl_kernel_params* params, double beta_bh,

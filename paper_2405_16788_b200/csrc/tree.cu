@@ -600,6 +600,28 @@ void tree_ensure_thresholds(Tree& t, double beta) {
   t.thr_valid = !std::isnan(beta);
 }
 
+// bounding box of the current point positions (OrientedPointCloud::bounding_box,
+// pointcloud.cpp:22-29); synchronous
+void tree_point_bbox(Tree& t, double lo[3], double hi[3]) {
+  const int B = 256;
+  const int64_t n = t.n;
+  int nb = (int)std::max<int64_t>(1, std::min<int64_t>(1024, (n + B - 1) / B));
+  double* part = sbuf<double>(t, 0, 6 * nb);
+  k_bbox_partial<<<nb, B, 0, t.stream>>>(t.pos64.as<double>(), n, part);
+  count_launch();
+  std::vector<double> hp(6 * nb);
+  DPL_CUDA(cudaMemcpyAsync(hp.data(), part, 6 * nb * 8, cudaMemcpyDeviceToHost, t.stream));
+  DPL_CUDA(cudaStreamSynchronize(t.stream));
+  for (int a = 0; a < 3; ++a) {
+    lo[a] = hp[a];
+    hi[a] = hp[3 + a];
+    for (int b = 1; b < nb; ++b) {
+      lo[a] = std::min(lo[a], hp[6 * b + a]);
+      hi[a] = std::max(hi[a], hp[6 * b + 3 + a]);
+    }
+  }
+}
+
 void tree_build(Tree& t, const double* pos, const double* nrm, const double* area,
                 const double* mu, int64_t n, int C, int max_leaf, int max_depth) {
   if (n <= 0) throw Error(2, "DipoleTree::build: empty cloud");
@@ -624,22 +646,8 @@ void tree_build(Tree& t, const double* pos, const double* nrm, const double* are
   tree_update_points(t, pos, nrm, area, mu);
 
   // root cell (:43-50)
-  int nb = (int)std::min<int64_t>(1024, (n + B - 1) / B);
-  double* part = sbuf<double>(t, 0, 6 * nb);
-  k_bbox_partial<<<nb, B, 0, s>>>(t.pos64.as<double>(), n, part);
-  count_launch();
-  std::vector<double> hp(6 * nb);
-  DPL_CUDA(cudaMemcpyAsync(hp.data(), part, 6 * nb * 8, cudaMemcpyDeviceToHost, s));
-  DPL_CUDA(cudaStreamSynchronize(s));
   double lo[3], hi[3];
-  for (int a = 0; a < 3; ++a) {
-    lo[a] = hp[a];
-    hi[a] = hp[3 + a];
-    for (int b = 1; b < nb; ++b) {
-      lo[a] = std::min(lo[a], hp[6 * b + a]);
-      hi[a] = std::max(hi[a], hp[6 * b + 3 + a]);
-    }
-  }
+  tree_point_bbox(t, lo, hi);
   double ctr[3], ext[3];
   for (int a = 0; a < 3; ++a) {
     ctr[a] = 0.5 * (lo[a] + hi[a]);

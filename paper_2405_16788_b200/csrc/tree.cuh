@@ -78,6 +78,7 @@ void tree_compute_moments(Tree& t);
 void tree_refresh_sorted_positions(Tree& t);  // pt_pos64 / pt_geo from pos64 / area64
 void tree_set_kinds(Tree& t, const uint8_t* kinds);
 void tree_ensure_thresholds(Tree& t, double beta);
+void tree_point_bbox(Tree& t, double lo[3], double hi[3]);  // current positions, synchronous
 void tree_export(Tree& t, double* geo, int32_t* topo, int32_t* order, int32_t* leaf_of);
 // fp64 normalised moments for all channels, both representations (dump)
 void tree_full_moments(Tree& t, std::vector<double>& mv, std::vector<double>& ms);

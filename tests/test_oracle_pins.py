@@ -169,3 +169,50 @@ def test_port_matches_reference_build(oracle_mod, seed, n, C):
     ma, na, da = a.adjoint(p, 2.0, xs, d, threads=1)
     mb, nb, db = b.adjoint(p, 2.0, xs, d, threads=1)
     assert np.array_equal(ma, mb) and np.array_equal(na, nb) and da == db
+
+
+def _sphere_model(O, n=1500, C=4, seed=5):
+    rng = np.random.default_rng(seed)
+    v = rng.standard_normal((n, 3))
+    pos = v / np.linalg.norm(v, axis=1, keepdims=True)
+    mu = np.concatenate([np.ones((n, 1)), rng.uniform(0, 1, (n, C - 1))], axis=1)
+    return O.Cloud(pos, pos.copy(), np.full(n, 4 * np.pi / n), mu)
+
+
+def sphere_rays(R, seed):
+    """Rays from radius 3 toward random targets near the unit sphere (some miss)."""
+    rng = np.random.default_rng(seed)
+    o = rng.standard_normal((R, 3))
+    o = 3.0 * o / np.linalg.norm(o, axis=1, keepdims=True)
+    tgt = rng.uniform(-1.3, 1.3, (R, 3))
+    d = tgt - o
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    return np.concatenate([o, d], axis=1)
+
+
+def test_port_matches_reference_sample_grid_and_rays(oracle_mod):
+    """sample_grid (meshing.cpp:33-59) and sample_ray (renderer.cpp:46-86): the
+    C restatement equals the reference's own code bitwise."""
+    O = oracle_mod
+    if not O.have_ref():
+        pytest.skip("oracle/_ref not built")
+    cloud = _sphere_model(O)
+    eps = 0.08
+    ref = O.RefModel(cloud, eps, beta=2.0)
+    port = O.OracleTree(cloud)
+    kinds = np.ones(cloud.C, np.uint8)
+    kinds[0] = 0
+    port.set_kinds(kinds)
+    p = O.Params(eps)
+    for lo, hi in (((0, 0, 0), (0, 0, 0)), ((-1.2, -1.1, -1.0), (1.0, 1.1, 1.3))):
+        a = port.sample_grid(p, 2.0, (9, 7, 5), lo, hi)
+        b = ref.sample_grid((9, 7, 5), lo, hi)
+        for x, y in zip(a, b):
+            assert np.array_equal(x, y)
+    rays = sphere_rays(200, 6)
+    counts = (256, 24, 48, 8, 80)
+    a = port.sample_rays(p, 2.0, rays, 2.0, 4.5, counts, 80)
+    b = ref.sample_rays(rays, 2.0, 4.5, counts, 80)
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
+    assert 0 < a[3].sum() < len(rays)  # both bracketed and missing rays
