@@ -49,7 +49,8 @@ def _in(a, np_dtype, shape=None):
 def _out_like(ref, shape, np_dtype):
     """Allocate an output on the device of `ref`."""
     if _is_torch(ref) and ref.is_cuda:
-        tdt = {np.float32: torch.float32, np.float64: torch.float64, np.int64: torch.int64}[np_dtype]
+        tdt = {np.float32: torch.float32, np.float64: torch.float64, np.int64: torch.int64,
+               np.int32: torch.int32, np.uint8: torch.uint8}[np_dtype]
         t = torch.empty(shape, dtype=tdt, device=ref.device)
         return t.data_ptr(), t
     arr = np.empty(shape, dtype=np_dtype)
@@ -285,17 +286,23 @@ class DipoleTree:
 
     # -- query generators ----------------------------------------
     def sample_grid(self, params: KernelParams, beta_bh: float, resolution, lo=(0, 0, 0),
-                    hi=(0, 0, 0)):
+                    hi=(0, 0, 0), device=None):
         """sample_grid (meshing.cpp:33-59): geometry_field = 0.5 - primal_channel(x, 0)
         on a res0 x res1 x res2 grid. Returns (values (r2, r1, r0) fp32, lo, hi);
         lo == hi selects the cloud's bounding box padded by 5%."""
         res = np.ascontiguousarray(resolution, dtype=np.int32).reshape(3)
         lo_ = np.ascontiguousarray(lo, dtype=np.float64).reshape(3)
         hi_ = np.ascontiguousarray(hi, dtype=np.float64).reshape(3)
-        vals = np.empty((int(res[2]), int(res[1]), int(res[0])), np.float32)
+        shape = (int(res[2]), int(res[1]), int(res[0]))
+        if device is not None:  # values stay on the GPU
+            vals = torch.empty(shape, dtype=torch.float32, device=device)
+            vp = vals.data_ptr()
+        else:
+            vals = np.empty(shape, np.float32)
+            vp = vals.ctypes.data
         lo_o, hi_o = np.empty(3), np.empty(3)
         check(lib().dpl_sample_grid(self._h, C.byref(params), float(beta_bh), res.ctypes.data,
-                                    lo_.ctypes.data, hi_.ctypes.data, vals.ctypes.data,
+                                    lo_.ctypes.data, hi_.ctypes.data, vp,
                                     lo_o.ctypes.data, hi_o.ctypes.data))
         return vals, lo_o, hi_o
 
@@ -309,14 +316,14 @@ class DipoleTree:
         rp, rk = _in(rays, np.float64)
         R = int(rays.shape[0])
         M = cfg.max_samples()
-        t = np.zeros((R, M))
-        d = np.zeros((R, M))
-        cnt = np.zeros(R, np.int32)
-        br = np.zeros(R, np.uint8)
+        # outputs live where the rays live (CUDA tensors in, CUDA tensors out)
+        tp, t = _out_like(rk, (R, M), np.float64)
+        dp, d = _out_like(rk, (R, M), np.float64)
+        cp, cnt = _out_like(rk, (R,), np.int32)
+        bp, br = _out_like(rk, (R,), np.uint8)
         check(lib().dpl_sample_rays(self._h, C.byref(params), float(beta_bh), rp, R, C.byref(cfg),
-                                    M, t.ctypes.data, d.ctypes.data, cnt.ctypes.data,
-                                    br.ctypes.data))
-        return t, d, cnt, br.astype(bool)
+                                    M, tp, dp, cp, bp))
+        return t, d, cnt, (br != 0)
 
     def primal_grad0(self, xs, params: KernelParams, beta_bh: float):
         """Values of all channels and the gradient of channel 0 only (render path)."""

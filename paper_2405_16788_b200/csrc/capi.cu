@@ -34,6 +34,8 @@ struct dpl_tree_s {
   bool built = false;
   DevBuf ws_xs, ws_perm, ws_out, ws_grad, ws_cnt, ws_morton, ws_dout, ws_dgrad, ws_flag, ws_mom,
       ws_nrm, ws_xs_adj;
+  DevBuf ws_gen_xs, ws_gen_v, ws_ray_prev, ws_ray_brk, ws_ray_act0, ws_ray_act1, ws_ray_n,
+      ws_ray_in, ws_ray_t, ws_ray_d, ws_ray_c, ws_ray_b;  // query generators, reused across calls
   cudaStream_t copy = nullptr, copy_out = nullptr;  // host<->device pipeline streams
   std::vector<cudaEvent_t> pipe_ev;                 // chunk hand-off events
   // host-async mode (dpl_tree_set_host_async): staging-buffer hazards between
@@ -477,9 +479,13 @@ static int64_t pipe_chunk(int64_t q) {
 
 extern "C" {
 
+// presorted: the caller's query order is already coherent (generated along rays
+// or grid rows); skip the Morton sort (dipole-channel values are independent of
+// the warp grouping, so results are unchanged)
 static int forward_common(dpl_tree_t h, const dpl_kernel_params* params, double beta,
                           const double* xs, int64_t q, float* out, float* grad,
-                          dpl_counters* counters, int grad_mode, int channel) {
+                          dpl_counters* counters, int grad_mode, int channel,
+                          bool presorted = false) {
   return guard([&] {
     check_tree(h);
     check_params(params);
@@ -558,13 +564,13 @@ static int forward_common(dpl_tree_t h, const dpl_kernel_params* params, double 
     if (h->host_async) h->sync_all();  // the staged path below is synchronous
     const double* xs_d = stage_in(t, xs, (size_t)q * 3, h->ws_xs);
     h->ws_perm.reserve(q * 4);
-    {
+    if (!presorted) {
       PhaseTimer pt(t, PH_SORT);
       morton_order(t, xs_d, q, h->ws_perm.as<int32_t>(), h->ws_morton);
     }
     FwdArgs a;
     a.xs = xs_d;
-    a.perm = h->ws_perm.as<int32_t>();
+    a.perm = presorted ? nullptr : h->ws_perm.as<int32_t>();
     a.q = q;
     a.overflow = overflow_flag(h);
     a.ilist = lists ? &h->il : nullptr;
@@ -651,7 +657,8 @@ int dpl_sample_grid(dpl_tree_t h, const dpl_kernel_params* params, double beta_b
     const int r[3] = {res[0], res[1], res[2]};
     const int64_t total = (int64_t)r[0] * r[1] * r[2];
     const int64_t slab = std::min<int64_t>(total, 1 << 24);
-    DevBuf xs, vals;
+    DevBuf& xs = h->ws_gen_xs;
+    DevBuf& vals = h->ws_gen_v;
     xs.reserve((size_t)slab * 24);
     vals.reserve((size_t)slab * 4);
     Out<float> o;
@@ -661,7 +668,8 @@ int dpl_sample_grid(dpl_tree_t h, const dpl_kernel_params* params, double beta_b
       grid_nodes(lo, hi, r, s0, n, xs.as<double>(), t.stream);
       // geometry_field = 0.5 - primal_channel(x, 0) (fields.cpp:27-29)
       check_rc(forward_common(h, params, beta_bh, xs.as<double>(), n, vals.as<float>(), nullptr,
-                              nullptr, 0, 0));
+                              nullptr, 0, 0));  // Morton-sorted: grid rows are coherent
+                                                 // along x only (presorted measured 1.6x slower)
       half_minus(vals.as<float>(), n, o.dev + s0, t.stream);
     }
     o.finish(t);
@@ -689,8 +697,9 @@ int dpl_sample_rays(dpl_tree_t h, const dpl_kernel_params* params, double beta_b
                  cfg->sparse_after, cfg->uniform_count};
     const int n = std::max(2, c.probe_count);
     const bool probe = cfg->t_far - cfg->t_near >= 1e-9;
-    DevBuf rays_tmp, prev, brk, act0, act1, nnext, xs, vals;
-    const double* rays_d = stage_in(t, rays, (size_t)R * 6, rays_tmp);
+    DevBuf &prev = h->ws_ray_prev, &brk = h->ws_ray_brk, &act0 = h->ws_ray_act0,
+           &act1 = h->ws_ray_act1, &nnext = h->ws_ray_n, &xs = h->ws_gen_xs, &vals = h->ws_gen_v;
+    const double* rays_d = stage_in(t, rays, (size_t)R * 6, h->ws_ray_in);
     prev.reserve((size_t)R * 4);
     brk.reserve((size_t)R * 4);
     DPL_CUDA(cudaMemsetAsync(prev.p, 0, (size_t)R * 4, t.stream));  // prev_f = 0 (:57)
@@ -705,9 +714,7 @@ int dpl_sample_rays(dpl_tree_t h, const dpl_kernel_params* params, double beta_b
       nnext.reserve(sizeof(int));
       xs.reserve((size_t)chunk * K * 24);
       vals.reserve((size_t)chunk * K * 4);
-      std::vector<int32_t> all(R);
-      for (int64_t i = 0; i < R; ++i) all[i] = (int32_t)i;
-      DPL_CUDA(cudaMemcpyAsync(act0.p, all.data(), (size_t)R * 4, cudaMemcpyHostToDevice, t.stream));
+      iota32(act0.as<int32_t>(), R, t.stream);
       int64_t n_act = R;
       int32_t* cur = act0.as<int32_t>();
       int32_t* nxt = act1.as<int32_t>();
@@ -717,8 +724,10 @@ int dpl_sample_rays(dpl_tree_t h, const dpl_kernel_params* params, double beta_b
         for (int64_t a0 = 0; a0 < n_act; a0 += chunk) {
           const int64_t na = std::min(chunk, n_act - a0);
           probe_points(rays_d, cur + a0, na, i0, kc, c, xs.as<double>(), t.stream);
+          // probes of a ray are consecutive and collinear: coherent without the sort
+          // (measured: sort 3.6 ms of 13.8 ms saved, traversal +1.5 ms)
           check_rc(forward_common(h, params, beta_bh, xs.as<double>(), na * kc, vals.as<float>(),
-                                  nullptr, nullptr, 0, 0));
+                                  nullptr, nullptr, 0, 0, true));
           probe_scan(vals.as<float>(), cur + a0, na, i0, kc, c, prev.as<float>(), brk.as<int32_t>(),
                      nxt, nnext.as<int>(), t.stream);
         }
@@ -732,11 +741,10 @@ int dpl_sample_rays(dpl_tree_t h, const dpl_kernel_params* params, double beta_b
     Out<double> to, dout;
     Out<int32_t> co;
     Out<uint8_t> bo;
-    DevBuf t_tmp, d_tmp, c_tmp, b_tmp;
-    to.bind(t, t_out, (size_t)R * max_samples, t_tmp);
-    dout.bind(t, delta_out, (size_t)R * max_samples, d_tmp);
-    co.bind(t, count_out, (size_t)R, c_tmp);
-    bo.bind(t, bracketed_out, (size_t)R, b_tmp);
+    to.bind(t, t_out, (size_t)R * max_samples, h->ws_ray_t);
+    dout.bind(t, delta_out, (size_t)R * max_samples, h->ws_ray_d);
+    co.bind(t, count_out, (size_t)R, h->ws_ray_c);
+    bo.bind(t, bracketed_out, (size_t)R, h->ws_ray_b);
     emit_samples(brk.as<int32_t>(), R, c, max_samples, to.dev, dout.dev, co.dev, bo.dev, t.stream);
     to.finish(t);
     dout.finish(t);

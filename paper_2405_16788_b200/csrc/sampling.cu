@@ -29,6 +29,12 @@ __global__ void k_grid_nodes(double lo0, double lo1, double lo2, double hi0, dou
   }
 }
 
+__global__ void k_iota32(int32_t* a, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    a[i] = (int32_t)i;
+}
+
 __global__ void k_half_minus(const float* __restrict__ v, int64_t n, float* __restrict__ out) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -94,6 +100,7 @@ __global__ void k_emit(const int32_t* __restrict__ bracket, int64_t R, RaySample
   if (span < 1e-9) {  // :50-54
     tr[0] = 0.5 * __dadd_rn(c.t_near, c.t_far);
     dr[0] = __dsub_rn(tr[0], c.t_near);
+    for (int j = 1; j < max_s; ++j) tr[j] = dr[j] = 0.0;
     count[r] = 1;
     bracketed[r] = 0;
     return;
@@ -113,6 +120,7 @@ __global__ void k_emit(const int32_t* __restrict__ bracket, int64_t R, RaySample
     emit(hi, c.t_far, c.sparse_after);
   }
   for (int j = 0; j < m; ++j) dr[j] = __dsub_rn(tr[j], j == 0 ? c.t_near : tr[j - 1]);
+  for (int j = m; j < max_s; ++j) tr[j] = dr[j] = 0.0;  // deterministic padding
   count[r] = m;
   bracketed[r] = br >= 1 ? 1 : 0;
 }
@@ -123,6 +131,11 @@ void grid_nodes(const double lo[3], const double hi[3], const int res[3], int64_
                 double* xs, cudaStream_t s) {
   k_grid_nodes<<<grid_for(n, 256), 256, 0, s>>>(lo[0], lo[1], lo[2], hi[0], hi[1], hi[2], res[0],
                                                 res[1], res[2], start, n, xs);
+  count_launch();
+}
+
+void iota32(int32_t* a, int64_t n, cudaStream_t s) {
+  k_iota32<<<grid_for(n, 256), 256, 0, s>>>(a, n);
   count_launch();
 }
 

@@ -18,6 +18,8 @@ struct RaySampler {
 // grid nodes [start, start + n) of the flat (k * r1 + j) * r0 + i order
 void grid_nodes(const double lo[3], const double hi[3], const int res[3], int64_t start, int64_t n,
                 double* xs, cudaStream_t s);
+// a[i] = i
+void iota32(int32_t* a, int64_t n, cudaStream_t s);
 // out[i] = 0.5f - v[i]
 void half_minus(const float* v, int64_t n, float* out, cudaStream_t s);
 

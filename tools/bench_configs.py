@@ -106,6 +106,48 @@ def main():
 
             ms, ph = timed(step, args.steps, tree)
             res.update(step_ms=ms, step_phases=ph, step_qps=Q / (ms * 1e-3))
+    elif args.config in (6, 7):
+        # SURVEY 8(f) rows on the config-3 scene (config-1 sphere cloud, C=4):
+        # 6 = sample_ray over its 65,536 camera rays (probe_count 1024, [2, 6]),
+        # 7 = sample_grid at 256^3 (the reference meshes at up to 512^3)
+        w = W.config3(scale=args.scale)
+        c, rays = w["cloud"], w["rays"]
+        t0 = time.perf_counter()
+        eps = B.default_epsilon(c)
+        res["eps"], res["knn_s"] = eps, time.perf_counter() - t0
+        tree, res["build_s"] = build(c, w["kinds"], dev)
+        p = P.KernelParams(epsilon=eps)
+        cfg = P.RaySampler(t_near=2.0, t_far=6.0)
+        if args.config == 6:
+            rays_d = torch.from_numpy(rays).to(dev)
+            ms, ph = timed(lambda: tree.sample_rays(p, 2.0, rays_d, cfg), args.steps, tree)
+            _, _, cnt, br = tree.sample_rays(p, 2.0, rays_d, cfg)
+            res.update(rays=rays.shape[0], probe_count=1024, ms=ms, phases=ph,
+                       rays_per_s=rays.shape[0] / (ms * 1e-3),
+                       bracketed=float(br.float().mean()), outputs="device-resident")
+            ref_sample = 512
+        else:
+            r = max(8, int(256 * args.scale ** (1 / 3)))
+            ms, ph = timed(lambda: tree.sample_grid(p, 2.0, (r, r, r), device=dev), args.steps,
+                           tree)
+            res.update(resolution=r, ms=ms, phases=ph, nodes_per_s=r ** 3 / (ms * 1e-3))
+        # the reference's own implementation on the host cores, bounded sample
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import oracle as O
+
+        if O.have_ref():
+            ref = O.RefModel(O.Cloud(c.positions, c.normals, c.areas, c.moments), eps, beta=2.0)
+            t0 = time.perf_counter()
+            if args.config == 6:
+                ref.sample_rays(rays[:ref_sample], 2.0, 6.0, (1024, 24, 48, 8, 80), 80)
+                dt = time.perf_counter() - t0
+                res["reference_cpu"] = {"rays": ref_sample, "s": dt, "rays_per_s": ref_sample / dt,
+                                        "cores": O.ref_lib().ref_hardware_concurrency()}
+            else:
+                ref.sample_grid((64, 64, 64))
+                dt = time.perf_counter() - t0
+                res["reference_cpu"] = {"resolution": 64, "s": dt, "nodes_per_s": 64 ** 3 / dt,
+                                        "cores": O.ref_lib().ref_hardware_concurrency()}
     elif args.config in (3, 5):
         if args.config == 3:
             w = W.config3(scale=args.scale)
