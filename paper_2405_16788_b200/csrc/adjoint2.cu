@@ -378,17 +378,29 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
           if (ownB) eps_acc += (double)(eB * rad[slotB]);
         }
       }
-      // vector quantities: transposed sum of vq[e][k][l] over l
-      const float4 v4 = reinterpret_cast<const float4*>(vq + e * 128)[lane];
-      float s = (v4.x + v4.y) + (v4.z + v4.w);
-      s += __shfl_xor_sync(FULL_MASK, s, 1);
-      s += __shfl_xor_sync(FULL_MASK, s, 2);
-      s += __shfl_xor_sync(FULL_MASK, s, 4);
-      if ((lane & 7) == 0 && s != 0.f) {
-        const int k = lane >> 3;  // 0..2 vector, 3 = d mu_0
-        double* dst = is_point ? (k < 3 ? acc.pt_n + 3 * src + k : acc.pt_mud + src)
-                               : acc.node_v + 3 * src + k;
-        if (is_point || k < 3) atomicAdd(dst, (double)s);
+    }
+    // vector quantities of the whole batch: lane L sums pair (e, k) = (L / 4, L % 4)
+    // of vq[e][k][0..31] (8 LDS.128, rotated by L so the 8 lanes of each phase
+    // hit distinct bank groups) and issues at most one RED
+    for (int p0 = 0; p0 < 4 * nent; p0 += 32) {
+      const int pr = p0 + lane;
+      if (pr < 4 * nent) {
+        const float4* row = reinterpret_cast<const float4*>(vq + pr * 32);
+        float s = 0.f;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float4 v4 = row[(j + lane) & 7];
+          s += (v4.x + v4.y) + (v4.z + v4.w);
+        }
+        const int e = pr >> 2, k = pr & 3;  // 0..2 vector, 3 = d mu_0
+        const int m = meta[e];
+        const bool is_point = m & (1 << 30);
+        const int64_t src = m & ((1 << 29) - 1);
+        if (s != 0.f && (is_point || k < 3)) {
+          double* dst = is_point ? (k < 3 ? acc.pt_n + 3 * src + k : acc.pt_mud + src)
+                                 : acc.node_v + 3 * src + k;
+          atomicAdd(dst, (double)s);
+        }
       }
     }
     __syncwarp();
