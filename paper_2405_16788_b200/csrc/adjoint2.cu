@@ -63,6 +63,15 @@ __device__ __forceinline__ void mma_bf16(float (&c)[4], const uint4& a, uint32_t
 }
 // smallest stride >= n floats with stride = 8 or 24 (mod 32): conflict-free
 // fragment gathers from a [32][stride] tile
+// packed fp32 FMA (Blackwell FFMA2): acc.{x,y} += a.{x,y} * b.{x,y}, one issue slot
+__device__ __forceinline__ void fma2(float2& acc, float2 a, float2 b) {
+  unsigned long long A, B, C;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(A) : "f"(a.x), "f"(a.y));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(B) : "f"(b.x), "f"(b.y));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(C) : "f"(acc.x), "f"(acc.y));
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(C) : "l"(A), "l"(B));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(acc.x), "=f"(acc.y) : "l"(C));
+}
 constexpr int tile_stride(int n) {
   int r = n;
   while (r % 32 != 8 && r % 32 != 24) ++r;
@@ -325,16 +334,16 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
       if constexpr (FF) {
         const bool near = m & (1 << 29);
         const float4* wr4 = reinterpret_cast<const float4*>(wR + e * WS);
-        float sA = 0.f, sB = 0.f;
+        // even / odd query partial sums on the packed FMA pipe (FFMA2)
+        float2 pA = make_float2(0.f, 0.f), pB = make_float2(0.f, 0.f);
 #pragma unroll
         for (int l4 = 0; l4 < 8; ++l4) {
           const float4 ww = wr4[l4];
-          const float wv[4] = {ww.x, ww.y, ww.z, ww.w};
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int l = 4 * l4 + u;
-            sA = fmaf(wv[u], colA[l], sA);
-            if (NB == 2) sB = fmaf(wv[u], colB[l], sB);
+          fma2(pA, make_float2(ww.x, ww.y), make_float2(colA[4 * l4], colA[4 * l4 + 1]));
+          fma2(pA, make_float2(ww.z, ww.w), make_float2(colA[4 * l4 + 2], colA[4 * l4 + 3]));
+          if (NB == 2) {
+            fma2(pB, make_float2(ww.x, ww.y), make_float2(colB[4 * l4], colB[4 * l4 + 1]));
+            fma2(pB, make_float2(ww.z, ww.w), make_float2(colB[4 * l4 + 2], colB[4 * l4 + 3]));
           }
         }
         if (NB == 1) {
@@ -343,13 +352,13 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
 #pragma unroll
           for (int i4 = 0; i4 < 4; ++i4) {
             const float4 ww = reinterpret_cast<const float4*>(wh)[i4];
-            sB = fmaf(ww.x, colB[4 * i4 + 0], sB);
-            sB = fmaf(ww.y, colB[4 * i4 + 1], sB);
-            sB = fmaf(ww.z, colB[4 * i4 + 2], sB);
-            sB = fmaf(ww.w, colB[4 * i4 + 3], sB);
+            fma2(pB, make_float2(ww.x, ww.y), make_float2(colB[4 * i4], colB[4 * i4 + 1]));
+            fma2(pB, make_float2(ww.z, ww.w), make_float2(colB[4 * i4 + 2], colB[4 * i4 + 3]));
           }
-          sB += __shfl_xor_sync(FULL_MASK, sB, 16);
         }
+        const float sA = pA.x + pA.y;
+        float sB = pB.x + pB.y;
+        if (NB == 1) sB += __shfl_xor_sync(FULL_MASK, sB, 16);
         double* dst_s = is_point ? acc.pt_mur + src * Cr : acc.node_s + src * Cr;
         if (okA && sA != 0.f) atomicAdd(dst_s + lane, (double)sA);
         const bool ownB = NB == 2 ? okB : (NB == 1 ? (okB && lane < 16) : false);
