@@ -136,12 +136,16 @@ struct AdjLayout {
 // MAXR: register cap (occupancy vs. spills; chosen by measurement)
 // LIST: replay the batch's interaction lists (ilist.cuh); warps whose list is
 // incomplete walk the tree as the fused kernel does (same entry order).
-template <int NB, int GM, int WARPS, int ENT, int RR, int MAXR = 128, int MT = 0, bool LIST = false>
+// REG: compiled for the regularized kernel (the mode tests fold away)
+template <int NB, int GM, int WARPS, int ENT, int RR, int MAXR = 128, int MT = 0, bool LIST = false,
+          bool REG = false>
 __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
-    k_adjoint2(TreeView tv, KParams kp, const double* __restrict__ xs,
+    k_adjoint2(TreeView tv, KParams kp_in, const double* __restrict__ xs,
                const int32_t* __restrict__ perm, int64_t q, const float* __restrict__ d_out,
                int dstride, const float* __restrict__ d_grad, int nr,
                const int* __restrict__ chmap, Adj2Ptrs acc, IListView lv, int* overflow) {
+  KParams kp = kp_in;
+  if (REG) kp.mode = KM_REGULARIZED;
   using L = AdjLayout<MT, ENT, RR>;
   constexpr int F4 = L::F4;
   constexpr int WS = L::WS;
@@ -617,32 +621,40 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
   if (lane == 0 && eps_acc != 0.0) atomicAdd(acc.d_eps, eps_acc);
 }
 
-template <int NB, int GM, int RR, int WARPS, int ENT, int MAXR, int MT, bool LIST>
+template <int NB, int GM, int RR, int WARPS, int ENT, int MAXR, int MT, bool LIST, bool REG>
 static void launch_adj2c(const Tree& t, const KParams& kp, const AdjArgs& a, GradBuf& b, int nr,
                          IListView lv) {
   const size_t smem = (size_t)WARPS * AdjLayout<MT, ENT, RR>::WARP_FLOATS * 4;
   static bool attr = false;
   if (!attr) {
-    DPL_CUDA(cudaFuncSetAttribute(k_adjoint2<NB, GM, WARPS, ENT, RR, MAXR, MT, LIST>,
+    DPL_CUDA(cudaFuncSetAttribute(k_adjoint2<NB, GM, WARPS, ENT, RR, MAXR, MT, LIST, REG>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
   Adj2Ptrs p{b.node_v, b.node_s, b.pt_mud, b.pt_mur, b.pt_n, b.d_eps};
   unsigned blocks = (unsigned)((a.q + WARPS * 32 - 1) / (WARPS * 32));
-  k_adjoint2<NB, GM, WARPS, ENT, RR, MAXR, MT, LIST><<<blocks, WARPS * 32, smem, t.stream>>>(
+  k_adjoint2<NB, GM, WARPS, ENT, RR, MAXR, MT, LIST, REG><<<blocks, WARPS * 32, smem, t.stream>>>(
       t.view(), kp, a.xs, a.perm, a.q, a.d_out, a.dstride, a.d_grad, nr, t.chmap.as<int>(), p, lv,
       a.overflow);
   count_launch();
 }
 
 // builds (or reuses) the interaction lists when the caller provides the workspace
-template <int NB, int GM, int RR, int WARPS = 4, int ENT = 8, int MAXR = 128, int MT = 0>
+// SPEC: also instantiate the regularized-mode kernels (production configurations)
+template <int NB, int GM, int RR, int WARPS = 4, int ENT = 8, int MAXR = 128, int MT = 0,
+          bool SPEC = false>
 static void launch_adj2(const Tree& t, const KParams& kp, const AdjArgs& a, GradBuf& b, int nr) {
+  const bool reg = SPEC && kp.mode == KM_REGULARIZED;
   if (a.ilist && !no_ilist()) {
     ilist_build(t, *a.ilist, a.xs, a.perm, a.q, a.beta, a.overflow);
-    launch_adj2c<NB, GM, RR, WARPS, ENT, MAXR, MT, true>(t, kp, a, b, nr, a.ilist->view());
+    if (reg)
+      launch_adj2c<NB, GM, RR, WARPS, ENT, MAXR, MT, true, SPEC>(t, kp, a, b, nr, a.ilist->view());
+    else
+      launch_adj2c<NB, GM, RR, WARPS, ENT, MAXR, MT, true, false>(t, kp, a, b, nr, a.ilist->view());
+  } else if (reg) {
+    launch_adj2c<NB, GM, RR, WARPS, ENT, MAXR, MT, false, SPEC>(t, kp, a, b, nr, IListView{});
   } else {
-    launch_adj2c<NB, GM, RR, WARPS, ENT, MAXR, MT, false>(t, kp, a, b, nr, IListView{});
+    launch_adj2c<NB, GM, RR, WARPS, ENT, MAXR, MT, false, false>(t, kp, a, b, nr, IListView{});
   }
 }
 
@@ -656,20 +668,12 @@ static bool adj2_plan(const Tree& t, const KParams& kp, const AdjArgs& a, GradBu
   if (tc) {  // rows staged up to the slots used
     if (nr <= 16) return launch_adj2<0, GM, 4, 4, 8, 128, 1>(t, kp, a, b, nr), true;
     if (nr <= 32) return launch_adj2<0, GM, 8, 4, 8, 128, 2>(t, kp, a, b, nr), true;
-    if (nr <= 48) {
-      const char* v = getenv("DPL_TUNE_ADJ");
-      switch (v ? atoi(v) : 0) {  // (warps, register cap) experiments
-        case 1: return launch_adj2<0, GM, 12, 4, 8, 168, 3>(t, kp, a, b, nr), true;
-        case 2: return launch_adj2<0, GM, 12, 3, 8, 168, 3>(t, kp, a, b, nr), true;
-        case 3: return launch_adj2<0, GM, 12, 2, 8, 160, 3>(t, kp, a, b, nr), true;
-        case 4: return launch_adj2<0, GM, 12, 4, 8, 144, 3>(t, kp, a, b, nr), true;
-        default: return launch_adj2<0, GM, 12, 4, 8, 128, 3>(t, kp, a, b, nr), true;
-      }
-    }
+    // best measured (warps, register cap) for the 48-channel tile: 2 warps, 160
+    if (nr <= 48) return launch_adj2<0, GM, 12, 2, 8, 160, 3>(t, kp, a, b, nr), true;
   }
   if (t.F4 - 1 > 16) return false;
-  if (nr <= 32) return launch_adj2<0, GM, 16>(t, kp, a, b, nr), true;
-  if (nr <= 48) return launch_adj2<1, GM, 16>(t, kp, a, b, nr), true;
+  if (nr <= 32) return launch_adj2<0, GM, 16, 4, 8, 128, 0, true>(t, kp, a, b, nr), true;
+  if (nr <= 48) return launch_adj2<1, GM, 16, 4, 8, 128, 0, true>(t, kp, a, b, nr), true;
   if (nr <= 64) return launch_adj2<2, GM, 16>(t, kp, a, b, nr), true;
   return false;
 }

@@ -72,13 +72,16 @@ constexpr int row_stride_floats(int f4) {
 // LIST: replay the batch's interaction lists (ilist.cuh) instead of walking the
 // tree; warps whose list is incomplete walk it as in the fused kernel. Both
 // paths run the same arithmetic in the same entry order -> identical results.
-template <int NT, int WARPS, int ENT, int MAXR, bool COUNT, bool LIST>
+// REG: compiled for the regularized kernel (the mode tests fold away)
+template <int NT, int WARPS, int ENT, int MAXR, bool COUNT, bool LIST, bool REG = false>
 __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
-    k_forward_tc(TreeView tv, KParams kp, const double* __restrict__ xs,
+    k_forward_tc(TreeView tv, KParams kp_in, const double* __restrict__ xs,
                  const int32_t* __restrict__ perm, int64_t q, int nr,
                  const int* __restrict__ chmap, float* __restrict__ out, int out_stride,
                  int only_ch, long long* __restrict__ counters, IListView lv, int* overflow) {
   static_assert(ENT % 8 == 0, "ENT must be a multiple of the mma K (8)");
+  KParams kp = kp_in;
+  if (REG) kp.mode = KM_REGULARIZED;
   constexpr int TR = 8 * NT;
   constexpr int F4 = 1 + TR / 4;               // global row float4 (dipole + radial)
   constexpr int RSF = row_stride_floats(F4);   // padded smem row stride (floats)
@@ -319,7 +322,7 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
     }
 }
 
-template <int NT, int WARPS, int ENT, int MAXR, bool COUNT, bool LIST>
+template <int NT, int WARPS, int ENT, int MAXR, bool COUNT, bool LIST, bool REG = false>
 static void launch_tc1(const Tree& t, const KParams& kp, const FwdArgs& a, int nr,
                        IListView lv = {}) {
   constexpr int F4 = 1 + 2 * NT;
@@ -328,27 +331,34 @@ static void launch_tc1(const Tree& t, const KParams& kp, const FwdArgs& a, int n
   const size_t smem = (size_t)WARPS * WARP_FLOATS * 4;
   static bool attr = false;
   if (!attr) {
-    DPL_CUDA(cudaFuncSetAttribute(k_forward_tc<NT, WARPS, ENT, MAXR, COUNT, LIST>,
+    DPL_CUDA(cudaFuncSetAttribute(k_forward_tc<NT, WARPS, ENT, MAXR, COUNT, LIST, REG>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
   unsigned blocks = (unsigned)((a.q + WARPS * 32 - 1) / (WARPS * 32));
-  k_forward_tc<NT, WARPS, ENT, MAXR, COUNT, LIST><<<blocks, WARPS * 32, smem, t.stream>>>(
+  k_forward_tc<NT, WARPS, ENT, MAXR, COUNT, LIST, REG><<<blocks, WARPS * 32, smem, t.stream>>>(
       t.view(), kp, a.xs, a.perm, a.q, nr, t.chmap.as<int>(), a.out, a.out_stride, a.only_ch,
       a.counters, lv, a.overflow);
   count_launch();
 }
 
-template <int NT, int WARPS, int ENT, int MAXR>
+// SPEC: also instantiate the regularized-mode kernels (production configurations)
+template <int NT, int WARPS, int ENT, int MAXR, bool SPEC = false>
 static void launch_tc(const Tree& t, const KParams& kp, const FwdArgs& a, int nr) {
-  if (a.counters)
+  const bool reg = SPEC && kp.mode == KM_REGULARIZED;
+  if (a.counters) {
     launch_tc1<NT, WARPS, ENT, MAXR, true, false>(t, kp, a, nr);
-  else if (a.ilist && !no_ilist()) {
+  } else if (a.ilist && !no_ilist()) {
     ilist_build(t, *a.ilist, a.xs, a.perm, a.q, a.beta, a.overflow);
-    launch_tc1<NT, WARPS, ENT, MAXR, false, true>(t, kp, a, nr, a.ilist->view());
-  }
-  else
+    if (reg)
+      launch_tc1<NT, WARPS, ENT, MAXR, false, true, SPEC>(t, kp, a, nr, a.ilist->view());
+    else
+      launch_tc1<NT, WARPS, ENT, MAXR, false, true>(t, kp, a, nr, a.ilist->view());
+  } else if (reg) {
+    launch_tc1<NT, WARPS, ENT, MAXR, false, false, SPEC>(t, kp, a, nr);
+  } else {
     launch_tc1<NT, WARPS, ENT, MAXR, false, false>(t, kp, a, nr);
+  }
 }
 
 // Tensor-core plan: one dipole slot and PR a multiple of 8 (8..64 radial).
@@ -359,7 +369,7 @@ bool forward_tc_launch(const Tree& t, const KParams& kp, const FwdArgs& a) {
   // (forward_tc / forward2), so it is bitwise primal()[c] at a fraction of the work
   const bool two_phase_values = t.PR == 0 || t.PR == 4 || t.PR == 16 || t.PR == 48 || t.PR == 64;
   if (a.only_ch >= 0 && t.Cd == 1 && t.kinds[a.only_ch] == 0 && two_phase_values)
-    return launch_tc<0, 4, 8, 128>(t, kp, a, 0), true;
+    return launch_tc<0, 4, 8, 128, true>(t, kp, a, 0), true;
   if (t.Cd != 1 || t.PR % 8 != 0) return false;
   const int nr = a.nr_limit >= 0 ? std::min(a.nr_limit, t.Cr) : t.Cr;
   const char* v = getenv("DPL_TUNE_TC");
@@ -372,7 +382,7 @@ bool forward_tc_launch(const Tree& t, const KParams& kp, const FwdArgs& a) {
         case 1: return launch_tc<6, 4, 16, 128>(t, kp, a, nr), true;
         case 2: return launch_tc<6, 4, 8, 112>(t, kp, a, nr), true;
         case 3: return launch_tc<6, 8, 8, 128>(t, kp, a, nr), true;
-        default: return launch_tc<6, 4, 8, 128>(t, kp, a, nr), true;  // measured best
+        default: return launch_tc<6, 4, 8, 128, true>(t, kp, a, nr), true;  // measured best
       }
     case 64: return launch_tc<8, 4, 8, 128>(t, kp, a, nr), true;
     default: return false;
