@@ -75,11 +75,13 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
 
   int cur = (int)wg;  // chunk being filled (warp w owns chunk w)
   int total = 0;      // entries written
+  int room = IL_CHUNK;  // free slots in the current chunk
+  uint2* wp = pool + (size_t)cur * IL_CHUNK;
   bool ok = true;
-  // lane 0 appends each entry with one 8-byte store (a warp's entries are
-  // contiguous within a chunk, so L2 merges them into full sectors)
+  // lane 0 appends each entry with one 8-byte store through a running pointer
+  // (a warp's entries are contiguous within a chunk: L2 merges full sectors)
   auto emit = [&](uint32_t src, uint32_t m) {
-    if (total > 0 && (total & (IL_CHUNK - 1)) == 0) {  // chunk full: link a fresh one
+    if (room == 0) {  // chunk full: link a fresh one
       unsigned long long c = 0;
       if (lane == 0) c = atomicAdd(ctr, 1ull);
       c = __shfl_sync(FULL_MASK, c, 0);
@@ -89,8 +91,12 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
       }
       if (lane == 0) next[cur] = (int)c;
       cur = (int)c;
+      wp = pool + (size_t)cur * IL_CHUNK;
+      room = IL_CHUNK;
     }
-    if (lane == 0) pool[(size_t)cur * IL_CHUNK + (total & (IL_CHUNK - 1))] = make_uint2(src, m);
+    if (lane == 0) *wp = make_uint2(src, m);
+    ++wp;
+    --room;
     ++total;
   };
 
