@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
   const bool singular = kp.mode == KM_SINGULAR;
   const float4* __restrict__ node_row = tv.node_row;
   const float4* __restrict__ pt_row = tv.pt_row;
-  const int F4g = tv.F4;  // row stride in HBM (== F4 unless NT = 0)
+  const int F4g = NT > 0 ? F4 : tv.F4;  // row stride in HBM (== F4, compile-time, unless NT = 0)
   int nent = 0;
 
   auto evaluate = [&]() {
