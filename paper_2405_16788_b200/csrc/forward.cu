@@ -229,8 +229,38 @@ __device__ __forceinline__ uint32_t spread10(uint32_t v) {
   return v;
 }
 
+// 3-D Hilbert index of 10-bit coordinates (Skilling's transpose form): no
+// long jumps between consecutive cells, so the 32 queries of a warp are more
+// compact than along the Morton curve
+__device__ __forceinline__ uint32_t hilbert3(uint32_t x, uint32_t y, uint32_t z) {
+  uint32_t X[3] = {x, y, z};
+  for (uint32_t Q = 1u << 9; Q > 1; Q >>= 1) {
+    const uint32_t P = Q - 1;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      if (X[i] & Q) {
+        X[0] ^= P;
+      } else {
+        const uint32_t t = (X[0] ^ X[i]) & P;
+        X[0] ^= t;
+        X[i] ^= t;
+      }
+    }
+  }
+  X[1] ^= X[0];
+  X[2] ^= X[1];
+  uint32_t t = 0;
+  for (uint32_t Q = 1u << 9; Q > 1; Q >>= 1)
+    if (X[2] & Q) t ^= Q - 1;
+  X[0] ^= t, X[1] ^= t, X[2] ^= t;
+  uint32_t key = 0;
+  for (int bit = 9; bit >= 0; --bit)
+    key = (key << 3) | (((X[0] >> bit) & 1) << 2) | (((X[1] >> bit) & 1) << 1) | ((X[2] >> bit) & 1);
+  return key;
+}
+
 __global__ void k_morton(const double* __restrict__ xs, int64_t q, double lx, double ly,
-                         double lz, double inv, uint32_t* keys, int32_t* idx) {
+                         double lz, double inv, int hilbert, uint32_t* keys, int32_t* idx) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= q) return;
   auto qz = [&](double v, double lo) {
@@ -239,7 +269,7 @@ __global__ void k_morton(const double* __restrict__ xs, int64_t q, double lx, do
     return (uint32_t)f;
   };
   uint32_t a = qz(xs[3 * i], lx), b = qz(xs[3 * i + 1], ly), c = qz(xs[3 * i + 2], lz);
-  keys[i] = spread10(a) | (spread10(b) << 1) | (spread10(c) << 2);
+  keys[i] = hilbert ? hilbert3(a, b, c) : (spread10(a) | (spread10(b) << 1) | (spread10(c) << 2));
   idx[i] = (int32_t)i;
 }
 
@@ -261,8 +291,11 @@ void morton_order(Tree& t, const double* xs_dev, int64_t q, int32_t* perm_out, D
   uint32_t* keys_s = keys + q;
   int32_t* idx = (int32_t*)(keys_s + q);
   void* tmp = (void*)(((uintptr_t)(idx + q) + 255) & ~(uintptr_t)255);
+  // Hilbert order by default (config 2: step 38.3 -> 36.0 ms vs Morton);
+  // DPL_ORDER_MORTON=1 restores the Morton curve
+  static const bool hilbert = getenv("DPL_ORDER_MORTON") == nullptr;
   k_morton<<<(unsigned)((q + 255) / 256), 256, 0, t.stream>>>(xs_dev, q, lo[0], lo[1], lo[2], inv,
-                                                               keys, idx);
+                                                               hilbert ? 1 : 0, keys, idx);
   count_launch();
   DPL_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, keys, keys_s, idx, perm_out, (int)q, 0, 30,
                                            t.stream));
