@@ -107,6 +107,30 @@ int dpl_tree_export_moments(dpl_tree_t tree, float* moments_v, float* moments_s)
 /* DipoleTree::dump "DPLT" v1 byte format (bhtree.cpp:465-494). */
 int dpl_tree_dump(dpl_tree_t tree, const char* path);
 
+/* ---- DPCK checkpoints (optimizer.cpp:294-388) -------------- */
+typedef struct {
+  int32_t iter;
+  int32_t head_variant; /* 0 direct-rgb, 1 tiny-mlp (HeadVariant, radiance.hpp) */
+  int32_t with_albedo;
+  int32_t reserved;
+  double lambda_scale, epsilon, background[3], beta_bh;
+} dpl_checkpoint_meta;
+/* save_checkpoint (:330-356): the tree's current cloud (positions, normals,
+ * areas, moments as last built / updated), the initial normals (N x 3; NULL =
+ * the current normals), the head's MLP (n_sizes = 0 for direct-rgb) and the
+ * scalars. Byte-identical to the reference's file for the same model. */
+int dpl_checkpoint_save(dpl_tree_t tree, const char* path, const dpl_checkpoint_meta* meta,
+                        const double* initial_normals, const int32_t* mlp_sizes, int32_t n_sizes,
+                        const double* mlp_w, int64_t n_w);
+/* load_checkpoint (:358-388), host side. Call with NULL arrays to read the
+ * counts (n, k_appearance, n_sizes, n_w), then with buffers: pos / nrm /
+ * initial_normals n x 3, area n, mu n x (1 + k_appearance), sizes, w.
+ * DataError on a bad magic / version / truncated file. */
+int dpl_checkpoint_read(const char* path, dpl_checkpoint_meta* meta, int64_t* n,
+                        int32_t* k_appearance, int32_t* n_sizes, int64_t* n_w, double* pos,
+                        double* nrm, double* area, double* mu, double* initial_normals,
+                        int32_t* sizes, double* w);
+
 /* ---- forward queries -------------------------------------------------------
  * DipoleTree::primal / primal_with_gradient (bhtree.cpp:188-234,276-334) for a
  * batch of q query points xs (q x 3, fp64 like Vec3). out: q x C fp32.

@@ -131,6 +131,7 @@ def ref_lib():
         lib.ref_erf_approx.argtypes = [C.c_double]
         lib.ref_normal_hazard.restype = C.c_double
         lib.ref_normal_hazard.argtypes = [C.c_double]
+        lib.ref_model_save_checkpoint.argtypes = [vp, C.c_int32, C.c_char_p]
         lib.ref_sample_grid.argtypes = [vp, _ip, _dp, _dp, C.c_int, _dp, _dp, _dp]
         lib.ref_sample_rays.argtypes = [vp, _dp, C.c_int64, C.c_double, C.c_double, _ip, C.c_int32,
                                         _dp, _dp, _ip, _up]
@@ -410,6 +411,10 @@ class RefModel:
         if getattr(self, "_h", None):
             self._lib.ref_model_free(self._h)
             self._h = None
+
+    def save_checkpoint(self, path, iter=0):
+        """The reference's own save_checkpoint (optimizer.cpp:330-356)."""
+        _check_ref(self._lib.ref_model_save_checkpoint(self._h, iter, str(path).encode()))
 
     def sample_grid(self, res, lo=(0, 0, 0), hi=(0, 0, 0), threads=0):
         """The reference's own sample_grid (meshing.cpp:33-59) on this model."""

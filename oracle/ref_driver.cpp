@@ -317,6 +317,11 @@ int ref_model_create(const double* pos, const double* nrm, const double* area, c
 
 void ref_model_free(ref_model* m) { delete m; }
 
+// ---- DPCK checkpoint (optimizer.cpp:330-356) ---------------------------------
+int ref_model_save_checkpoint(ref_model* m, int32_t iter, const char* path) {
+  return guard([&] { save_checkpoint(m->model, iter, path); });
+}
+
 // ---- query generators ----------------------------------------
 // sample_grid (meshing.cpp:33-59) on the model: values (r2 x r1 x r0), box used
 int ref_sample_grid(ref_model* m, const int32_t* res, const double* lo, const double* hi,

@@ -70,6 +70,14 @@ class RaySampler(C.Structure):
                    self.sparse_before + max(1, self.dense_at) + self.sparse_after)
 
 
+class CheckpointMeta(C.Structure):
+    """dpl_checkpoint_meta: DPCK scalars (optimizer.cpp:330-356)."""
+
+    _fields_ = [("iter", C.c_int32), ("head_variant", C.c_int32), ("with_albedo", C.c_int32),
+                ("reserved", C.c_int32), ("lambda_scale", C.c_double), ("epsilon", C.c_double),
+                ("background", C.c_double * 3), ("beta_bh", C.c_double)]
+
+
 _lib = None
 
 _vp = C.c_void_p
@@ -102,6 +110,11 @@ _sig = {
                                   _vp, _vp]),
     "dpl_sample_rays": (C.c_int, [_vp, C.POINTER(KernelParams), C.c_double, _vp, C.c_int64,
                                   C.POINTER(RaySampler), C.c_int32, _vp, _vp, _vp, _vp]),
+    "dpl_checkpoint_save": (C.c_int, [_vp, C.c_char_p, C.POINTER(CheckpointMeta), _vp, _vp,
+                                      C.c_int32, _vp, C.c_int64]),
+    "dpl_checkpoint_read": (C.c_int, [C.c_char_p, C.POINTER(CheckpointMeta), C.POINTER(C.c_int64),
+                                      C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                      C.POINTER(C.c_int64), _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "dpl_gradbuf_create": (C.c_int, [_vp, C.POINTER(_vp)]),
     "dpl_gradbuf_destroy": (C.c_int, [_vp]),
     "dpl_gradbuf_zero": (C.c_int, [_vp]),

@@ -284,6 +284,26 @@ class DipoleTree:
         check(lib().dpl_primal(self._h, C.byref(params), float(beta_bh), xp, q, op, gp, None))
         return out, grad
 
+    # -- DPCK checkpoints (optimizer.cpp:294-388) --------------------------------
+    def save_checkpoint(self, path, iter=0, lambda_scale=20.0, epsilon=0.0, background=(0, 0, 0),
+                        beta_bh=2.0, initial_normals=None, head_variant=0, with_albedo=False,
+                        mlp_sizes=(), mlp_w=()):
+        """save_checkpoint (optimizer.cpp:330-356) of the tree's current cloud."""
+        from ._lib import CheckpointMeta
+
+        m = CheckpointMeta(int(iter), int(head_variant), int(bool(with_albedo)), 0,
+                           float(lambda_scale), float(epsilon),
+                           (C.c_double * 3)(*[float(b) for b in background]), float(beta_bh))
+        ip = None
+        if initial_normals is not None:
+            inn = np.ascontiguousarray(initial_normals, dtype=np.float64).reshape(-1, 3)
+            ip = inn.ctypes.data
+        sz = np.ascontiguousarray(mlp_sizes, dtype=np.int32)
+        wv = np.ascontiguousarray(mlp_w, dtype=np.float64)
+        check(lib().dpl_checkpoint_save(self._h, str(path).encode(), C.byref(m), ip,
+                                        sz.ctypes.data if sz.size else None, int(sz.size),
+                                        wv.ctypes.data if wv.size else None, int(wv.size)))
+
     # -- query generators (SURVEY §8(f)) ----------------------------------------
     def sample_grid(self, params: KernelParams, beta_bh: float, resolution, lo=(0, 0, 0),
                     hi=(0, 0, 0), device=None):
@@ -460,3 +480,26 @@ def peak_fp64(device=0) -> float:
     v = C.c_double()
     check(lib().dpl_peak_fp64(int(device), C.byref(v)))
     return v.value
+
+
+def load_checkpoint(path):
+    """load_checkpoint (optimizer.cpp:358-388): host arrays + scalars of a DPCK file."""
+    from ._lib import CheckpointMeta
+
+    m = CheckpointMeta()
+    n, K, ns, nw = C.c_int64(), C.c_int32(), C.c_int32(), C.c_int64()
+    p = str(path).encode()
+    check(lib().dpl_checkpoint_read(p, C.byref(m), C.byref(n), C.byref(K), C.byref(ns),
+                                    C.byref(nw), None, None, None, None, None, None, None))
+    N, Cc = n.value, K.value + 1
+    pos, nrm, inn = (np.empty((N, 3)) for _ in range(3))
+    area, mu = np.empty(N), np.empty((N, Cc))
+    sizes, w = np.empty(ns.value, np.int32), np.empty(nw.value)
+    check(lib().dpl_checkpoint_read(p, C.byref(m), C.byref(n), C.byref(K), C.byref(ns),
+                                    C.byref(nw), pos.ctypes.data, nrm.ctypes.data,
+                                    area.ctypes.data, mu.ctypes.data, inn.ctypes.data,
+                                    sizes.ctypes.data, w.ctypes.data))
+    return dict(iter=m.iter, cloud=OrientedPointCloud(pos, nrm, area, mu), initial_normals=inn,
+                head_variant=m.head_variant, with_albedo=bool(m.with_albedo), mlp_sizes=sizes,
+                mlp_w=w, lambda_scale=m.lambda_scale, epsilon=m.epsilon,
+                background=np.array(m.background[:]), beta_bh=m.beta_bh)

@@ -352,6 +352,132 @@ int dpl_tree_export_moments(dpl_tree_t h, float* moments_v, float* moments_s) {
   });
 }
 
+// ---------------------------------------------------------------- checkpoints
+// DPCK v1 (optimizer.cpp:294-388): little-endian, the reference's field order.
+int dpl_checkpoint_save(dpl_tree_t h, const char* path, const dpl_checkpoint_meta* meta,
+                        const double* initial_normals, const int32_t* mlp_sizes, int32_t n_sizes,
+                        const double* mlp_w, int64_t n_w) {
+  return guard([&] {
+    check_tree(h);
+    require(path && meta, DPL_ERR_USAGE, "null argument");
+    require(n_sizes >= 0 && n_w >= 0 && (n_sizes == 0 || mlp_sizes) && (n_w == 0 || mlp_w),
+            DPL_ERR_USAGE, "bad mlp description");
+    Tree& t = h->t;
+    DPL_CUDA(cudaSetDevice(t.device));
+    const int64_t n = t.n;
+    const int C = t.C;
+    std::vector<double> pos(n * 3), nrm(n * 3), area(n), mu(n * (size_t)C);
+    DPL_CUDA(cudaMemcpyAsync(pos.data(), t.pos64.p, n * 24, cudaMemcpyDeviceToHost, t.stream));
+    DPL_CUDA(cudaMemcpyAsync(nrm.data(), t.nrm64.p, n * 24, cudaMemcpyDeviceToHost, t.stream));
+    DPL_CUDA(cudaMemcpyAsync(area.data(), t.area64.p, n * 8, cudaMemcpyDeviceToHost, t.stream));
+    DPL_CUDA(cudaMemcpyAsync(mu.data(), t.mu64.p, n * (size_t)C * 8, cudaMemcpyDeviceToHost,
+                             t.stream));
+    DPL_CUDA(cudaStreamSynchronize(t.stream));
+    std::ofstream out(path, std::ios::binary);
+    if (!out) throw Error(DPL_ERR_DATA, std::string("save_checkpoint: cannot open ") + path);
+    auto put = [&](const void* p, size_t b) { out.write((const char*)p, (std::streamsize)b); };
+    const uint32_t version = 1;
+    const int32_t iter = meta->iter, K = C - 1;
+    const uint64_t M = (uint64_t)n;
+    put("DPCK", 4);
+    put(&version, 4);
+    put(&iter, 4);
+    put(&K, 4);
+    put(&M, 8);
+    for (int64_t i = 0; i < n; ++i) {  // position, normal, area, geometry, appearance
+      put(&pos[3 * i], 24);
+      put(&nrm[3 * i], 24);
+      put(&area[i], 8);
+      put(&mu[i * C], 8 * (size_t)C);
+    }
+    put(initial_normals ? initial_normals : nrm.data(), 24 * (size_t)n);
+    const uint8_t variant = (uint8_t)meta->head_variant, albedo = meta->with_albedo ? 1 : 0;
+    put(&variant, 1);
+    put(&albedo, 1);
+    const uint32_t ns = (uint32_t)n_sizes;
+    put(&ns, 4);
+    put(mlp_sizes, 4 * (size_t)n_sizes);
+    const uint64_t nw = (uint64_t)n_w;
+    put(&nw, 8);
+    put(mlp_w, 8 * (size_t)n_w);
+    put(&meta->lambda_scale, 8);
+    put(&meta->epsilon, 8);
+    put(meta->background, 24);
+    put(&meta->beta_bh, 8);
+    if (!out) throw Error(DPL_ERR_DATA, std::string("save_checkpoint: write failed for ") + path);
+  });
+}
+
+int dpl_checkpoint_read(const char* path, dpl_checkpoint_meta* meta, int64_t* n_out,
+                        int32_t* k_out, int32_t* ns_out, int64_t* nw_out, double* pos,
+                        double* nrm, double* area, double* mu, double* initial_normals,
+                        int32_t* sizes, double* w) {
+  return guard([&] {
+    require(path && meta && n_out && k_out && ns_out && nw_out, DPL_ERR_USAGE, "null argument");
+    std::ifstream in(path, std::ios::binary);
+    if (!in) throw Error(DPL_ERR_DATA, std::string("load_checkpoint: cannot open ") + path);
+    auto get = [&](void* p, size_t b) {
+      in.read((char*)p, (std::streamsize)b);
+      if (!in) throw Error(DPL_ERR_DATA, "load_checkpoint: truncated file");
+    };
+    char magic[4];
+    in.read(magic, 4);
+    if (!in || std::memcmp(magic, "DPCK", 4) != 0)
+      throw Error(DPL_ERR_DATA, std::string("load_checkpoint: bad magic in ") + path);
+    uint32_t version = 0;
+    get(&version, 4);
+    if (version != 1)
+      throw Error(DPL_ERR_DATA, std::string("load_checkpoint: unsupported version in ") + path);
+    int32_t iter = 0, K = 0;
+    uint64_t M = 0;
+    get(&iter, 4);
+    get(&K, 4);
+    get(&M, 8);
+    const bool fill = pos != nullptr;
+    const size_t C = (size_t)K + 1;
+    std::vector<double> rec(7 + C);
+    for (uint64_t i = 0; i < M; ++i) {
+      get(rec.data(), 8 * rec.size());
+      if (fill) {
+        std::memcpy(pos + 3 * i, rec.data(), 24);
+        std::memcpy(nrm + 3 * i, rec.data() + 3, 24);
+        area[i] = rec[6];
+        std::memcpy(mu + i * C, rec.data() + 7, 8 * C);
+      }
+    }
+    for (uint64_t i = 0; i < M; ++i) {
+      double v[3];
+      get(v, 24);
+      if (fill && initial_normals) std::memcpy(initial_normals + 3 * i, v, 24);
+    }
+    uint8_t variant = 0, albedo = 0;
+    get(&variant, 1);
+    get(&albedo, 1);
+    uint32_t ns = 0;
+    get(&ns, 4);
+    std::vector<int32_t> sz(ns);
+    get(sz.data(), 4 * (size_t)ns);
+    uint64_t nw = 0;
+    get(&nw, 8);
+    std::vector<double> wv(nw);
+    get(wv.data(), 8 * (size_t)nw);
+    if (fill && sizes) std::memcpy(sizes, sz.data(), 4 * (size_t)ns);
+    if (fill && w) std::memcpy(w, wv.data(), 8 * (size_t)nw);
+    meta->iter = iter;
+    meta->head_variant = variant;
+    meta->with_albedo = albedo;
+    meta->reserved = 0;
+    get(&meta->lambda_scale, 8);
+    get(&meta->epsilon, 8);
+    get(meta->background, 24);
+    get(&meta->beta_bh, 8);
+    *n_out = (int64_t)M;
+    *k_out = K;
+    *ns_out = (int32_t)ns;
+    *nw_out = (int64_t)nw;
+  });
+}
+
 int dpl_tree_dump(dpl_tree_t h, const char* path) {
   return guard([&] {
     check_tree(h);

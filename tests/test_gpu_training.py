@@ -94,3 +94,30 @@ def test_point_adam_step_matches_oracle(oracle_mod):
     got = t.primal(xs, p, 2.0)
     want = r.primal(O.Params(0.05), 2.0, xs)
     assert np.all(np.abs(got - want) <= 1e-6 + 1e-4 * np.abs(want))
+
+
+def test_checkpoint_save_matches_reference_bytes(tmp_path):
+    """save_checkpoint (optimizer.cpp:330-356) from the GPU tree writes the
+    reference's bytes; a load -> build round trip reproduces the tree."""
+    import oracle as O
+    import paper_2405_16788_b200 as P
+    from paper_2405_16788_b200.bhtree import load_checkpoint
+
+    if not O.have_ref():
+        pytest.skip("oracle/_ref not built")
+    from test_oracle_pins import _sphere_model
+
+    cloud = _sphere_model(O, n=500, C=4, seed=11).as_f64()
+    ref = O.RefModel(cloud, 0.06, lam=20.0, beta=2.0, background=(0.0, 0.5, 1.0))
+    ref.save_checkpoint(tmp_path / "ref.dpck", iter=7)
+    t = P.DipoleTree(0)
+    t.build(P.OrientedPointCloud(cloud.pos, cloud.nrm, cloud.area, cloud.mu))
+    t.save_checkpoint(tmp_path / "gpu.dpck", iter=7, lambda_scale=20.0, epsilon=0.06,
+                      background=(0.0, 0.5, 1.0), beta_bh=2.0)
+    assert (tmp_path / "gpu.dpck").read_bytes() == (tmp_path / "ref.dpck").read_bytes()
+    ck = load_checkpoint(tmp_path / "gpu.dpck")
+    t2 = P.DipoleTree(0)
+    t2.build(ck["cloud"])
+    a, b = t.export(), t2.export()
+    for k in ("topo", "order", "geo"):
+        assert np.array_equal(a[k], b[k])

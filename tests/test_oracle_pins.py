@@ -216,3 +216,35 @@ def test_port_matches_reference_sample_grid_and_rays(oracle_mod):
     for x, y in zip(a, b):
         assert np.array_equal(x, y)
     assert 0 < a[3].sum() < len(rays)  # both bracketed and missing rays
+
+
+def test_checkpoint_reader_parses_reference_dpck(oracle_mod, tmp_path):
+    """load_checkpoint (optimizer.cpp:358-388) on a file the reference's own
+    save_checkpoint wrote; malformed files raise DataError like the reference."""
+    O = oracle_mod
+    if not O.have_ref():
+        pytest.skip("oracle/_ref not built")
+    from paper_2405_16788_b200 import DataError
+    from paper_2405_16788_b200.bhtree import load_checkpoint
+
+    cloud = _sphere_model(O, n=300, C=5, seed=9)
+    ref = O.RefModel(cloud, 0.07, lam=17.0, beta=2.5, background=(0.1, 0.2, 0.3))
+    path = tmp_path / "ref.dpck"
+    ref.save_checkpoint(path, iter=42)
+    ck = load_checkpoint(path)
+    c = cloud.as_f64()
+    assert ck["iter"] == 42 and ck["head_variant"] == 0 and not ck["with_albedo"]
+    assert np.array_equal(ck["cloud"].positions, c.pos)
+    assert np.array_equal(ck["cloud"].normals, c.nrm)
+    assert np.array_equal(ck["cloud"].areas, c.area)
+    assert np.array_equal(ck["cloud"].moments, c.mu)
+    assert np.array_equal(ck["initial_normals"], c.nrm)
+    assert (ck["lambda_scale"], ck["epsilon"], ck["beta_bh"]) == (17.0, 0.07, 2.5)
+    assert np.array_equal(ck["background"], [0.1, 0.2, 0.3])
+    data = path.read_bytes()
+    (tmp_path / "bad.dpck").write_bytes(b"XXXX" + data[4:])
+    with pytest.raises(DataError):
+        load_checkpoint(tmp_path / "bad.dpck")
+    (tmp_path / "short.dpck").write_bytes(data[:len(data) // 2])
+    with pytest.raises(DataError):
+        load_checkpoint(tmp_path / "short.dpck")
