@@ -219,6 +219,16 @@ int dpl_render_forward(dpl_tree_t tree, const dpl_kernel_params* params,
 int dpl_render_backward(dpl_tree_t tree, const dpl_kernel_params* params,
                         const dpl_render_params* rp, dpl_tape_t tape, const float* d_rgb,
                         dpl_gradbuf_t buf, double* d_lambda, double* d_background);
+/* Tiny-MLP radiance head (HeadVariant::TinyMlp, radiance.hpp)
+ * for the render step: sizes run from 22 + (C - 1) inputs (x, sh(omega), normal,
+ * appearance) to 3 outputs; w: the reference's flat fp64 layout (per layer rows
+ * x cols weights then the bias, radiance.cpp:44-57). n_sizes = 0 restores the
+ * direct-rgb head. The layers run as fp32 GEMMs (cuBLAS). */
+int dpl_tree_set_mlp_head(dpl_tree_t tree, const int32_t* sizes, int32_t n_sizes, const double* w,
+                          int64_t n_w);
+/* RenderGrads::d_head_w accumulated (fp64) by dpl_render_backward since the
+ * last call; the accumulator is reset. */
+int dpl_head_grads(dpl_tree_t tree, double* d_w, int64_t n_w);
 /* The sampler's uniform draw, exported so host code can reproduce it. */
 double dpl_uniform(uint64_t seed, uint64_t counter);
 

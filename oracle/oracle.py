@@ -132,6 +132,8 @@ def ref_lib():
         lib.ref_normal_hazard.restype = C.c_double
         lib.ref_normal_hazard.argtypes = [C.c_double]
         lib.ref_model_save_checkpoint.argtypes = [vp, C.c_int32, C.c_char_p]
+        lib.ref_model_set_mlp_head.argtypes = [vp, _ip, C.c_int32, _dp, C.c_int64]
+        lib.ref_model_head_grads.argtypes = [vp, _dp]
         lib.ref_sample_grid.argtypes = [vp, _ip, _dp, _dp, C.c_int, _dp, _dp, _dp]
         lib.ref_sample_rays.argtypes = [vp, _dp, C.c_int64, C.c_double, C.c_double, _ip, C.c_int32,
                                         _dp, _dp, _ip, _up]
@@ -411,6 +413,19 @@ class RefModel:
         if getattr(self, "_h", None):
             self._lib.ref_model_free(self._h)
             self._h = None
+
+    def set_mlp_head(self, sizes, w):
+        """Tiny-MLP radiance head (radiance.cpp:40-180) with the given weights."""
+        sz = np.ascontiguousarray(sizes, dtype=np.int32)
+        self._w = _d(w).ravel()
+        _check_ref(self._lib.ref_model_set_mlp_head(self._h, _ptr(sz, _ip), len(sz),
+                                                    _ptr(self._w), len(self._w)))
+
+    def head_grads(self):
+        """d_head_w accumulated by the last render_step (RenderGrads::d_head_w)."""
+        out = np.zeros(len(self._w))
+        _check_ref(self._lib.ref_model_head_grads(self._h, _ptr(out)))
+        return out
 
     def save_checkpoint(self, path, iter=0):
         """The reference's own save_checkpoint (optimizer.cpp:330-356)."""

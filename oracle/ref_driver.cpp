@@ -98,6 +98,7 @@ struct ref_tree {
 
 struct ref_model {
   SceneModel model;
+  std::vector<double> d_head_w;  // head weight gradient of the last ref_render_step
 };
 
 extern "C" {
@@ -419,7 +420,30 @@ int ref_render_step(ref_model* mm, const double* rays, const double* ts, const d
     }
     *d_lambda = dl;
     for (int a = 0; a < 3; ++a) d_bg[a] = db[a];
+    mm->d_head_w.assign(model.head.mlp.w.size(), 0.0);
+    for (auto& g : rgs)
+      for (size_t k = 0; k < g.d_head_w.size() && k < mm->d_head_w.size(); ++k)
+        mm->d_head_w[k] += g.d_head_w[k];
   });
+}
+
+// tiny-MLP radiance head (radiance.hpp: RadianceHead, HeadVariant::TinyMlp)
+// with the caller's weights (layer-major rows x cols then bias, radiance.cpp:44-57)
+int ref_model_set_mlp_head(ref_model* mm, const int32_t* sizes, int32_t n_sizes, const double* w,
+                           int64_t n_w) {
+  return guard([&] {
+    RadianceHead& h = mm->model.head;
+    h.variant = HeadVariant::TinyMlp;
+    h.k_appearance = mm->model.cloud.k_appearance;
+    h.mlp.sizes.assign(sizes, sizes + n_sizes);
+    h.mlp.w.assign(w, w + n_w);
+    if (h.mlp.sizes.front() != h.mlp_input_dim() || h.mlp.sizes.back() != h.output_dim())
+      throw DataError("ref_model_set_mlp_head: layer sizes do not match the head");
+  });
+}
+
+int ref_model_head_grads(const ref_model* mm, double* out) {
+  return guard([&] { std::memcpy(out, mm->d_head_w.data(), mm->d_head_w.size() * sizeof(double)); });
 }
 
 // Adam::step (proj/src/optimizer.cpp:65-81) on a flat parameter group.

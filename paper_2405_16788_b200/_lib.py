@@ -115,6 +115,8 @@ _sig = {
     "dpl_checkpoint_read": (C.c_int, [C.c_char_p, C.POINTER(CheckpointMeta), C.POINTER(C.c_int64),
                                       C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                                       C.POINTER(C.c_int64), _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "dpl_tree_set_mlp_head": (C.c_int, [_vp, _vp, C.c_int32, _vp, C.c_int64]),
+    "dpl_head_grads": (C.c_int, [_vp, _vp, C.c_int64]),
     "dpl_gradbuf_create": (C.c_int, [_vp, C.POINTER(_vp)]),
     "dpl_gradbuf_destroy": (C.c_int, [_vp]),
     "dpl_gradbuf_zero": (C.c_int, [_vp]),

@@ -284,6 +284,23 @@ class DipoleTree:
         check(lib().dpl_primal(self._h, C.byref(params), float(beta_bh), xp, q, op, gp, None))
         return out, grad
 
+    # -- tiny-MLP radiance head (radiance.cpp:40-180) ---------------------------
+    def set_mlp_head(self, sizes, w):
+        """Render with the tiny-MLP head: sizes [22 + K, hidden..., 3], w the
+        reference's flat fp64 weights. sizes=() restores the direct-rgb head."""
+        sz = np.ascontiguousarray(sizes, dtype=np.int32)
+        wv = np.ascontiguousarray(w, dtype=np.float64).ravel()
+        self._head_nw = int(wv.size) if sz.size else 0
+        check(lib().dpl_tree_set_mlp_head(self._h, sz.ctypes.data if sz.size else None,
+                                          int(sz.size), wv.ctypes.data if wv.size else None,
+                                          int(wv.size)))
+
+    def head_grads(self):
+        """RenderGrads::d_head_w since the last call (fp64); resets the accumulator."""
+        out = np.zeros(self._head_nw)
+        check(lib().dpl_head_grads(self._h, out.ctypes.data, out.size))
+        return out
+
     # -- DPCK checkpoints (optimizer.cpp:294-388) --------------------------------
     def save_checkpoint(self, path, iter=0, lambda_scale=20.0, epsilon=0.0, background=(0, 0, 0),
                         beta_bh=2.0, initial_normals=None, head_variant=0, with_albedo=False,

@@ -17,6 +17,7 @@
 #include "adjoint.cuh"
 #include "forward.cuh"
 #include "knn.cuh"
+#include "mlp_head.cuh"
 #include "train.cuh"
 #include "render.cuh"
 #include "sampling.cuh"
@@ -42,6 +43,7 @@ struct dpl_tree_s {
   // calls are tracked with events instead of a synchronize per call
   bool host_async = false;
   IList il;  // interaction lists of the last batch (ilist.cuh)
+  MlpHead head;  // tiny-MLP radiance head (inactive: the direct-rgb head)
   // List policy. Building lists costs one extra pass (~5 ms per 4M queries),
   // repaid only when an adjoint follows a primal on the same batch. The
   // handle watches the call pattern: after a primal -> adjoint pair on the
@@ -88,7 +90,9 @@ struct dpl_tape_s {
   int S = 0;
   int C = 0;
   double t_near = 0;
-  DevBuf rays, ts, deltas, xs, perm, vals, g0, tape, dout, dgrad, sums, morton;
+  DevBuf rays, ts, deltas, xs, perm, vals, g0, tape, dout, dgrad, sums, morton, head_raw, d_raw,
+      mlp_x, mlp_dx;
+  int vstride = 4;  // values per sample in vals (4: direct-rgb head, C: tiny-MLP head)
   bool has_deltas = false;
 };
 
@@ -475,6 +479,30 @@ int dpl_checkpoint_read(const char* path, dpl_checkpoint_meta* meta, int64_t* n_
     *k_out = K;
     *ns_out = (int32_t)ns;
     *nw_out = (int64_t)nw;
+  });
+}
+
+int dpl_tree_set_mlp_head(dpl_tree_t h, const int32_t* sizes, int32_t n_sizes, const double* w,
+                          int64_t n_w) {
+  return guard([&] {
+    check_tree(h);
+    require(n_sizes >= 0 && n_w >= 0 && (n_sizes == 0 || (sizes && w)), DPL_ERR_USAGE,
+            "bad mlp head");
+    DPL_CUDA(cudaSetDevice(h->t.device));
+    std::vector<int> sz(sizes, sizes + n_sizes);
+    mlp_set(h->head, h->t, sz.data(), n_sizes, w, (size_t)n_w);
+  });
+}
+
+int dpl_head_grads(dpl_tree_t h, double* d_w, int64_t n_w) {
+  return guard([&] {
+    check_tree(h);
+    require(h->head.active, DPL_ERR_USAGE, "no tiny-MLP head set");
+    require(d_w && (size_t)n_w == h->head.n_w, DPL_ERR_USAGE, "d_w size mismatch");
+    Tree& t = h->t;
+    DPL_CUDA(cudaMemcpyAsync(d_w, h->head.dw64.p, (size_t)n_w * 8, cudaMemcpyDefault, t.stream));
+    DPL_CUDA(cudaMemsetAsync(h->head.dw64.p, 0, (size_t)n_w * 8, t.stream));
+    DPL_CUDA(cudaStreamSynchronize(t.stream));
   });
 }
 
@@ -1114,23 +1142,41 @@ int dpl_render_forward(dpl_tree_t h, const dpl_kernel_params* params, const dpl_
       PhaseTimer pt(t, PH_SORT);
       morton_order(t, tape->xs.as<double>(), Q, tape->perm.as<int32_t>(), tape->morton);
     }
-    tape->vals.reserve(Q * 16);
+    const bool mlp = h->head.active;
+    tape->vstride = mlp ? t.C : 4;
+    tape->vals.reserve(Q * 4 * tape->vstride);
     tape->g0.reserve(Q * 12);
     FwdArgs a;
     a.xs = tape->xs.as<double>();
     a.perm = tape->perm.as<int32_t>();
     a.q = Q;
     a.out = tape->vals.as<float>();
-    a.out_stride = 4;
+    a.out_stride = tape->vstride;
     a.grad = tape->g0.as<float>();
     a.grad_mode = 2;
     a.overflow = overflow_flag(h);
     // the direct-rgb head reads channels 0..3 only (radiance.cpp:133-145):
-    // radial slots 0..2 are channels 1..3 in SceneModel's layout
-    a.nr_limit = 3;
+    // radial slots 0..2 are channels 1..3 in SceneModel's layout; the tiny-MLP
+    // head reads every appearance channel
+    a.nr_limit = mlp ? -1 : 3;
     {
       PhaseTimer pt(t, PH_FORWARD);
       forward_launch(t, kp, a);
+    }
+    if (mlp) {  // head raw outputs, in sample chunks (RadianceHead::eval, radiance.cpp:146-154)
+      const int din = h->head.din();
+      const int64_t chunk = std::min<int64_t>(Q, 1 << 16);
+      tape->head_raw.reserve(Q * 12);
+      tape->mlp_x.reserve((size_t)chunk * din * 4);
+      PhaseTimer pt(t, PH_RENDER);
+      for (int64_t q0 = 0; q0 < Q; q0 += chunk) {
+        const int64_t qc = std::min(chunk, Q - q0);
+        mlp_inputs(t.stream, tape->rays.as<double>(), S, tape->xs.as<double>(),
+                   tape->vals.as<float>(), t.C, tape->g0.as<float>(), q0, qc, h->head.K,
+                   tape->mlp_x.as<float>());
+        mlp_forward(h->head, t.stream, tape->mlp_x.as<float>(), qc,
+                    tape->head_raw.as<float>() + 3 * q0);
+      }
     }
     Out<float> o;
     o.bind(t, rgb, R * 3, h->ws_out);
@@ -1138,8 +1184,9 @@ int dpl_render_forward(dpl_tree_t h, const dpl_kernel_params* params, const dpl_
     double bg[3] = {rp->background[0], rp->background[1], rp->background[2]};
     render_composite(t.stream, tape->rays.as<double>(), R, S, tape->ts.as<double>(),
                      tape->has_deltas ? tape->deltas.as<double>() : nullptr, rp->t_near,
-                     tape->vals.as<float>(), tape->g0.as<float>(), rp->lambda_scale, bg,
-                     tape->tape.as<double>(), o.dev);
+                     tape->vals.as<float>(), tape->vstride,
+                     mlp ? tape->head_raw.as<float>() : nullptr, tape->g0.as<float>(),
+                     rp->lambda_scale, bg, tape->tape.as<double>(), o.dev);
     o.finish(t);
     DPL_CUDA(cudaGetLastError());
     if (o.host) DPL_CUDA(cudaStreamSynchronize(t.stream));
@@ -1165,23 +1212,47 @@ int dpl_render_backward(dpl_tree_t h, const dpl_kernel_params* params, const dpl
     tree_ensure_thresholds(t, rp->beta_bh);
     DevBuf drgb_tmp;
     const float* drgb_d = stage_in(t, d_rgb, (size_t)R * 3, drgb_tmp);
-    tape->dout.reserve(Q * 16);
+    const bool mlp = tape->vstride != 4 || h->head.active;
+    require(!mlp || (h->head.active && tape->vstride == t.C), DPL_ERR_USAGE,
+            "render_backward: the radiance head changed since render_forward");
+    const int ds = tape->vstride;
+    tape->dout.reserve(Q * 4 * ds);
     tape->dgrad.reserve(Q * 12);
     tape->sums.reserve(32);
     DPL_CUDA(cudaMemsetAsync(tape->sums.p, 0, 32, t.stream));
     double bg[3] = {rp->background[0], rp->background[1], rp->background[2]};
+    if (mlp) tape->d_raw.reserve(Q * 12);
     render_backward_rays(t.stream, tape->rays.as<double>(), R, S, tape->tape.as<double>(), drgb_d,
-                         rp->lambda_scale, bg, tape->dout.as<float>(), tape->dgrad.as<float>(),
+                         rp->lambda_scale, bg, tape->dout.as<float>(), ds,
+                         mlp ? tape->d_raw.as<float>() : nullptr, tape->dgrad.as<float>(),
                          tape->sums.as<double>());
+    if (mlp) {  // head backward (radiance.cpp:176-179) -> appearance / normal adjoints
+      const int din = h->head.din();
+      const int64_t chunk = std::min<int64_t>(Q, 1 << 16);
+      tape->mlp_x.reserve((size_t)chunk * din * 4);
+      tape->mlp_dx.reserve((size_t)chunk * din * 4);
+      PhaseTimer pt(t, PH_RENDER);
+      for (int64_t q0 = 0; q0 < Q; q0 += chunk) {
+        const int64_t qc = std::min(chunk, Q - q0);
+        mlp_inputs(t.stream, tape->rays.as<double>(), S, tape->xs.as<double>(),
+                   tape->vals.as<float>(), t.C, tape->g0.as<float>(), q0, qc, h->head.K,
+                   tape->mlp_x.as<float>());
+        mlp_backward(h->head, t.stream, tape->mlp_x.as<float>(), qc,
+                     tape->d_raw.as<float>() + 3 * q0, tape->mlp_dx.as<float>());
+        render_mlp_scatter(t.stream, tape->mlp_dx.as<float>(), din, q0, qc, h->head.K,
+                           tape->g0.as<float>(), tape->dout.as<float>(), t.C,
+                           tape->dgrad.as<float>());
+      }
+    }
     AdjArgs a;
     a.xs = tape->xs.as<double>();
     a.perm = tape->perm.as<int32_t>();
     a.q = Q;
     a.d_out = tape->dout.as<float>();
-    a.dstride = 4;
+    a.dstride = ds;
     a.d_grad = tape->dgrad.as<float>();
     a.grad_mode = 2;
-    a.nr_limit = 3;
+    a.nr_limit = mlp ? -1 : 3;
     a.overflow = overflow_flag(h);
     {
       PhaseTimer pt(t, PH_ADJOINT);

@@ -1,0 +1,258 @@
+// mlp_head.cu — tiny-MLP radiance head for the batched render step (see
+// mlp_head.cuh). Reference: Mlp::forward / Mlp::backward and
+// RadianceHead::eval / backward (radiance.cpp:59-180).
+#include <algorithm>
+#include <cstdlib>
+
+#include <dlfcn.h>
+
+#include "mlp_head.cuh"
+
+#include "../../include/dipole_b200.h"
+
+namespace dpl {
+
+namespace {
+
+#define BLAS(x)                                                                       \
+  do {                                                                                \
+    cublasStatus_t st_ = (x);                                                         \
+    if (st_ != CUBLAS_STATUS_SUCCESS) throw Error(DPL_ERR_CUDA, "cuBLAS call failed"); \
+  } while (0)
+
+inline unsigned blocks_for(int64_t n, int b) {
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + b - 1) / b, 148 * 32));
+}
+
+// real spherical harmonics up to degree 3 (sh_encode, radiance.cpp:7-28)
+__device__ __forceinline__ void sh_encode(double x, double y, double z, float* o) {
+  const double x2 = x * x, y2 = y * y, z2 = z * z;
+  o[0] = 0.28209479177387814f;
+  o[1] = (float)(0.4886025119029199 * y);
+  o[2] = (float)(0.4886025119029199 * z);
+  o[3] = (float)(0.4886025119029199 * x);
+  o[4] = (float)(1.0925484305920792 * x * y);
+  o[5] = (float)(1.0925484305920792 * y * z);
+  o[6] = (float)(0.31539156525252005 * (3.0 * z2 - 1.0));
+  o[7] = (float)(1.0925484305920792 * x * z);
+  o[8] = (float)(0.5462742152960396 * (x2 - y2));
+  o[9] = (float)(0.5900435899266435 * y * (3.0 * x2 - y2));
+  o[10] = (float)(2.890611442640554 * x * y * z);
+  o[11] = (float)(0.4570457994644658 * y * (5.0 * z2 - 1.0));
+  o[12] = (float)(0.3731763325901154 * z * (5.0 * z2 - 3.0));
+  o[13] = (float)(0.4570457994644658 * x * (5.0 * z2 - 1.0));
+  o[14] = (float)(1.445305721320277 * z * (x2 - y2));
+  o[15] = (float)(0.5900435899266435 * x * (x2 - 3.0 * y2));
+}
+
+// head input rows (RadianceHead::eval, radiance.cpp:146-152; n_hat and omega_head
+// as render_ray builds them, renderer.cpp:111,128-130)
+__global__ void k_inputs(const double* __restrict__ rays, int S, const double* __restrict__ xs,
+                         const float* __restrict__ vals, int C, const float* __restrict__ g0,
+                         int64_t q0, int64_t q, int K, float* __restrict__ X) {
+  const int din = 22 + K;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < q;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t g = q0 + i;
+    const double* dir = rays + 6 * (g / S) + 3;
+    const double ox = -dir[0], oy = -dir[1], oz = -dir[2];
+    float* row = X + i * din;
+    row[0] = (float)xs[3 * g], row[1] = (float)xs[3 * g + 1], row[2] = (float)xs[3 * g + 2];
+    sh_encode(ox, oy, oz, row + 3);
+    const double gx = -(double)g0[3 * g], gy = -(double)g0[3 * g + 1], gz = -(double)g0[3 * g + 2];
+    const double gn = sqrt((gx * gx + gy * gy) + gz * gz);
+    if (gn > 1e-12) {
+      row[19] = (float)(gx / gn), row[20] = (float)(gy / gn), row[21] = (float)(gz / gn);
+    } else {
+      row[19] = (float)ox, row[20] = (float)oy, row[21] = (float)oz;
+    }
+    for (int k = 0; k < K; ++k) row[22 + k] = vals[g * C + 1 + k];
+  }
+}
+
+// y = y + bias (+ ReLU unless last), row-major q x rows
+__global__ void k_bias_act(float* __restrict__ y, const float* __restrict__ b, int64_t q, int rows,
+                           int relu) {
+  const int64_t n = q * rows;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float v = y[i] + b[i % rows];
+    y[i] = relu ? fmaxf(v, 0.f) : v;
+  }
+}
+
+// ReLU gate of the backward pass: delta = 0 where the layer output <= 0 (:105-107)
+__global__ void k_gate(float* __restrict__ d, const float* __restrict__ out, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    if (out[i] <= 0.f) d[i] = 0.f;
+}
+
+// bias gradient: column sums of delta (q x rows) into db
+__global__ void k_colsum(const float* __restrict__ d, int64_t q, int rows, float* __restrict__ db) {
+  const int c = blockIdx.x;
+  float s = 0.f;
+  for (int64_t i = threadIdx.x; i < q; i += blockDim.x) s += d[i * rows + c];
+  __shared__ float red[256];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) db[c] = red[0];
+}
+
+__global__ void k_acc64(double* __restrict__ dst, const float* __restrict__ src, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] += (double)src[i];
+}
+
+__global__ void k_to_f32(const double* __restrict__ a, int64_t n, float* __restrict__ b) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    b[i] = (float)a[i];
+}
+
+}  // namespace
+
+MlpHead::~MlpHead() {
+  if (blas) cublasDestroy(blas);
+}
+
+int MlpHead::widest() const {
+  int w = 0;
+  for (int s : sizes) w = std::max(w, s);
+  return w;
+}
+
+void mlp_set(MlpHead& m, const Tree& t, const int* sizes, int n_sizes, const double* w,
+             size_t n_w) {
+  if (n_sizes == 0) {
+    m.active = false;
+    m.sizes.clear();
+    return;
+  }
+  m.K = t.C - 1;
+  m.sizes.assign(sizes, sizes + n_sizes);
+  if (n_sizes < 2 || m.sizes.front() != 22 + m.K || m.sizes.back() != 3)
+    throw Error(DPL_ERR_DATA, "mlp head: sizes must run from 22 + K inputs to 3 outputs");
+  m.offs.clear();
+  size_t n = 0;
+  for (int l = 0; l + 1 < n_sizes; ++l) {
+    m.offs.push_back(n);
+    n += (size_t)m.sizes[l + 1] * m.sizes[l] + m.sizes[l + 1];
+  }
+  if (n != n_w) throw Error(DPL_ERR_DATA, "mlp head: weight count does not match the sizes");
+  m.n_w = n;
+  if (!m.blas) {
+    BLAS(cublasCreate(&m.blas));
+    // fp32 GEMMs on the tensor cores through cuBLAS's BF16x9 fp32 emulation
+    // (fp32-accurate, Blackwell, cuBLAS >= 12.9) when the process's cuBLAS has
+    // it — a host that loaded an older libcublas.so.12 first (e.g. a framework's
+    // bundled copy) keeps the plain FFMA SGEMM; DPL_MLP_SGEMM=1 forces SGEMM
+    using set_emu_t = cublasStatus_t (*)(cublasHandle_t, cublasEmulationStrategy_t);
+    static const auto set_emu = (set_emu_t)dlsym(RTLD_DEFAULT, "cublasSetEmulationStrategy");
+    static const bool plain = getenv("DPL_MLP_SGEMM") != nullptr || set_emu == nullptr;
+    m.emulated = !plain;
+    if (plain) {
+      BLAS(cublasSetMathMode(m.blas, CUBLAS_DEFAULT_MATH));
+    } else {
+      BLAS(cublasSetMathMode(m.blas, CUBLAS_FP32_EMULATED_BF16X9_MATH));
+      BLAS(set_emu(m.blas, CUBLAS_EMULATION_STRATEGY_EAGER));
+    }
+  }
+  // fp32 weights: the host fp64 array goes up once, converted on the device
+  DevBuf w64;
+  w64.reserve(n * 8);
+  DPL_CUDA(cudaMemcpyAsync(w64.p, w, n * 8, cudaMemcpyHostToDevice, t.stream));
+  m.w32.reserve(n * 4);
+  k_to_f32<<<blocks_for(n, 256), 256, 0, t.stream>>>(w64.as<double>(), n, m.w32.as<float>());
+  count_launch();
+  m.dw64.reserve(n * 8);
+  DPL_CUDA(cudaMemsetAsync(m.dw64.p, 0, n * 8, t.stream));
+  m.dw32.reserve(n * 4);
+  DPL_CUDA(cudaStreamSynchronize(t.stream));
+  m.active = true;
+}
+
+void mlp_inputs(cudaStream_t s, const double* rays, int S, const double* xs, const float* vals,
+                int C, const float* g0, int64_t q0, int64_t q, int K, float* X) {
+  k_inputs<<<blocks_for(q, 256), 256, 0, s>>>(rays, S, xs, vals, C, g0, q0, q, K, X);
+  count_launch();
+}
+
+// layer l: out (q x rows) = in (q x cols) . W^T + b  (cuBLAS column-major view)
+static void layer_fwd(MlpHead& m, cudaStream_t s, int l, const float* in, int64_t q, float* out) {
+  const int rows = m.sizes[l + 1], cols = m.sizes[l];
+  const float one = 1.f, zero = 0.f;
+  const float* W = m.w32.as<float>() + m.offs[l];
+  BLAS(cublasSetStream(m.blas, s));
+  BLAS(cublasSgemm(m.blas, CUBLAS_OP_T, CUBLAS_OP_N, rows, (int)q, cols, &one, W, cols, in, cols,
+                   &zero, out, rows));
+  const bool last = l + 2 == (int)m.sizes.size();
+  k_bias_act<<<blocks_for(q * rows, 256), 256, 0, s>>>(out, W + (size_t)rows * cols, q, rows,
+                                                       last ? 0 : 1);
+  count_launch();
+}
+
+void mlp_forward(MlpHead& m, cudaStream_t s, const float* X, int64_t q, float* raw) {
+  const int L = (int)m.sizes.size() - 1;
+  const size_t wide = (size_t)m.widest();
+  m.ws.reserve(2 * (size_t)q * wide * 4);
+  float* buf[2] = {m.ws.as<float>(), m.ws.as<float>() + (size_t)q * wide};
+  const float* in = X;
+  for (int l = 0; l < L; ++l) {
+    float* out = l + 1 == L ? raw : buf[l & 1];
+    layer_fwd(m, s, l, in, q, out);
+    in = out;
+  }
+}
+
+void mlp_backward(MlpHead& m, cudaStream_t s, const float* X, int64_t q, const float* d_raw,
+                  float* dX) {
+  const int L = (int)m.sizes.size() - 1;
+  // recompute the chunk's activations (Mlp::Tape), then walk back (:95-119)
+  size_t acts = 0;
+  for (int l = 1; l <= L; ++l) acts += (size_t)m.sizes[l];
+  const size_t wide = (size_t)m.widest();
+  m.ws.reserve(((size_t)q * acts + 2 * (size_t)q * wide) * 4);
+  std::vector<float*> act(L + 1);
+  act[0] = const_cast<float*>(X);
+  float* p = m.ws.as<float>();
+  for (int l = 1; l <= L; ++l) {
+    act[l] = p;
+    p += (size_t)q * m.sizes[l];
+  }
+  float* dbuf[2] = {p, p + (size_t)q * wide};
+  for (int l = 0; l < L; ++l) layer_fwd(m, s, l, act[l], q, act[l + 1]);
+  const float one = 1.f, zero = 0.f;
+  const float* delta = d_raw;
+  for (int l = L - 1; l >= 0; --l) {
+    const int rows = m.sizes[l + 1], cols = m.sizes[l];
+    float* dl = const_cast<float*>(delta);
+    if (l + 1 < L) {  // ReLU gate with this layer's output
+      k_gate<<<blocks_for(q * rows, 256), 256, 0, s>>>(dl, act[l + 1], q * rows);
+      count_launch();
+    }
+    const float* W = m.w32.as<float>() + m.offs[l];
+    float* dW = m.dw32.as<float>() + m.offs[l];
+    // dW (rows x cols) = delta^T . in ; db = column sums of delta
+    BLAS(cublasSgemm(m.blas, CUBLAS_OP_N, CUBLAS_OP_T, cols, rows, (int)q, &one, act[l], cols,
+                     delta, rows, &zero, dW, cols));
+    k_colsum<<<rows, 256, 0, s>>>(delta, q, rows, dW + (size_t)rows * cols);
+    count_launch();
+    // d_in (q x cols) = delta . W
+    float* din = l == 0 ? dX : dbuf[l & 1];
+    BLAS(cublasSgemm(m.blas, CUBLAS_OP_N, CUBLAS_OP_N, cols, (int)q, rows, &one, W, cols, delta,
+                     rows, &zero, din, cols));
+    delta = din;
+  }
+  // fold the chunk's fp32 gradient into the fp64 accumulator (RenderGrads::d_head_w)
+  k_acc64<<<blocks_for(m.n_w, 256), 256, 0, s>>>(m.dw64.as<double>(), m.dw32.as<float>(),
+                                                 (int64_t)m.n_w);
+  count_launch();
+}
+
+}  // namespace dpl

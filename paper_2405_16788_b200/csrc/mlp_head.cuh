@@ -1,0 +1,56 @@
+// mlp_head.cuh — the tiny-MLP radiance head (radiance.hpp /
+// radiance.cpp:40-180) for the batched render step.
+//
+// Input per sample (RadianceHead::eval, radiance.cpp:146-154): x (3),
+// sh_encode(omega_head) (16), implicit normal (3), appearance channels (K).
+// Dense ReLU layers, linear last layer, rgb = logistic(raw). Weights keep the
+// reference's flat layout (per layer: rows x cols matrix, then the bias).
+// The layers are fp32 cuBLAS GEMMs (plain library GEMMs) with our own
+// bias / ReLU / gather kernels; the weight gradient accumulates in fp64 over
+// sample chunks like RenderGrads::d_head_w.
+#pragma once
+
+#include <cublas_v2.h>
+
+#include <vector>
+
+#include "tree.cuh"
+
+namespace dpl {
+
+constexpr int kShDim = 16;
+
+struct MlpHead {
+  bool active = false;
+  bool emulated = false;     // GEMMs through cuBLAS's BF16x9 fp32 emulation
+  int K = 0;                 // appearance channels (= tree C - 1)
+  std::vector<int> sizes;    // sizes[0] = 22 + K, back() = 3
+  std::vector<size_t> offs;  // layer offsets into the flat weights
+  size_t n_w = 0;
+  DevBuf w32;   // fp32 weights, reference layout
+  DevBuf dw64;  // fp64 weight gradient accumulator
+  DevBuf dw32;  // one chunk's fp32 weight gradient
+  DevBuf ws;    // activations / deltas of one chunk
+  cublasHandle_t blas = nullptr;
+  ~MlpHead();
+  int din() const { return sizes.empty() ? 0 : sizes.front(); }
+  int widest() const;
+};
+
+// set (or, with n_sizes == 0, clear) the head; w: host fp64, reference layout
+void mlp_set(MlpHead& m, const Tree& t, const int* sizes, int n_sizes, const double* w, size_t n_w);
+
+// X rows (fp32, q x din) from the render tape: x (fp64 positions), omega_head =
+// -dir, n_hat from the channel-0 gradient (renderer.cpp:124-130), appearance
+// = channels 1..K of vals (q x C)
+void mlp_inputs(cudaStream_t s, const double* rays, int S, const double* xs, const float* vals,
+                int C, const float* g0, int64_t q0, int64_t q, int K, float* X);
+
+// raw outputs (q x 3, fp32) of the samples [q0, q0 + q)
+void mlp_forward(MlpHead& m, cudaStream_t s, const float* X, int64_t q, float* raw);
+
+// backward of a chunk: d_raw (q x 3) -> d_X (q x din); accumulates dW (fp64)
+void mlp_backward(MlpHead& m, cudaStream_t s, const float* X, int64_t q, const float* d_raw,
+                  float* dX);
+
+}  // namespace dpl

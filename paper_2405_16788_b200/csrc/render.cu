@@ -12,6 +12,8 @@
 //            d_out_0 = -d_f, d_grad_0 = -d grad f, d_out_{1..3} = p d_rgb r(1-r),
 //            which feed K7 (the tree adjoint) for all samples at once.
 // The per-ray scans are sequential in fp64 (tiny next to the traversals).
+#include <algorithm>
+
 #include "render.cuh"
 
 namespace dpl {
@@ -70,7 +72,8 @@ __device__ __forceinline__ double logistic_d(double x) {  // radiance.cpp:30-38
 __global__ void k_composite(const double* __restrict__ rays, int64_t R, int S,
                             const double* __restrict__ ts, const double* __restrict__ deltas,
                             double t_near,
-                            const float* __restrict__ vals /* RS x 4 */,
+                            const float* __restrict__ vals /* RS x vstride */, int vstride,
+                            const float* __restrict__ head_raw /* RS x 3 or null */,
                             const float* __restrict__ g0 /* RS x 3 */, double lambda, double bg0,
                             double bg1, double bg2, double* tape /* RS x 8 */, float* rgb_out) {
   int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -82,12 +85,14 @@ __global__ void k_composite(const double* __restrict__ rays, int64_t R, int S,
     double t = ts[g];
     double delta = deltas ? deltas[g] : t - prev;  // delta_0 = t_0 - t_near (renderer.hpp:324)
     prev = t;
-    double f = 0.5 - (double)vals[4 * g];
+    double f = 0.5 - (double)vals[(int64_t)vstride * g];
     double gx = -(double)g0[3 * g], gy = -(double)g0[3 * g + 1], gz = -(double)g0[3 * g + 2];
     double s = (dir[0] * gx + dir[1] * gy) + dir[2] * gz;
     double sigma = lambda * hazard(lambda * f) * fabs(s);
-    double h0 = logistic_d(vals[4 * g + 1]), h1 = logistic_d(vals[4 * g + 2]),
-           h2 = logistic_d(vals[4 * g + 3]);
+    // head rgb: logistic of the direct-rgb channels 1..3 (radiance.cpp:133-145)
+    // or of the tiny-MLP's raw outputs (:153-154)
+    const float* hr = head_raw ? head_raw + 3 * g : vals + (int64_t)vstride * g + 1;
+    double h0 = logistic_d(hr[0]), h1 = logistic_d(hr[1]), h2 = logistic_d(hr[2]);
     double E = exp(-sigma * delta);
     double p = trans * (1.0 - E);
     c0 += p * h0, c1 += p * h1, c2 += p * h2;
@@ -105,7 +110,9 @@ __global__ void k_composite(const double* __restrict__ rays, int64_t R, int S,
 __global__ void k_backward_ray(const double* __restrict__ rays, int64_t R, int S,
                                const double* __restrict__ tape, const float* __restrict__ d_rgb,
                                double lambda, double bg0, double bg1, double bg2,
-                               float* d_out /* RS x 4 */, float* d_grad0 /* RS x 3 */,
+                               float* d_out /* RS x dstride */, int dstride,
+                               float* d_raw /* RS x 3: head raw-output adjoint, or null */,
+                               float* d_grad0 /* RS x 3 */,
                                double* sums /* d_lambda, d_bg0..2 */) {
   int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   double dl = 0, db0 = 0, db1 = 0, db2 = 0;
@@ -134,14 +141,16 @@ __global__ void k_backward_ray(const double* __restrict__ rays, int64_t R, int S
       double d_f = dsig * lambda * lambda * abs_s * dhaz;
       dl += dsig * (haz * abs_s + lambda * abs_s * dhaz * f);
       double k = dsig * lambda * haz * sgn_s;
-      d_out[4 * g] = (float)(-d_f);
+      d_out[(int64_t)dstride * g] = (float)(-d_f);
       d_grad0[3 * g] = (float)(-k * dir[0]);
       d_grad0[3 * g + 1] = (float)(-k * dir[1]);
       d_grad0[3 * g + 2] = (float)(-k * dir[2]);
-      // direct-rgb head backward (radiance.cpp:166,170-171)
-      d_out[4 * g + 1] = (float)(p * dr0 * tp[4] * (1.0 - tp[4]));
-      d_out[4 * g + 2] = (float)(p * dr1 * tp[5] * (1.0 - tp[5]));
-      d_out[4 * g + 3] = (float)(p * dr2 * tp[6] * (1.0 - tp[6]));
+      // head backward d_raw = d_radiance * rgb (1 - rgb) (radiance.cpp:166): the
+      // direct-rgb head's channel adjoints, or the tiny-MLP's output adjoint
+      float* dr = d_raw ? d_raw + 3 * g : d_out + (int64_t)dstride * g + 1;
+      dr[0] = (float)(p * dr0 * tp[4] * (1.0 - tp[4]));
+      dr[1] = (float)(p * dr1 * tp[5] * (1.0 - tp[5]));
+      dr[2] = (float)(p * dr2 * tp[6] * (1.0 - tp[6]));
     }
   }
   // warp-reduce the ray sums, one fp64 atomic per warp and quantity
@@ -159,6 +168,36 @@ __global__ void k_backward_ray(const double* __restrict__ rays, int64_t R, int S
   }
 }
 
+// d_grad_f += (d_normal - n (n . d_normal)) / |grad f| (renderer.cpp:206-211);
+// d_grad[0] = -d_grad_f, d_out[1 + k] = d_appearance[k] (:226-229)
+__global__ void k_mlp_scatter(const float* __restrict__ dX, int din, int64_t q0, int64_t q, int K,
+                              const float* __restrict__ g0, float* __restrict__ d_out, int C,
+                              float* __restrict__ d_grad0) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < q;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t g = q0 + i;
+    const float* r = dX + i * din;
+    for (int k = 0; k < K; ++k) d_out[g * C + 1 + k] = r[22 + k];
+    const double gx = -(double)g0[3 * g], gy = -(double)g0[3 * g + 1], gz = -(double)g0[3 * g + 2];
+    const double gn = sqrt((gx * gx + gy * gy) + gz * gz);
+    if (gn > 1e-12) {
+      const double nx = gx / gn, ny = gy / gn, nz = gz / gn;
+      const double dnx = r[19], dny = r[20], dnz = r[21];
+      const double dot = (nx * dnx + ny * dny) + nz * dnz;
+      d_grad0[3 * g] -= (float)((dnx - nx * dot) / gn);
+      d_grad0[3 * g + 1] -= (float)((dny - ny * dot) / gn);
+      d_grad0[3 * g + 2] -= (float)((dnz - nz * dot) / gn);
+    }
+  }
+}
+
+void render_mlp_scatter(cudaStream_t s, const float* dX, int din, int64_t q0, int64_t q, int K,
+                        const float* g0, float* d_out, int C, float* d_grad0) {
+  const unsigned b = (unsigned)std::max<int64_t>(1, std::min<int64_t>((q + 255) / 256, 148 * 32));
+  k_mlp_scatter<<<b, 256, 0, s>>>(dX, din, q0, q, K, g0, d_out, C, d_grad0);
+  count_launch();
+}
+
 void render_samples(cudaStream_t s, const double* rays, int64_t R, int S, const double* ts_in,
                     double t_near, double t_far, uint64_t seed, double* ts_out, double* xs) {
   int64_t tot = R * S;
@@ -168,18 +207,21 @@ void render_samples(cudaStream_t s, const double* rays, int64_t R, int S, const 
 }
 
 void render_composite(cudaStream_t s, const double* rays, int64_t R, int S, const double* ts,
-                      const double* deltas, double t_near, const float* vals, const float* g0, double lambda,
-                      const double* bg, double* tape, float* rgb) {
-  k_composite<<<(unsigned)((R + 127) / 128), 128, 0, s>>>(rays, R, S, ts, deltas, t_near, vals, g0, lambda,
-                                                         bg[0], bg[1], bg[2], tape, rgb);
+                      const double* deltas, double t_near, const float* vals, int vstride,
+                      const float* head_raw, const float* g0, double lambda, const double* bg,
+                      double* tape, float* rgb) {
+  k_composite<<<(unsigned)((R + 127) / 128), 128, 0, s>>>(rays, R, S, ts, deltas, t_near, vals,
+                                                         vstride, head_raw, g0, lambda, bg[0],
+                                                         bg[1], bg[2], tape, rgb);
   count_launch();
 }
 
 void render_backward_rays(cudaStream_t s, const double* rays, int64_t R, int S,
                           const double* tape, const float* d_rgb, double lambda, const double* bg,
-                          float* d_out, float* d_grad0, double* sums) {
+                          float* d_out, int dstride, float* d_raw, float* d_grad0, double* sums) {
   k_backward_ray<<<(unsigned)((R + 127) / 128), 128, 0, s>>>(rays, R, S, tape, d_rgb, lambda, bg[0],
-                                                            bg[1], bg[2], d_out, d_grad0, sums);
+                                                            bg[1], bg[2], d_out, dstride, d_raw,
+                                                            d_grad0, sums);
   count_launch();
 }
 

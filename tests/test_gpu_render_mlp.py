@@ -1,0 +1,69 @@
+"""Render step with the tiny-MLP radiance head (radiance.cpp:40-180,
+renderer.cpp:106-231) against the reference's own implementation (oracle/_ref,
+HeadVariant::TinyMlp): colours, point gradients, d_epsilon, d_lambda,
+d_background and the head-weight gradient RenderGrads::d_head_w."""
+import numpy as np
+import pytest
+
+from test_gpu_parity import close, make, rel_scale_err
+
+pytestmark = pytest.mark.gpu
+
+
+def he_weights(sizes, seed):
+    """Mlp::init's He initialisation (radiance.cpp:44-57) with numpy draws."""
+    rng = np.random.default_rng(seed)
+    w = []
+    for cols, rows in zip(sizes[:-1], sizes[1:]):
+        w.append(np.sqrt(2.0 / cols) * rng.standard_normal(rows * cols))
+        w.append(0.05 * rng.standard_normal(rows))  # non-zero biases exercise db
+    return np.concatenate(w)
+
+
+@pytest.mark.parametrize("hidden", [(32,), (64, 64)])
+def test_render_step_tiny_mlp_head(oracle_mod, hidden):
+    import paper_2405_16788_b200 as eng
+    from paper_2405_16788_b200 import renderer as Rn
+    from paper_2405_16788_b200 import workloads as W
+
+    O = oracle_mod
+    if not O.have_ref():
+        pytest.skip("oracle/_ref not built")
+    w = W.config3(scale=0.02)
+    c = w["cloud"]
+    t, _ = make(eng, O, c.positions, c.normals, c.areas, c.moments, w["kinds"])
+    eps = 1.5 * O.mean_knn_spacing(c.positions)
+    K = c.channels - 1
+    sizes = [22 + K, *hidden, 3]
+    wts = he_weights(sizes, 5)
+    t.set_mlp_head(sizes, wts)
+    ref = O.RefModel(O.Cloud(c.positions, c.normals, c.areas, c.moments), eps, lam=20.0, beta=2.0)
+    ref.set_mlp_head(sizes, wts)
+
+    rays = w["rays"][:192]
+    S = 32
+    target = w["target"][:192]
+    rs = Rn.RenderSettings(t_near=2.0, t_far=6.0, seed=3)
+    p = eng.KernelParams(epsilon=eps)
+    rgb, tape = Rn.render_forward(t, p, rs, rays, S)
+    scale = 2.0 / (3.0 * rays.shape[0])
+    d_rgb = (scale * (rgb.astype(np.float64) - target)).astype(np.float32)
+    buf = t.make_buffer()
+    dl, dbg = Rn.render_backward(t, p, rs, tape, d_rgb, buf)
+    g = t.flush_gradients(buf)
+    dw = t.head_grads()
+
+    ts, dlt = O.stratified_samples(rays.shape[0], S, 2.0, 6.0, 3)
+    want = ref.render_step(rays, ts, dlt, target, scale)
+    assert close(rgb, want["rgb"])[0] == 0
+    assert rel_scale_err(g.moments, want["moments"]) < 1e-4
+    assert rel_scale_err(g.normals, want["normals"]) < 1e-4
+    assert abs(g.d_epsilon - want["d_eps"]) <= 1e-4 * abs(want["d_eps"]) + 1e-6
+    assert abs(dl - want["d_lambda"]) <= 1e-4 * abs(want["d_lambda"]) + 1e-8
+    assert np.abs(dbg - want["d_bg"]).max() <= 1e-4 * np.abs(want["d_bg"]).max() + 1e-8
+    assert rel_scale_err(dw, ref.head_grads()) < 1e-4
+    # the accumulator was reset; the direct-rgb head is restored by an empty size list
+    assert np.all(t.head_grads() == 0)
+    t.set_mlp_head((), ())
+    rgb2, _ = Rn.render_forward(t, p, rs, rays, S)
+    assert not np.allclose(rgb2, rgb)

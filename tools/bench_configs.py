@@ -148,6 +148,57 @@ def main():
                 dt = time.perf_counter() - t0
                 res["reference_cpu"] = {"resolution": 64, "s": dt, "nodes_per_s": 64 ** 3 / dt,
                                         "cores": O.ref_lib().ref_hardware_concurrency()}
+    elif args.config == 8:
+        # config-3 render step with the tiny-MLP head (4 x 256 hidden,
+        # the paper preset's depth and width) instead of the direct-rgb head
+        w = W.config3(scale=args.scale)
+        c, rays, S = w["cloud"], w["rays"], w["S"]
+        t0 = time.perf_counter()
+        eps = B.default_epsilon(c)
+        res["eps"], res["knn_s"] = eps, time.perf_counter() - t0
+        tree, res["build_s"] = build(c, w["kinds"], dev)
+        K = c.channels - 1
+        sizes = [22 + K, 256, 256, 256, 256, 3]
+        rng = np.random.default_rng(5)
+        wts = np.concatenate([np.concatenate([np.sqrt(2.0 / a) * rng.standard_normal(a * b),
+                                              np.zeros(b)]) for a, b in zip(sizes[:-1], sizes[1:])])
+        tree.set_mlp_head(sizes, wts)
+        R = rays.shape[0]
+        rays_d = torch.from_numpy(rays).to(dev)
+        target = torch.rand((R, 3), device=dev, generator=torch.Generator(device=dev).manual_seed(4))
+        p = P.KernelParams(epsilon=eps)
+        rs = Rn.RenderSettings(t_near=2.0, t_far=6.0, seed=3)
+        buf = tree.make_buffer()
+        mom = torch.empty((c.size, c.channels), device=dev)
+        nrm = torch.empty((c.size, 3), device=dev)
+        tape = Rn.Tape()
+        scale = 2.0 / (3.0 * R)
+
+        def step():
+            rgb, _ = Rn.render_forward(tree, p, rs, rays_d, S, tape=tape)
+            d_rgb = (scale * (rgb - target)).float()
+            Rn.render_backward(tree, p, rs, tape, d_rgb, buf)
+            tree.flush_gradients(buf, out=(mom, nrm))
+
+        ms, ph = timed(step, args.steps, tree)
+        tree.head_grads()
+        Q = R * S
+        flops = 2 * Q * sum(a * b for a, b in zip(sizes[:-1], sizes[1:])) * 4  # fwd, fwd again, 2x bwd
+        res.update(points=c.size, rays=R, samples=S, queries=Q, mlp=sizes, step_ms=ms, phases=ph,
+                   samples_per_s=Q / (ms * 1e-3), mlp_tflops=flops / (ph.get("render", ms) * 1e-3) / 1e12)
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import oracle as O
+
+        if O.have_ref():  # the reference's own render step with the same head, bounded sample
+            ref = O.RefModel(O.Cloud(c.positions, c.normals, c.areas, c.moments), eps, beta=2.0)
+            ref.set_mlp_head(sizes, wts)
+            nr = 256
+            ts, dlt = O.stratified_samples(nr, S, 2.0, 6.0, 3)
+            t0 = time.perf_counter()
+            ref.render_step(rays[:nr], ts, dlt, np.full((nr, 3), 0.5), scale)
+            dt = time.perf_counter() - t0
+            res["reference_cpu"] = {"rays": nr, "s": dt, "samples_per_s": nr * S / dt,
+                                    "cores": O.ref_lib().ref_hardware_concurrency()}
     elif args.config in (3, 5):
         if args.config == 3:
             w = W.config3(scale=args.scale)
