@@ -457,19 +457,39 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
           }
         }
       }
-    } else if (far) {
-      const Co c = adj_coeffs<GM>(s, kp);
-      nr_ = c.near;
-      r_ = A * c.R;
-      e_ = A * c.dR_de;
-      const float aWds = A * c.W * ds0;
-      u0 = aWds * fx, u1 = aWds * fy, u2 = aWds * fz;
-      if (c.near || GM) {
-        const float4 v = __ldg(tv.node_row + (size_t)node * F4g);
-        const float vd = fmaf(v.x, fx, fmaf(v.y, fy, v.z * fz));
-        float e = ds0 * A * c.dW_de * vd;  // :370
-        if (GM) {                          // :372-374
-          const float gd = fmaf(dg0, fx, fmaf(dg1, fy, dg2 * fz));
+    } else {
+      // d_grad present (render path). Far lanes beyond 6.5 eps: tau = 1, so
+      // W = R / r, Wp_r = -3 W R and every epsilon term vanishes (the moment row
+      // is not even read); the series and the epsilon terms run under a
+      // warp-uniform branch for the near lanes only
+      const bool slow = far && !(kp.mode == KM_SINGULAR ||
+                                 (kp.mode == KM_REGULARIZED && s >= kp.near2));
+      if (far) {
+        const float inv_r = rsqrtf(s);
+        const float R = inv_r * inv_r;
+        const float W = R * inv_r;
+        const float Wp_r = -3.0f * W * R;
+        r_ = A * R;
+        const float aWds = A * W * ds0;
+        u0 = aWds * fx, u1 = aWds * fy, u2 = aWds * fz;
+        const float gd = fmaf(dg0, fx, fmaf(dg1, fy, dg2 * fz));  // :372-374
+        const float t = Wp_r * gd;
+        u0 -= A * fmaf(W, dg0, t * fx);
+        u1 -= A * fmaf(W, dg1, t * fy);
+        u2 -= A * fmaf(W, dg2, t * fz);
+      }
+      if (__any_sync(FULL_MASK, slow)) {
+        if (slow) {
+          const Co c = adj_coeffs<GM>(s, kp);
+          nr_ = c.near;
+          r_ = A * c.R;
+          e_ = A * c.dR_de;
+          const float aWds = A * c.W * ds0;
+          u0 = aWds * fx, u1 = aWds * fy, u2 = aWds * fz;
+          const float4 v = __ldg(tv.node_row + (size_t)node * F4g);
+          const float vd = fmaf(v.x, fx, fmaf(v.y, fy, v.z * fz));
+          float e = ds0 * A * c.dW_de * vd;  // :370
+          const float gd = fmaf(dg0, fx, fmaf(dg1, fy, dg2 * fz));  // :372-374
           const float t = c.Wp_r * gd;
           u0 -= A * fmaf(c.W, dg0, t * fx);
           u1 -= A * fmaf(c.W, dg1, t * fy);
@@ -477,8 +497,8 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
           const float k2 = c.dWp_r_de * vd;
           e -= A * fmaf(dg0, fmaf(c.dW_de, v.x, k2 * fx),
                         fmaf(dg1, fmaf(c.dW_de, v.y, k2 * fy), dg2 * fmaf(c.dW_de, v.z, k2 * fz)));
+          eps_acc += (double)e;
         }
-        eps_acc += (double)e;
       }
     }
     wR[nent * WS + lane] = r_;
