@@ -1,4 +1,4 @@
-"""e2e step timing breakdown (host-async mode, alternating pinned batches)."""
+"""e2e step timing breakdown on config 2: synchronous vs host-async mode, same vs alternating pinned query batches (python tools/e2e_breakdown.py on a GPU box)."""
 import sys, time, numpy as np, torch
 sys.path.insert(0, '.')
 import paper_2405_16788_b200 as P

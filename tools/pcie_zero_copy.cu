@@ -1,4 +1,4 @@
-// zero-copy PCIe microbenchmark: device kernels reading / writing pinned host rows
+// PCIe microbenchmark (nvcc -O3 -gencode arch=compute_100a,code=sm_100a tools/pcie_zero_copy.cu): kernels reading / writing pinned host rows vs cudaMemcpy. Measured on B200: memcpy 55 GB/s each way, zero-copy row reads 26 GB/s, row writes 18.5 GB/s -> host batches go through copy engines on their own streams (host-async mode), not zero-copy.
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
