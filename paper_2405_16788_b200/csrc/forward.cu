@@ -29,12 +29,10 @@ struct FAcc {
 };
 
 template <int TD, int TR, int GRAD>
-__device__ __forceinline__ void f_interact(FAcc<TD, TR, GRAD>& a, double dx, double dy, double dz,
-                                           double dist2, float A, const float4* __restrict__ pd,
+__device__ __forceinline__ void f_interact(FAcc<TD, TR, GRAD>& a, float fx, float fy, float fz,
+                                           float r2, float A, const float4* __restrict__ pd,
                                            const float* __restrict__ pr, int nd, int nr,
                                            const KParams& kp, bool& near) {
-  const float fx = (float)dx, fy = (float)dy, fz = (float)dz;
-  const float r2 = (float)dist2;
   Co c = coeffs<GRAD ? 1 : 0>(r2, kp);
   near = c.near;
   const float aW = A * c.W, aR = A * c.R;
@@ -111,6 +109,9 @@ __global__ void __launch_bounds__(FWD_WARPS * 32)
   }
   const unsigned active = __ballot_sync(FULL_MASK, valid);
   if (!active) return;
+  // double-float query + the fp64 position re-read only on the exact paths
+  const QueryDF qx = make_qdf(x, tv.cmax);
+  const double* xq = xs + 3 * qi;
   FAcc<TD, TR, GRAD> a;
 #pragma unroll
   for (int k = 0; k < (TD > 0 ? TD : 1); ++k) a.vd[k] = 0.f;
@@ -138,16 +139,20 @@ __global__ void __launch_bounds__(FWD_WARPS * 32)
     const int node = e.x;
     const unsigned mask = (unsigned)e.y;
     const bool mine = (mask >> lane) & 1u;
-    const double4 dec = ld_dec(tv.node_dec + node);
-    const int4 tp = __ldg(tv.node_topo + node);
-    double dx, dy, dz;
-    const double dist2 = dist2_rn(dec.x, dec.y, dec.z, x, dx, dy, dz);
-    const bool far = mine && (dist2 > dec.w);
+    // the reference's opening test (bhtree.cpp:202-204) decided in fp32 on the
+    // double-float record, exactly in fp64 inside the error band (traverse.cuh)
+    const NodeRec* rec = tv.node_rec + node;
+    const float4 hi = __ldg(&rec->hi);
+    const float4 lo = __ldg(&rec->lo);
+    const int4 tp = __ldg(&rec->topo);
+    float dx, dy, dz;
+    const float s = dist2_df(hi, lo, qx, dx, dy, dz);
+    const bool far = mine && far_test(s, hi, qx, xq, tv.node_dec + node);
     const unsigned farm = __ballot_sync(FULL_MASK, far);
     if (COUNT && mine) ++c_vis;
     if (far && (__ldg(tv.node_flag + node) & 1)) {
       bool near;
-      f_interact<TD, TR, GRAD>(a, dx, dy, dz, dist2, __ldg(tv.node_geo + node).w,
+      f_interact<TD, TR, GRAD>(a, dx, dy, dz, s, lo.w,
                                pdn + (int64_t)node * tv.F4, prn + (int64_t)node * 4 * tv.F4,
                                nd, nr,
                                kp, near);
@@ -158,13 +163,14 @@ __global__ void __launch_bounds__(FWD_WARPS * 32)
       if (tp.y == 0) {
         if ((openm >> lane) & 1u) {
           for (int j = tp.z; j < tp.w; ++j) {
-            double px = __ldg(tv.pt_pos64 + 3 * (int64_t)j);
-            double py = __ldg(tv.pt_pos64 + 3 * (int64_t)j + 1);
-            double pz = __ldg(tv.pt_pos64 + 3 * (int64_t)j + 2);
-            const double r2 = dist2_rn(px, py, pz, x, dx, dy, dz);
-            if (r2 == 0.0 && skip_coincident) continue;
+            const PtRec* pr = tv.pt_rec + j;
+            const float4 ph = __ldg(&pr->hi);
+            const float r2 = dist2_df(ph, __ldg(&pr->lo), qx, dx, dy, dz);
+            // exact coincidence (fp64) is only possible when the fp32 r2 is 0
+            if (skip_coincident && r2 == 0.f && coincident_exact(tv.pt_pos64 + 3 * (size_t)j, xq))
+              continue;
             bool near;
-            f_interact<TD, TR, GRAD>(a, dx, dy, dz, r2, __ldg(tv.pt_geo + j).w,
+            f_interact<TD, TR, GRAD>(a, dx, dy, dz, r2, ph.w,
                                      pdp + (int64_t)j * tv.F4, prp + (int64_t)j * 4 * tv.F4,
                                      nd, nr,
                                      kp, near);
