@@ -76,10 +76,10 @@ __device__ __forceinline__ Co coeffs(float r2, const KParams& kp) {
     float inv_r = rsqrtf(r2);  // inf at r2 == 0, handled by the near branch
     float r = r2 * inv_r;
     float t = r * kp.inv_eps;
-    if (r2 > 0.f && t >= 6.5f) {
-      float inv_r2 = 1.0f / r2;
+    if (r2 > 0.f && t >= 6.5f) {  // tau = 1 (kernels.cpp:50-55); products of rsqrt, no divide
+      const float inv_r2 = inv_r * inv_r;
       c.R = inv_r2;
-      c.W = inv_r * inv_r2;
+      c.W = inv_r2 * inv_r;
       if (ORDER >= 1) {
         c.Wp_r = -3.0f * c.W * inv_r2;
         c.Rp_r = -2.0f * inv_r2 * inv_r2;
@@ -120,8 +120,8 @@ __device__ __forceinline__ Co coeffs(float r2, const KParams& kp) {
     return c;
   }
   if (kp.mode == KM_SINGULAR) {  // kernels.cpp:112-121; callers guarantee r2 > 0
-    float inv_r2 = 1.0f / r2;
     float inv_r = rsqrtf(r2);
+    float inv_r2 = inv_r * inv_r;
     c.R = inv_r2;
     c.W = inv_r * inv_r2;
     if (ORDER >= 1) {
