@@ -127,7 +127,9 @@ struct AdjLayout {
   static constexpr int TILE = MT ? 32 * S : 0;
   static constexpr int UNION = BATCH > TILE ? BATCH : TILE;
   static constexpr int ALO = MT * 2 * 32 * 4;  // BF16 A_lo fragments (uint32 words)
-  static constexpr int WARP_FLOATS = (UNION + ALO + ENT + (ENT & 1) + 2 * DPL_STACK_PER_WARP + 3) & ~3;
+  static constexpr int PTR = 2 * ENT;  // per-entry radial destination row (double*)
+  static constexpr int WARP_FLOATS =
+      (UNION + ALO + PTR + ENT + (ENT & 1) + 2 * DPL_STACK_PER_WARP + 3) & ~3;
 };
 
 // NB: 0 -> Cr <= 32; 1 -> 32 < Cr <= 48 (split); 2 -> Cr <= 64 (FFMA phase B).
@@ -159,7 +161,9 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
   float* vq = wE + ENT * WS;
   float4* rows = reinterpret_cast<float4*>(vq + ENT * 128);
   const uint4* alo = reinterpret_cast<const uint4*>(base + L::UNION);
-  int* meta = reinterpret_cast<int*>(base + L::UNION + L::ALO);
+  // per entry: the radial destination row, resolved once by lane 0 in phase A
+  double** dptr = reinterpret_cast<double**>(base + L::UNION + L::ALO);
+  int* meta = reinterpret_cast<int*>(base + L::UNION + L::ALO + L::PTR);
   int2* stk = reinterpret_cast<int2*>(meta + ENT + (ENT & 1));
   const uint32_t s_rows = smem_u32(rows) + 16u * lane;
   const int F4g = tv.F4;               // global row stride
@@ -333,8 +337,6 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
     }
     for (int e = 0; e < nent; ++e) {
       const int m = meta[e];
-      const bool is_point = m & (1 << 30);
-      const int64_t src = m & ((1 << 29) - 1);
       if constexpr (FF) {
         const bool near = m & (1 << 29);
         const float4* wr4 = reinterpret_cast<const float4*>(wR + e * WS);
@@ -363,10 +365,10 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
         const float sA = pA.x + pA.y;
         float sB = pB.x + pB.y;
         if (NB == 1) sB += __shfl_xor_sync(FULL_MASK, sB, 16);
-        double* dst_s = is_point ? acc.pt_mur + src * Cr : acc.node_s + src * Cr;
-        if (okA && sA != 0.f) atomicAdd(dst_s + lane, (double)sA);
+        double* dst_s = dptr[e];
+        red_add_if(dst_s + lane, (double)sA, okA && sA != 0.f);
         const bool ownB = NB == 2 ? okB : (NB == 1 ? (okB && lane < 16) : false);
-        if (ownB && sB != 0.f) atomicAdd(dst_s + slotB, (double)sB);
+        if (NB > 0) red_add_if(dst_s + slotB, (double)sB, ownB && sB != 0.f);
         if (near) {  // radial epsilon terms (:379, :409)
           const float4* we4 = reinterpret_cast<const float4*>(wE + e * WS);
           float eA = 0.f, eB = 0.f;
@@ -409,11 +411,9 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
         const int m = meta[e];
         const bool is_point = m & (1 << 30);
         const int64_t src = m & ((1 << 29) - 1);
-        if (s != 0.f && (is_point || k < 3)) {
-          double* dst = is_point ? (k < 3 ? acc.pt_n + 3 * src + k : acc.pt_mud + src)
-                                 : acc.node_v + 3 * src + k;
-          atomicAdd(dst, (double)s);
-        }
+        double* dst = is_point ? (k < 3 ? acc.pt_n + 3 * src + k : acc.pt_mud + src)
+                               : acc.node_v + 3 * src + k;
+        red_add_if(dst, (double)s, s != 0.f && (is_point || k < 3));
       }
     }
     __syncwarp();
@@ -436,7 +436,7 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
       const bool slow = far && !(kp.mode == KM_SINGULAR ||
                                  (kp.mode == KM_REGULARIZED && s >= kp.near2));
       if (far) {
-        const float inv_r = rsqrtf(s);
+        const float inv_r = rsqrt_pos(s);
         const float R = inv_r * inv_r;
         r_ = A * R;
         const float aWds = A * (R * inv_r) * ds0;
@@ -465,7 +465,7 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
       const bool slow = far && !(kp.mode == KM_SINGULAR ||
                                  (kp.mode == KM_REGULARIZED && s >= kp.near2));
       if (far) {
-        const float inv_r = rsqrtf(s);
+        const float inv_r = rsqrt_pos(s);
         const float R = inv_r * inv_r;
         const float W = R * inv_r;
         const float Wp_r = -3.0f * W * R;
@@ -504,11 +504,15 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
     wR[nent * WS + lane] = r_;
     wE[nent * WS + lane] = e_;
     float* vqe = vq + nent * 128;
-    vqe[lane] = u0, vqe[32 + lane] = u1, vqe[64 + lane] = u2, vqe[96 + lane] = 0.f;
+    vqe[lane] = u0, vqe[32 + lane] = u1, vqe[64 + lane] = u2;  // slot 3 (d mu_0) is never read for nodes
     const bool any_near = __any_sync(FULL_MASK, nr_);
-    if (any_near && lane < F4c)
-      cp_async16(s_rows + 16u * F4 * nent, tv.node_row + (size_t)node * F4g + lane);
-    if (lane == 0) meta[nent] = node | (any_near ? (1 << 29) : 0);
+    if (any_near) {  // warp-uniform; rare beyond the first tree levels
+      if (lane < F4c) cp_async16(s_rows + 16u * F4 * nent, tv.node_row + (size_t)node * F4g + lane);
+    }
+    if (lane == 0) {
+      meta[nent] = node | (any_near ? (1 << 29) : 0);
+      dptr[nent] = acc.node_s + (size_t)node * Cr;
+    }
     ++nent;
   };
   // the points of an opened leaf for the lanes in `me_open` (:382-412)
@@ -556,9 +560,13 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
       float* vqe = vq + nent * 128;
       vqe[lane] = n0, vqe[32 + lane] = n1, vqe[64 + lane] = n2, vqe[96 + lane] = dmu;
       const bool any_near = __any_sync(FULL_MASK, nr_);
-      if (any_near && lane < F4c)
-        cp_async16(s_rows + 16u * F4 * nent, tv.pt_row + (size_t)j * F4g + lane);
-      if (lane == 0) meta[nent] = j | (1 << 30) | (any_near ? (1 << 29) : 0);
+      if (any_near) {
+        if (lane < F4c) cp_async16(s_rows + 16u * F4 * nent, tv.pt_row + (size_t)j * F4g + lane);
+      }
+      if (lane == 0) {
+        meta[nent] = j | (1 << 30) | (any_near ? (1 << 29) : 0);
+        dptr[nent] = acc.pt_mur + (size_t)j * Cr;
+      }
       ++nent;
     }
   };
