@@ -73,7 +73,7 @@ __device__ __forceinline__ Co coeffs(float r2, const KParams& kp) {
   c.Wp_r = c.Rp_r = c.dW_de = c.dWp_r_de = c.dR_de = 0.f;
   c.near = false;
   if (kp.mode == KM_REGULARIZED) {
-    float inv_r = rsqrtf(r2);  // inf at r2 == 0, handled by the near branch
+    float inv_r = rsqrt_pos(r2);  // r2 == 0 (coincidence) is handled by the near branch
     float r = r2 * inv_r;
     float t = r * kp.inv_eps;
     if (r2 > 0.f && t >= 6.5f) {  // tau = 1 (kernels.cpp:50-55); products of rsqrt, no divide

@@ -99,4 +99,25 @@ struct ChanMap {
 
 inline int round_up4(int x) { return (x + 3) & ~3; }
 
+#ifdef __CUDACC__
+// 1/sqrt(x): the MUFU.RSQ that rsqrtf issues for normal inputs (bit-identical
+// there), without rsqrtf's denormal rescaling — x is clamped to FLT_MIN instead.
+// Callers either have x >= FLT_MIN (far field: x > the opening threshold) or
+// discard the result (r2 == 0 at coincidence takes the near-field series)
+__device__ __forceinline__ float rsqrt_pos(float x) {
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(fmaxf(x, 1.17549435e-38f)));
+  return r;
+}
+
+// fp64 RED under a PTX predicate (no C++ branch; the address needs no guard)
+__device__ __forceinline__ void red_add_if(double* p, double v, bool pred) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q red.global.add.f64 [%0], %1;\n\t}\n" ::"l"(p),
+      "d"(v), "r"((int)pred)
+      : "memory");
+}
+
+#endif
+
 }  // namespace dpl

@@ -33,7 +33,7 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 // lane weights of one source: (A W dx, A W dy, A W dz, A R)
 __device__ __forceinline__ float4 fwd_weights(float fx, float fy, float fz, float r2, float A,
                                               const KParams& kp) {
-  const float inv_r = rsqrtf(r2);
+  const float inv_r = rsqrt_pos(r2);
   float W, R;
   if (kp.mode == KM_SINGULAR || (kp.mode == KM_REGULARIZED && r2 >= kp.near2)) {
     R = inv_r * inv_r;  // tau = 1 beyond t = 6.5 (kernels.cpp:50-55)

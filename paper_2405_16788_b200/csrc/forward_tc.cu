@@ -47,7 +47,7 @@ __device__ __forceinline__ void mma_tf32(float (&c)[4], const uint32_t (&a)[4], 
 
 __device__ __forceinline__ float4 fwd_w(float fx, float fy, float fz, float r2, float A,
                                         const KParams& kp) {
-  const float inv_r = rsqrtf(r2);
+  const float inv_r = rsqrt_pos(r2);
   float W, R;
   if (kp.mode == KM_SINGULAR || (kp.mode == KM_REGULARIZED && r2 >= kp.near2)) {
     R = inv_r * inv_r;

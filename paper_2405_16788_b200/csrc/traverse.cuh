@@ -119,24 +119,6 @@ __device__ __forceinline__ bool coincident_exact(const double* __restrict__ p, c
   return dist2_rn(__ldg(p), __ldg(p + 1), __ldg(p + 2), x, ex, ey, ez) == 0.0;
 }
 
-// 1/sqrt(x) for x > 0: the MUFU.RSQ that rsqrtf issues for normal inputs,
-// without rsqrtf's denormal rescaling (x is clamped to FLT_MIN instead; a
-// far-field or leaf distance^2 below 1.2e-38 does not occur in practice, and
-// exact coincidence never reaches the callers)
-__device__ __forceinline__ float rsqrt_pos(float x) {
-  float r;
-  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(fmaxf(x, 1.17549435e-38f)));
-  return r;
-}
-
-// fp64 RED under a predicate, without a divergent branch around it
-__device__ __forceinline__ void red_add_if(double* p, double v, bool pred) {
-  asm volatile(
-      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q red.global.add.f64 [%0], %1;\n\t}\n" ::"l"(p),
-      "d"(v), "r"((int)pred)
-      : "memory");
-}
-
 __device__ __forceinline__ double4 ld_dec(const double4* p) {
   const double2* q = reinterpret_cast<const double2*>(p);
   double2 a = __ldg(q), b = __ldg(q + 1);
