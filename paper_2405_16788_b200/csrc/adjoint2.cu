@@ -425,8 +425,11 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
     if (nent == ENT) evaluate();
   };
 
-  // one far source (node) for the lanes in `far` (bhtree.cpp:361-381)
-  auto far_entry = [&](int node, float A, float s, float fx, float fy, float fz, bool far) {
+  // one far source (node) for the lanes in `far` (bhtree.cpp:361-381).
+  // hint: the list's NEAR flag (0: no far lane needs the series, 1: some may),
+  // -1 on the tree walk (decided by a vote)
+  auto far_entry = [&](int node, float A, float s, float fx, float fy, float fz, bool far,
+                       int hint) {
     begin_entry();
     float r_ = 0.f, e_ = 0.f, u0 = 0.f, u1 = 0.f, u2 = 0.f;
     bool nr_ = false;
@@ -443,7 +446,7 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
         const float aWds = A * (R * inv_r) * ds0;
         u0 = aWds * fx, u1 = aWds * fy, u2 = aWds * fz;
       }
-      if (__any_sync(FULL_MASK, slow)) {
+      if (hint != 0 && (hint > 0 || __any_sync(FULL_MASK, slow))) {
         if (slow) {
           const Co c = coeffs<2>(s, kp);
           nr_ = c.near;
@@ -479,7 +482,7 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
         u1 -= A * fmaf(W, dg1, t * fy);
         u2 -= A * fmaf(W, dg2, t * fz);
       }
-      if (__any_sync(FULL_MASK, slow)) {
+      if (hint != 0 && (hint > 0 || __any_sync(FULL_MASK, slow))) {
         if (slow) {
           const Co c = adj_coeffs<GM>(s, kp);
           nr_ = c.near;
@@ -506,7 +509,7 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
     wE[nent * WS + lane] = e_;
     float* vqe = vq + nent * 128;
     vqe[lane] = u0, vqe[32 + lane] = u1, vqe[64 + lane] = u2;  // slot 3 (d mu_0) is never read for nodes
-    const bool any_near = __any_sync(FULL_MASK, nr_);
+    const bool any_near = hint != 0 && __any_sync(FULL_MASK, nr_);
     if (any_near) {  // warp-uniform; rare beyond the first tree levels
       if (lane < F4c) cp_async16(s_rows + 16u * F4 * nent, tv.node_row + (size_t)node * F4g + lane);
     }
@@ -600,7 +603,7 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
           const float4 hi = rb[i].hi, lo = rb[i].lo;
           float fx, fy, fz;
           const float s = dist2_df(hi, lo, qx, fx, fy, fz);
-          far_entry((int)(src & IL_NODE), lo.w, s, fx, fy, fz, mine);
+          far_entry((int)(src & IL_NODE), lo.w, s, fx, fy, fz, mine, (src & IL_NEAR) ? 1 : 0);
         } else {
           leaf_points(rb[i].topo, mine);
         }
@@ -627,7 +630,7 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
     const bool far = mine && far_test(s, hi, qx, xq, tv.node_dec + node);
     const unsigned farm = __ballot_sync(FULL_MASK, far);
     if (farm && A > 0.f) {
-      far_entry(node, A, s, fx, fy, fz, far);
+      far_entry(node, A, s, fx, fy, fz, far, -1);
     }
     const unsigned openm = mask & ~farm;
     if (openm) {
@@ -675,7 +678,7 @@ template <int NB, int GM, int RR, int WARPS = 4, int ENT = 8, int MAXR = 128, in
 static void launch_adj2(const Tree& t, const KParams& kp, const AdjArgs& a, GradBuf& b, int nr) {
   const bool reg = SPEC && kp.mode == KM_REGULARIZED;
   if (a.ilist && !no_ilist()) {
-    ilist_build(t, *a.ilist, a.xs, a.perm, a.q, a.beta, a.overflow);
+    ilist_build(t, *a.ilist, a.xs, a.perm, a.q, a.beta, ilist_near_thr(kp), a.overflow);
     if (reg)
       launch_adj2c<NB, GM, RR, WARPS, ENT, MAXR, MT, true, SPEC>(t, kp, a, b, nr, a.ilist->view());
     else

@@ -62,6 +62,16 @@ __device__ __forceinline__ float4 fwd_w(float fx, float fy, float fz, float r2, 
   return make_float4(aW * fx, aW * fy, aW * fz, A * R);
 }
 
+// fwd_w's far-field branch for every lane (tau = 1; the list says no far lane
+// of this entry is within 6.5 eps, or the kernel is singular)
+__device__ __forceinline__ float4 fwd_w_far(float fx, float fy, float fz, float r2, float A) {
+  const float inv_r = rsqrt_pos(r2);
+  const float R = inv_r * inv_r;
+  const float W = R * inv_r;
+  const float aW = A * W;
+  return make_float4(aW * fx, aW * fy, aW * fz, A * R);
+}
+
 constexpr int row_stride_floats(int f4) {
   int r = 4 * f4;
   while (r % 32 != 8 && r % 32 != 24) r += 4;
@@ -216,7 +226,12 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
           const float4 hi = rb[i].hi, lo = rb[i].lo;
           float dx, dy, dz;
           const float s = dist2_df(hi, lo, qx, dx, dy, dz);
-          const float4 wv = mine ? fwd_w(dx, dy, dz, s, lo.w, kp) : make_float4(0.f, 0.f, 0.f, 0.f);
+          float4 wv = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (src & IL_NEAR) {
+            if (mine) wv = fwd_w(dx, dy, dz, s, lo.w, kp);
+          } else if (mine) {
+            wv = fwd_w_far(dx, dy, dz, s, lo.w);
+          }
           append(wv, node_row + (size_t)node * F4g);
         } else {
           const int4 tp = rb[i].topo;
@@ -350,7 +365,7 @@ static void launch_tc(const Tree& t, const KParams& kp, const FwdArgs& a, int nr
   if (a.counters) {
     launch_tc1<NT, WARPS, ENT, MAXR, true, false>(t, kp, a, nr);
   } else if (a.ilist && !no_ilist()) {
-    ilist_build(t, *a.ilist, a.xs, a.perm, a.q, a.beta, a.overflow);
+    ilist_build(t, *a.ilist, a.xs, a.perm, a.q, a.beta, ilist_near_thr(kp), a.overflow);
     if (reg)
       launch_tc1<NT, WARPS, ENT, MAXR, false, true, SPEC>(t, kp, a, nr, a.ilist->view());
     else

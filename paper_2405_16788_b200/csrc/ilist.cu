@@ -53,7 +53,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
     k_build_list(TreeView tv, const double* __restrict__ xs, const int32_t* __restrict__ perm,
                  int64_t q, uint2* __restrict__ pool, int* __restrict__ next,
                  int* __restrict__ count, unsigned long long* ctr, int64_t chunks,
-                 const int* skip, int* overflow) {
+                 float near_thr, const int* skip, int* overflow) {
   if (skip && *skip) return;  // lists of this exact batch are already in place
   __shared__ int2 stk_all[WARPS][DPL_STACK_PER_WARP];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -118,7 +118,10 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
     const float s = dist2_df(hi, lo, qx, dx, dy, dz);
     const bool far = mine && far_test(s, hi, qx, xq, tv.node_dec + node);
     const unsigned farm = __ballot_sync(FULL_MASK, far);
-    if (farm && lo.w > 0.f) emit((uint32_t)node, farm);
+    if (farm && lo.w > 0.f) {
+      const bool nr = __any_sync(FULL_MASK, far && s < near_thr);
+      emit((uint32_t)node | (nr ? IL_NEAR : 0u), farm);
+    }
     const unsigned openm = mask & ~farm;
     if (openm && ok) {
       if (tp.y == 0) {
@@ -138,7 +141,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
 }
 
 void ilist_build(const Tree& t, IList& il, const double* xs, const int32_t* perm, int64_t q,
-                 double beta, int* overflow) {
+                 double beta, float near_thr, int* overflow) {
   constexpr int WARPS = 4, MINB = 12;
   const int64_t nwarps = (q + 31) / 32;
   static const char* pool_env = getenv("DPL_ILIST_POOL");  // chunks per warp (tests: 1 forces
@@ -154,7 +157,8 @@ void ilist_build(const Tree& t, IList& il, const double* xs, const int32_t* perm
   }
   il.same.reserve(sizeof(int));
   const int* skip = nullptr;
-  if (il.valid && il.q == q && il.beta == beta && il.tree_version == t.version) {
+  if (il.valid && il.q == q && il.beta == beta && il.near_thr == near_thr &&
+      il.tree_version == t.version) {
     k_set_int<<<1, 1, 0, t.stream>>>(il.same.as<int>(), 1);
     k_compare<<<4 * 148, 256, 0, t.stream>>>(reinterpret_cast<const unsigned long long*>(xs),
                                               il.xs_copy.as<unsigned long long>(), 3 * q,
@@ -179,7 +183,7 @@ void ilist_build(const Tree& t, IList& il, const double* xs, const int32_t* perm
   const unsigned blocks = (unsigned)((nwarps + WARPS - 1) / WARPS);
   k_build_list<WARPS, MINB><<<blocks, WARPS * 32, 0, t.stream>>>(
       t.view(), xs, perm, q, il.pool.as<uint2>(), il.next.as<int>(), il.count.as<int>(),
-      il.ctr.as<unsigned long long>(), chunks, skip, overflow);
+      il.ctr.as<unsigned long long>(), chunks, near_thr, skip, overflow);
   count_launch();
   // chunks actually used, read back without a sync (sizes the next build)
   unsigned long long* used_dev = nullptr;
@@ -196,6 +200,7 @@ void ilist_build(const Tree& t, IList& il, const double* xs, const int32_t* perm
   il.valid = true;
   il.q = q;
   il.beta = beta;
+  il.near_thr = near_thr;
   il.tree_version = t.version;
 }
 

@@ -25,6 +25,17 @@ namespace dpl {
 constexpr int IL_CHUNK = 128;             // entries per pool chunk (1 KB)
 constexpr uint32_t IL_LEAF = 1u << 30;    // entry.x flag: opened leaf
 constexpr uint32_t IL_NODE = IL_LEAF - 1;  // entry.x node-index mask
+// entry.x flag on far sources: some far lane has dist^2 < near_thr (the
+// lanes that need the near-field coefficient series); a far entry without
+// it is evaluated with tau = 1 by every lane, no per-lane branch or vote
+constexpr uint32_t IL_NEAR = 1u << 31;
+
+// near_thr for the NEAR flag: regularized kernel (6.5 eps)^2 (kernels.cpp:50-55),
+// singular never near, desingularized always (its coefficients have no far form)
+inline float ilist_near_thr(const KParams& kp) {
+  if (kp.mode == KM_REGULARIZED) return kp.near2;
+  return kp.mode == KM_SINGULAR ? -1.0f : __builtin_huge_valf();
+}
 
 struct IListView {
   const uint2* pool = nullptr;  // [chunks][IL_CHUNK] entries {src, lane mask}
@@ -41,6 +52,7 @@ struct IList {
   bool valid = false;
   int64_t q = 0;
   double beta = 0;
+  float near_thr = 0;
   uint64_t tree_version = 0;
   DevBuf xs_copy;  // the queries the list was built for (exact reuse check)
   DevBuf same;     // device int: 1 when this batch equals xs_copy (set per call)
@@ -68,7 +80,7 @@ inline bool ilist_always() {
 // no host sync) the build kernels exit at once and the lists are reused:
 // the decisions depend only on (tree geometry, beta, xs).
 void ilist_build(const Tree& t, IList& il, const double* xs, const int32_t* perm, int64_t q,
-                 double beta, int* overflow);
+                 double beta, float near_thr, int* overflow);
 
 // Device-side iteration of warp wg's list: entries [base, base + 32) of the
 // list live at pool[chunk * IL_CHUNK + base % IL_CHUNK + lane].
