@@ -243,7 +243,7 @@ def run_reference(args):
         "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 # ------------------------------------------------------------------ our arm
@@ -256,7 +256,8 @@ def run_ours(args):
 
     rank, world, local = env_rank()
     dist = None
-    if world > 1:
+    # DPL_BENCH_DIST=1 exercises the NCCL path at world size 1 (one GPU boxes)
+    if world > 1 or os.environ.get("DPL_BENCH_DIST"):
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -466,12 +467,27 @@ def run_ours(args):
         "e2e": e2e,
         "cpu_baseline": cpu,
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
     if dist is not None:
         dist.destroy_process_group()
 
 
+_JSON_OUT = None
+
+
+def emit(line):
+    """The one JSON line, on the process's original stdout."""
+    out = _JSON_OUT or sys.stdout
+    print(json.dumps(line), file=out, flush=True)
+
+
 def main():
+    global _JSON_OUT
+    # stdout carries exactly one JSON line: anything else native code prints
+    # there (e.g. NCCL's version banner at communicator creation) goes to stderr
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     args = parse()
     if args.impl == "reference":
         run_reference(args)

@@ -336,6 +336,7 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
         }
       }
     }
+#pragma unroll 2
     for (int e = 0; e < nent; ++e) {
       const int m = meta[e];
       if constexpr (FF) {
