@@ -119,12 +119,15 @@ struct Adj2Ptrs {
 
 // Per-warp shared-memory layout. The d_out tile staged by the tensor-core
 // prologue aliases the batch arrays (it is consumed before the first entry).
-template <int MT, int ENT, int RR>
+// VR: radial channels reduced with the vector quantities (NB = 3, nr <= 4):
+// 8 per-lane slots per entry, no weight rows and no staged payload rows.
+template <int MT, int ENT, int RR, bool VR = false>
 struct AdjLayout {
   static constexpr int WS = MT ? 36 : 32;  // weight row stride: conflict-free B gathers
-  static constexpr int F4 = 1 + RR;        // smem row capacity (float4)
+  static constexpr int F4 = VR ? 0 : 1 + RR;  // smem row capacity (float4)
+  static constexpr int VQ = VR ? 8 : 4;       // per-lane slots per entry
   static constexpr int S = tile_stride(16 * (MT ? MT : 1));
-  static constexpr int BATCH = ENT * WS * 2 + ENT * 128 + ENT * F4 * 4;
+  static constexpr int BATCH = (VR ? 0 : ENT * WS * 2) + ENT * 32 * VQ + ENT * F4 * 4;
   static constexpr int TILE = MT ? 32 * S : 0;
   static constexpr int UNION = BATCH > TILE ? BATCH : TILE;
   static constexpr int ALO = MT * 2 * 32 * 4;  // BF16 A_lo fragments (uint32 words)
@@ -133,7 +136,9 @@ struct AdjLayout {
       (UNION + ALO + PTR + ENT + (ENT & 1) + 2 * DPL_STACK_PER_WARP + 3) & ~3;
 };
 
-// NB: 0 -> Cr <= 32; 1 -> 32 < Cr <= 48 (split); 2 -> Cr <= 64 (FFMA phase B).
+// NB: 0 -> Cr <= 32; 1 -> 32 < Cr <= 48 (split); 2 -> Cr <= 64 (FFMA phase B);
+//     3 -> Cr <= 4 (render path: each lane forms A R ds_c for its own query and
+//     the radial sums ride along the vector-quantity reduction, no d_out tile).
 // MT: > 0 selects the tensor-core phase B with MT m-tiles (Cr <= 16 MT); NB unused.
 // GM: 0 no d_grad; 1 d_grad q x dstride x 3; 2 d_grad q x 3 (channel 0).
 // MAXR: register cap (occupancy vs. spills; chosen by measurement)
@@ -149,7 +154,10 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
                const int* __restrict__ chmap, Adj2Ptrs acc, IListView lv, int* overflow) {
   KParams kp = kp_in;
   if (REG) kp.mode = KM_REGULARIZED;
-  using L = AdjLayout<MT, ENT, RR>;
+  constexpr bool VR = NB == 3;
+  static_assert(!VR || MT == 0, "VR is an FFMA-path layout");
+  using L = AdjLayout<MT, ENT, RR, VR>;
+  constexpr int VQ = L::VQ;
   constexpr int F4 = L::F4;
   constexpr int WS = L::WS;
   static_assert(MT == 0 || ENT == 8, "tensor-core phase B uses one n-tile of 8 entries");
@@ -159,8 +167,8 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
   float* base = reinterpret_cast<float*>(smem_f4) + (size_t)w * L::WARP_FLOATS;
   float* wR = base;
   float* wE = wR + ENT * WS;
-  float* vq = wE + ENT * WS;
-  float4* rows = reinterpret_cast<float4*>(vq + ENT * 128);
+  float* vq = VR ? base : wE + ENT * WS;
+  float4* rows = reinterpret_cast<float4*>(vq + ENT * 32 * VQ);
   const uint4* alo = reinterpret_cast<const uint4*>(base + L::UNION);
   // per entry: the radial destination row, resolved once by lane 0 in phase A
   double** dptr = reinterpret_cast<double**>(base + L::UNION + L::ALO);
@@ -196,14 +204,21 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
   }
   // FFMA phase B: transposed radial tile in registers (lanes = channels)
   constexpr bool FF = MT == 0;
-  float colA[FF ? 32 : 1];
+  float colA[FF && !VR ? 32 : 1];
   float colB[FF ? (NB == 2 ? 32 : (NB == 1 ? 16 : 1)) : 1];
+  // VR: this lane's own radial upstream gradients (slots >= nr read as 0)
+  float dsr[4] = {0.f, 0.f, 0.f, 0.f};
+  if constexpr (VR) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      if (valid && c < nr) dsr[c] = __ldg(d_out + qi * dstride + __ldg(chmap + 1 + c));
+  }
   const bool okA = lane < nr;
   const int slotB = NB == 1 ? 32 + (lane & 15) : 32 + lane;
   const bool okB = FF && NB > 0 && slotB < nr;
   // tensor-core phase B: A = d_out tile^T [channel][query] as TF32 fragments
   uint32_t ahi[MT ? MT : 1][4][4];
-  if constexpr (FF) {
+  if constexpr (FF && !VR) {
     const int chA = okA ? __ldg(chmap + 1 + lane) : 0;
     const int chB = okB ? __ldg(chmap + 1 + slotB) : 0;
 #pragma unroll
@@ -339,7 +354,7 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
 #pragma unroll 2
     for (int e = 0; e < nent; ++e) {
       const int m = meta[e];
-      if constexpr (FF) {
+      if constexpr (FF && !VR) {
         const bool near = m & (1 << 29);
         const float4* wr4 = reinterpret_cast<const float4*>(wR + e * WS);
         // even / odd query partial sums on the packed FMA pipe (FFMA2)
@@ -396,12 +411,12 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
         }
       }
     }
-    // vector quantities of the whole batch: lane L sums pair (e, k) = (L / 4, L % 4)
+    // vector quantities of the whole batch: lane L sums pair (e, k) = (L / VQ, L % VQ)
     // of vq[e][k][0..31] (8 LDS.128, rotated by L so the 8 lanes of each phase
     // hit distinct bank groups) and issues at most one RED
-    for (int p0 = 0; p0 < 4 * nent; p0 += 32) {
+    for (int p0 = 0; p0 < VQ * nent; p0 += 32) {
       const int pr = p0 + lane;
-      if (pr < 4 * nent) {
+      if (pr < VQ * nent) {
         const float4* row = reinterpret_cast<const float4*>(vq + pr * 32);
         float s = 0.f;
 #pragma unroll
@@ -409,17 +424,38 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
           const float4 v4 = row[(j + lane) & 7];
           s += (v4.x + v4.y) + (v4.z + v4.w);
         }
-        const int e = pr >> 2, k = pr & 3;  // 0..2 vector, 3 = d mu_0
+        const int e = pr / VQ, k = pr % VQ;  // 0..2 vector, 3 = d mu_0, 4.. radial (VR)
         const int m = meta[e];
         const bool is_point = m & (1 << 30);
         const int64_t src = m & ((1 << 29) - 1);
         double* dst = is_point ? (k < 3 ? acc.pt_n + 3 * src + k : acc.pt_mud + src)
                                : acc.node_v + 3 * src + k;
-        red_add_if(dst, (double)s, s != 0.f && (is_point || k < 3));
+        bool use = is_point || k < 3;
+        if (VR && k >= 4) {
+          dst = dptr[e] + (k - 4);
+          use = k - 4 < nr;
+        }
+        red_add_if(dst, (double)s, s != 0.f && use);
       }
     }
     __syncwarp();
     nent = 0;
+  };
+
+  // VR: this lane's slots of the current entry — vector terms, d mu_0, and the
+  // radial products A R ds_c; the radial epsilon terms (:379, :409) are formed
+  // per lane from the source's first radial float4 (e_ != 0 only within 6.5 eps)
+  auto vr_store = [&](float r_, float e_, float v0, float v1, float v2, float v3,
+                      const float4* row) {
+    if (e_ != 0.f) {
+      const float4 rad = __ldg(row + 1);
+      eps_acc += (double)(e_ * fmaf(dsr[0], rad.x, fmaf(dsr[1], rad.y,
+                                                          fmaf(dsr[2], rad.z, dsr[3] * rad.w))));
+    }
+    float* vqe = vq + nent * 32 * VQ;
+    vqe[lane] = v0, vqe[32 + lane] = v1, vqe[64 + lane] = v2, vqe[96 + lane] = v3;
+    vqe[128 + lane] = r_ * dsr[0], vqe[160 + lane] = r_ * dsr[1];
+    vqe[192 + lane] = r_ * dsr[2], vqe[224 + lane] = r_ * dsr[3];
   };
 
   auto begin_entry = [&]() {
@@ -506,6 +542,15 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
         }
       }
     }
+    if constexpr (VR) {
+      vr_store(r_, e_, u0, u1, u2, 0.f, tv.node_row + (size_t)node * F4g);
+      if (lane == 0) {
+        meta[nent] = node;
+        dptr[nent] = acc.node_s + (size_t)node * Cr;
+      }
+      ++nent;
+      return;
+    }
     wR[nent * WS + lane] = r_;
     wE[nent * WS + lane] = e_;
     float* vqe = vq + nent * 128;
@@ -559,6 +604,15 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
           }
           eps_acc += (double)e;
         }
+      }
+      if constexpr (VR) {
+        vr_store(r_, e_, n0, n1, n2, dmu, tv.pt_row + (size_t)j * F4g);
+        if (lane == 0) {
+          meta[nent] = j | (1 << 30);
+          dptr[nent] = acc.pt_mur + (size_t)j * Cr;
+        }
+        ++nent;
+        continue;
       }
       wR[nent * WS + lane] = r_;
       wE[nent * WS + lane] = e_;
@@ -657,7 +711,7 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
 template <int NB, int GM, int RR, int WARPS, int ENT, int MAXR, int MT, bool LIST, bool REG>
 static void launch_adj2c(const Tree& t, const KParams& kp, const AdjArgs& a, GradBuf& b, int nr,
                          IListView lv) {
-  const size_t smem = (size_t)WARPS * AdjLayout<MT, ENT, RR>::WARP_FLOATS * 4;
+  const size_t smem = (size_t)WARPS * AdjLayout<MT, ENT, RR, NB == 3>::WARP_FLOATS * 4;
   static bool attr = false;
   if (!attr) {
     DPL_CUDA(cudaFuncSetAttribute(k_adjoint2<NB, GM, WARPS, ENT, RR, MAXR, MT, LIST, REG>,
@@ -705,6 +759,7 @@ static bool adj2_plan(const Tree& t, const KParams& kp, const AdjArgs& a, GradBu
     if (nr <= 48) return launch_adj2<0, GM, 12, 2, 8, 160, 3>(t, kp, a, b, nr), true;
   }
   if (t.F4 - 1 > 16) return false;
+  if (nr <= 4) return launch_adj2<3, GM, 1, 4, 8, 96, 0, true>(t, kp, a, b, nr), true;
   if (nr <= 32) return launch_adj2<0, GM, 16, 4, 8, 128, 0, true>(t, kp, a, b, nr), true;
   if (nr <= 48) return launch_adj2<1, GM, 16, 4, 8, 128, 0, true>(t, kp, a, b, nr), true;
   if (nr <= 64) return launch_adj2<2, GM, 16>(t, kp, a, b, nr), true;
