@@ -58,6 +58,9 @@ struct dpl_tree_s {
   } last_fwd;
   bool last_was_fwd = false;
   bool want_lists = false;
+  // render steps: lists when render_backward follows render_forward (training);
+  // a listed forward whose tape no backward consumed switches them off
+  bool render_lists = false, render_unconsumed = false;
   cudaEvent_t ev_fwd_in = nullptr, ev_fwd_out = nullptr, ev_adj_in = nullptr;
   void sync_all() {
     if (copy) DPL_CUDA(cudaStreamSynchronize(copy));
@@ -94,6 +97,7 @@ struct dpl_tape_s {
       mlp_x, mlp_dx;
   int vstride = 4;  // values per sample in vals (4: direct-rgb head, C: tiny-MLP head)
   bool has_deltas = false;
+  bool listed = false;  // render_forward built interaction lists for xs
 };
 
 static thread_local std::string g_err;
@@ -1155,6 +1159,11 @@ int dpl_render_forward(dpl_tree_t h, const dpl_kernel_params* params, const dpl_
     a.grad = tape->g0.as<float>();
     a.grad_mode = 2;
     a.overflow = overflow_flag(h);
+    if (h->render_unconsumed) h->render_lists = false;
+    tape->listed = (h->render_lists || ilist_always()) && !no_ilist();
+    h->render_unconsumed = tape->listed;
+    a.ilist = tape->listed ? &h->il : nullptr;
+    a.beta = rp->beta_bh;
     // the direct-rgb head reads channels 0..3 only (radiance.cpp:133-145):
     // radial slots 0..2 are channels 1..3 in SceneModel's layout; the tiny-MLP
     // head reads every appearance channel
@@ -1254,6 +1263,11 @@ int dpl_render_backward(dpl_tree_t h, const dpl_kernel_params* params, const dpl
     a.grad_mode = 2;
     a.nr_limit = mlp ? -1 : 3;
     a.overflow = overflow_flag(h);
+    // replays the forward's lists (verified on the device to describe tape->xs)
+    a.ilist = tape->listed ? &h->il : nullptr;
+    a.beta = rp->beta_bh;
+    h->render_lists = true;
+    h->render_unconsumed = false;
     {
       PhaseTimer pt(t, PH_ADJOINT);
       adjoint_launch(t, kp, a, buf->b);

@@ -86,17 +86,26 @@ __device__ __forceinline__ void f_interact(FAcc<TD, TR, GRAD>& a, float fx, floa
   }
 }
 
+namespace {
+__device__ __forceinline__ void cp_async16(uint32_t smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(smem), "l"(gmem));
+}
+}  // namespace
+
 // GRAD: 0 values only; 1 gradients of every channel in the tile; 2 gradient of
 // dipole slot 0 only (render step). single: write column 0 of a q x 1 output.
-template <int TD, int TR, int GRAD, bool COUNT>
+// LIST: replay the batch's interaction lists (ilist.cuh; same entries in the
+// same order as the walk, so identical results); incomplete warps walk.
+template <int TD, int TR, int GRAD, bool COUNT, bool LIST = false>
 __global__ void __launch_bounds__(FWD_WARPS * 32)
     k_forward(TreeView tv, KParams kp, const float4* __restrict__ payd_n,
               const float* __restrict__ payr_n, const float4* __restrict__ payd_p,
               const float* __restrict__ payr_p, const double* __restrict__ xs,
               const int32_t* __restrict__ perm, int64_t q, int d0, int nd, int r0, int nr,
               const int* __restrict__ chmap, float* __restrict__ out, int out_stride, int single,
-              float* __restrict__ grad, long long* __restrict__ counters, int* overflow) {
-  __shared__ int2 stk[FWD_WARPS][DPL_STACK_PER_WARP];
+              float* __restrict__ grad, long long* __restrict__ counters, IListView lv,
+              int* overflow) {
+  __shared__ __align__(16) int2 stk[FWD_WARPS][DPL_STACK_PER_WARP];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t sidx = ((int64_t)blockIdx.x * FWD_WARPS + w) * 32 + lane;
   const bool valid = sidx < q;
@@ -129,8 +138,65 @@ __global__ void __launch_bounds__(FWD_WARPS * 32)
   const float* prp = reinterpret_cast<const float*>(payd_p + tv.Cd) + r0;
   const bool skip_coincident = GRAD != 0 || kp.mode == KM_SINGULAR;  // :219 vs :316
 
-  int sp = 1;
-  if (lane == 0) stk[w][0] = make_int2(0, (int)active);
+  // the points of an opened leaf for this lane (bhtree.cpp:214-229, :311-329)
+  auto leaf = [&](const int4 tp) {
+    for (int j = tp.z; j < tp.w; ++j) {
+      const PtRec* pr = tv.pt_rec + j;
+      const float4 ph = __ldg(&pr->hi);
+      float dx, dy, dz;
+      const float r2 = dist2_df(ph, __ldg(&pr->lo), qx, dx, dy, dz);
+      // exact coincidence (fp64) is only possible when the fp32 r2 is 0
+      if (skip_coincident && r2 == 0.f && coincident_exact(tv.pt_pos64 + 3 * (size_t)j, xq))
+        continue;
+      bool near;
+      f_interact<TD, TR, GRAD>(a, dx, dy, dz, r2, ph.w, pdp + (int64_t)j * tv.F4,
+                               prp + (int64_t)j * 4 * tv.F4, nd, nr, kp, near);
+      if (COUNT) near ? ++c_pn : ++c_pf;
+    }
+  };
+
+  const int64_t wg = (int64_t)blockIdx.x * FWD_WARPS + w;
+  const int total = LIST ? __ldg(lv.count + wg) : -1;
+  if (LIST && total >= 0) {
+    // 32 entries at a time, their node records prefetched into the (unused)
+    // stack region with cp.async and read back as broadcast loads
+    const NodeRec* rb = reinterpret_cast<const NodeRec*>(stk[w]);
+    const uint32_t s_rb = (uint32_t)__cvta_generic_to_shared(stk[w]) + 48u * lane;
+    int chunk = (int)wg;
+    for (int base = 0; base < total; base += 32) {
+      if (base > 0 && base % IL_CHUNK == 0) chunk = __ldg(lv.next + chunk);
+      const uint2 my = il_load(lv, chunk, base, total, lane);
+      const int n = min(32, total - base);
+      __syncwarp();  // the previous window's records are consumed
+      if (lane < n) {
+        const NodeRec* r = tv.node_rec + (my.x & IL_NODE);
+        cp_async16(s_rb, &r->hi);
+        cp_async16(s_rb + 16u, &r->lo);
+        cp_async16(s_rb + 32u, &r->topo);
+      }
+      asm volatile("cp.async.wait_all;\n" ::: "memory");
+      __syncwarp();
+      for (int i = 0; i < n; ++i) {
+        const uint32_t src = __shfl_sync(FULL_MASK, my.x, i);
+        const unsigned m = __shfl_sync(FULL_MASK, my.y, i);
+        if (!((m >> lane) & 1u)) continue;
+        const int node = (int)(src & IL_NODE);
+        if (!(src & IL_LEAF)) {
+          const float4 hi = rb[i].hi, lo = rb[i].lo;
+          float dx, dy, dz;
+          const float s = dist2_df(hi, lo, qx, dx, dy, dz);
+          bool near;
+          f_interact<TD, TR, GRAD>(a, dx, dy, dz, s, lo.w, pdn + (int64_t)node * tv.F4,
+                                   prn + (int64_t)node * 4 * tv.F4, nd, nr, kp, near);
+        } else {
+          leaf(rb[i].topo);
+        }
+      }
+    }
+  }
+
+  int sp = (LIST && total >= 0) ? 0 : 1;
+  if (sp && lane == 0) stk[w][0] = make_int2(0, (int)active);
   __syncwarp();
   while (sp > 0) {
     --sp;
@@ -161,22 +227,7 @@ __global__ void __launch_bounds__(FWD_WARPS * 32)
     const unsigned openm = mask & ~farm;
     if (openm) {
       if (tp.y == 0) {
-        if ((openm >> lane) & 1u) {
-          for (int j = tp.z; j < tp.w; ++j) {
-            const PtRec* pr = tv.pt_rec + j;
-            const float4 ph = __ldg(&pr->hi);
-            const float r2 = dist2_df(ph, __ldg(&pr->lo), qx, dx, dy, dz);
-            // exact coincidence (fp64) is only possible when the fp32 r2 is 0
-            if (skip_coincident && r2 == 0.f && coincident_exact(tv.pt_pos64 + 3 * (size_t)j, xq))
-              continue;
-            bool near;
-            f_interact<TD, TR, GRAD>(a, dx, dy, dz, r2, ph.w,
-                                     pdp + (int64_t)j * tv.F4, prp + (int64_t)j * 4 * tv.F4,
-                                     nd, nr,
-                                     kp, near);
-            if (COUNT) near ? ++c_pn : ++c_pf;
-          }
-        }
+        if ((openm >> lane) & 1u) leaf(tp);
         __syncwarp();
       } else {
         if (sp + tp.y > DPL_STACK_PER_WARP) {
@@ -309,20 +360,28 @@ void morton_order(Tree& t, const double* xs_dev, int64_t q, int32_t* perm_out, D
 }
 
 // ---------------------------------------------------------------- dispatch
-template <int TD, int TR, int GRAD>
+// LISTS: also instantiate the list-replay kernel (used when a.ilist is set)
+template <int TD, int TR, int GRAD, bool LISTS = false>
 static void launch_one(const Tree& t, const KParams& kp, FwdArgs& a, int d0, int nd, int r0,
                        int nr) {
   TreeView tv = t.view();
   unsigned blocks = (unsigned)((a.q + FWD_WARPS * 32 - 1) / (FWD_WARPS * 32));
+  IListView lv{};
   auto run = [&](auto kern) {
     kern<<<blocks, FWD_WARPS * 32, 0, t.stream>>>(
-        tv, kp, t.node_row.as<float4>(), nullptr, t.pt_row.as<float4>(), nullptr, a.xs, a.perm, a.q, d0, nd, r0, nr, t.chmap.as<int>(), a.out,
-        a.out_stride, a.single, a.grad, a.counters, a.overflow);
+        tv, kp, t.node_row.as<float4>(), nullptr, t.pt_row.as<float4>(), nullptr, a.xs, a.perm,
+        a.q, d0, nd, r0, nr, t.chmap.as<int>(), a.out, a.out_stride, a.single, a.grad, a.counters,
+        lv, a.overflow);
   };
-  if (a.counters)
+  if (a.counters) {
     run(k_forward<TD, TR, GRAD, true>);
-  else
+  } else if (LISTS && a.ilist && !no_ilist()) {
+    ilist_build(t, *a.ilist, a.xs, a.perm, a.q, a.beta, ilist_near_thr(kp), a.overflow);
+    lv = a.ilist->view();
+    run(k_forward<TD, TR, GRAD, false, true>);
+  } else {
     run(k_forward<TD, TR, GRAD, false>);
+  }
   a.counters = nullptr;  // later tiles re-walk the same decisions: count once
   count_launch();
 }
@@ -353,7 +412,7 @@ void forward_launch(const Tree& t, const KParams& kp, FwdArgs a) {
   }
   if (a.grad_mode == 2) {  // values of all channels + gradient of dipole slot 0
     if (Cd < 1) throw Error(1, "grad0 requires a dipole channel 0");
-    if (Cd == 1 && Cr <= 4) return launch_one<1, 4, 2>(t, kp, a, 0, 1, 0, Cr);
+    if (Cd == 1 && Cr <= 4) return launch_one<1, 4, 2, true>(t, kp, a, 0, 1, 0, Cr);
     if (Cd == 1 && Cr <= 16) return launch_one<1, 16, 2>(t, kp, a, 0, 1, 0, Cr);
     if (Cd == 1 && Cr <= 48) return launch_one<1, 48, 2>(t, kp, a, 0, 1, 0, Cr);
     launch_one<1, 0, 2>(t, kp, a, 0, 1, 0, 0);
