@@ -28,12 +28,28 @@ struct FAcc {
   float gr[(GRAD == 1 && TR > 0) ? TR : 1][3];
 };
 
+// coeffs()'s tau = 1 branch (kernels.cpp:50-55, and the singular kernel), for
+// list entries whose far lanes are all beyond 6.5 eps (IL_NEAR clear)
+template <int ORDER>
+__device__ __forceinline__ Co far_coeffs(float r2) {
+  Co c;
+  const float inv_r = rsqrt_pos(r2);
+  const float inv_r2 = inv_r * inv_r;
+  c.R = inv_r2;
+  c.W = inv_r2 * inv_r;
+  c.Wp_r = ORDER >= 1 ? -3.0f * c.W * inv_r2 : 0.f;
+  c.Rp_r = ORDER >= 1 ? -2.0f * inv_r2 * inv_r2 : 0.f;
+  c.dW_de = c.dWp_r_de = c.dR_de = 0.f;
+  c.near = false;
+  return c;
+}
+
 template <int TD, int TR, int GRAD>
 __device__ __forceinline__ void f_interact(FAcc<TD, TR, GRAD>& a, float fx, float fy, float fz,
                                            float r2, float A, const float4* __restrict__ pd,
                                            const float* __restrict__ pr, int nd, int nr,
-                                           const KParams& kp, bool& near) {
-  Co c = coeffs<GRAD ? 1 : 0>(r2, kp);
+                                           const KParams& kp, bool& near, bool tau1 = false) {
+  Co c = tau1 ? far_coeffs<GRAD ? 1 : 0>(r2) : coeffs<GRAD ? 1 : 0>(r2, kp);
   near = c.near;
   const float aW = A * c.W, aR = A * c.R;
 #pragma unroll
@@ -96,9 +112,12 @@ __device__ __forceinline__ void cp_async16(uint32_t smem, const void* gmem) {
 // dipole slot 0 only (render step). single: write column 0 of a q x 1 output.
 // LIST: replay the batch's interaction lists (ilist.cuh; same entries in the
 // same order as the walk, so identical results); incomplete warps walk.
-template <int TD, int TR, int GRAD, bool COUNT, bool LIST = false>
+// SPEC: regularized kernel and a full tile (nd == TD, every radial slot of the
+// tile evaluated — rows are padded — and only the first nr stored), so the
+// mode and slot tests fold away
+template <int TD, int TR, int GRAD, bool COUNT, bool LIST = false, bool SPEC = false>
 __global__ void __launch_bounds__(FWD_WARPS * 32)
-    k_forward(TreeView tv, KParams kp, const float4* __restrict__ payd_n,
+    k_forward(TreeView tv, KParams kp_in, const float4* __restrict__ payd_n,
               const float* __restrict__ payr_n, const float4* __restrict__ payd_p,
               const float* __restrict__ payr_p, const double* __restrict__ xs,
               const int32_t* __restrict__ perm, int64_t q, int d0, int nd, int r0, int nr,
@@ -106,6 +125,9 @@ __global__ void __launch_bounds__(FWD_WARPS * 32)
               float* __restrict__ grad, long long* __restrict__ counters, IListView lv,
               int* overflow) {
   __shared__ __align__(16) int2 stk[FWD_WARPS][DPL_STACK_PER_WARP];
+  KParams kp = kp_in;
+  if (SPEC) kp.mode = KM_REGULARIZED;
+  const int ndi = SPEC ? TD : nd, nri = SPEC ? TR : nr;  // slots evaluated
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t sidx = ((int64_t)blockIdx.x * FWD_WARPS + w) * 32 + lane;
   const bool valid = sidx < q;
@@ -150,7 +172,7 @@ __global__ void __launch_bounds__(FWD_WARPS * 32)
         continue;
       bool near;
       f_interact<TD, TR, GRAD>(a, dx, dy, dz, r2, ph.w, pdp + (int64_t)j * tv.F4,
-                               prp + (int64_t)j * 4 * tv.F4, nd, nr, kp, near);
+                               prp + (int64_t)j * 4 * tv.F4, ndi, nri, kp, near);
       if (COUNT) near ? ++c_pn : ++c_pf;
     }
   };
@@ -187,7 +209,8 @@ __global__ void __launch_bounds__(FWD_WARPS * 32)
           const float s = dist2_df(hi, lo, qx, dx, dy, dz);
           bool near;
           f_interact<TD, TR, GRAD>(a, dx, dy, dz, s, lo.w, pdn + (int64_t)node * tv.F4,
-                                   prn + (int64_t)node * 4 * tv.F4, nd, nr, kp, near);
+                                   prn + (int64_t)node * 4 * tv.F4, ndi, nri, kp, near,
+                                   !(src & IL_NEAR));
         } else {
           leaf(rb[i].topo);
         }
@@ -220,7 +243,7 @@ __global__ void __launch_bounds__(FWD_WARPS * 32)
       bool near;
       f_interact<TD, TR, GRAD>(a, dx, dy, dz, s, lo.w,
                                pdn + (int64_t)node * tv.F4, prn + (int64_t)node * 4 * tv.F4,
-                               nd, nr,
+                               ndi, nri,
                                kp, near);
       if (COUNT) near ? ++c_fn : ++c_ff;
     }
@@ -378,7 +401,12 @@ static void launch_one(const Tree& t, const KParams& kp, FwdArgs& a, int d0, int
   } else if (LISTS && a.ilist && !no_ilist()) {
     ilist_build(t, *a.ilist, a.xs, a.perm, a.q, a.beta, ilist_near_thr(kp), a.overflow);
     lv = a.ilist->view();
-    run(k_forward<TD, TR, GRAD, false, true>);
+    if (kp.mode == KM_REGULARIZED && nd == TD && nr >= 1)
+      run(k_forward<TD, TR, GRAD, false, true, true>);
+    else
+      run(k_forward<TD, TR, GRAD, false, true>);
+  } else if (LISTS && kp.mode == KM_REGULARIZED && nd == TD && nr >= 1) {
+    run(k_forward<TD, TR, GRAD, false, false, true>);
   } else {
     run(k_forward<TD, TR, GRAD, false>);
   }

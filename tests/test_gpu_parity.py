@@ -277,6 +277,38 @@ def test_render_step_parity(eng, oracle_mod):
     assert np.abs(dbg - want["d_bg"]).max() <= 1e-4 * np.abs(want["d_bg"]).max() + 1e-8
 
 
+def test_render_steps_switch_to_lists(eng, oracle_mod):
+    """A render_backward after render_forward makes the next render step build
+    and replay interaction lists (the training pattern): the colours of the
+    listed step match the walked one (same entries in the same order; a lane
+    within an ulp of 6.5 eps may take the tau = 1 form), its gradients agree."""
+    from paper_2405_16788_b200 import renderer as Rn
+    from paper_2405_16788_b200 import workloads as W
+
+    O = oracle_mod
+    w = W.config3(scale=0.02)
+    c = w["cloud"]
+    t, _ = make(eng, O, c.positions, c.normals, c.areas, c.moments, w["kinds"])
+    eps = 1.5 * O.mean_knn_spacing(c.positions)
+    rays = w["rays"][:512]
+    rs = Rn.RenderSettings(t_near=2.0, t_far=6.0, seed=5)
+    p = eng.KernelParams(epsilon=eps)
+    d_rgb = np.full((rays.shape[0], 3), 1e-3, np.float32)
+    res = []
+    for _ in range(3):  # walk, lists, lists
+        rgb, tape = Rn.render_forward(t, p, rs, rays, 48)
+        buf = t.make_buffer()
+        dl, _ = Rn.render_backward(t, p, rs, tape, d_rgb, buf)
+        g = t.flush_gradients(buf)
+        res.append((rgb, g.moments, g.normals, g.d_epsilon, dl))
+    for rgb, mom, nrm, de, dl in res[1:]:
+        assert np.abs(rgb - res[0][0]).max() <= 1e-6 * np.abs(res[0][0]).max()
+        assert rel_scale_err(mom, res[0][1]) < 1e-6
+        assert rel_scale_err(nrm, res[0][2]) < 1e-6
+        assert abs(de - res[0][3]) <= 1e-6 * abs(res[0][3]) + 1e-12
+        assert abs(dl - res[0][4]) <= 1e-6 * abs(res[0][4]) + 1e-12
+
+
 @pytest.mark.parametrize("C", [2, 17, 33, 49, 65, 70])
 def test_many_channel_forward_adjoint(eng, oracle_mod, C):
     """Config-2 channel layouts (1 Dipole + C-1 Radial, N(0,1) moments and
