@@ -432,7 +432,7 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
                                : acc.node_v + 3 * src + k;
         bool use = is_point || k < 3;
         if (VR && k >= 4) {
-          dst = dptr[e] + (k - 4);
+          dst = (is_point ? acc.pt_mur : acc.node_s) + src * Cr + (k - 4);
           use = k - 4 < nr;
         }
         red_add_if(dst, (double)s, s != 0.f && use);
@@ -442,18 +442,19 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
     nent = 0;
   };
 
-  // VR: this lane's slots of the current entry — vector terms, d mu_0, and the
-  // radial products A R ds_c; the radial epsilon terms (:379, :409) are formed
-  // per lane from the source's first radial float4 (e_ != 0 only within 6.5 eps)
-  auto vr_store = [&](float r_, float e_, float v0, float v1, float v2, float v3,
-                      const float4* row) {
-    if (e_ != 0.f) {
-      const float4 rad = __ldg(row + 1);
-      eps_acc += (double)(e_ * fmaf(dsr[0], rad.x, fmaf(dsr[1], rad.y,
-                                                          fmaf(dsr[2], rad.z, dsr[3] * rad.w))));
-    }
+  // VR: the radial epsilon terms (:379, :409) of a lane within 6.5 eps, from the
+  // source's first radial float4 (called inside the near-field branches only)
+  auto vr_eps = [&](float e_, const float4* row) {
+    const float4 rad = __ldg(row + 1);
+    eps_acc += (double)(e_ * fmaf(dsr[0], rad.x, fmaf(dsr[1], rad.y,
+                                                        fmaf(dsr[2], rad.z, dsr[3] * rad.w))));
+  };
+  // VR: this lane's slots of the current entry — vector terms, d mu_0 (points),
+  // and the radial products A R ds_c
+  auto vr_store = [&](float r_, float v0, float v1, float v2, float v3, bool point) {
     float* vqe = vq + nent * 32 * VQ;
-    vqe[lane] = v0, vqe[32 + lane] = v1, vqe[64 + lane] = v2, vqe[96 + lane] = v3;
+    vqe[lane] = v0, vqe[32 + lane] = v1, vqe[64 + lane] = v2;
+    if (point) vqe[96 + lane] = v3;  // slot 3 is never read for nodes
     vqe[128 + lane] = r_ * dsr[0], vqe[160 + lane] = r_ * dsr[1];
     vqe[192 + lane] = r_ * dsr[2], vqe[224 + lane] = r_ * dsr[3];
   };
@@ -489,6 +490,7 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
           nr_ = c.near;
           r_ = A * c.R;
           e_ = A * c.dR_de;
+          if (VR && e_ != 0.f) vr_eps(e_, tv.node_row + (size_t)node * F4g);
           const float aWds = A * c.W * ds0;
           u0 = aWds * fx, u1 = aWds * fy, u2 = aWds * fz;
           if (c.near) {
@@ -525,6 +527,7 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
           nr_ = c.near;
           r_ = A * c.R;
           e_ = A * c.dR_de;
+          if (VR && e_ != 0.f) vr_eps(e_, tv.node_row + (size_t)node * F4g);
           const float aWds = A * c.W * ds0;
           u0 = aWds * fx, u1 = aWds * fy, u2 = aWds * fz;
           const float4 v = __ldg(tv.node_row + (size_t)node * F4g);
@@ -543,11 +546,8 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
       }
     }
     if constexpr (VR) {
-      vr_store(r_, e_, u0, u1, u2, 0.f, tv.node_row + (size_t)node * F4g);
-      if (lane == 0) {
-        meta[nent] = node;
-        dptr[nent] = acc.node_s + (size_t)node * Cr;
-      }
+      vr_store(r_, u0, u1, u2, 0.f, false);
+      if (lane == 0) meta[nent] = node;
       ++nent;
       return;
     }
@@ -583,6 +583,7 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
           nr_ = c.near;
           r_ = Am * c.R;
           e_ = Am * c.dR_de;
+          if (VR && e_ != 0.f) vr_eps(e_, tv.pt_row + (size_t)j * F4g);
           const float mu = __ldg(tv.pt_mu + j);
           const float nx = __ldg(tv.pt_nrm + 3 * (size_t)j), ny = __ldg(tv.pt_nrm + 3 * (size_t)j + 1),
                       nz = __ldg(tv.pt_nrm + 3 * (size_t)j + 2);
@@ -606,11 +607,8 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
         }
       }
       if constexpr (VR) {
-        vr_store(r_, e_, n0, n1, n2, dmu, tv.pt_row + (size_t)j * F4g);
-        if (lane == 0) {
-          meta[nent] = j | (1 << 30);
-          dptr[nent] = acc.pt_mur + (size_t)j * Cr;
-        }
+        vr_store(r_, n0, n1, n2, dmu, true);
+        if (lane == 0) meta[nent] = j | (1 << 30);
         ++nent;
         continue;
       }

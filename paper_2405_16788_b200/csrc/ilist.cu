@@ -74,14 +74,16 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
   const double* xq = xs + 3 * qi;
 
   int cur = (int)wg;  // chunk being filled (warp w owns chunk w)
-  int total = 0;      // entries written
-  int room = IL_CHUNK;  // free slots in the current chunk
-  uint2* wp = pool + (size_t)cur * IL_CHUNK;
+  int total = 0;      // entries written to the pool
   bool ok = true;
-  // lane 0 appends each entry with one 8-byte store through a running pointer
-  // (a warp's entries are contiguous within a chunk: L2 merges full sectors)
-  auto emit = [&](uint32_t src, uint32_t m) {
-    if (room == 0) {  // chunk full: link a fresh one
+  // entries are collected in registers — lane k holds entry k of the current
+  // block of 32 — and written as one coalesced 256-byte store per block (a
+  // chunk holds 4 blocks, so a block never straddles two chunks)
+  uint2 pend = make_uint2(0u, 0u);
+  int npend = 0;
+  auto flush = [&]() {
+    const int b = total >> 5;  // block index: total is a multiple of 32 here
+    if (b > 0 && (b & 3) == 0) {  // chunk full: link a fresh one
       unsigned long long c = 0;
       if (lane == 0) c = atomicAdd(ctr, 1ull);
       c = __shfl_sync(FULL_MASK, c, 0);
@@ -91,13 +93,14 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
       }
       if (lane == 0) next[cur] = (int)c;
       cur = (int)c;
-      wp = pool + (size_t)cur * IL_CHUNK;
-      room = IL_CHUNK;
     }
-    if (lane == 0) *wp = make_uint2(src, m);
-    ++wp;
-    --room;
-    ++total;
+    if (lane < npend) pool[(size_t)cur * IL_CHUNK + (b & 3) * 32 + lane] = pend;
+    total += npend;
+    npend = 0;
+  };
+  auto emit = [&](uint32_t src, uint32_t m) {
+    if (lane == npend) pend = make_uint2(src, m);
+    if (++npend == 32) flush();
   };
 
   int sp = 1;
@@ -137,6 +140,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
       }
     }
   }
+  if (ok && npend) flush();
   if (lane == 0) count[wg] = ok ? total : -1;
 }
 
