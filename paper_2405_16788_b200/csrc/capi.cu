@@ -1189,7 +1189,7 @@ int dpl_render_forward(dpl_tree_t h, const dpl_kernel_params* params, const dpl_
     }
     Out<float> o;
     o.bind(t, rgb, R * 3, h->ws_out);
-    tape->tape.reserve(Q * 64);
+    tape->tape.reserve(Q * 16 + R * 8);  // T_j, p_j per sample; sum p per ray
     double bg[3] = {rp->background[0], rp->background[1], rp->background[2]};
     render_composite(t.stream, tape->rays.as<double>(), R, S, tape->ts.as<double>(),
                      tape->has_deltas ? tape->deltas.as<double>() : nullptr, rp->t_near,
@@ -1231,8 +1231,12 @@ int dpl_render_backward(dpl_tree_t h, const dpl_kernel_params* params, const dpl
     DPL_CUDA(cudaMemsetAsync(tape->sums.p, 0, 32, t.stream));
     double bg[3] = {rp->background[0], rp->background[1], rp->background[2]};
     if (mlp) tape->d_raw.reserve(Q * 12);
-    render_backward_rays(t.stream, tape->rays.as<double>(), R, S, tape->tape.as<double>(), drgb_d,
-                         rp->lambda_scale, bg, tape->dout.as<float>(), ds,
+    render_backward_rays(t.stream, tape->rays.as<double>(), R, S, tape->ts.as<double>(),
+                         tape->has_deltas ? tape->deltas.as<double>() : nullptr, tape->t_near,
+                         tape->vals.as<float>(), tape->vstride,
+                         mlp ? tape->head_raw.as<float>() : nullptr, tape->g0.as<float>(),
+                         tape->tape.as<double>(), drgb_d, rp->lambda_scale, bg,
+                         tape->dout.as<float>(), ds,
                          mlp ? tape->d_raw.as<float>() : nullptr, tape->dgrad.as<float>(),
                          tape->sums.as<double>());
     if (mlp) {  // head backward (radiance.cpp:176-179) -> appearance / normal adjoints

@@ -68,39 +68,58 @@ __device__ __forceinline__ double logistic_d(double x) {  // radiance.cpp:30-38
   return e / (1.0 + e);
 }
 
-// one thread per ray: composite (renderer.cpp:120-168)
+// Per-sample inputs of the composite, re-read (not taped) by the backward:
+// f = 1/2 - D_0, s = dir . grad f, the head colours and delta — the same
+// expressions in both kernels, so the backward sees the forward's exact values.
+struct SampleIn {
+  double f, s, h0, h1, h2, delta;
+};
+__device__ __forceinline__ SampleIn sample_in(const double* dir, int64_t g, double t, double prev,
+                                              const double* __restrict__ deltas,
+                                              const float* __restrict__ vals, int vstride,
+                                              const float* __restrict__ head_raw,
+                                              const float* __restrict__ g0) {
+  SampleIn a;
+  a.delta = deltas ? deltas[g] : t - prev;  // delta_0 = t_0 - t_near (renderer.hpp:324)
+  a.f = 0.5 - (double)vals[(int64_t)vstride * g];
+  const double gx = -(double)g0[3 * g], gy = -(double)g0[3 * g + 1], gz = -(double)g0[3 * g + 2];
+  a.s = (dir[0] * gx + dir[1] * gy) + dir[2] * gz;
+  // head rgb: logistic of the direct-rgb channels 1..3 (radiance.cpp:133-145)
+  // or of the tiny-MLP's raw outputs (:153-154)
+  const float* hr = head_raw ? head_raw + 3 * g : vals + (int64_t)vstride * g + 1;
+  a.h0 = logistic_d(hr[0]), a.h1 = logistic_d(hr[1]), a.h2 = logistic_d(hr[2]);
+  return a;
+}
+
+// one thread per ray: composite (renderer.cpp:120-168). The tape keeps only
+// the sequential state per sample — T_j and p_j — plus sum_j p_j per ray
+// (tape + 2 RS); everything else is recomputed from the forward's outputs.
 __global__ void k_composite(const double* __restrict__ rays, int64_t R, int S,
                             const double* __restrict__ ts, const double* __restrict__ deltas,
                             double t_near,
                             const float* __restrict__ vals /* RS x vstride */, int vstride,
                             const float* __restrict__ head_raw /* RS x 3 or null */,
                             const float* __restrict__ g0 /* RS x 3 */, double lambda, double bg0,
-                            double bg1, double bg2, double* tape /* RS x 8 */, float* rgb_out) {
+                            double bg1, double bg2, double* tape /* RS x 2 + R */, float* rgb_out) {
   int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (r >= R) return;
   const double* dir = rays + 6 * r + 3;
-  double trans = 1.0, c0 = 0, c1 = 0, c2 = 0, prev = t_near;
+  double trans = 1.0, c0 = 0, c1 = 0, c2 = 0, prev = t_near, sum_p = 0;
+#pragma unroll 4
   for (int j = 0; j < S; ++j) {
     int64_t g = r * S + j;
     double t = ts[g];
-    double delta = deltas ? deltas[g] : t - prev;  // delta_0 = t_0 - t_near (renderer.hpp:324)
+    const SampleIn a = sample_in(dir, g, t, prev, deltas, vals, vstride, head_raw, g0);
     prev = t;
-    double f = 0.5 - (double)vals[(int64_t)vstride * g];
-    double gx = -(double)g0[3 * g], gy = -(double)g0[3 * g + 1], gz = -(double)g0[3 * g + 2];
-    double s = (dir[0] * gx + dir[1] * gy) + dir[2] * gz;
-    double sigma = lambda * hazard(lambda * f) * fabs(s);
-    // head rgb: logistic of the direct-rgb channels 1..3 (radiance.cpp:133-145)
-    // or of the tiny-MLP's raw outputs (:153-154)
-    const float* hr = head_raw ? head_raw + 3 * g : vals + (int64_t)vstride * g + 1;
-    double h0 = logistic_d(hr[0]), h1 = logistic_d(hr[1]), h2 = logistic_d(hr[2]);
-    double E = exp(-sigma * delta);
+    double sigma = lambda * hazard(lambda * a.f) * fabs(a.s);
+    double E = exp(-sigma * a.delta);
     double p = trans * (1.0 - E);
-    c0 += p * h0, c1 += p * h1, c2 += p * h2;
-    double* tp = tape + 8 * g;
-    tp[0] = f, tp[1] = s, tp[2] = trans, tp[3] = p, tp[4] = h0, tp[5] = h1, tp[6] = h2;
-    tp[7] = delta;
+    c0 += p * a.h0, c1 += p * a.h1, c2 += p * a.h2;
+    sum_p += p;
+    reinterpret_cast<double2*>(tape)[g] = make_double2(trans, p);
     trans *= E;
   }
+  tape[2 * R * S + r] = sum_p;
   rgb_out[3 * r] = (float)(c0 + trans * bg0);
   rgb_out[3 * r + 1] = (float)(c1 + trans * bg1);
   rgb_out[3 * r + 2] = (float)(c2 + trans * bg2);
@@ -108,6 +127,9 @@ __global__ void k_composite(const double* __restrict__ rays, int64_t R, int S,
 
 // one thread per ray: render_ray_backward up to the tree adjoint (:184-228)
 __global__ void k_backward_ray(const double* __restrict__ rays, int64_t R, int S,
+                               const double* __restrict__ ts, const double* __restrict__ deltas,
+                               double t_near, const float* __restrict__ vals, int vstride,
+                               const float* __restrict__ head_raw, const float* __restrict__ g0,
                                const double* __restrict__ tape, const float* __restrict__ d_rgb,
                                double lambda, double bg0, double bg1, double bg2,
                                float* d_out /* RS x dstride */, int dstride,
@@ -119,20 +141,23 @@ __global__ void k_backward_ray(const double* __restrict__ rays, int64_t R, int S
   if (r < R) {
     const double* dir = rays + 6 * r + 3;
     double dr0 = d_rgb[3 * r], dr1 = d_rgb[3 * r + 1], dr2 = d_rgb[3 * r + 2];
-    double sum_p = 0;
-    for (int j = 0; j < S; ++j) sum_p += tape[8 * (r * S + j) + 3];
+    const double sum_p = tape[2 * R * S + r];  // summed in sample order by the composite
     db0 = (1.0 - sum_p) * dr0, db1 = (1.0 - sum_p) * dr1, db2 = (1.0 - sum_p) * dr2;
     double suffix = 0;
+#pragma unroll 4
     for (int j = S - 1; j >= 0; --j) {
       int64_t g = r * S + j;
-      const double* tp = tape + 8 * g;
-      double dp = (dr0 * (tp[4] - bg0) + dr1 * (tp[5] - bg1)) + dr2 * (tp[6] - bg2);
-      double trans = tp[2], p = tp[3];
+      const double t = ts[g];
+      const double prev = j > 0 ? ts[g - 1] : t_near;
+      const SampleIn a = sample_in(dir, g, t, prev, deltas, vals, vstride, head_raw, g0);
+      const double2 tp = reinterpret_cast<const double2*>(tape)[g];
+      double dp = (dr0 * (a.h0 - bg0) + dr1 * (a.h1 - bg1)) + dr2 * (a.h2 - bg2);
+      double trans = tp.x, p = tp.y;
       double E = trans > 0 ? 1.0 - p / trans : 0.0;
-      double dsig = tp[7] * (trans * E * dp - suffix);
+      double dsig = a.delta * (trans * E * dp - suffix);
       suffix += p * dp;
       // hazard chain rule (:213-221)
-      double f = tp[0], s = tp[1];
+      double f = a.f, s = a.s;
       double u = lambda * f;
       double haz = hazard(u);
       double dhaz = -u * haz - haz * haz;
@@ -148,9 +173,9 @@ __global__ void k_backward_ray(const double* __restrict__ rays, int64_t R, int S
       // head backward d_raw = d_radiance * rgb (1 - rgb) (radiance.cpp:166): the
       // direct-rgb head's channel adjoints, or the tiny-MLP's output adjoint
       float* dr = d_raw ? d_raw + 3 * g : d_out + (int64_t)dstride * g + 1;
-      dr[0] = (float)(p * dr0 * tp[4] * (1.0 - tp[4]));
-      dr[1] = (float)(p * dr1 * tp[5] * (1.0 - tp[5]));
-      dr[2] = (float)(p * dr2 * tp[6] * (1.0 - tp[6]));
+      dr[0] = (float)(p * dr0 * a.h0 * (1.0 - a.h0));
+      dr[1] = (float)(p * dr1 * a.h1 * (1.0 - a.h1));
+      dr[2] = (float)(p * dr2 * a.h2 * (1.0 - a.h2));
     }
   }
   // warp-reduce the ray sums, one fp64 atomic per warp and quantity
@@ -216,12 +241,14 @@ void render_composite(cudaStream_t s, const double* rays, int64_t R, int S, cons
   count_launch();
 }
 
-void render_backward_rays(cudaStream_t s, const double* rays, int64_t R, int S,
-                          const double* tape, const float* d_rgb, double lambda, const double* bg,
-                          float* d_out, int dstride, float* d_raw, float* d_grad0, double* sums) {
-  k_backward_ray<<<(unsigned)((R + 127) / 128), 128, 0, s>>>(rays, R, S, tape, d_rgb, lambda, bg[0],
-                                                            bg[1], bg[2], d_out, dstride, d_raw,
-                                                            d_grad0, sums);
+void render_backward_rays(cudaStream_t s, const double* rays, int64_t R, int S, const double* ts,
+                          const double* deltas, double t_near, const float* vals, int vstride,
+                          const float* head_raw, const float* g0, const double* tape,
+                          const float* d_rgb, double lambda, const double* bg, float* d_out,
+                          int dstride, float* d_raw, float* d_grad0, double* sums) {
+  k_backward_ray<<<(unsigned)((R + 127) / 128), 128, 0, s>>>(
+      rays, R, S, ts, deltas, t_near, vals, vstride, head_raw, g0, tape, d_rgb, lambda, bg[0],
+      bg[1], bg[2], d_out, dstride, d_raw, d_grad0, sums);
   count_launch();
 }
 

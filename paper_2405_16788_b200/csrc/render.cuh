@@ -16,9 +16,13 @@ void render_composite(cudaStream_t s, const double* rays, int64_t R, int S, cons
                       double* tape, float* rgb);
 // d_out: RS x dstride adjoint inputs; d_raw: RS x 3 head output adjoints for the
 // tiny-MLP (null: written into d_out channels 1..3, the direct-rgb head)
-void render_backward_rays(cudaStream_t s, const double* rays, int64_t R, int S,
-                          const double* tape, const float* d_rgb, double lambda, const double* bg,
-                          float* d_out, int dstride, float* d_raw, float* d_grad0, double* sums);
+// (ts, deltas, vals, head_raw, g0: the forward's inputs, re-read per sample;
+// tape: T_j, p_j per sample and sum_j p_j per ray from render_composite)
+void render_backward_rays(cudaStream_t s, const double* rays, int64_t R, int S, const double* ts,
+                          const double* deltas, double t_near, const float* vals, int vstride,
+                          const float* head_raw, const float* g0, const double* tape,
+                          const float* d_rgb, double lambda, const double* bg, float* d_out,
+                          int dstride, float* d_raw, float* d_grad0, double* sums);
 // tiny-MLP input adjoint -> tree adjoint inputs for samples [q0, q0 + q): appearance
 // channels into d_out (stride C), the implicit-normal term into d_grad0
 // (renderer.cpp:206-211, 226-227)

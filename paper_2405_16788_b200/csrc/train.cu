@@ -23,20 +23,26 @@ __device__ __forceinline__ double adam1(double p, double g, double& m, double& v
   return __dsub_rn(p, step);
 }
 
-// one thread per point (original order)
-__global__ void k_point_adam(int64_t n, int C, double* __restrict__ mu, double* __restrict__ nrm,
-                             const float* __restrict__ g_mu, const float* __restrict__ g_n,
-                             double* __restrict__ m_mu, double* __restrict__ v_mu,
-                             double* __restrict__ m_n, double* __restrict__ v_n, double lr,
-                             double b1, double b2, double eps, double c1, double c2) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  for (int c = 0; c < C; ++c) {
-    const int64_t k = i * C + c;
+// appearance / geometry moments: one thread per (point, channel) element,
+// coalesced (the groups are elementwise, optimizer.cpp:65-81)
+__global__ void k_moment_adam(int64_t nm, double* __restrict__ mu, const float* __restrict__ g_mu,
+                              double* __restrict__ m_mu, double* __restrict__ v_mu, double lr,
+                              double b1, double b2, double eps, double c1, double c2) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nm;
+       k += (int64_t)gridDim.x * blockDim.x) {
     double m = m_mu[k], v = v_mu[k];
     mu[k] = adam1(mu[k], (double)g_mu[k], m, v, lr, b1, b2, eps, c1, c2);
     m_mu[k] = m, v_mu[k] = v;
   }
+}
+
+// raw normals: one thread per point (original order), renormalised only when
+// the update changed them (optimizer.cpp:196-200)
+__global__ void k_normal_adam(int64_t n, double* __restrict__ nrm, const float* __restrict__ g_n,
+                              double* __restrict__ m_n, double* __restrict__ v_n, double lr,
+                              double b1, double b2, double eps, double c1, double c2) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
   double old[3], nw[3];
   for (int a = 0; a < 3; ++a) {
     const int64_t k = 3 * i + a;
@@ -69,10 +75,11 @@ void point_adam_step(Tree& t, PointAdam& o, const float* g_mu, const float* g_n,
   const double c2 = 1.0 - std::pow(b2, (double)o.t);
   size_t nm = (size_t)t.n * t.C, nn = (size_t)t.n * 3;
   double* s = o.state.as<double>();
-  k_point_adam<<<(unsigned)((t.n + 255) / 256), 256, 0, t.stream>>>(
-      t.n, t.C, t.mu64.as<double>(), t.nrm64.as<double>(), g_mu, g_n, s, s + nm, s + 2 * nm,
-      s + 2 * nm + nn, lr, b1, b2, eps, c1, c2);
-  count_launch();
+  k_moment_adam<<<148 * 16, 256, 0, t.stream>>>((int64_t)nm, t.mu64.as<double>(), g_mu, s,
+                                                 s + nm, lr, b1, b2, eps, c1, c2);
+  k_normal_adam<<<(unsigned)((t.n + 255) / 256), 256, 0, t.stream>>>(
+      t.n, t.nrm64.as<double>(), g_n, s + 2 * nm, s + 2 * nm + nn, lr, b1, b2, eps, c1, c2);
+  count_launch(2);
   DPL_CUDA(cudaGetLastError());
   tree_compute_moments(t);  // update_moments (bhtree.cpp:171-176)
 }
