@@ -6,10 +6,11 @@
 // per batch of ENT entries:
 //     out[32 queries x TR radial] += Wr[32 x ENT] . Rows[ENT x TR]
 // with Wr[l][e] = A R of lane l for entry e (0 when lane l does not take e).
-// Each operand is split a = hi + lo (hi = tf32(a), lo = tf32(a - hi)) and
-// hi.hi + hi.lo + lo.hi is accumulated in fp32 (error ~2^-21 relative per
-// product, i.e. fp32-class; the dropped lo.lo term is < 2^-22). The dipole
-// slot (3 FMA per entry) stays on the FP32 pipe.
+// Each operand is split a = hi + lo (hi = a truncated to tf32, lo = a - hi
+// exact, read by the tensor core at tf32 precision) and hi.hi + hi.lo + lo.hi
+// is accumulated in fp32 (error <~ 2^-19 relative per product; the dropped
+// lo.lo term is < 2^-20). The dipole slot (3 FMA per entry) stays on the FP32
+// pipe.
 // Shared-memory strides are padded so every fragment load is bank-conflict
 // free: weights Wr[ENT][40], rows [ENT][RSF] with RSF = 8 or 24 mod 32 floats.
 #include "forward.cuh"
@@ -27,15 +28,12 @@ __device__ __forceinline__ void cp_async_wait_all() {
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
-// cvt.rna.tf32.f32 for finite a (round to nearest, ties away: add half a tf32
-// ulp to the magnitude bits, truncate): 2 integer ops instead of the 4 that the
-// cvt lowers to on sm_100 (its inf / NaN guard is not needed here)
-__device__ __forceinline__ uint32_t to_tf32(float a) {
-  return (__float_as_uint(a) + 0x1000u) & 0xffffe000u;
-}
+// a = hi + lo with hi = a truncated to tf32 (exact residual lo, |lo| < 2^-10 |a|);
+// lo goes to the MMA as raw fp32 bits — the tensor core reads its top 19 bits,
+// an error <= 2^-10 |lo| <= 2^-20 |a|. 2 instructions instead of 2 roundings.
 __device__ __forceinline__ void split_tf32(float a, uint32_t& hi, uint32_t& lo) {
-  hi = to_tf32(a);
-  lo = to_tf32(a - __uint_as_float(hi));
+  hi = __float_as_uint(a) & 0xffffe000u;
+  lo = __float_as_uint(a - __uint_as_float(hi));
 }
 __device__ __forceinline__ void mma_tf32(float (&c)[4], const uint32_t (&a)[4], uint32_t b0,
                                          uint32_t b1) {
