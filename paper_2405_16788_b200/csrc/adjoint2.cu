@@ -477,12 +477,12 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
       // branch, so a batch without near lanes never issues it
       const bool slow = far && !(kp.mode == KM_SINGULAR ||
                                  (kp.mode == KM_REGULARIZED && s >= kp.near2));
-      if (far) {
+      {  // branch-free: every lane evaluates, non-far lanes select 0
         const float inv_r = rsqrt_pos(s);
         const float R = inv_r * inv_r;
-        r_ = A * R;
         const float aWds = A * (R * inv_r) * ds0;
-        u0 = aWds * fx, u1 = aWds * fy, u2 = aWds * fz;
+        r_ = far ? A * R : 0.f;
+        u0 = far ? aWds * fx : 0.f, u1 = far ? aWds * fy : 0.f, u2 = far ? aWds * fz : 0.f;
       }
       if (hint != 0 && (hint > 0 || __any_sync(FULL_MASK, slow))) {
         if (slow) {
@@ -507,19 +507,18 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
       // warp-uniform branch for the near lanes only
       const bool slow = far && !(kp.mode == KM_SINGULAR ||
                                  (kp.mode == KM_REGULARIZED && s >= kp.near2));
-      if (far) {
+      {  // branch-free: every lane evaluates, non-far lanes select 0
         const float inv_r = rsqrt_pos(s);
         const float R = inv_r * inv_r;
         const float W = R * inv_r;
         const float Wp_r = -3.0f * W * R;
-        r_ = A * R;
         const float aWds = A * W * ds0;
-        u0 = aWds * fx, u1 = aWds * fy, u2 = aWds * fz;
         const float gd = fmaf(dg0, fx, fmaf(dg1, fy, dg2 * fz));  // :372-374
         const float t = Wp_r * gd;
-        u0 -= A * fmaf(W, dg0, t * fx);
-        u1 -= A * fmaf(W, dg1, t * fy);
-        u2 -= A * fmaf(W, dg2, t * fz);
+        r_ = far ? A * R : 0.f;
+        u0 = far ? aWds * fx - A * fmaf(W, dg0, t * fx) : 0.f;
+        u1 = far ? aWds * fy - A * fmaf(W, dg1, t * fy) : 0.f;
+        u2 = far ? aWds * fz - A * fmaf(W, dg2, t * fz) : 0.f;
       }
       if (hint != 0 && (hint > 0 || __any_sync(FULL_MASK, slow))) {
         if (slow) {

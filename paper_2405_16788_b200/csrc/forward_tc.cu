@@ -224,11 +224,13 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
           const float4 hi = rb[i].hi, lo = rb[i].lo;
           float dx, dy, dz;
           const float s = dist2_df(hi, lo, qx, dx, dy, dz);
-          float4 wv = make_float4(0.f, 0.f, 0.f, 0.f);
+          float4 wv;
           if (src & IL_NEAR) {
-            if (mine) wv = fwd_w(dx, dy, dz, s, lo.w, kp);
-          } else if (mine) {
-            wv = fwd_w_far(dx, dy, dz, s, lo.w);
+            wv = mine ? fwd_w(dx, dy, dz, s, lo.w, kp) : make_float4(0.f, 0.f, 0.f, 0.f);
+          } else {  // branch-free: every lane evaluates, non-members select 0
+            const float4 f = fwd_w_far(dx, dy, dz, s, lo.w);
+            wv.x = mine ? f.x : 0.f, wv.y = mine ? f.y : 0.f;
+            wv.z = mine ? f.z : 0.f, wv.w = mine ? f.w : 0.f;
           }
           append(wv, node_row + (size_t)node * F4g);
         } else {
