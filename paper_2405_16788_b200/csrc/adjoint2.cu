@@ -546,22 +546,21 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
     }
     if constexpr (VR) {
       vr_store(r_, u0, u1, u2, 0.f, false);
-      if (lane == 0) meta[nent] = node;
+      meta[nent] = node;  // every lane stores the same word: no branch
       ++nent;
       return;
     }
     wR[nent * WS + lane] = r_;
-    wE[nent * WS + lane] = e_;
     float* vqe = vq + nent * 128;
     vqe[lane] = u0, vqe[32 + lane] = u1, vqe[64 + lane] = u2;  // slot 3 (d mu_0) is never read for nodes
     const bool any_near = hint != 0 && __any_sync(FULL_MASK, nr_);
     if (any_near) {  // warp-uniform; rare beyond the first tree levels
+      wE[nent * WS + lane] = e_;  // read by phase B for near entries only
       if (lane < F4c) cp_async16(s_rows + 16u * F4 * nent, tv.node_row + (size_t)node * F4g + lane);
     }
-    if (lane == 0) {
-      meta[nent] = node | (any_near ? (1 << 29) : 0);
-      dptr[nent] = acc.node_s + (size_t)node * Cr;
-    }
+    // every lane stores the same words: no branch
+    meta[nent] = node | (any_near ? (1 << 29) : 0);
+    dptr[nent] = acc.node_s + (size_t)node * Cr;
     ++nent;
   };
   // the points of an opened leaf for the lanes in `me_open` (:382-412)
@@ -607,22 +606,20 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
       }
       if constexpr (VR) {
         vr_store(r_, n0, n1, n2, dmu, true);
-        if (lane == 0) meta[nent] = j | (1 << 30);
+        meta[nent] = j | (1 << 30);
         ++nent;
         continue;
       }
       wR[nent * WS + lane] = r_;
-      wE[nent * WS + lane] = e_;
       float* vqe = vq + nent * 128;
       vqe[lane] = n0, vqe[32 + lane] = n1, vqe[64 + lane] = n2, vqe[96 + lane] = dmu;
       const bool any_near = __any_sync(FULL_MASK, nr_);
       if (any_near) {
+        wE[nent * WS + lane] = e_;
         if (lane < F4c) cp_async16(s_rows + 16u * F4 * nent, tv.pt_row + (size_t)j * F4g + lane);
       }
-      if (lane == 0) {
-        meta[nent] = j | (1 << 30) | (any_near ? (1 << 29) : 0);
-        dptr[nent] = acc.pt_mur + (size_t)j * Cr;
-      }
+      meta[nent] = j | (1 << 30) | (any_near ? (1 << 29) : 0);
+      dptr[nent] = acc.pt_mur + (size_t)j * Cr;
       ++nent;
     }
   };
