@@ -383,9 +383,12 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
         float sB = pB.x + pB.y;
         if (NB == 1) sB += __shfl_xor_sync(FULL_MASK, sB, 16);
         double* dst_s = dptr[e];
-        red_add_if(dst_s + lane, (double)sA, okA && sA != 0.f);
+        if (NB > 0)  // nr > 32: every lane owns an A channel; no predicate, no branch
+          red_add_f32(dst_s + lane, sA);
+        else
+          red_add_f32_if(dst_s + lane, sA, okA && sA != 0.f);
         const bool ownB = NB == 2 ? okB : (NB == 1 ? (okB && lane < 16) : false);
-        if (NB > 0) red_add_if(dst_s + slotB, (double)sB, ownB && sB != 0.f);
+        if (NB > 0) red_add_f32_if(dst_s + slotB, sB, ownB && sB != 0.f);
         if (near) {  // radial epsilon terms (:379, :409)
           const float4* we4 = reinterpret_cast<const float4*>(wE + e * WS);
           float eA = 0.f, eB = 0.f;

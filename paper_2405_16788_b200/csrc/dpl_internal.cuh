@@ -118,6 +118,21 @@ __device__ __forceinline__ void red_add_if(double* p, double v, bool pred) {
       : "memory");
 }
 
+// fp32 value added to an fp64 accumulator: conversion and RED in one predicated
+// PTX block (keeps ptxas from branching around the pair)
+__device__ __forceinline__ void red_add_f32_if(double* p, float v, bool pred) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\t.reg .f64 d;\n\tsetp.ne.b32 q, %2, 0;\n\t"
+      "cvt.f64.f32 d, %1;\n\t@q red.global.add.f64 [%0], d;\n\t}\n" ::"l"(p),
+      "f"(v), "r"((int)pred)
+      : "memory");
+}
+__device__ __forceinline__ void red_add_f32(double* p, float v) {
+  asm volatile("{\n\t.reg .f64 d;\n\tcvt.f64.f32 d, %1;\n\tred.global.add.f64 [%0], d;\n\t}\n" ::"l"(p),
+               "f"(v)
+               : "memory");
+}
+
 #endif
 
 }  // namespace dpl
