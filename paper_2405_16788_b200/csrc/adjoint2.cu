@@ -161,6 +161,7 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
   constexpr int F4 = L::F4;
   constexpr int WS = L::WS;
   static_assert(MT == 0 || ENT == 8, "tensor-core phase B uses one n-tile of 8 entries");
+  static_assert((ENT & (ENT - 1)) == 0 && ENT <= 32, "ENT: a power of two <= 32");
   extern __shared__ float4 smem_f4[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int g = lane >> 2, tq = lane & 3;  // mma fragment coordinates
@@ -355,7 +356,6 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
     for (int e = 0; e < nent; ++e) {
       const int m = meta[e];
       if constexpr (FF && !VR) {
-        const bool near = m & (1 << 29);
         const float4* wr4 = reinterpret_cast<const float4*>(wR + e * WS);
         // even / odd query partial sums on the packed FMA pipe (FFMA2)
         float2 pA = make_float2(0.f, 0.f), pB = make_float2(0.f, 0.f);
@@ -389,29 +389,37 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
           red_add_f32_if(dst_s + lane, sA, okA && sA != 0.f);
         const bool ownB = NB == 2 ? okB : (NB == 1 ? (okB && lane < 16) : false);
         if (NB > 0) red_add_f32_if(dst_s + slotB, sB, ownB && sB != 0.f);
-        if (near) {  // radial epsilon terms (:379, :409)
-          const float4* we4 = reinterpret_cast<const float4*>(wE + e * WS);
-          float eA = 0.f, eB = 0.f;
+      }
+    }
+    if constexpr (FF && !VR) {
+      // radial epsilon terms (:379, :409) of the batch's near entries, out of
+      // the main loop so it carries no per-entry branch
+      unsigned nm = __ballot_sync(FULL_MASK, lane < nent && ((meta[lane & (ENT - 1)] >> 29) & 1));
+      while (nm) {
+        const int e = __ffs(nm) - 1;
+        nm &= nm - 1;
+        const bool ownB = NB == 2 ? okB : (NB == 1 ? (okB && lane < 16) : false);
+        const float4* we4 = reinterpret_cast<const float4*>(wE + e * WS);
+        float eA = 0.f, eB = 0.f;
 #pragma unroll
-          for (int l4 = 0; l4 < 8; ++l4) {
-            const float4 ww = we4[l4];
-            const float wv[4] = {ww.x, ww.y, ww.z, ww.w};
+        for (int l4 = 0; l4 < 8; ++l4) {
+          const float4 ww = we4[l4];
+          const float wv[4] = {ww.x, ww.y, ww.z, ww.w};
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              eA = fmaf(wv[u], colA[4 * l4 + u], eA);
-              if (NB == 2) eB = fmaf(wv[u], colB[4 * l4 + u], eB);
-            }
+          for (int u = 0; u < 4; ++u) {
+            eA = fmaf(wv[u], colA[4 * l4 + u], eA);
+            if (NB == 2) eB = fmaf(wv[u], colB[4 * l4 + u], eB);
           }
-          if (NB == 1) {
-            const float* wh = wE + e * WS + 16 * (lane >> 4);
-#pragma unroll
-            for (int i = 0; i < 16; ++i) eB = fmaf(wh[i], colB[i], eB);
-            eB += __shfl_xor_sync(FULL_MASK, eB, 16);
-          }
-          const float* rad = reinterpret_cast<const float*>(rows + e * F4 + 1);
-          if (okA) eps_acc += (double)(eA * rad[lane]);
-          if (ownB) eps_acc += (double)(eB * rad[slotB]);
         }
+        if (NB == 1) {
+          const float* wh = wE + e * WS + 16 * (lane >> 4);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) eB = fmaf(wh[i], colB[i], eB);
+          eB += __shfl_xor_sync(FULL_MASK, eB, 16);
+        }
+        const float* rad = reinterpret_cast<const float*>(rows + e * F4 + 1);
+        if (okA) eps_acc += (double)(eA * rad[lane]);
+        if (ownB) eps_acc += (double)(eB * rad[slotB]);
       }
     }
     // vector quantities of the whole batch: lane L sums pair (e, k) = (L / VQ, L % VQ)
