@@ -639,7 +639,7 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
   if (LIST && total >= 0) {
     // replay the interaction list (ilist.cuh): 32 entries at a time, their node
     // records prefetched into the (unused) stack region with cp.async
-    const NodeRec* rb = reinterpret_cast<const NodeRec*>(stk);
+    NodeRec* rb = reinterpret_cast<NodeRec*>(stk);
     const uint32_t s_rb = smem_u32(stk) + 48u * lane;
     int chunk = (int)wg;
     for (int base = 0; base < total; base += 32) {
@@ -654,10 +654,15 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
         cp_async16(s_rb + 32u, &r->topo);
       }
       cp_async_wait_all();
+      // the entry itself goes into its record's unused child fields (topo.x/y;
+      // the replay reads only the point range z/w): one broadcast LDS.128 per
+      // entry instead of two shuffles
+      if (lane < n) *reinterpret_cast<uint2*>(&rb[lane].topo) = my;
       __syncwarp();
       for (int i = 0; i < n; ++i) {
-        const uint32_t src = __shfl_sync(FULL_MASK, my.x, i);
-        const unsigned m = __shfl_sync(FULL_MASK, my.y, i);
+        const int4 tpi = rb[i].topo;
+        const uint32_t src = (uint32_t)tpi.x;
+        const unsigned m = (unsigned)tpi.y;
         const bool mine = (m >> lane) & 1u;
         if (!(src & IL_LEAF)) {
           const float4 hi = rb[i].hi, lo = rb[i].lo;
@@ -665,7 +670,7 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
           const float s = dist2_df(hi, lo, qx, fx, fy, fz);
           far_entry((int)(src & IL_NODE), lo.w, s, fx, fy, fz, mine, (src & IL_NEAR) ? 1 : 0);
         } else {
-          leaf_points(rb[i].topo, mine);
+          leaf_points(tpi, mine);
         }
       }
     }

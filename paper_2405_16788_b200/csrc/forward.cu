@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(FWD_WARPS * 32)
   if (LIST && total >= 0) {
     // 32 entries at a time, their node records prefetched into the (unused)
     // stack region with cp.async and read back as broadcast loads
-    const NodeRec* rb = reinterpret_cast<const NodeRec*>(stk[w]);
+    NodeRec* rb = reinterpret_cast<NodeRec*>(stk[w]);
     const uint32_t s_rb = (uint32_t)__cvta_generic_to_shared(stk[w]) + 48u * lane;
     int chunk = (int)wg;
     for (int base = 0; base < total; base += 32) {
@@ -197,10 +197,15 @@ __global__ void __launch_bounds__(FWD_WARPS * 32)
         cp_async16(s_rb + 32u, &r->topo);
       }
       asm volatile("cp.async.wait_all;\n" ::: "memory");
+      // the entry itself goes into its record's unused child fields (topo.x/y;
+      // the replay reads only the point range z/w): one broadcast LDS.128 per
+      // entry instead of two shuffles
+      if (lane < n) *reinterpret_cast<uint2*>(&rb[lane].topo) = my;
       __syncwarp();
       for (int i = 0; i < n; ++i) {
-        const uint32_t src = __shfl_sync(FULL_MASK, my.x, i);
-        const unsigned m = __shfl_sync(FULL_MASK, my.y, i);
+        const int4 tpi = rb[i].topo;
+        const uint32_t src = (uint32_t)tpi.x;
+        const unsigned m = (unsigned)tpi.y;
         if (!((m >> lane) & 1u)) continue;
         const int node = (int)(src & IL_NODE);
         if (!(src & IL_LEAF)) {
@@ -212,7 +217,7 @@ __global__ void __launch_bounds__(FWD_WARPS * 32)
                                    prn + (int64_t)node * 4 * tv.F4, ndi, nri, kp, near,
                                    !(src & IL_NEAR));
         } else {
-          leaf(rb[i].topo);
+          leaf(tpi);
         }
       }
     }

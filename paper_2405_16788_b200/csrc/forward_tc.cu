@@ -198,7 +198,7 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
   if (LIST && total >= 0) {
     // 32 entries at a time; their node records are prefetched into the
     // (unused) stack region with cp.async, read back as broadcast LDS.128
-    const NodeRec* rb = reinterpret_cast<const NodeRec*>(stk);
+    NodeRec* rb = reinterpret_cast<NodeRec*>(stk);
     const uint32_t s_rb = smem_u32(stk) + 48u * lane;
     const double* xq = xs + 3 * qi;
     int chunk = (int)wg;
@@ -214,10 +214,15 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
         cp_async16(s_rb + 32u, &r->topo);
       }
       cp_async_wait_all();
+      // the entry itself goes into its record's unused child fields (topo.x/y;
+      // the replay reads only the point range z/w): one broadcast LDS.128 per
+      // entry instead of two shuffles
+      if (lane < n) *reinterpret_cast<uint2*>(&rb[lane].topo) = my;
       __syncwarp();
       for (int i = 0; i < n; ++i) {
-        const uint32_t src = __shfl_sync(FULL_MASK, my.x, i);
-        const unsigned m = __shfl_sync(FULL_MASK, my.y, i);
+        const int4 tpi = rb[i].topo;
+        const uint32_t src = (uint32_t)tpi.x;
+        const unsigned m = (unsigned)tpi.y;
         const int node = (int)(src & IL_NODE);
         const bool mine = (m >> lane) & 1u;
         if (!(src & IL_LEAF)) {
@@ -234,7 +239,7 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
           }
           append(wv, node_row + (size_t)node * F4g);
         } else {
-          const int4 tp = rb[i].topo;
+          const int4 tp = tpi;
           for (int j = tp.z; j < tp.w; ++j) {
             float4 wv = make_float4(0.f, 0.f, 0.f, 0.f);
             if (mine) {
