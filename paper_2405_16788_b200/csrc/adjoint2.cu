@@ -574,6 +574,33 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
     dptr[nent] = acc.node_s + (size_t)node * Cr;
     ++nent;
   };
+  // two list entries r[0], r[1]: far nodes whose far lanes are all beyond 6.5 eps
+  // (GM = 0, FFMA phase B) — far_entry's fast path for both, interleaved
+  auto far_pair = [&](const NodeRec* r) {
+    const int4 ta = r[0].topo, tb = r[1].topo;
+    const float4 ha = r[0].hi, la = r[0].lo, hb = r[1].hi, lb = r[1].lo;
+    float ax, ay, az, bx, by, bz;
+    const float sa = dist2_df(ha, la, qx, ax, ay, az);
+    const float sb = dist2_df(hb, lb, qx, bx, by, bz);
+    const bool fa = ((unsigned)ta.y >> lane) & 1u, fb = ((unsigned)tb.y >> lane) & 1u;
+    const float ia = rsqrt_pos(sa), ib = rsqrt_pos(sb);
+    const float Ra = ia * ia, Rb = ib * ib;
+    const float wa = la.w * (Ra * ia) * ds0, wb = lb.w * (Rb * ib) * ds0;
+    const int na = ta.x & IL_NODE, nb = tb.x & IL_NODE;
+    wR[nent * WS + lane] = fa ? la.w * Ra : 0.f;
+    wR[(nent + 1) * WS + lane] = fb ? lb.w * Rb : 0.f;
+    float* va = vq + nent * 128;
+    float* vb = va + 128;
+    va[lane] = fa ? wa * ax : 0.f, va[32 + lane] = fa ? wa * ay : 0.f;
+    va[64 + lane] = fa ? wa * az : 0.f;
+    vb[lane] = fb ? wb * bx : 0.f, vb[32 + lane] = fb ? wb * by : 0.f;
+    vb[64 + lane] = fb ? wb * bz : 0.f;
+    meta[nent] = na, meta[nent + 1] = nb;
+    dptr[nent] = acc.node_s + (size_t)na * Cr;
+    dptr[nent + 1] = acc.node_s + (size_t)nb * Cr;
+    nent += 2;
+    if (nent == ENT) evaluate();  // keeps nent + 2 <= ENT checks cheap
+  };
   // the points of an opened leaf for the lanes in `me_open` (:382-412)
   auto leaf_points = [&](const int4 tp, bool me_open) {
     for (int j = tp.z; j < tp.w; ++j) {
@@ -659,9 +686,21 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
       // entry instead of two shuffles
       if (lane < n) *reinterpret_cast<uint2*>(&rb[lane].topo) = my;
       __syncwarp();
-      for (int i = 0; i < n; ++i) {
+      for (int i = 0; i < n;) {
         const int4 tpi = rb[i].topo;
         const uint32_t src = (uint32_t)tpi.x;
+        if constexpr (GM == 0 && FF && !VR) {
+          // two consecutive far entries without near lanes that fit the batch:
+          // one interleaved pass (independent dependency chains for the
+          // scheduler); batches fill exactly as on the tree walk, so results
+          // stay bitwise those of the walk
+          if (nent + 2 <= ENT && i + 1 < n &&
+              !((src | (uint32_t)rb[i + 1].topo.x) & (IL_LEAF | IL_NEAR))) {
+            far_pair(rb + i);
+            i += 2;
+            continue;
+          }
+        }
         const unsigned m = (unsigned)tpi.y;
         const bool mine = (m >> lane) & 1u;
         if (!(src & IL_LEAF)) {
@@ -672,6 +711,7 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
         } else {
           leaf_points(tpi, mine);
         }
+        ++i;
       }
     }
   }
