@@ -181,12 +181,15 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
     nent = 0;
   };
 
-  auto append = [&](float4 wv, const float4* rowsrc) {
-    if (nent == ENT) evaluate();
+  auto store_entry = [&](float4 wv, const float4* rowsrc) {  // nent < ENT
     wd[nent * 32 + lane] = make_float4(wv.x, wv.y, wv.z, 0.f);
     wr[nent * WSTR + lane] = wv.w;
     if (lane < F4) cp_async16(s_rows + 4u * RSF * nent, rowsrc + lane);
     ++nent;
+  };
+  auto append = [&](float4 wv, const float4* rowsrc) {
+    if (nent == ENT) evaluate();
+    store_entry(wv, rowsrc);
   };
 
   // COUNT: per-query replay counters (visited, far near/far, point near/far)
@@ -222,6 +225,25 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
       for (int i = 0; i < n; ++i) {
         const int4 tpi = rb[i].topo;
         const uint32_t src = (uint32_t)tpi.x;
+        if (nent == ENT) evaluate();  // as append() would, before deciding on a pair
+        // two consecutive far entries without near lanes that fit the batch:
+        // one interleaved pass; batches fill exactly as on the tree walk
+        if (nent + 2 <= ENT && i + 1 < n &&
+            !((src | (uint32_t)rb[i + 1].topo.x) & (IL_LEAF | IL_NEAR))) {
+          const int4 tb = rb[i + 1].topo;
+          const float4 ha = rb[i].hi, la = rb[i].lo, hb = rb[i + 1].hi, lb = rb[i + 1].lo;
+          float ax, ay, az, bx, by, bz;
+          const float sa = dist2_df(ha, la, qx, ax, ay, az);
+          const float sb = dist2_df(hb, lb, qx, bx, by, bz);
+          const bool fa = ((unsigned)tpi.y >> lane) & 1u, fb = ((unsigned)tb.y >> lane) & 1u;
+          const float4 wa = fwd_w_far(ax, ay, az, sa, la.w), wb = fwd_w_far(bx, by, bz, sb, lb.w);
+          store_entry(make_float4(fa ? wa.x : 0.f, fa ? wa.y : 0.f, fa ? wa.z : 0.f, fa ? wa.w : 0.f),
+                      node_row + (size_t)(src & IL_NODE) * F4g);
+          store_entry(make_float4(fb ? wb.x : 0.f, fb ? wb.y : 0.f, fb ? wb.z : 0.f, fb ? wb.w : 0.f),
+                      node_row + (size_t)((uint32_t)tb.x & IL_NODE) * F4g);
+          ++i;
+          continue;
+        }
         const unsigned m = (unsigned)tpi.y;
         const int node = (int)(src & IL_NODE);
         const bool mine = (m >> lane) & 1u;
