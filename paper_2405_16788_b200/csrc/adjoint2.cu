@@ -30,6 +30,8 @@
 //     A_hi B_hi + A_hi B_lo (TF32) + A_lo B_hi (BF16): per-product error
 //     ~2^-19 relative, fp32-class. The epilogue REDs 8 consecutive channels of
 //     4 entries per instruction (8 sectors per 32 lanes, as the FFMA path).
+#include <type_traits>
+
 #include "adjoint.cuh"
 #include "traverse.cuh"
 
@@ -574,32 +576,37 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
     dptr[nent] = acc.node_s + (size_t)node * Cr;
     ++nent;
   };
-  // two list entries r[0], r[1]: far nodes whose far lanes are all beyond 6.5 eps
-  // (GM = 0, FFMA phase B) — far_entry's fast path for both, interleaved
-  auto far_pair = [&](const NodeRec* r) {
-    const int4 ta = r[0].topo, tb = r[1].topo;
-    const float4 ha = r[0].hi, la = r[0].lo, hb = r[1].hi, lb = r[1].lo;
-    float ax, ay, az, bx, by, bz;
-    const float sa = dist2_df(ha, la, qx, ax, ay, az);
-    const float sb = dist2_df(hb, lb, qx, bx, by, bz);
-    const bool fa = ((unsigned)ta.y >> lane) & 1u, fb = ((unsigned)tb.y >> lane) & 1u;
-    const float ia = rsqrt_pos(sa), ib = rsqrt_pos(sb);
-    const float Ra = ia * ia, Rb = ib * ib;
-    const float wa = la.w * (Ra * ia) * ds0, wb = lb.w * (Rb * ib) * ds0;
-    const int na = ta.x & IL_NODE, nb = tb.x & IL_NODE;
-    wR[nent * WS + lane] = fa ? la.w * Ra : 0.f;
-    wR[(nent + 1) * WS + lane] = fb ? lb.w * Rb : 0.f;
-    float* va = vq + nent * 128;
-    float* vb = va + 128;
-    va[lane] = fa ? wa * ax : 0.f, va[32 + lane] = fa ? wa * ay : 0.f;
-    va[64 + lane] = fa ? wa * az : 0.f;
-    vb[lane] = fb ? wb * bx : 0.f, vb[32 + lane] = fb ? wb * by : 0.f;
-    vb[64 + lane] = fb ? wb * bz : 0.f;
-    meta[nent] = na, meta[nent + 1] = nb;
-    dptr[nent] = acc.node_s + (size_t)na * Cr;
-    dptr[nent + 1] = acc.node_s + (size_t)nb * Cr;
-    nent += 2;
-    if (nent == ENT) evaluate();  // keeps nent + 2 <= ENT checks cheap
+  // K consecutive list entries r[0..K): far nodes whose far lanes are all beyond
+  // 6.5 eps (GM = 0, FFMA phase B) — far_entry's fast path for each, interleaved
+  auto far_group = [&](const NodeRec* r, auto kc) {
+    constexpr int K = decltype(kc)::value;
+    float s[K], fx[K], fy[K], fz[K], A[K];
+    bool f[K];
+    int nd[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int4 t = r[k].topo;
+      const float4 h = r[k].hi, l = r[k].lo;
+      s[k] = dist2_df(h, l, qx, fx[k], fy[k], fz[k]);
+      f[k] = ((unsigned)t.y >> lane) & 1u;
+      nd[k] = t.x & IL_NODE;
+      A[k] = l.w;
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const float ir = rsqrt_pos(s[k]);
+      const float R = ir * ir;
+      const float w = A[k] * (R * ir) * ds0;
+      const int e = nent + k;
+      wR[e * WS + lane] = f[k] ? A[k] * R : 0.f;
+      float* v = vq + e * 128;
+      v[lane] = f[k] ? w * fx[k] : 0.f, v[32 + lane] = f[k] ? w * fy[k] : 0.f;
+      v[64 + lane] = f[k] ? w * fz[k] : 0.f;
+      meta[e] = nd[k];
+      dptr[e] = acc.node_s + (size_t)nd[k] * Cr;
+    }
+    nent += K;
+    if (nent == ENT) evaluate();  // keeps the nent + K <= ENT checks cheap
   };
   // the points of an opened leaf for the lanes in `me_open` (:382-412)
   auto leaf_points = [&](const int4 tp, bool me_open) {
@@ -692,11 +699,11 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
         if constexpr (GM == 0 && FF && !VR) {
           // two consecutive far entries without near lanes that fit the batch:
           // one interleaved pass (independent dependency chains for the
-          // scheduler); batches fill exactly as on the tree walk, so results
-          // stay bitwise those of the walk
+          // scheduler; groups of 4 measured no faster); batches fill exactly as
+          // on the tree walk, so results stay bitwise those of the walk
           if (nent + 2 <= ENT && i + 1 < n &&
               !((src | (uint32_t)rb[i + 1].topo.x) & (IL_LEAF | IL_NEAR))) {
-            far_pair(rb + i);
+            far_group(rb + i, std::integral_constant<int, 2>{});
             i += 2;
             continue;
           }
