@@ -476,6 +476,29 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
     if (nent == ENT) evaluate();
   };
 
+  // far-field lane values beyond 6.5 eps (tau = 1: W = R / r, Wp_r = -3 W R, no
+  // epsilon terms; kernels.cpp:50-55), branch-free: every lane evaluates,
+  // non-far lanes select 0 (bhtree.cpp:361-376)
+  auto far_fast = [&](float A, float s, float fx, float fy, float fz, bool far, float& r_,
+                      float& u0, float& u1, float& u2) {
+    const float inv_r = rsqrt_pos(s);
+    const float R = inv_r * inv_r;
+    r_ = far ? A * R : 0.f;
+    if (GM == 0) {
+      const float aWds = A * (R * inv_r) * ds0;
+      u0 = far ? aWds * fx : 0.f, u1 = far ? aWds * fy : 0.f, u2 = far ? aWds * fz : 0.f;
+    } else {  // with the query-gradient adjoint d_grad (:372-376)
+      const float W = R * inv_r;
+      const float Wp_r = -3.0f * W * R;
+      const float aWds = A * W * ds0;
+      const float gd = fmaf(dg0, fx, fmaf(dg1, fy, dg2 * fz));
+      const float t = Wp_r * gd;
+      u0 = far ? aWds * fx - A * fmaf(W, dg0, t * fx) : 0.f;
+      u1 = far ? aWds * fy - A * fmaf(W, dg1, t * fy) : 0.f;
+      u2 = far ? aWds * fz - A * fmaf(W, dg2, t * fz) : 0.f;
+    }
+  };
+
   // one far source (node) for the lanes in `far` (bhtree.cpp:361-381).
   // hint: the list's NEAR flag (0: no far lane needs the series, 1: some may),
   // -1 on the tree walk (decided by a vote)
@@ -490,13 +513,7 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
       // branch, so a batch without near lanes never issues it
       const bool slow = far && !(kp.mode == KM_SINGULAR ||
                                  (kp.mode == KM_REGULARIZED && s >= kp.near2));
-      {  // branch-free: every lane evaluates, non-far lanes select 0
-        const float inv_r = rsqrt_pos(s);
-        const float R = inv_r * inv_r;
-        const float aWds = A * (R * inv_r) * ds0;
-        r_ = far ? A * R : 0.f;
-        u0 = far ? aWds * fx : 0.f, u1 = far ? aWds * fy : 0.f, u2 = far ? aWds * fz : 0.f;
-      }
+      far_fast(A, s, fx, fy, fz, far, r_, u0, u1, u2);
       if (hint != 0 && (hint > 0 || __any_sync(FULL_MASK, slow))) {
         if (slow) {
           const Co c = coeffs<2>(s, kp);
@@ -520,19 +537,7 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
       // warp-uniform branch for the near lanes only
       const bool slow = far && !(kp.mode == KM_SINGULAR ||
                                  (kp.mode == KM_REGULARIZED && s >= kp.near2));
-      {  // branch-free: every lane evaluates, non-far lanes select 0
-        const float inv_r = rsqrt_pos(s);
-        const float R = inv_r * inv_r;
-        const float W = R * inv_r;
-        const float Wp_r = -3.0f * W * R;
-        const float aWds = A * W * ds0;
-        const float gd = fmaf(dg0, fx, fmaf(dg1, fy, dg2 * fz));  // :372-374
-        const float t = Wp_r * gd;
-        r_ = far ? A * R : 0.f;
-        u0 = far ? aWds * fx - A * fmaf(W, dg0, t * fx) : 0.f;
-        u1 = far ? aWds * fy - A * fmaf(W, dg1, t * fy) : 0.f;
-        u2 = far ? aWds * fz - A * fmaf(W, dg2, t * fz) : 0.f;
-      }
+      far_fast(A, s, fx, fy, fz, far, r_, u0, u1, u2);
       if (hint != 0 && (hint > 0 || __any_sync(FULL_MASK, slow))) {
         if (slow) {
           const Co c = adj_coeffs<GM>(s, kp);
@@ -577,7 +582,7 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
     ++nent;
   };
   // K consecutive list entries r[0..K): far nodes whose far lanes are all beyond
-  // 6.5 eps (GM = 0, FFMA phase B) — far_entry's fast path for each, interleaved
+  // 6.5 eps — far_entry's fast path for each, interleaved
   auto far_group = [&](const NodeRec* r, auto kc) {
     constexpr int K = decltype(kc)::value;
     float s[K], fx[K], fy[K], fz[K], A[K];
@@ -594,18 +599,20 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
     }
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-      const float ir = rsqrt_pos(s[k]);
-      const float R = ir * ir;
-      const float w = A[k] * (R * ir) * ds0;
-      const int e = nent + k;
-      wR[e * WS + lane] = f[k] ? A[k] * R : 0.f;
-      float* v = vq + e * 128;
-      v[lane] = f[k] ? w * fx[k] : 0.f, v[32 + lane] = f[k] ? w * fy[k] : 0.f;
-      v[64 + lane] = f[k] ? w * fz[k] : 0.f;
-      meta[e] = nd[k];
-      dptr[e] = acc.node_s + (size_t)nd[k] * Cr;
+      float r_, u0, u1, u2;
+      far_fast(A[k], s[k], fx[k], fy[k], fz[k], f[k], r_, u0, u1, u2);
+      if constexpr (VR) {
+        vr_store(r_, u0, u1, u2, 0.f, false);
+        meta[nent] = nd[k];
+      } else {
+        wR[nent * WS + lane] = r_;
+        float* v = vq + nent * 128;
+        v[lane] = u0, v[32 + lane] = u1, v[64 + lane] = u2;
+        meta[nent] = nd[k];
+        dptr[nent] = acc.node_s + (size_t)nd[k] * Cr;
+      }
+      ++nent;
     }
-    nent += K;
     if (nent == ENT) evaluate();  // keeps the nent + K <= ENT checks cheap
   };
   // the points of an opened leaf for the lanes in `me_open` (:382-412)
@@ -696,7 +703,7 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
       for (int i = 0; i < n;) {
         const int4 tpi = rb[i].topo;
         const uint32_t src = (uint32_t)tpi.x;
-        if constexpr (GM == 0 && FF && !VR) {
+        if constexpr (FF) {
           // two consecutive far entries without near lanes that fit the batch:
           // one interleaved pass (independent dependency chains for the
           // scheduler; groups of 4 measured no faster); batches fill exactly as

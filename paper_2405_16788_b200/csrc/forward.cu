@@ -206,6 +206,26 @@ __global__ void __launch_bounds__(FWD_WARPS * 32)
         const int4 tpi = rb[i].topo;
         const uint32_t src = (uint32_t)tpi.x;
         const unsigned m = (unsigned)tpi.y;
+        if (i + 1 < n && !((src | (uint32_t)rb[i + 1].topo.x) & (IL_LEAF | IL_NEAR))) {
+          // two far entries without near lanes, interleaved and branch-free:
+          // a lane outside an entry's mask adds exact zeros (area 0, finite r)
+          const int4 tpj = rb[i + 1].topo;
+          const bool ma = (m >> lane) & 1u, mb = ((unsigned)tpj.y >> lane) & 1u;
+          const float4 ha = rb[i].hi, la = rb[i].lo, hb = rb[i + 1].hi, lb = rb[i + 1].lo;
+          float ax, ay, az, bx, by, bz;
+          const float sa = dist2_df(ha, la, qx, ax, ay, az);
+          const float sb = dist2_df(hb, lb, qx, bx, by, bz);
+          const int na = (int)(src & IL_NODE), nb = (int)((uint32_t)tpj.x & IL_NODE);
+          bool near;
+          f_interact<TD, TR, GRAD>(a, ax, ay, az, ma ? sa : 1.f, ma ? la.w : 0.f,
+                                   pdn + (int64_t)na * tv.F4, prn + (int64_t)na * 4 * tv.F4, ndi,
+                                   nri, kp, near, true);
+          f_interact<TD, TR, GRAD>(a, bx, by, bz, mb ? sb : 1.f, mb ? lb.w : 0.f,
+                                   pdn + (int64_t)nb * tv.F4, prn + (int64_t)nb * 4 * tv.F4, ndi,
+                                   nri, kp, near, true);
+          ++i;
+          continue;
+        }
         if (!((m >> lane) & 1u)) continue;
         const int node = (int)(src & IL_NODE);
         if (!(src & IL_LEAF)) {
