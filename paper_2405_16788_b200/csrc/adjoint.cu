@@ -353,13 +353,26 @@ __global__ void k_flush_points(int64_t n, int C, int Cd, int Cr, const int* __re
     double am = a * mu[m * C + ch];
     dn0 += am * g[0], dn1 += am * g[1], dn2 += am * g[2];
   }
-  if (moments)
-    for (int k = 0; k < Cr; ++k) {
-      int ch = chmap[Cd + k];
-      moments[m * C + ch] = (float)(pmur[j * Cr + k] + a * gs[leaf * Cr + k]);
-    }
   if (normals) {
     normals[3 * m] = (float)dn0, normals[3 * m + 1] = (float)dn1, normals[3 * m + 2] = (float)dn2;
+  }
+}
+
+// radial moments: one warp per point, lanes over its radial slots (coalesced;
+// same arithmetic as the per-point loop it replaces)
+__global__ void k_flush_radial(int64_t n, int C, int Cd, int Cr, const int* __restrict__ chmap,
+                               const int32_t* __restrict__ order,
+                               const int32_t* __restrict__ pt_leaf,
+                               const double* __restrict__ area, const double* __restrict__ gs,
+                               const double* __restrict__ pmur, float* moments) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < n; j += nw) {
+    const int64_t m = order[j];
+    const int64_t leaf = pt_leaf[j];
+    const double a = area[m];
+    for (int k = lane; k < Cr; k += 32)
+      moments[m * C + chmap[Cd + k]] = (float)(pmur[j * Cr + k] + a * gs[leaf * Cr + k]);
   }
 }
 
@@ -455,6 +468,12 @@ void flush_launch(Tree& t, GradBuf& b, float* moments, float* normals) {
       t.area64.as<double>(), t.nrm64.as<double>(), t.mu64.as<double>(), b.node_v, b.node_s,
       b.pt_mud, b.pt_mur, b.pt_n, moments, normals);
   count_launch();
+  if (moments && t.Cr > 0) {
+    k_flush_radial<<<148 * 16, B, 0, t.stream>>>(t.n, t.C, t.Cd, t.Cr, t.chmap.as<int>(),
+                                                t.order.as<int32_t>(), t.pt_leaf.as<int32_t>(),
+                                                t.area64.as<double>(), b.node_s, b.pt_mur, moments);
+    count_launch();
+  }
   DPL_CUDA(cudaGetLastError());
 }
 
