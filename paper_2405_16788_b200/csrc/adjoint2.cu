@@ -469,7 +469,8 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
     vqe[lane] = v0, vqe[32 + lane] = v1, vqe[64 + lane] = v2;
     if (point) vqe[96 + lane] = v3;  // slot 3 is never read for nodes
     vqe[128 + lane] = r_ * dsr[0], vqe[160 + lane] = r_ * dsr[1];
-    vqe[192 + lane] = r_ * dsr[2], vqe[224 + lane] = r_ * dsr[3];
+    vqe[192 + lane] = r_ * dsr[2];
+    if (nr > 3) vqe[224 + lane] = r_ * dsr[3];  // slot 7 is read only when nr == 4
   };
 
   auto begin_entry = [&]() {
@@ -483,19 +484,19 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
                       float& u0, float& u1, float& u2) {
     const float inv_r = rsqrt_pos(s);
     const float R = inv_r * inv_r;
-    r_ = far ? A * R : 0.f;
+    r_ = sel0(far, A * R);
     if (GM == 0) {
       const float aWds = A * (R * inv_r) * ds0;
-      u0 = far ? aWds * fx : 0.f, u1 = far ? aWds * fy : 0.f, u2 = far ? aWds * fz : 0.f;
+      u0 = sel0(far, aWds * fx), u1 = sel0(far, aWds * fy), u2 = sel0(far, aWds * fz);
     } else {  // with the query-gradient adjoint d_grad (:372-376)
       const float W = R * inv_r;
       const float Wp_r = -3.0f * W * R;
       const float aWds = A * W * ds0;
       const float gd = fmaf(dg0, fx, fmaf(dg1, fy, dg2 * fz));
       const float t = Wp_r * gd;
-      u0 = far ? aWds * fx - A * fmaf(W, dg0, t * fx) : 0.f;
-      u1 = far ? aWds * fy - A * fmaf(W, dg1, t * fy) : 0.f;
-      u2 = far ? aWds * fz - A * fmaf(W, dg2, t * fz) : 0.f;
+      u0 = sel0(far, aWds * fx - A * fmaf(W, dg0, t * fx));
+      u1 = sel0(far, aWds * fy - A * fmaf(W, dg1, t * fy));
+      u2 = sel0(far, aWds * fz - A * fmaf(W, dg2, t * fz));
     }
   };
 

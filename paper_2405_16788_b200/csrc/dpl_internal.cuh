@@ -110,6 +110,16 @@ __device__ __forceinline__ float rsqrt_pos(float x) {
   return r;
 }
 
+// p ? a : 0 as one SEL the compiler cannot turn back into a branch around the
+// computation of a (keeps branch-free lane values branch-free)
+__device__ __forceinline__ float sel0(bool p, float a) {
+  float r;
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\tselp.f32 %0, %1, 0f00000000, q;\n\t}\n"
+      : "=f"(r)
+      : "f"(a), "r"((int)p));
+  return r;
+}
+
 // fp64 RED under a PTX predicate (no C++ branch; the address needs no guard)
 __device__ __forceinline__ void red_add_if(double* p, double v, bool pred) {
   asm volatile(
