@@ -254,6 +254,25 @@ int dpl_point_adam_step(dpl_tree_t tree, dpl_point_adam_t opt, const float* g_mo
 /* Current cloud parameters (original order, fp64): normals N x 3, moments N x C. */
 int dpl_tree_get_points(dpl_tree_t tree, double* normals, double* moments);
 
+/* ---- Sharded point update for G ranks ----------
+ * Each rank owns the points [lo, hi) of the original order: it reduce-scatters
+ * the flushed gradients, calls dpl_point_adam_step_range with its slice
+ * (g_moments (hi - lo) x C, g_normals (hi - lo) x 3; one Adam step per call,
+ * no update_moments), all-gathers the updated slices read with
+ * dpl_tree_get_points_range, writes the other ranks' slices with
+ * dpl_tree_set_points_range, then calls dpl_tree_refresh_moments — the same
+ * parameters and node moments as dpl_point_adam_step on the summed gradients.
+ * Arrays: host or device, fp64 parameters, original point order. */
+int dpl_point_adam_step_range(dpl_tree_t tree, dpl_point_adam_t opt, const float* g_moments,
+                              const float* g_normals, int64_t lo, int64_t hi, double lr,
+                              double beta1, double beta2, double eps);
+int dpl_tree_get_points_range(dpl_tree_t tree, int64_t lo, int64_t hi, double* normals,
+                              double* moments);
+int dpl_tree_set_points_range(dpl_tree_t tree, int64_t lo, int64_t hi, const double* normals,
+                              const double* moments);
+/* update_moments (bhtree.cpp:171-176) from the tree's current parameters. */
+int dpl_tree_refresh_moments(dpl_tree_t tree);
+
 /* ---- Adam (optimizer.cpp:65-81) on device parameter groups ------------------ */
 /* In-place Adam on n fp32 params with fp32 grads and fp32 m/v state; step t is
  * the 1-based iteration after increment. */

@@ -141,6 +141,11 @@ _sig = {
     "dpl_point_adam_step": (C.c_int, [_vp, _vp, _vp, _vp, C.c_double, C.c_double, C.c_double,
                                       C.c_double]),
     "dpl_tree_get_points": (C.c_int, [_vp, _vp, _vp]),
+    "dpl_point_adam_step_range": (C.c_int, [_vp, _vp, _vp, _vp, C.c_int64, C.c_int64, C.c_double,
+                                            C.c_double, C.c_double, C.c_double]),
+    "dpl_tree_get_points_range": (C.c_int, [_vp, C.c_int64, C.c_int64, _vp, _vp]),
+    "dpl_tree_set_points_range": (C.c_int, [_vp, C.c_int64, C.c_int64, _vp, _vp]),
+    "dpl_tree_refresh_moments": (C.c_int, [_vp]),
     "dpl_adam_step": (C.c_int, [_vp, _vp, _vp, _vp, _vp, C.c_int64, C.c_double, C.c_double,
                                 C.c_double, C.c_double, C.c_int64]),
 }

@@ -463,6 +463,47 @@ class PointAdam:
                                         self.beta2, self.eps))
 
 
+    def step_range(self, g_moments, g_normals, lo: int, hi: int, lr=None):
+        """Sharded update: Adam on points [lo, hi) with that slice's
+        summed gradients ((hi - lo) x C, (hi - lo) x 3); no update_moments —
+        exchange the slices (get_points_range / set_points_range), then
+        refresh_moments. One Adam step per call."""
+        k = hi - lo
+        Cc = self.tree.channels()
+        gm, k1 = _in(g_moments, np.float32, (k, Cc)) if k > 0 else (None, None)
+        gn, k2 = _in(g_normals, np.float32, (k, 3)) if k > 0 else (None, None)
+        check(lib().dpl_point_adam_step_range(self.tree._h, self._h, gm, gn, int(lo), int(hi),
+                                              float(self.lr if lr is None else lr), self.beta1,
+                                              self.beta2, self.eps))
+
+
+def get_points_range(tree: DipoleTree, lo: int, hi: int, normals=None, moments=None):
+    """Parameters of points [lo, hi) (original order, fp64) into the given arrays
+    (host numpy or torch, any device) or new numpy arrays."""
+    k, Cc = hi - lo, tree.channels()
+    if normals is None:
+        normals = np.zeros((k, 3))
+    if moments is None:
+        moments = np.zeros((k, Cc))
+    pn = normals.data_ptr() if _is_torch(normals) else normals.ctypes.data
+    pm = moments.data_ptr() if _is_torch(moments) else moments.ctypes.data
+    check(lib().dpl_tree_get_points_range(tree._h, int(lo), int(hi), pn, pm))
+    return normals, moments
+
+
+def set_points_range(tree: DipoleTree, lo: int, hi: int, normals, moments):
+    """Overwrite the parameters of points [lo, hi) (fp64, original order)."""
+    k, Cc = hi - lo, tree.channels()
+    pn, k1 = _in(normals, np.float64, (k, 3))
+    pm, k2 = _in(moments, np.float64, (k, Cc))
+    check(lib().dpl_tree_set_points_range(tree._h, int(lo), int(hi), pn, pm))
+
+
+def refresh_moments(tree: DipoleTree):
+    """update_moments (bhtree.cpp:171-176) from the tree's current parameters."""
+    check(lib().dpl_tree_refresh_moments(tree._h))
+
+
 def get_points(tree: DipoleTree):
     """(normals N x 3, moments N x C) fp64 of the tree's current cloud."""
     n, Cc = tree.point_count(), tree.channels()

@@ -1416,6 +1416,65 @@ int dpl_tree_get_points(dpl_tree_t h, double* nrm, double* mu) {
   });
 }
 
+int dpl_point_adam_step_range(dpl_tree_t h, dpl_point_adam_t o, const float* g_moments,
+                              const float* g_normals, int64_t lo, int64_t hi, double lr,
+                              double beta1, double beta2, double eps) {
+  return guard([&] {
+    check_tree(h);
+    require(o != nullptr && o->tree == h, DPL_ERR_USAGE, "optimizer belongs to another tree");
+    require(o->a.n == h->t.n && o->a.C == h->t.C, DPL_ERR_DATA, "optimizer / tree size mismatch");
+    require(0 <= lo && lo <= hi && hi <= h->t.n, DPL_ERR_USAGE, "bad point range");
+    require(hi == lo || (g_moments && g_normals), DPL_ERR_USAGE, "null gradient");
+    Tree& t = h->t;
+    DPL_CUDA(cudaSetDevice(t.device));
+    DevBuf tm, tn;
+    const float* gm = hi > lo ? stage_in(t, g_moments, (size_t)(hi - lo) * t.C, tm) : nullptr;
+    const float* gn = hi > lo ? stage_in(t, g_normals, (size_t)(hi - lo) * 3, tn) : nullptr;
+    point_adam_step_range(t, o->a, gm, gn, lo, hi, lr, beta1, beta2, eps);
+    DPL_CUDA(cudaStreamSynchronize(t.stream));
+  });
+}
+
+int dpl_tree_get_points_range(dpl_tree_t h, int64_t lo, int64_t hi, double* nrm, double* mu) {
+  return guard([&] {
+    check_tree(h);
+    Tree& t = h->t;
+    require(0 <= lo && lo <= hi && hi <= t.n, DPL_ERR_USAGE, "bad point range");
+    if (nrm && hi > lo)
+      DPL_CUDA(cudaMemcpyAsync(nrm, t.nrm64.as<double>() + 3 * lo, (hi - lo) * 24,
+                               cudaMemcpyDefault, t.stream));
+    if (mu && hi > lo)
+      DPL_CUDA(cudaMemcpyAsync(mu, t.mu64.as<double>() + (size_t)lo * t.C,
+                               (hi - lo) * (size_t)t.C * 8, cudaMemcpyDefault, t.stream));
+    DPL_CUDA(cudaStreamSynchronize(t.stream));
+  });
+}
+
+int dpl_tree_set_points_range(dpl_tree_t h, int64_t lo, int64_t hi, const double* nrm,
+                              const double* mu) {
+  return guard([&] {
+    check_tree(h);
+    Tree& t = h->t;
+    require(0 <= lo && lo <= hi && hi <= t.n, DPL_ERR_USAGE, "bad point range");
+    if (nrm && hi > lo)
+      DPL_CUDA(cudaMemcpyAsync(t.nrm64.as<double>() + 3 * lo, nrm, (hi - lo) * 24,
+                               cudaMemcpyDefault, t.stream));
+    if (mu && hi > lo)
+      DPL_CUDA(cudaMemcpyAsync(t.mu64.as<double>() + (size_t)lo * t.C, mu,
+                               (hi - lo) * (size_t)t.C * 8, cudaMemcpyDefault, t.stream));
+    DPL_CUDA(cudaStreamSynchronize(t.stream));
+  });
+}
+
+int dpl_tree_refresh_moments(dpl_tree_t h) {
+  return guard([&] {
+    check_tree(h);
+    DPL_CUDA(cudaSetDevice(h->t.device));
+    tree_compute_moments(h->t);
+    DPL_CUDA(cudaStreamSynchronize(h->t.stream));
+  });
+}
+
 int dpl_mean_knn_spacing(int device, const double* pos, int64_t n, int32_t k, double* out) {
   return guard([&] {
     require(out != nullptr, DPL_ERR_USAGE, "null out");

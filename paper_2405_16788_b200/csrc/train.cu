@@ -68,6 +68,25 @@ void point_adam_alloc(PointAdam& o, const Tree& t) {
   DPL_CUDA(cudaMemsetAsync(o.state.p, 0, (2 * nm + 2 * nn) * sizeof(double), t.stream));
 }
 
+void point_adam_step_range(Tree& t, PointAdam& o, const float* g_mu, const float* g_n,
+                           int64_t lo, int64_t hi, double lr, double b1, double b2, double eps) {
+  ++o.t;  // one step per call, as Adam::step (:73)
+  if (hi <= lo) return;
+  const double c1 = 1.0 - std::pow(b1, (double)o.t);
+  const double c2 = 1.0 - std::pow(b2, (double)o.t);
+  const size_t nm = (size_t)t.n * t.C, nn = (size_t)t.n * 3;
+  const int64_t cnt = hi - lo;
+  double* s = o.state.as<double>();
+  const size_t om = (size_t)lo * t.C, on = (size_t)lo * 3;
+  k_moment_adam<<<148 * 16, 256, 0, t.stream>>>(cnt * t.C, t.mu64.as<double>() + om, g_mu, s + om,
+                                                 s + nm + om, lr, b1, b2, eps, c1, c2);
+  k_normal_adam<<<(unsigned)((cnt + 255) / 256), 256, 0, t.stream>>>(
+      cnt, t.nrm64.as<double>() + on, g_n, s + 2 * nm + on, s + 2 * nm + nn + on, lr, b1, b2, eps,
+      c1, c2);
+  count_launch(2);
+  DPL_CUDA(cudaGetLastError());
+}
+
 void point_adam_step(Tree& t, PointAdam& o, const float* g_mu, const float* g_n, double lr,
                      double b1, double b2, double eps) {
   ++o.t;  // Adam::step increments before use (:73)

@@ -79,3 +79,94 @@ def test_two_rank_adjoint_allreduce_matches_single(tmp_path, oracle_mod):
     assert np.abs(got["m"] - m).max() <= 1e-12 * s
     assert np.abs(got["n"] - n).max() <= 1e-12 * np.abs(n).max()
     assert abs(float(got["de"]) - de) <= 1e-12 * abs(de)
+
+
+# ---------------------------------------------------------------- sharded point update
+class _OracleEngine:
+    """sharded_point_update's device side restated on the oracle's Adam (CPU):
+    fp64 parameters / state arrays, normals renormalised when changed."""
+
+    def __init__(self, mu, nrm):
+        import sys
+
+        sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle"))
+        import oracle as O
+
+        self.O = O
+        self.mu, self.nrm = mu.copy(), nrm.copy()
+        self.m_mu, self.v_mu = np.zeros_like(mu), np.zeros_like(mu)
+        self.m_n, self.v_n = np.zeros_like(nrm), np.zeros_like(nrm)
+        self.t = 0
+
+    def adam_range(self, g_mom, g_nrm, lo, hi):
+        O = self.O
+        self.t += 1
+        if hi <= lo:
+            return
+        lib = O.port_lib()
+        gm = np.ascontiguousarray(g_mom.numpy(), np.float64)
+        gn = np.ascontiguousarray(g_nrm.numpy(), np.float64)
+        for p, g, m, v in ((self.mu, gm, self.m_mu, self.v_mu), (self.nrm, gn, self.m_n, self.v_n)):
+            ps, ms, vs = (np.ascontiguousarray(a[lo:hi]) for a in (p, m, v))
+            lib.ora_adam_step(ps.ctypes.data_as(O._dp), g.ctypes.data_as(O._dp), ms.ctypes.data_as(O._dp),
+                              vs.ctypes.data_as(O._dp), ps.size, 1e-2, 0.9, 0.999, 1e-8, self.t)
+            if p is self.nrm:
+                old = p[lo:hi]
+                changed = np.any(ps != old, axis=1)
+                lens = np.sqrt((ps[:, 0] ** 2 + ps[:, 1] ** 2) + ps[:, 2] ** 2)
+                ok = changed & (lens > 1e-12)
+                ps[ok] = ps[ok] / lens[ok, None]
+                ps[~ok] = old[~ok]
+            p[lo:hi], m[lo:hi], v[lo:hi] = ps, ms, vs
+
+    def get_range(self, lo, hi, nrm_out, mom_out):
+        nrm_out.copy_(torch.from_numpy(self.nrm[lo:hi]))
+        mom_out.copy_(torch.from_numpy(self.mu[lo:hi]))
+
+    def set_all(self, nrm, mom):
+        self.nrm, self.mu = nrm.numpy().copy(), mom.numpy().copy()
+
+    def refresh(self):
+        pass
+
+
+def _sharded_case():
+    rng = np.random.default_rng(9)
+    n, C = 301, 5  # uneven split: chunks of 151 / 150
+    mu = rng.standard_normal((n, C))
+    nrm = rng.standard_normal((n, 3))
+    nrm /= np.linalg.norm(nrm, axis=1, keepdims=True)
+    g = [(rng.standard_normal((n, C)).astype(np.float32), rng.standard_normal((n, 3)).astype(np.float32))
+         for _ in range(2)]  # per-rank flushed gradients
+    return n, C, mu, nrm, g
+
+
+def _sharded_worker(rank, world, port, out_dir):
+    from paper_2405_16788_b200.parallel import sharded_point_update
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    n, C, mu, nrm, g = _sharded_case()
+    eng = _OracleEngine(mu, nrm)
+    for _ in range(2):  # two steps: the Adam state of each slice carries over
+        sharded_point_update(eng, torch.from_numpy(g[rank][0]), torch.from_numpy(g[rank][1]), n, C)
+    np.savez(os.path.join(out_dir, f"sharded{rank}.npz"), mu=eng.mu, nrm=eng.nrm)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_sharded_point_update_matches_single(tmp_path, oracle_mod):
+    """Reduce-scatter -> Adam on each rank's slice -> all-gather (gloo, 2 ranks)
+    leaves every rank with the parameters of one Adam step on the summed
+    gradients."""
+    mp.spawn(_sharded_worker, args=(2, _free_port(), str(tmp_path)), nprocs=2, join=True)
+    n, C, mu, nrm, g = _sharded_case()
+    ref = _OracleEngine(mu, nrm)
+    gm = torch.from_numpy(g[0][0] + g[1][0])
+    gn = torch.from_numpy(g[0][1] + g[1][1])
+    for _ in range(2):
+        ref.adam_range(gm, gn, 0, n)
+    for r in range(2):
+        got = np.load(tmp_path / f"sharded{r}.npz")
+        assert np.array_equal(got["mu"], ref.mu)
+        assert np.array_equal(got["nrm"], ref.nrm)

@@ -121,3 +121,55 @@ def test_checkpoint_save_matches_reference_bytes(tmp_path):
     a, b = t.export(), t2.export()
     for k in ("topo", "order", "geo"):
         assert np.array_equal(a[k], b[k])
+
+
+def test_sharded_point_update_equals_full_step(oracle_mod):
+    """SURVEY 8(e) config-5 step on one GPU, the two ranks run one after the
+    other (no collective): rank r steps Adam on its point slice only
+    (dpl_point_adam_step_range), the slices are exchanged with
+    dpl_tree_get/set_points_range and both trees refresh their moments — the
+    parameters and query results equal a full PointAdam.step bit for bit."""
+    import torch
+
+    import paper_2405_16788_b200 as P
+    from paper_2405_16788_b200.bhtree import (PointAdam, get_points, get_points_range,
+                                              refresh_moments, set_points_range)
+    from paper_2405_16788_b200.parallel import TreeEngine, point_chunk, sharded_point_update
+
+    n, C = 2501, 4
+    pos, nrm, area, mu = cloud(n, 43, C)
+    kinds = np.array([0, 1, 1, 1], np.uint8)
+
+    def tree():
+        t = P.DipoleTree(0)
+        t.build(P.OrientedPointCloud(pos, nrm, area, mu))
+        t.set_channel_kernels(kinds)
+        return t
+
+    full, ranks, single = tree(), [tree(), tree()], tree()
+    opt_full = PointAdam(full, lr=1e-2)
+    opts = [PointAdam(t, lr=1e-2) for t in ranks]
+    eng = TreeEngine(single, PointAdam(single, lr=1e-2))  # sharded_point_update, one rank
+    rng = np.random.default_rng(44)
+    xs = rng.uniform(-1.2, 1.2, (600, 3))
+    p = P.KernelParams(epsilon=0.05)
+    for _ in range(2):
+        gm = rng.standard_normal((n, C)).astype(np.float32)
+        gn = rng.standard_normal((n, 3)).astype(np.float32)
+        opt_full.step(P.PointGradients(C, gm, gn, 0.0))
+        sharded_point_update(eng, torch.from_numpy(gm).cuda(), torch.from_numpy(gn).cuda(), n, C)
+        slices = []
+        for r, (t, o) in enumerate(zip(ranks, opts)):
+            lo, hi, _ = point_chunk(n, r, 2)
+            o.step_range(torch.from_numpy(gm[lo:hi]).cuda(), torch.from_numpy(gn[lo:hi]).cuda(), lo, hi)
+            slices.append((lo, hi) + get_points_range(t, lo, hi))
+        for t in ranks:
+            for lo, hi, sn, sm in slices:
+                set_points_range(t, lo, hi, sn, sm)
+            refresh_moments(t)
+    wn, wm = get_points(full)
+    want = full.primal(xs, p, 2.0)
+    for t in ranks + [single]:
+        gn_, gm_ = get_points(t)
+        assert np.array_equal(gm_, wm) and np.array_equal(gn_, wn)
+        assert np.array_equal(t.primal(xs, p, 2.0), want)
