@@ -309,7 +309,7 @@ def test_render_steps_switch_to_lists(eng, oracle_mod):
         assert abs(dl - res[0][4]) <= 1e-6 * abs(res[0][4]) + 1e-12
 
 
-@pytest.mark.parametrize("C", [2, 17, 33, 49, 65, 70])
+@pytest.mark.parametrize("C", [2, 4, 5, 17, 33, 49, 65, 70])
 def test_many_channel_forward_adjoint(eng, oracle_mod, C):
     """Config-2 channel layouts (1 Dipole + C-1 Radial, N(0,1) moments and
     upstream gradients): covers the two-phase kernels' column splits (<=32,
