@@ -704,7 +704,7 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
       for (int i = 0; i < n;) {
         const int4 tpi = rb[i].topo;
         const uint32_t src = (uint32_t)tpi.x;
-        if constexpr (FF) {
+        if constexpr (true) {  // FFMA and tensor-core phase B alike
           // two consecutive far entries without near lanes that fit the batch:
           // one interleaved pass (independent dependency chains for the
           // scheduler; groups of 4 measured no faster); batches fill exactly as
