@@ -296,8 +296,10 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
 #pragma unroll
     for (int ks = 0; ks < 4; ++ks) {
       const float b0 = wrow[8 * ks + tq], b1 = wrow[8 * ks + tq + 4];
-      const uint32_t h0 = to_tf32(b0), h1 = to_tf32(b1);
-      const uint32_t l0 = to_tf32(b0 - __uint_as_float(h0)), l1 = to_tf32(b1 - __uint_as_float(h1));
+      // truncating split, the residual read by the tensor core at tf32 precision
+      const uint32_t h0 = __float_as_uint(b0) & 0xffffe000u, h1 = __float_as_uint(b1) & 0xffffe000u;
+      const uint32_t l0 = __float_as_uint(b0 - __uint_as_float(h0));
+      const uint32_t l1 = __float_as_uint(b1 - __uint_as_float(h1));
 #pragma unroll
       for (int mt = 0; mt < (MT ? MT : 1); ++mt) {
         mma_tf32(d[mt], ahi[mt][ks], h0, h1);
@@ -323,16 +325,12 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
         const int e = 2 * tq + j;
-        if (e < nent) {
-          const int m = meta[e];
-          const int64_t src = m & ((1 << 29) - 1);
-          double* dst = (m & (1 << 30)) ? acc.pt_mur + src * Cr : acc.node_s + src * Cr;
+        double* dst = dptr[e];  // stale beyond nent: those REDs are predicated off
 #pragma unroll
-          for (int mt = 0; mt < (MT ? MT : 1); ++mt) {
-            const int c = 16 * mt + g;
-            if (c < nr && d[mt][j] != 0.f) atomicAdd(dst + c, (double)d[mt][j]);
-            if (c + 8 < nr && d[mt][2 + j] != 0.f) atomicAdd(dst + c + 8, (double)d[mt][2 + j]);
-          }
+        for (int mt = 0; mt < (MT ? MT : 1); ++mt) {
+          const int c = 16 * mt + g;
+          red_add_f32_if(dst + c, d[mt][j], e < nent && c < nr);
+          red_add_f32_if(dst + c + 8, d[mt][2 + j], e < nent && c + 8 < nr);
         }
       }
       // radial epsilon terms (:379, :409) for entries with a lane within 6.5 eps
@@ -818,10 +816,11 @@ static bool adj2_plan(const Tree& t, const KParams& kp, const AdjArgs& a, GradBu
   // into spills or lower occupancy) -> opt-in experiment.
   static const bool tc = getenv("DPL_ADJOINT_TC") != nullptr;
   if (tc) {  // rows staged up to the slots used
-    if (nr <= 16) return launch_adj2<0, GM, 4, 4, 8, 128, 1>(t, kp, a, b, nr), true;
-    if (nr <= 32) return launch_adj2<0, GM, 8, 4, 8, 128, 2>(t, kp, a, b, nr), true;
-    // best measured (warps, register cap) for the 48-channel tile: 2 warps, 160
-    if (nr <= 48) return launch_adj2<0, GM, 12, 2, 8, 160, 3>(t, kp, a, b, nr), true;
+    if (nr <= 16) return launch_adj2<0, GM, 4, 4, 8, 128, 1, true>(t, kp, a, b, nr), true;
+    if (nr <= 32) return launch_adj2<0, GM, 8, 4, 8, 128, 2, true>(t, kp, a, b, nr), true;
+    // best measured (warps, register cap) for the 48-channel tile: 2 warps at 160
+    // (2 at 144 / 136 and 4 at 128 spill and run slower)
+    if (nr <= 48) return launch_adj2<0, GM, 12, 2, 8, 160, 3, true>(t, kp, a, b, nr), true;
   }
   if (t.F4 - 1 > 16) return false;
   if (nr <= 4) return launch_adj2<3, GM, 1, 4, 8, 96, 0, true>(t, kp, a, b, nr), true;
