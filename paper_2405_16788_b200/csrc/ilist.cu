@@ -72,63 +72,64 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
   if (!active) return;  // evaluation kernels return for such warps too
   const QueryDF qx = make_qdf(x, tv.cmax);
   const double* xq = xs + 3 * qi;
+  const unsigned lanebit = 1u << lane;
 
   int cur = (int)wg;  // chunk being filled (warp w owns chunk w)
   int total = 0;      // entries written to the pool
-  bool ok = true;
   // entries are collected in registers — lane k holds entry k of the current
   // block of 32 — and written as one coalesced 256-byte store per block (a
-  // chunk holds 4 blocks, so a block never straddles two chunks)
+  // chunk holds 4 blocks, so a block never straddles two chunks). Returns false
+  // when the pool is exhausted: the warp then leaves its list incomplete (count
+  // -1) and the evaluation kernels walk the tree for it.
   uint2 pend = make_uint2(0u, 0u);
   int npend = 0;
-  auto flush = [&]() {
+  auto flush = [&]() -> bool {
     const int b = total >> 5;  // block index: total is a multiple of 32 here
     if (b > 0 && (b & 3) == 0) {  // chunk full: link a fresh one
       unsigned long long c = 0;
       if (lane == 0) c = atomicAdd(ctr, 1ull);
       c = __shfl_sync(FULL_MASK, c, 0);
-      if (c >= (unsigned long long)chunks) {  // pool exhausted: this warp traverses itself
-        ok = false;
-        return;
-      }
+      if (c >= (unsigned long long)chunks) return false;
       if (lane == 0) next[cur] = (int)c;
       cur = (int)c;
     }
     if (lane < npend) pool[(size_t)cur * IL_CHUNK + (b & 3) * 32 + lane] = pend;
     total += npend;
     npend = 0;
-  };
-  auto emit = [&](uint32_t src, uint32_t m) {
-    if (lane == npend) pend = make_uint2(src, m);
-    if (++npend == 32) flush();
+    return true;
   };
 
   int sp = 1;
   if (lane == 0) stk[0] = make_int2(0, (int)active);
   __syncwarp();
-  while (sp > 0 && ok) {
+  // the exhaustion exits are gotos, so the loop carries no status flag
+  while (sp > 0) {
     --sp;
+    // no __syncwarp after the pop: every lane has consumed e (the record
+    // address) before the ballot below, the warp's next convergence point,
+    // and pushes happen only after it
     const int2 e = stk[sp];
-    __syncwarp();
     const int node = e.x;
     const unsigned mask = (unsigned)e.y;
-    const bool mine = (mask >> lane) & 1u;
+    const bool mine = (mask & lanebit) != 0u;
     const NodeRec* rec = tv.node_rec + node;
     const float4 hi = __ldg(&rec->hi);
     const float4 lo = __ldg(&rec->lo);
     const int4 tp = __ldg(&rec->topo);
     float dx, dy, dz;
     const float s = dist2_df(hi, lo, qx, dx, dy, dz);
-    const bool far = mine && far_test(s, hi, qx, xq, tv.node_dec + node);
+    const bool far = far_test_masked(s, hi, qx, xq, tv.node_dec + node, mine);
     const unsigned farm = __ballot_sync(FULL_MASK, far);
     if (farm && lo.w > 0.f) {
       const bool nr = __any_sync(FULL_MASK, far && s < near_thr);
-      emit((uint32_t)node | (nr ? IL_NEAR : 0u), farm);
+      if (lane == npend) pend = make_uint2((uint32_t)node | (nr ? IL_NEAR : 0u), farm);
+      if (++npend == 32 && !flush()) goto exhausted;
     }
     const unsigned openm = mask & ~farm;
-    if (openm && ok) {
+    if (openm) {
       if (tp.y == 0) {
-        emit((uint32_t)node | IL_LEAF, openm);
+        if (lane == npend) pend = make_uint2((uint32_t)node | IL_LEAF, openm);
+        if (++npend == 32 && !flush()) goto exhausted;
       } else {
         if (sp + tp.y > DPL_STACK_PER_WARP) {
           if (lane == 0) atomicExch(overflow, 1);
@@ -140,8 +141,11 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
       }
     }
   }
-  if (ok && npend) flush();
-  if (lane == 0) count[wg] = ok ? total : -1;
+  if (npend && !flush()) goto exhausted;
+  if (lane == 0) count[wg] = total;
+  return;
+exhausted:
+  if (lane == 0) count[wg] = -1;
 }
 
 void ilist_build(const Tree& t, IList& il, const double* xs, const int32_t* perm, int64_t q,

@@ -105,6 +105,34 @@ __device__ __forceinline__ bool far_test(float s, const float4& hi, const QueryD
   return dist2_rn(a.x, a.y, b.x, x, ex, ey, ez) > b.y;
 }
 
+// exact fp64 opening test out of line: the call is one (predicated) instruction
+// on the common path, where an inlined body would be if-converted into ~17
+// predicated-off instructions issued on every pop
+static __device__ __noinline__ bool far_exact(const double* __restrict__ xq,
+                                              const double4* __restrict__ dec) {
+  const double2 a = __ldg(reinterpret_cast<const double2*>(dec));
+  const double2 b = __ldg(reinterpret_cast<const double2*>(dec) + 1);
+  const QueryPos x{xq[0], xq[1], xq[2]};
+  double ex, ey, ez;
+  return dist2_rn(a.x, a.y, b.x, x, ex, ey, ez) > b.y;
+}
+
+// The same decision with the lane mask folded in: every lane forms the fp32
+// verdict without a branch (|diff| > band decides by the sign of diff, as the
+// two one-sided tests above), and only member lanes inside the band (or with a
+// NaN / inf threshold) take the exact fp64 path. Bitwise the same decisions as
+// `mine && far_test(...)`, fewer instructions on the common path.
+__device__ __forceinline__ bool far_test_masked(float s, const float4& hi, const QueryDF& q,
+                                                const double* __restrict__ xq,
+                                                const double4* __restrict__ dec, bool mine) {
+  const float thr = hi.w;
+  const float band = 2e-6f * (s + thr) + q.m;
+  const float diff = s - thr;
+  bool far = mine && diff > 0.f;
+  if (mine && !(fabsf(diff) > band)) far = far_exact(xq, dec);
+  return far;
+}
+
 // exact fp64 coincidence check for a leaf point (bhtree.cpp:219,316,387)
 __device__ __forceinline__ bool coincident_exact(const double* __restrict__ p,
                                                  const double* __restrict__ xq) {
