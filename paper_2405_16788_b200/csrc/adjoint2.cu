@@ -21,7 +21,8 @@
 //     channel. The 4 per-lane vector quantities are reduced with one LDS.128,
 //     3 FADD and 3 shuffles and land in node_v / point_n / point_mu_0 with at
 //     most 4 REDs. Accumulators are fp64 (SURVEY §7 hard part 4).
-//   tensor-core phase B (MT > 0, the default for Cr <= 64): the radial product
+//   tensor-core phase B (MT > 0, opt-in with DPL_ADJOINT_TC=1; measured slower
+//     than the FFMA phase B on config 2, see adj2_plan): the radial product
 //     D[channel][entry] = sum_l dsT[channel][l] wR[entry][l] (and its epsilon
 //     twin with wE) runs on mma.sync: A = the warp's transposed d_out tile,
 //     held as TF32 fragments in registers for the whole traversal (16 MT
@@ -478,8 +479,30 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
   // far-field lane values beyond 6.5 eps (tau = 1: W = R / r, Wp_r = -3 W R, no
   // epsilon terms; kernels.cpp:50-55), branch-free: every lane evaluates,
   // non-far lanes select 0 (bhtree.cpp:361-376)
+  // REG: one select on the area instead of one per value (rsqrt_far keeps the
+  // non-member lanes finite, kept lanes are bit-identical)
   auto far_fast = [&](float A, float s, float fx, float fy, float fz, bool far, float& r_,
                       float& u0, float& u1, float& u2) {
+    if (REG) {
+      const float Am = sel0(far, A);
+      const float inv_r = rsqrt_far(s, kp.near2);
+      const float R = inv_r * inv_r;
+      r_ = Am * R;
+      if (GM == 0) {
+        const float aWds = Am * (R * inv_r) * ds0;
+        u0 = aWds * fx, u1 = aWds * fy, u2 = aWds * fz;
+      } else {  // with the query-gradient adjoint d_grad (:372-376)
+        const float W = R * inv_r;
+        const float Wp_r = -3.0f * W * R;
+        const float aWds = Am * W * ds0;
+        const float gd = fmaf(dg0, fx, fmaf(dg1, fy, dg2 * fz));
+        const float t = Wp_r * gd;
+        u0 = aWds * fx - Am * fmaf(W, dg0, t * fx);
+        u1 = aWds * fy - Am * fmaf(W, dg1, t * fy);
+        u2 = aWds * fz - Am * fmaf(W, dg2, t * fz);
+      }
+      return;
+    }
     const float inv_r = rsqrt_pos(s);
     const float R = inv_r * inv_r;
     r_ = sel0(far, A * R);
@@ -794,7 +817,7 @@ static void launch_adj2c(const Tree& t, const KParams& kp, const AdjArgs& a, Gra
 template <int NB, int GM, int RR, int WARPS = 4, int ENT = 8, int MAXR = 128, int MT = 0,
           bool SPEC = false>
 static void launch_adj2(const Tree& t, const KParams& kp, const AdjArgs& a, GradBuf& b, int nr) {
-  const bool reg = SPEC && kp.mode == KM_REGULARIZED;
+  const bool reg = SPEC && kp.mode == KM_REGULARIZED && kp.near2 >= REG_MIN_NEAR2;
   if (a.ilist && !no_ilist()) {
     ilist_build(t, *a.ilist, a.xs, a.perm, a.q, a.beta, ilist_near_thr(kp), a.overflow);
     if (reg)

@@ -99,6 +99,12 @@ struct ChanMap {
 
 inline int round_up4(int x) { return (x + 3) & ~3; }
 
+// smallest (6.5 eps)^2 for which the regularized-mode kernels zero a far
+// entry's non-member lanes through their area: R <= 1e12, W <= 1e18 and the
+// query-gradient term W R <= 1e30 stay finite (eps >= 1.6e-7; smaller eps runs
+// the generic kernels)
+constexpr float REG_MIN_NEAR2 = 1e-12f;
+
 #ifdef __CUDACC__
 // 1/sqrt(x): the MUFU.RSQ that rsqrtf issues for normal inputs (bit-identical
 // there), without rsqrtf's denormal rescaling — x is clamped to FLT_MIN instead.
@@ -107,6 +113,16 @@ inline int round_up4(int x) { return (x + 3) & ~3; }
 __device__ __forceinline__ float rsqrt_pos(float x) {
   float r;
   asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(fmaxf(x, 1.17549435e-38f)));
+  return r;
+}
+
+// 1/sqrt(max(x, m)) for the regularized far field beyond 6.5 eps: every lane
+// whose value is kept has x >= m = (6.5 eps)^2, so the clamp changes nothing
+// for it; the other lanes get a finite W <= m^-1.5 (hosts only pick these
+// kernels when m >= REG_MIN_NEAR2), which their zeroed area turns into exact 0s
+__device__ __forceinline__ float rsqrt_far(float x, float m) {
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(fmaxf(x, m)));
   return r;
 }
 

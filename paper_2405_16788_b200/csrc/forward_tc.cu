@@ -70,6 +70,16 @@ __device__ __forceinline__ float4 fwd_w_far(float fx, float fy, float fz, float 
   return make_float4(aW * fx, aW * fy, aW * fz, A * R);
 }
 
+// fwd_w_far with the non-member lanes' area already zeroed (regularized
+// kernels: members have r2 >= near2, see rsqrt_far)
+__device__ __forceinline__ float4 fwd_w_far_m(float fx, float fy, float fz, float r2, float Am,
+                                              float near2) {
+  const float inv_r = rsqrt_far(r2, near2);
+  const float R = inv_r * inv_r;
+  const float aW = Am * (R * inv_r);
+  return make_float4(aW * fx, aW * fy, aW * fz, Am * R);
+}
+
 constexpr int row_stride_floats(int f4) {
   int r = 4 * f4;
   while (r % 32 != 8 && r % 32 != 24) r += 4;
@@ -236,11 +246,18 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
           const float sa = dist2_df(ha, la, qx, ax, ay, az);
           const float sb = dist2_df(hb, lb, qx, bx, by, bz);
           const bool fa = ((unsigned)tpi.y >> lane) & 1u, fb = ((unsigned)tb.y >> lane) & 1u;
-          const float4 wa = fwd_w_far(ax, ay, az, sa, la.w), wb = fwd_w_far(bx, by, bz, sb, lb.w);
-          store_entry(make_float4(fa ? wa.x : 0.f, fa ? wa.y : 0.f, fa ? wa.z : 0.f, fa ? wa.w : 0.f),
-                      node_row + (size_t)(src & IL_NODE) * F4g);
-          store_entry(make_float4(fb ? wb.x : 0.f, fb ? wb.y : 0.f, fb ? wb.z : 0.f, fb ? wb.w : 0.f),
-                      node_row + (size_t)((uint32_t)tb.x & IL_NODE) * F4g);
+          if (REG) {  // one select on the area per entry (see rsqrt_far)
+            store_entry(fwd_w_far_m(ax, ay, az, sa, sel0(fa, la.w), kp.near2),
+                        node_row + (size_t)(src & IL_NODE) * F4g);
+            store_entry(fwd_w_far_m(bx, by, bz, sb, sel0(fb, lb.w), kp.near2),
+                        node_row + (size_t)((uint32_t)tb.x & IL_NODE) * F4g);
+          } else {
+            const float4 wa = fwd_w_far(ax, ay, az, sa, la.w), wb = fwd_w_far(bx, by, bz, sb, lb.w);
+            store_entry(make_float4(fa ? wa.x : 0.f, fa ? wa.y : 0.f, fa ? wa.z : 0.f, fa ? wa.w : 0.f),
+                        node_row + (size_t)(src & IL_NODE) * F4g);
+            store_entry(make_float4(fb ? wb.x : 0.f, fb ? wb.y : 0.f, fb ? wb.z : 0.f, fb ? wb.w : 0.f),
+                        node_row + (size_t)((uint32_t)tb.x & IL_NODE) * F4g);
+          }
           ++i;
           continue;
         }
@@ -254,6 +271,8 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
           float4 wv;
           if (src & IL_NEAR) {
             wv = mine ? fwd_w(dx, dy, dz, s, lo.w, kp) : make_float4(0.f, 0.f, 0.f, 0.f);
+          } else if (REG) {  // branch-free, one select on the area
+            wv = fwd_w_far_m(dx, dy, dz, s, sel0(mine, lo.w), kp.near2);
           } else {  // branch-free: every lane evaluates, non-members select 0
             const float4 f = fwd_w_far(dx, dy, dz, s, lo.w);
             wv.x = mine ? f.x : 0.f, wv.y = mine ? f.y : 0.f;
@@ -388,7 +407,7 @@ static void launch_tc1(const Tree& t, const KParams& kp, const FwdArgs& a, int n
 // SPEC: also instantiate the regularized-mode kernels (production configurations)
 template <int NT, int WARPS, int ENT, int MAXR, bool SPEC = false>
 static void launch_tc(const Tree& t, const KParams& kp, const FwdArgs& a, int nr) {
-  const bool reg = SPEC && kp.mode == KM_REGULARIZED;
+  const bool reg = SPEC && kp.mode == KM_REGULARIZED && kp.near2 >= REG_MIN_NEAR2;
   if (a.counters) {
     launch_tc1<NT, WARPS, ENT, MAXR, true, false>(t, kp, a, nr);
   } else if (a.ilist && !no_ilist()) {
