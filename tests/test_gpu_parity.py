@@ -344,6 +344,41 @@ def test_many_channel_forward_adjoint(eng, oracle_mod, C):
     assert abs(g.d_epsilon - we) <= 1e-4 * abs(we) + 1e-6
 
 
+@pytest.mark.parametrize("eps", [1e-8, 0.06])
+def test_regularized_specialisation_bounds(eng, oracle_mod, eps):
+    """The regularized kernels zero a far entry's non-member lanes through their
+    area with 1/r clamped at (6.5 eps)^2; they are chosen only when
+    (6.5 eps)^2 >= 1e-12. eps = 1e-8 takes the generic kernels, eps = 0.06 the
+    specialised ones; both batches hold queries ON data points (r = 0 for the
+    lanes that are not members of those points' far entries)."""
+    O = oracle_mod
+    C = 49
+    rng = np.random.default_rng(7)
+    pos, nrm, area, _ = random_cloud(3000, 77, 1)
+    mu = rng.standard_normal((3000, C))
+    kinds = np.ones(C, np.uint8)
+    kinds[0] = 0
+    t, r = make(eng, O, pos, nrm, area, mu, kinds)
+    xs = rng.uniform(-1.5, 1.5, (1500, 3)).astype(np.float32).astype(np.float64)
+    xs[::25] = pos[rng.choice(3000, len(xs[::25]), replace=False)]
+    p = eng.KernelParams(epsilon=eps)
+    want = r.primal(O.Params(eps), 2.0, xs)
+    d_out = rng.standard_normal((len(xs), C)).astype(np.float32)
+    wm, wn, we = r.adjoint(O.Params(eps), 2.0, xs, d_out.astype(np.float64))
+    for _ in range(2):  # the second primal -> adjoint pair replays interaction lists
+        got = t.primal(xs, p, 2.0)
+        assert np.isfinite(got).all()
+        nbad, mx = close(got, want)
+        assert nbad == 0, (nbad, mx)
+        buf = t.make_buffer()
+        t.adjoint(xs, p, 2.0, d_out, None, buf)
+        g = t.flush_gradients(buf)
+        assert np.isfinite(g.moments).all() and np.isfinite(g.normals).all()
+        assert rel_scale_err(g.moments, wm) < 1e-5
+        assert rel_scale_err(g.normals, wn) < 1e-5
+        assert abs(g.d_epsilon - we) <= 1e-4 * abs(we) + 1e-6
+
+
 # ---------------------------------------------------------------- errors
 def test_error_behaviour(eng, oracle_mod):
     t = eng.DipoleTree(0)
