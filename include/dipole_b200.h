@@ -2,7 +2,7 @@
  *
  * This is the drop-in boundary for the reference's hot path
  * (`dipole::DipoleTree`, proj/include/dipole/bhtree.hpp:51-130, and the render
- * step proj/include/dipole/renderer.hpp:365-385). The reference is a C++20
+ * step proj/include/dipole/renderer.hpp:86-106). The reference is a C++20
  * library with no FFI; a maintainer swapping the CPU tree for this engine binds
  * these symbols from C++ (include/dipole_b200.hpp re-exposes the reference
  * class API on top of them) or from Python via ctypes.
@@ -45,7 +45,7 @@ typedef struct dpl_tree_s* dpl_tree_t;
 typedef struct dpl_gradbuf_s* dpl_gradbuf_t;
 typedef struct dpl_tape_s* dpl_tape_t;
 
-/* KernelParams (kernels.hpp:156-161); epsilon <= 0 selects the singular kernel */
+/* KernelParams (kernels.hpp:24-29); epsilon <= 0 selects the singular kernel */
 typedef struct {
   double epsilon;
   int32_t desingularized;
@@ -67,7 +67,10 @@ int dpl_version(void);
 int64_t dpl_launch_count(void);
 
 /* ---- tree lifecycle: DipoleTree::build / update_moments / set_channel_kernels */
-/* stream: a cudaStream_t, or NULL for a library-owned non-blocking stream. */
+/* stream: a cudaStream_t, or NULL for a library-owned BLOCKING stream
+ * (cudaStreamDefault flags): it orders against the legacy default stream, so
+ * device arrays produced there (e.g. by torch) are complete before the tree's
+ * kernels read them. */
 int dpl_tree_create(int device, void* stream, dpl_tree_t* out);
 int dpl_tree_destroy(dpl_tree_t tree);
 int dpl_tree_set_stream(dpl_tree_t tree, void* stream);
@@ -198,7 +201,7 @@ int dpl_flush(dpl_tree_t tree, dpl_gradbuf_t* bufs, int32_t nbuf, float* moments
  * Rays are (origin, dir) fp64 (R x 6). Samples per ray: S; when ts is NULL the
  * stratified sampler t_j = t_near + (t_far - t_near) * ((j + u_j) / S) with
  * u_j = dpl_uniform(seed, ray * S + j) is used (identical bits in the oracle);
- * otherwise ts / deltas are R x S fp64 (RaySamples, renderer.hpp:322-326).
+ * otherwise ts / deltas are R x S fp64 (RaySamples, renderer.hpp:43-47).
  * The head is direct-rgb (radiance.cpp:133-145): rgb = logistic(D_1..3). */
 typedef struct {
   double lambda_scale;   /* SceneModel::lambda_scale (fields.hpp:17) */

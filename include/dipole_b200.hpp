@@ -38,7 +38,7 @@ inline void check(int rc) {
 
 enum class ChannelKernel : uint8_t { Dipole = DPL_DIPOLE, Radial = DPL_RADIAL };
 
-struct KernelParams {  // kernels.hpp:156-161
+struct KernelParams {  // kernels.hpp:24-29
   double epsilon = 0.0;
   bool desingularized = false;
   double desing_delta = 0.0;

@@ -29,7 +29,7 @@ _up = C.POINTER(C.c_uint8)
 
 
 class Params(C.Structure):
-    """KernelParams (kernels.hpp:156-161) / dpl_kernel_params."""
+    """KernelParams (kernels.hpp:24-29) / dpl_kernel_params."""
 
     _fields_ = [
         ("epsilon", C.c_double),

@@ -32,7 +32,7 @@ class CudaError(RuntimeError):
 
 
 class KernelParams(C.Structure):
-    """KernelParams (kernels.hpp:156-161) == dpl_kernel_params."""
+    """KernelParams (kernels.hpp:24-29) == dpl_kernel_params."""
 
     _fields_ = [("epsilon", C.c_double), ("desingularized", C.c_int32), ("reserved", C.c_int32),
                 ("desing_delta", C.c_double), ("coincident_value", C.c_double)]

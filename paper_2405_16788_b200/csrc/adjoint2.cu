@@ -798,12 +798,8 @@ template <int NB, int GM, int RR, int WARPS, int ENT, int MAXR, int MT, bool LIS
 static void launch_adj2c(const Tree& t, const KParams& kp, const AdjArgs& a, GradBuf& b, int nr,
                          IListView lv) {
   const size_t smem = (size_t)WARPS * AdjLayout<MT, ENT, RR, NB == 3>::WARP_FLOATS * 4;
-  static bool attr = false;
-  if (!attr) {
-    DPL_CUDA(cudaFuncSetAttribute(k_adjoint2<NB, GM, WARPS, ENT, RR, MAXR, MT, LIST, REG>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
-  }
+  static std::atomic<unsigned long long> attr{0};
+  ensure_max_dyn_smem(k_adjoint2<NB, GM, WARPS, ENT, RR, MAXR, MT, LIST, REG>, t.device, smem, attr);
   Adj2Ptrs p{b.node_v, b.node_s, b.pt_mud, b.pt_mur, b.pt_n, b.d_eps};
   unsigned blocks = (unsigned)((a.q + WARPS * 32 - 1) / (WARPS * 32));
   k_adjoint2<NB, GM, WARPS, ENT, RR, MAXR, MT, LIST, REG><<<blocks, WARPS * 32, smem, t.stream>>>(

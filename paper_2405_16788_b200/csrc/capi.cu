@@ -1103,8 +1103,11 @@ double dpl_uniform(uint64_t seed, uint64_t counter) { return host_uniform(seed, 
 
 static void check_render_layout(Tree& t) {
   require(t.C >= 4, DPL_ERR_DATA, "direct-rgb head needs at least 3 appearance channels");
-  require(t.kinds[0] == 0 && t.kinds[1] == 1 && t.kinds[2] == 1 && t.kinds[3] == 1, DPL_ERR_DATA,
-          "render step expects SceneModel's layout: channel 0 Dipole, 1..K Radial");
+  // every channel, not only the ones the direct-rgb head reads: the render
+  // kernels address dipole slots by channel (SceneModel::prepare, fields.cpp:15-17)
+  bool ok = t.kinds[0] == 0;
+  for (int c = 1; c < t.C; ++c) ok = ok && t.kinds[c] == 1;
+  require(ok, DPL_ERR_DATA, "render step expects SceneModel's layout: channel 0 Dipole, 1..K Radial");
 }
 
 int dpl_render_forward(dpl_tree_t h, const dpl_kernel_params* params, const dpl_render_params* rp,

@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <stdexcept>
 #include <string>
 
@@ -40,6 +41,18 @@ struct Error : std::runtime_error {
   } while (0)
 
 void count_launch(int n = 1);
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is a per-device property of
+// a kernel: `done` keeps one bit per device (benign race: two threads may both
+// set the same attribute value).
+template <typename K>
+inline void ensure_max_dyn_smem(K* kernel, int device, size_t smem,
+                                std::atomic<unsigned long long>& done) {
+  const unsigned long long bit = 1ull << (device & 63);
+  if (done.load(std::memory_order_acquire) & bit) return;
+  DPL_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  done.fetch_or(bit, std::memory_order_acq_rel);
+}
 
 // kernel radial-profile mode
 enum KMode : int { KM_REGULARIZED = 0, KM_SINGULAR = 1, KM_DESING = 2 };

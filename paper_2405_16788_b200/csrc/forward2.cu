@@ -209,12 +209,8 @@ template <int TD, int TR, int WARPS, int ENT, int MAXR, bool COUNT>
 static void launch2c(const Tree& t, const KParams& kp, const FwdArgs& a, int nd, int nr) {
   constexpr int F4 = TD + TR / 4;
   const size_t smem = (size_t)WARPS * (ENT * 32 + ENT * F4 + DPL_STACK_PER_WARP / 2) * 16;
-  static bool attr = false;
-  if (!attr) {
-    DPL_CUDA(cudaFuncSetAttribute(k_forward2<TD, TR, WARPS, ENT, MAXR, COUNT>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
-  }
+  static std::atomic<unsigned long long> attr{0};
+  ensure_max_dyn_smem(k_forward2<TD, TR, WARPS, ENT, MAXR, COUNT>, t.device, smem, attr);
   unsigned blocks = (unsigned)((a.q + WARPS * 32 - 1) / (WARPS * 32));
   k_forward2<TD, TR, WARPS, ENT, MAXR, COUNT><<<blocks, WARPS * 32, smem, t.stream>>>(
       t.view(), kp, a.xs, a.perm, a.q, nd, nr, t.chmap.as<int>(), a.out, a.out_stride, a.only_ch,

@@ -391,12 +391,8 @@ static void launch_tc1(const Tree& t, const KParams& kp, const FwdArgs& a, int n
   constexpr int RSF = row_stride_floats(F4);
   constexpr int WARP_FLOATS = ENT * 32 * 4 + ENT * 40 + ENT * RSF + 2 * DPL_STACK_PER_WARP;
   const size_t smem = (size_t)WARPS * WARP_FLOATS * 4;
-  static bool attr = false;
-  if (!attr) {
-    DPL_CUDA(cudaFuncSetAttribute(k_forward_tc<NT, WARPS, ENT, MAXR, COUNT, LIST, REG>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
-  }
+  static std::atomic<unsigned long long> attr{0};
+  ensure_max_dyn_smem(k_forward_tc<NT, WARPS, ENT, MAXR, COUNT, LIST, REG>, t.device, smem, attr);
   unsigned blocks = (unsigned)((a.q + WARPS * 32 - 1) / (WARPS * 32));
   k_forward_tc<NT, WARPS, ENT, MAXR, COUNT, LIST, REG><<<blocks, WARPS * 32, smem, t.stream>>>(
       t.view(), kp, a.xs, a.perm, a.q, nr, t.chmap.as<int>(), a.out, a.out_stride, a.only_ch,

@@ -863,9 +863,13 @@ __global__ void k_full_moments(int64_t nodes, int C, const int4* __restrict__ to
   if (a > 0) {
     for (int32_t j = tp.z; j < tp.w; ++j) {
       int64_t m = order[j];
-      double am = area[m] * mu[m * C + c];
-      v0 += am * nrm[3 * m], v1 += am * nrm[3 * m + 1], v2 += am * nrm[3 * m + 2];
-      s += am;
+      // the reference rounds am * normal before the add (bhtree.cpp:146-147):
+      // explicit _rn intrinsics keep nvcc from contracting them into an FMA
+      double am = __dmul_rn(area[m], mu[m * C + c]);
+      v0 = __dadd_rn(v0, __dmul_rn(am, nrm[3 * m]));
+      v1 = __dadd_rn(v1, __dmul_rn(am, nrm[3 * m + 1]));
+      v2 = __dadd_rn(v2, __dmul_rn(am, nrm[3 * m + 2]));
+      s = __dadd_rn(s, am);
     }
     v0 /= a, v1 /= a, v2 /= a, s /= a;
   }
