@@ -1,29 +1,40 @@
 #!/usr/bin/env python
 """bench.py — Barnes-Hut dipole-sum queries/sec on B200 (BASELINE.json metric).
 
-Workload (N=1 default): BASELINE config 2 — N = 1,000,000 points (95% noisy
-torus + 5% outliers), C = 49 channels (ch 0 Dipole, 1..48 Radial), Q = 4,000,000
-uniform queries in [-2,2]^3, beta = 2, leaf 8, eps = 1.5 x mean 8-NN spacing.
-One STEP = forward primal of all Q queries + adjoint of the same Q queries with
-N(0,1) upstream gradients + flush_gradients (push-down to per-point gradients);
-with N > 1 GPUs each rank owns its own Q queries (weak scaling) against a
-replicated tree and the per-point gradients are NCCL-allreduced every step.
+Workload (default): BASELINE config 4 — N = 8,000,000 points (64 random
+spheres / tori + 3% outliers), C = 49 channels (ch 0 Dipole, 1..48 Radial),
+Q = 64,000,000 Morton-unsorted uniform queries in [-2,2]^3, beta = 2, leaf 8,
+eps = 1.5 x mean 8-NN spacing (the reference's value, recorded in workloads).
+One STEP = forward primal of all Q queries + adjoint of the same Q queries
+with N(0,1) upstream gradients + flush_gradients. With N GPUs the Q queries of
+the step are sharded (STRONG scaling: every rank takes a contiguous 1/N of the
+same global batch) against a replicated, bit-identical tree, and the per-point
+gradients (moments, normals, d_eps) are NCCL-all-reduced in point chunks
+overlapped with the gradient push-down (parallel.flush_allreduce).
 
-value = (N_ranks x Q) / step time  [queries/s; each query is evaluated forward
-and adjoint], max over ranks, CUDA events, inputs resident in HBM. e2e = the
-same through the public API from pinned HOST buffers (H2D of queries and
-upstream gradients, D2H of outputs and gradients inside the timed region).
-Inputs per step (~0.9 GB) exceed the 126 MB L2, so no explicit L2 flush.
+value = Q / step time [queries/s; every query is evaluated forward AND
+adjoint], CUDA events on the tree's stream, max over ranks, inputs resident in
+HBM. e2e = the same through the public API from pinned HOST buffers (H2D of the
+queries once per step and of d_out, D2H of the outputs and point gradients,
+all inside the timed region). Step inputs (1.5 GB queries + 12.5 GB d_out at
+N=1) exceed the 126 MB L2, so no explicit flush.
 
---impl reference: the reference's own CPU path (oracle/_ref, compiled from
-/root/reference sources unmodified) on the box's host cores, on a bounded
-query sample of the same workload; rank 0 only.
+`python bench.py --gpus N` without WORLD_SIZE in the environment launches N
+ranks itself (torch.distributed.run on 127.0.0.1); under torchrun it is one
+rank. --config 2 selects BASELINE config 2 (N=1e6, Q=4e6) instead; at N=1 the
+config-4 line also carries config 2 under "extra".
+
+--impl reference: the reference's own CPU path (oracle/_ref, compiled from the
+reference's sources unmodified) on the box's host cores, on a fixed 1M-query
+subset of the same config-4 batch; rank 0 only.
 """
 from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -45,11 +56,16 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=4, choices=[2, 4])
     ap.add_argument("--scale", type=float, default=1.0, help="shrink N and Q (development only)")
+    ap.add_argument("--chunks", type=int, default=8, help="point chunks of the overlapped all-reduce")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--cpu-sample", type=int, default=400_000,
-                    help="queries per reference CPU sample (bounded: ~20 s on 16 cores)")
+    ap.add_argument("--no-extra", action="store_true", help="skip the config-2 extra line")
+    ap.add_argument("--ref-subset", type=int, default=1_000_000,
+                    help="reference arm: queries of the fixed subset covered by the timed steps")
+    ap.add_argument("--ref-workers", type=int, default=4,
+                    help="reference arm: adjoint GradientBuffers (SURVEY §8(d): <= 4 at config 4)")
     return ap.parse_args()
 
 
@@ -75,7 +91,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -129,76 +145,44 @@ def flops_model(tot, Cd, Cr):
     return fwd, adj
 
 
-# ------------------------------------------------------------------ reference arm
-def reference_measure(w, eps, sample, steps=None, warmup=0, threads=None):
-    """Reference CPU path (oracle/_ref): DipoleTree::primal over a query sample with
-    parallel_for, adjoint with one GradientBuffer per worker, flush_gradients."""
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import oracle as O
-    from paper_2405_16788_b200 import workloads as W
+# ------------------------------------------------------------------ workloads
+class Workload:
+    """One BASELINE configuration, with this rank's shard of the global query
+    batches (strong scaling: the global batch is the same for every rank count)."""
 
-    if not O.have_ref():
-        raise RuntimeError("oracle/_ref/libdipole_ref.so missing (built by __graft_entry__.build())")
-    c = w["cloud"]
-    t0 = time.time()
-    tree = O.OracleTree(O.Cloud(c.positions, c.normals, c.areas, c.moments), backend="ref")
-    tree.set_kinds(w["kinds"])
-    build_s = time.time() - t0
-    cores = threads or O.ref_lib().ref_hardware_concurrency()
-    # adjoint buffers are ~ (nodes*C*4 + N*(C+3)) doubles per worker (bhtree.cpp:336-343)
-    nodes = tree.node_count()
-    buf_bytes = 8.0 * (nodes * c.channels * 4 + c.size * (c.channels + 3))
-    try:
-        import psutil
+    def __init__(self, config, scale, rank, world, queries=True):
+        from paper_2405_16788_b200 import parallel as Pl
+        from paper_2405_16788_b200 import workloads as W
 
-        avail = psutil.virtual_memory().available
-    except Exception:
-        avail = 16e9
-    adj_workers = int(max(1, min(cores, 0.5 * avail // buf_bytes)))
-    p = O.Params(eps)
-    xs_all = w["xs"]
-    C = c.channels
-
-    def one(qs):
-        xs = xs_all[:qs]
-        d_out = W.upstream(qs, C, w.get("d_out_seed", [0, 2])).astype(np.float64)
-        t = time.time()
-        tree.primal(p, BETA, xs, threads=cores)
-        tf = time.time() - t
-        t = time.time()
-        tree.adjoint(p, BETA, xs, d_out, threads=adj_workers)
-        ta = time.time() - t
-        return tf, ta
-
-    # The reference adjoint has a per-step fixed cost independent of the query
-    # count: allocating / zeroing one GradientBuffer per worker and the
-    # single-threaded flush_gradients (bhtree.cpp:419-459). Calibrate it with a
-    # tiny batch, then time bounded samples and extrapolate the FULL workload's
-    # step (Q forward + Q adjoint + one flush) — amortising the fixed cost over
-    # Q queries, i.e. the reference's best case. The sample is a fixed-size
-    # prefix of the workload's queries (bounded CPU time, not the whole step).
-    Q = xs_all.shape[0]
-    q0 = 256
-    _, fixed = one(q0)
-    n_steps = 1 if steps is None else steps + warmup
-    sample = int(min(Q, max(q0 * 4, sample)))
-    times = []
-    for i in range(n_steps):
-        tf, ta = one(sample)
-        if steps is None or i >= warmup:
-            times.append((tf, ta))
-    tf = float(np.mean([x[0] for x in times]))
-    ta = float(np.mean([x[1] for x in times]))
-    ta_q = max(1e-12, (ta - fixed) / sample)  # per-query adjoint cost
-    full_fwd = Q * tf / sample
-    full_adj = Q * ta_q + fixed
-    return dict(value=Q / (full_fwd + full_adj), forward_qps=sample / tf,
-                adjoint_qps=Q / full_adj, sample=sample, cores=cores, adjoint_workers=adj_workers,
-                build_s=build_s, ms_per_step=1e3 * (full_fwd + full_adj),
-                measured={"sample_forward_s": tf, "sample_adjoint_flush_s": ta,
-                          "fixed_flush_buffers_s": fixed, "extrapolated_to_queries": Q})
+        self.config = config
+        if config == 4:
+            w = W.config4(scale=scale, queries=False)
+            self.q_total = w["q"]
+            self.eps = W.EPSILON["config4"] / math.sqrt(scale)
+            self.desc = ("config4: N=8e6 (64 spheres/tori + 3% outliers), C=49 (1 Dipole + 48 "
+                         "Radial), Q=64e6 Morton-unsorted uniform queries in [-2,2]^3, beta=2, leaf 8, "
+                         "forward+adjoint+flush per step")
+            lo, hi = Pl.shard_range(self.q_total, rank, world)
+            self.lo, self.hi = lo, hi
+            self.batches = ([W.config4_queries(lo, hi, batch=b) for b in (0, 1)] if queries
+                            else None)
+        else:
+            w = W.config2(scale=scale)
+            self.q_total = w["xs"].shape[0]
+            self.eps = W.epsilon_for("config2", scale)
+            self.desc = ("config2: N=1e6 torus+outliers, C=49 (1 Dipole + 48 Radial), Q=4e6 "
+                         "uniform queries in [-2,2]^3, beta=2, leaf 8, forward+adjoint+flush per step")
+            lo, hi = Pl.shard_range(self.q_total, rank, world)
+            self.lo, self.hi = lo, hi
+            b1 = W.step_queries(w, 0, 1)
+            self.batches = [w["xs"][lo:hi], b1[lo:hi]] if queries else None
+            self.xs0_full = w["xs"]
+        self.cloud = w["cloud"]
+        self.kinds = w["kinds"]
+        self.name = w["name"]
 
 
+# ------------------------------------------------------------------ reference (CPU)
 def cpu_info():
     try:
         out = subprocess.run(["lscpu"], capture_output=True, text=True).stdout
@@ -210,94 +194,160 @@ def cpu_info():
     return "unknown"
 
 
+def ref_tree(wl):
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+
+    if not O.have_ref():
+        raise RuntimeError("oracle/_ref/libdipole_ref.so missing (built by __graft_entry__.build())")
+    c = wl.cloud
+    t0 = time.time()
+    tree = O.OracleTree(O.Cloud(c.positions, c.normals, c.areas, c.moments), backend="ref")
+    tree.set_kinds(wl.kinds)
+    return O, tree, time.time() - t0
+
+
+def ref_workers(tree, want):
+    """Adjoint GradientBuffers: <= want, and <= what half the host RAM holds
+    (each is nodes x C x 4 + N x (C + 3) doubles, bhtree.cpp:336-343)."""
+    bb = 8.0 * (tree.node_count() * tree.C * 4 + tree.n * (tree.C + 3))
+    try:
+        import psutil
+
+        avail = psutil.virtual_memory().available
+    except Exception:
+        avail = 16e9
+    return int(max(1, min(want, 0.5 * avail // bb))), bb
+
+
+def reference_sample(O, tree, wl, n_fwd, n_adj, workers, threads):
+    """Reference path on bounded samples: DipoleTree::primal over n_fwd queries
+    (parallel_for, `threads` workers), adjoint over n_adj queries into `workers`
+    caller-held GradientBuffers, one flush_gradients. Returns per-query costs and
+    the per-step fixed cost (buffer setup + flush), and the extrapolated rate."""
+    from paper_2405_16788_b200 import workloads as W
+
+    p = O.Params(wl.eps)
+    xs = W.config4_queries(0, max(n_fwd, n_adj)) if wl.config == 4 else wl.xs0_full[:max(n_fwd, n_adj)]
+    d_out = W.upstream(n_adj, tree.C, [11, 0]).astype(np.float64)
+    t = time.time()
+    tree.primal(p, BETA, xs[:n_fwd], threads=threads)
+    tf = time.time() - t
+    t = time.time()
+    bufs = tree.gradient_buffers(workers)
+    tsetup = time.time() - t
+    t = time.time()
+    bufs.adjoint(p, BETA, xs[:n_adj], d_out)
+    ta = time.time() - t
+    t = time.time()
+    bufs.flush(want=False)
+    tflush = time.time() - t
+    del bufs
+    Q = wl.q_total
+    full = Q * tf / n_fwd + Q * ta / n_adj + tsetup + tflush
+    return dict(value=Q / full, full_step_s=full, forward_qps=n_fwd / tf, adjoint_qps=n_adj / ta,
+                t_forward_s=tf, t_adjoint_s=ta, t_buffer_setup_s=tsetup, t_flush_s=tflush)
+
+
 def run_reference(args):
     rank, world, _ = env_rank()
     if rank != 0:
         return
     from paper_2405_16788_b200 import workloads as W
 
-    w = W.config2(scale=args.scale)
-    eps = W.epsilon_for("config2", args.scale)
-    # >= 25 s per step: the adjoint's fixed cost (~14 s of GradientBuffer
-    # allocation + flush on 16 workers) must not dominate the per-query fit
-    # each reference step pays ~14 s of per-call GradientBuffer setup + flush on
-    # config 2; shrink the per-step sample for long runs so the arm stays bounded
-    n = args.steps + args.warmup
-    sample = args.cpu_sample if n <= 8 else max(50_000, args.cpu_sample * 8 // n)
-    r = reference_measure(w, eps, sample, steps=args.steps, warmup=args.warmup)
-    sample_desc = (f"{r['sample']} of {w['xs'].shape[0]} config-2 queries timed per step (forward + "
-                   f"adjoint + flush, {r['adjoint_workers']} GradientBuffers); full-workload step "
-                   f"extrapolated as Q*t_query + fixed flush cost; reference sources compiled -O3 "
-                   f"without -march; CPU {cpu_info()}")
+    wl = Workload(args.config, args.scale, 0, 1, queries=False)
+    O, tree, build_s = ref_tree(wl)
+    cores = O.ref_lib().ref_hardware_concurrency()
+    workers, buf_bytes = ref_workers(tree, args.ref_workers)
+    p = O.Params(wl.eps)
+    C = tree.C
+    Q = wl.q_total
+    # fixed subset: the first `sub` queries of the step's batch (the batch is
+    # i.i.d. uniform, so a prefix is a random subset); the timed steps cover it
+    # in K contiguous slices; warm-up steps use small slices after it
+    sub = int(min(Q, args.ref_subset))
+    K, Wm = max(1, args.steps), max(0, args.warmup)
+    s = -(-sub // K)
+    wq = max(1, min(2000, s))
+    xq = (W.config4_queries(0, sub + Wm * wq) if wl.config == 4
+          else W.config2(scale=args.scale)["xs"][:sub + Wm * wq])
+    d_out = W.upstream(xq.shape[0], C, [11, 1]).astype(np.float64)
+    t = time.time()
+    bufs = tree.gradient_buffers(workers)  # make_buffer per worker (per-step fixed cost)
+    t_setup = time.time() - t
+    for i in range(Wm):
+        a, b = sub + i * wq, sub + (i + 1) * wq
+        tree.primal(p, BETA, xq[a:b], threads=cores)
+        bufs.adjoint(p, BETA, xq[a:b], d_out[a:b])
+    bufs.flush(want=False)  # warm-up contributions do not reach the timed flush
+    t_f = t_a = 0.0
+    t0 = time.time()
+    for k in range(K):
+        a, b = k * s, min(sub, (k + 1) * s)
+        if b <= a:
+            continue
+        t = time.time()
+        tree.primal(p, BETA, xq[a:b], threads=cores)
+        t_f += time.time() - t
+        t = time.time()
+        bufs.adjoint(p, BETA, xq[a:b], d_out[a:b])
+        t_a += time.time() - t
+    t = time.time()
+    bufs.flush(want=False)  # flush_gradients(span) of the timed queries (zeroes the buffers)
+    t_flush = time.time() - t
+    timed = time.time() - t0
+    full = Q * (t_f + t_a) / sub + t_setup + t_flush
+    value = Q / full
+    desc = (f"fixed {sub}-query prefix of the config-{wl.config} batch (of {Q}) covered by the "
+            f"{K} timed steps ({s} queries each: forward with {cores} threads + adjoint into "
+            f"{workers} GradientBuffers), one flush_gradients after them; full step "
+            f"extrapolated as Q*(t_fwd+t_adj)/subset + buffer setup + flush; reference sources "
+            f"compiled -O3 without -march; CPU {cpu_info()}")
     line = {
-        "impl": "reference", "metric": METRIC, "value": r["value"], "unit": UNIT,
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded config-2 generator)",
-        "config": {"workload": "config2: N=1e6 torus+outliers, C=49, Q=4e6, beta=2, forward+adjoint",
-                   "sample_queries": r["sample"]},
-        "forward_qps": r["forward_qps"], "adjoint_qps": r["adjoint_qps"],
-        "reference_timings": r["measured"],
-        "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": r["cores"],
-                         "kind": "reference", "sample": sample_desc},
-        "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": 0},
+        "ms_per_step": 1e3 * timed / K, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": f"synthetic (seeded config-{wl.config} generator)",
+        "config": {"workload": wl.desc, "subset_queries": sub, "queries_per_timed_step": s},
+        "ms_per_step_note": "measured: the timed region (K sample steps + the flush) / K",
+        "extrapolated_full_step_ms": 1e3 * full,
+        "forward_qps": sub / t_f, "adjoint_qps": sub / t_a,
+        "reference_timings": {"forward_s": t_f, "adjoint_s": t_a, "flush_s": t_flush,
+                              "buffer_setup_s": t_setup, "tree_build_s": build_s,
+                              "gradient_buffer_bytes": buf_bytes},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "adjoint_workers": workers,
+                         "kind": "reference", "sample": desc},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     emit(line)
 
 
 # ------------------------------------------------------------------ our arm
-def run_ours(args):
+def measure_device(tree, wl, params, dev, steps, warmup, dist, chunks, local):
+    """The step on device-resident inputs: returns timing, phases, counters."""
     import torch
 
-    import paper_2405_16788_b200 as P
     from paper_2405_16788_b200 import bhtree as B
-    from paper_2405_16788_b200 import workloads as W
+    from paper_2405_16788_b200 import parallel as Pl
 
-    rank, world, local = env_rank()
-    dist = None
-    # DPL_BENCH_DIST=1 exercises the NCCL path at world size 1 (one GPU boxes)
-    if world > 1 or os.environ.get("DPL_BENCH_DIST"):
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream()
-
-    w = W.config2(scale=args.scale)
-    eps = W.epsilon_for("config2", args.scale)
-    c = w["cloud"]
-    xs_np = W.rank_queries(w, rank)
-    Q, N, C = xs_np.shape[0], c.size, c.channels
-    params = P.KernelParams(epsilon=eps)
-
-    tree = P.DipoleTree(local, stream=stream)
-    t0 = time.time()
-    tree.build(c)
-    tree.set_channel_kernels(w["kinds"])
-    torch.cuda.synchronize()
-    build_s = time.time() - t0
-    nodes = tree.node_count()
-
-    # two query batches, alternated step by step: every step's primal must
-    # traverse afresh (the adjoint then reuses that step's interaction lists)
-    xs_np2 = W.step_queries(w, rank, 1)
-    xs_b = [torch.from_numpy(xs_np).to(dev), torch.from_numpy(xs_np2).to(dev)]
-    xs = xs_b[0]
-    d_out = torch.from_numpy(W.upstream(Q, C, w["d_out_seed"] + [rank])).to(dev)
-    out = torch.empty((Q, C), dtype=torch.float32, device=dev)
+    N, C = wl.cloud.size, wl.cloud.channels
+    xs_b = [torch.from_numpy(b).to(dev) for b in wl.batches]
+    Qr = xs_b[0].shape[0]
+    g = torch.Generator(device=dev).manual_seed(1000 + wl.lo)
+    d_out = torch.randn((Qr, C), generator=g, device=dev, dtype=torch.float32)
+    out = torch.empty((Qr, C), dtype=torch.float32, device=dev)
     mom = torch.empty((N, C), dtype=torch.float32, device=dev)
     nrm = torch.empty((N, 3), dtype=torch.float32, device=dev)
-    deps = torch.zeros(1, dtype=torch.float64, device=dev)
+    rows = torch.empty((N, C + 3), dtype=torch.float32, device=dev) if dist is not None else None
     buf = tree.make_buffer()
 
     # counting pass (untimed): replays the opening decisions -> algorithmic work
     tot = 0
     for xb in xs_b:
         _, cnt = tree.primal(xb, params, BETA, out=out, visited=True)
-        tot = tot + cnt.sum(dim=0).cpu().numpy() / len(xs_b)  # mean per batch
-    f_fwd, f_adj = flops_model(tot, 1, C - 1)
+        tot = tot + cnt.sum(dim=0).cpu().numpy() / len(xs_b)
+        del cnt
     it = [0]
 
     def step():
@@ -305,14 +355,12 @@ def run_ours(args):
         it[0] += 1
         tree.primal(xs, params, BETA, out=out)
         tree.adjoint(xs, params, BETA, d_out, None, buf)
-        g = tree.flush_gradients(buf, out=(mom, nrm))
-        if dist is not None:
-            deps.fill_(g.d_epsilon)
-            dist.all_reduce(mom)
-            dist.all_reduce(nrm)
-            dist.all_reduce(deps)
+        if dist is None:
+            tree.flush_gradients(buf, out=(mom, nrm))
+        else:
+            Pl.flush_allreduce(tree, buf, rows=rows, chunks=chunks, out=(mom, nrm))
 
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         step()
     torch.cuda.synchronize()
     B.profile_read(tree)
@@ -324,59 +372,126 @@ def run_ours(args):
             dist.barrier()
         torch.cuda.synchronize()
         e0.record(stream)
-        for _ in range(args.steps):
+        for _ in range(steps):
             step()
         e1.record(stream)
         torch.cuda.synchronize()
         if dist is not None:
             dist.barrier()
     launches = B.launch_count() - launches0
-    ms = e0.elapsed_time(e1) / args.steps
+    ms = e0.elapsed_time(e1) / steps
     prof = B.profile_read(tree)
     B.profile_enable(tree, False)
     ms_t = torch.tensor([ms], device=dev)
     if dist is not None:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
-    ms_max = float(ms_t.item())
-    value = world * Q / (ms_max * 1e-3)
+    ph = {k: prof[k][0] / max(1, prof[k][1]) for k in ("forward", "adjoint")}
+    ph["morton_sort_x2"] = prof["sort"][0] / steps
+    ph["flush"] = prof["flush"][0] / steps
+    del xs_b, d_out, out
+    return dict(ms=float(ms_t.item()), ms_local=ms, phases=ph, tot=tot, launches=int(launches),
+                clocks=clk.summary(), buf=buf, mom=mom, nrm=nrm, rows=rows, Qr=Qr)
 
-    fwd_ms = prof["forward"][0] / max(1, prof["forward"][1])
-    adj_ms = prof["adjoint"][0] / max(1, prof["adjoint"][1])
-    sort_ms = prof["sort"][0] / max(1, args.steps)
-    flush_ms = prof["flush"][0] / max(1, prof["flush"][1])
+
+def roofline_for(tot, Cd, Cr, ph, peak32, traffic):
+    f_fwd, f_adj = flops_model(tot, Cd, Cr)
+    dom = "adjoint" if ph["adjoint"] >= ph["forward"] else "forward"
+    fl = f_adj if dom == "adjoint" else f_fwd
+    achieved = fl / (ph[dom] * 1e-3) / 1e12
+    return dom, {"bound": "fp32", "achieved": achieved, "peak": peak32, "unit": "TFLOP/s",
+                 "frac": achieved / peak32, "flops_per_launch": fl,
+                 "traffic": (traffic or {}).get(dom)}
+
+
+def load_traffic(config):
+    """DRAM bytes per launch of the dominant kernels from the committed ncu capture."""
+    for name in (f"r02_traffic_config{config}.json", "r01_traffic.json" if config == 2 else ""):
+        if not name:
+            continue
+        try:
+            with open(os.path.join(ROOT, "profiles", name)) as f:
+                tj = json.load(f)
+            out = {"_source": tj["_source"]}
+            for k in ("adjoint", "forward"):
+                if k in tj:
+                    out[k] = tj[k]["dram_read"] + tj[k]["dram_write"]
+            return out
+        except (OSError, KeyError, ValueError):
+            continue
+    return None
+
+
+def run_ours(args):
+    import torch
+
+    import paper_2405_16788_b200 as P
+    from paper_2405_16788_b200 import bhtree as B
+    from paper_2405_16788_b200 import parallel as Pl
+
+    rank, world, local = env_rank()
+    dist = None
+    # DPL_BENCH_DIST=1 exercises the NCCL path at world size 1 (one-GPU boxes)
+    if world > 1 or os.environ.get("DPL_BENCH_DIST"):
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
+
+    t0 = time.time()
+    wl = Workload(args.config, args.scale, rank, world)
+    gen_s = time.time() - t0
+    c = wl.cloud
+    N, C = c.size, c.channels
+    params = P.KernelParams(epsilon=wl.eps)
+    tree = P.DipoleTree(local, stream=stream)
+    t0 = time.time()
+    tree.build(c)
+    tree.set_channel_kernels(wl.kinds)
+    torch.cuda.synchronize()
+    build_s = time.time() - t0
+    nodes = tree.node_count()
+
+    m = measure_device(tree, wl, params, dev, args.steps, args.warmup, dist, args.chunks, local)
+    Qr, ph, tot = m["Qr"], m["phases"], m["tot"]
+    value = wl.q_total / (m["ms"] * 1e-3)
 
     # ------------------------------------------------------------ e2e (host buffers)
     e2e = None
     if not args.no_e2e:
-        xs_hb = [torch.from_numpy(xs_np).pin_memory(), torch.from_numpy(xs_np2).pin_memory()]
-        do_h = d_out.cpu().pin_memory()
-        out_h = torch.empty((Q, C), dtype=torch.float32).pin_memory()
-        mom_h = torch.empty((N, C), dtype=torch.float32).pin_memory()
-        nrm_h = torch.empty((N, 3), dtype=torch.float32).pin_memory()
-
-        # host-async mode: primal/adjoint return once queued, so the d_out H2D
-        # overlaps the forward kernel and the out D2H overlaps the adjoint;
-        # flush_gradients synchronizes every stream (all host results complete)
+        xs_hb = [torch.from_numpy(b).pin_memory() for b in wl.batches]
+        do_h = torch.empty((Qr, C), dtype=torch.float32, pin_memory=True)
+        do_h.copy_(torch.randn((Qr, C), generator=torch.Generator(device=dev).manual_seed(7 + rank),
+                               device=dev))
+        out_h = torch.empty((Qr, C), dtype=torch.float32, pin_memory=True)
+        mom_h = torch.empty((N, C), dtype=torch.float32, pin_memory=True)
+        nrm_h = torch.empty((N, 3), dtype=torch.float32, pin_memory=True)
+        buf = m["buf"]
+        rows = m["rows"]
+        # host-async mode: primal / adjoint return once queued, so the d_out H2D
+        # overlaps the forward kernel and the out D2H overlaps the adjoint; the
+        # adjoint reuses the primal's device copy of the queries (xs=None); the
+        # flush synchronizes every stream (all host results complete)
         tree.set_host_async(True)
+        it = [0]
 
         def step_host():
             xs_h = xs_hb[it[0] % 2]
             it[0] += 1
             tree.primal(xs_h, params, BETA, out=out_h)
-            tree.adjoint(xs_h, params, BETA, do_h, None, buf)
-            g = tree.flush_gradients(buf, out=(mom_h, nrm_h))
-            if dist is not None:
-                m = mom_h.to(dev, non_blocking=True)
-                dist.all_reduce(m)
-                mom_h.copy_(m)
-            return g
+            tree.adjoint(None, params, BETA, do_h, None, buf)
+            if dist is None:
+                tree.flush_gradients(buf, out=(mom_h, nrm_h))
+            else:
+                Pl.flush_allreduce(tree, buf, rows=rows, chunks=args.chunks, out=(mom_h, nrm_h))
 
         step_host()
         torch.cuda.synchronize()
         if dist is not None:
             dist.barrier()
-        t0 = time.perf_counter()
         k2 = max(1, min(args.steps, 5))
+        t0 = time.perf_counter()
         for _ in range(k2):
             step_host()
         torch.cuda.synchronize()
@@ -386,92 +501,115 @@ def run_ours(args):
         if dist is not None:
             dist.all_reduce(t_t, op=dist.ReduceOp.MAX)
         e2e_s = float(t_t.item())
-        h2d = 2 * xs_np.nbytes + Q * C * 4
-        d2h = Q * C * 4 + N * C * 4 + N * 12 + 8
-        e2e = {"value": world * Q / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+        h2d = Qr * 24 + Qr * C * 4
+        d2h = Qr * C * 4 + N * C * 4 + N * 12 + 8
+        e2e = {"value": wl.q_total / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": 1e3 * e2e_s,
                "timing": "wall clock around public-API calls on pinned host buffers (host-async "
-                         "mode; flush_gradients synchronizes, all results on the host)"}
+                         "mode: the adjoint reuses the primal's device copy of the queries; the "
+                         "flush synchronizes, all results on the host), max over ranks",
+               "bytes": "per rank"}
+        del xs_hb, do_h, out_h
 
     if rank != 0:
         if dist is not None:
             dist.destroy_process_group()
         return
 
-    # DRAM bytes per launch of the dominant kernel from the committed ncu capture
-    traffic = {}
-    try:
-        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as f:
-            tj = json.load(f)
-        traffic["_source"] = tj["_source"]
-        for k in ("adjoint", "forward"):
-            traffic[k] = {"bytes": tj[k]["dram_read"] + tj[k]["dram_write"]}
-    except (OSError, KeyError, ValueError):
-        pass
+    traffic = load_traffic(args.config)
     peak32 = B.peak_fp32(local)
-    peak64 = B.peak_fp64(local)
-    dom = "adjoint" if adj_ms >= fwd_ms else "forward"
-    dom_flops = f_adj if dom == "adjoint" else f_fwd
-    dom_ms = adj_ms if dom == "adjoint" else fwd_ms
-    achieved = dom_flops / (dom_ms * 1e-3) / 1e12
-    clocks = clk.summary()
+    dom, roof = roofline_for(tot, 1, C - 1, ph, peak32, traffic)
+    roof.update({"kernel": {"adjoint": "k_adjoint2 (interaction-list replay)",
+                            "forward": "k_forward_tc (interaction-list replay)"}[dom],
+                 "peak_source": "measured FFMA microbenchmark in this run (dpl_peak_fp32); "
+                                "MEASURED_PEAKS.json has no FP32 figure",
+                 "flop_model": "SURVEY §8(d) cost model v1 on replayed counters (rank 0's shard)",
+                 "traffic_source": (traffic or {}).get("_source"),
+                 "peak_fp64_measured": B.peak_fp64(local)})
+    # per-launch duration of the dominant kernel: CUDA events around each launch
+    # on the tree's stream (dpl_profile), mean over the timed steps
 
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         try:
-            r = reference_measure(w, eps, args.cpu_sample)
-            cpu = {"value": r["value"], "unit": UNIT, "cores": r["cores"], "kind": "reference",
-                   "sample": f"{r['sample']} config-2 queries timed (forward + adjoint + "
-                             f"flush, {r['adjoint_workers']} GradientBuffers), full 4M-query "
-                             f"step extrapolated (Q*t_query + fixed flush cost); reference "
+            O, rtree, rbuild = ref_tree(wl)
+            cores = O.ref_lib().ref_hardware_concurrency()
+            workers, _ = ref_workers(rtree, 4)
+            n_fwd, n_adj = (200_000, 40_000) if args.config == 4 else (400_000, 100_000)
+            n_fwd, n_adj = (max(1000, int(n_fwd * args.scale)), max(500, int(n_adj * args.scale)))
+            r = reference_sample(O, rtree, wl, n_fwd, n_adj, workers, cores)
+            del rtree
+            cpu = {"value": r["value"], "unit": UNIT, "cores": cores, "kind": "reference",
+                   "adjoint_workers": workers,
+                   "sample": f"{n_fwd} forward queries ({cores} threads) + {n_adj} adjoint "
+                             f"queries ({workers} GradientBuffers) + one flush_gradients of the "
+                             f"config-{args.config} workload; the {wl.q_total}-query step "
+                             f"extrapolated as Q*t_query + buffer setup + flush; reference "
                              f"sources compiled unmodified; CPU {cpu_info()}",
-                   "measured": r["measured"],
-                   "forward_qps": r["forward_qps"], "adjoint_qps": r["adjoint_qps"]}
+                   "measured": {k: v for k, v in r.items() if k != "value"},
+                   "tree_build_s": rbuild}
         except Exception as e:  # report, do not hide
             cpu = {"value": None, "error": str(e)}
 
-    bytes_fwd = Q * (24 + 4 * C) + nodes * (32 + 16 + 16 + 16 + 4 * 48) + N * (24 + 16 + 16 + 4 * 48)
+    Qsh = m["Qr"]
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32 (fp64 opening tests and accumulators)",
-        "data": "synthetic (seeded config-2 generator; no dataset)",
-        "config": {"workload": "config2: N=1e6 torus+outliers, C=49 (1 Dipole + 48 Radial), "
-                               "Q=4e6 per GPU uniform in [-2,2]^3, beta=2, leaf 8, forward+adjoint+flush",
-                   "points": N, "queries_per_gpu": Q, "channels": C, "nodes": nodes,
-                   "epsilon": eps, "l2": "inputs > L2 (0.9 GB/step), no explicit flush",
+        "warmup": args.warmup, "ms_per_step": m["ms"], "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None,
+        "dtype": "f32 (fp64 opening tests and accumulators)",
+        "data": f"synthetic (seeded config-{args.config} generator; no dataset)",
+        "config": {"workload": wl.desc, "points": N, "queries": wl.q_total,
+                   "queries_per_gpu": Qsh, "channels": C, "nodes": nodes, "epsilon": wl.eps,
+                   "l2": "inputs > L2 (queries + d_out per step >> 126 MB), no explicit flush",
                    "batches": "2 query batches alternated per step (no cross-step reuse); "
                               "the adjoint reuses its own step's interaction lists",
                    "parallelism": f"replicated tree, {world}-way query sharding"
-                                  + (", NCCL allreduce of point gradients" if world > 1 else "")},
-        "forward_qps": world * Q / ((fwd_ms + sort_ms / 2) * 1e-3),
-        "adjoint_qps": world * Q / ((adj_ms + sort_ms / 2 + flush_ms) * 1e-3),
-        "phase_ms": {"morton_sort_x2": sort_ms, "forward": fwd_ms, "adjoint": adj_ms,
-                     "flush": flush_ms},
-        "interactions_per_query": float((tot[1] + tot[2] + tot[3] + tot[4]) / Q),
-        "visited_per_query": float(tot[0] / Q),
-        "roofline": {"bound": "fp32", "kernel": {"adjoint": "k_adjoint2 (interaction-list replay)",
-                                                 "forward": "k_build_list + k_forward_tc"}[dom],
-                     "achieved": achieved, "peak": peak32, "unit": "TFLOP/s",
-                     "frac": achieved / peak32,
-                     "peak_source": "measured FFMA microbenchmark in this run (dpl_peak_fp32); "
-                                    "MEASURED_PEAKS.json has no FP32 figure",
-                     "flops_per_launch": dom_flops, "flop_model": "SURVEY §8(d) cost model v1",
-                     "traffic": traffic.get(dom, {}).get("bytes"),
-                     "traffic_source": traffic.get("_source"),
-                     "hbm_compulsory_bytes_forward": bytes_fwd,
-                     "peak_fp64_measured": peak64},
-        "gpu_launches": int(launches),
-        "clocks": clocks,
-        "build_s": build_s,
+                                  + (f", NCCL all-reduce of point gradients in {args.chunks} "
+                                     "chunks overlapped with the push-down" if world > 1 else "")},
+        "forward_qps": wl.q_total / ((ph["forward"] + ph["morton_sort_x2"] / 2) * 1e-3),
+        "adjoint_qps": wl.q_total / ((ph["adjoint"] + ph["morton_sort_x2"] / 2 + ph["flush"]) * 1e-3),
+        "phase_ms": ph,
+        "interactions_per_query": float((tot[1] + tot[2] + tot[3] + tot[4]) / Qsh),
+        "visited_per_query": float(tot[0] / Qsh),
+        "roofline": roof,
+        "gpu_launches": m["launches"],
+        "clocks": m["clocks"],
+        "build_s": build_s, "generate_s": gen_s,
         "e2e": e2e,
         "cpu_baseline": cpu,
     }
+    del m
+    if world == 1 and args.config == 4 and not args.no_extra:
+        try:
+            line["extra"] = {"config2": extra_config2(args, dev, local, peak32)}
+        except Exception as e:
+            line["extra"] = {"config2": {"error": str(e)}}
     emit(line)
     if dist is not None:
         dist.destroy_process_group()
 
 
+def extra_config2(args, dev, local, peak32):
+    """BASELINE config 2 on the same GPU (device-resident inputs), N=1."""
+    import torch
+
+    import paper_2405_16788_b200 as P
+
+    wl = Workload(2, args.scale, 0, 1)
+    params = P.KernelParams(epsilon=wl.eps)
+    tree = P.DipoleTree(local, stream=torch.cuda.current_stream())
+    tree.build(wl.cloud)
+    tree.set_channel_kernels(wl.kinds)
+    m = measure_device(tree, wl, params, dev, max(args.steps, 10), args.warmup, None, 1, local)
+    _, roof = roofline_for(m["tot"], 1, wl.cloud.channels - 1, m["phases"], peak32,
+                           load_traffic(2))
+    return {"workload": wl.desc, "value": wl.q_total / (m["ms"] * 1e-3), "unit": UNIT,
+            "ms_per_step": m["ms"], "phase_ms": m["phases"], "roofline_frac": roof["frac"],
+            "roofline_achieved_tflops": roof["achieved"], "gpu_launches": m["launches"],
+            "clocks": m["clocks"]}
+
+
+# ------------------------------------------------------------------ launcher
 _JSON_OUT = None
 
 
@@ -481,14 +619,35 @@ def emit(line):
     print(json.dumps(line), file=out, flush=True)
 
 
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def spawn_ranks(n, json_fd):
+    """`--gpus N` outside torchrun: launch N ranks of this script (one per GPU)
+    with torch.distributed.run on 127.0.0.1; rank 0's JSON line goes straight
+    to our stdout."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, stdout=json_fd, stderr=sys.stderr)
+
+
 def main():
     global _JSON_OUT
     # stdout carries exactly one JSON line: anything else native code prints
     # there (e.g. NCCL's version banner at communicator creation) goes to stderr
     sys.stdout.flush()
-    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    json_fd = os.dup(1)
+    _JSON_OUT = os.fdopen(json_fd, "w")
     os.dup2(2, 1)
     args = parse()
+    if args.impl == "ours" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args.gpus, json_fd))
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -187,7 +187,9 @@ int dpl_gradbuf_zero(dpl_gradbuf_t buf);
 /* DipoleTree::adjoint (bhtree.cpp:345-417) for q queries: d_out q x C,
  * d_grad NULL or q x C x 3 (radial channels ignore d_grad, as the reference).
  * Warp-aggregated accumulation into node / leaf-point buffers; no per-point
- * ancestor walk here. */
+ * ancestor walk here. xs == NULL reuses the queries of the immediately
+ * preceding dpl_primal on this handle (same q; its device copy, so a host
+ * batch crosses PCIe once per primal -> adjoint pair); usage error otherwise. */
 int dpl_adjoint(dpl_tree_t tree, const dpl_kernel_params* params, double beta_bh,
                 const double* xs, int64_t q, const float* d_out, const float* d_grad,
                 dpl_gradbuf_t buf);
@@ -196,6 +198,23 @@ int dpl_adjoint(dpl_tree_t tree, const dpl_kernel_params* params, double beta_bh
  * buffers. moments N x C, normals N x 3 (fp32, any may be NULL), d_epsilon. */
 int dpl_flush(dpl_tree_t tree, dpl_gradbuf_t* bufs, int32_t nbuf, float* moments,
               float* normals, double* d_epsilon);
+
+/* flush_gradients split for a cross-rank sum: every rank holds
+ * the bit-identical tree, so per-point gradients in TREE order line up across
+ * ranks and can be all-reduced chunk by chunk while later chunks are computed.
+ *  - dpl_flush_begin: sums the buffers into bufs[0], node push-down, returns
+ *    this rank's d_epsilon;
+ *  - dpl_flush_rows: rows (hi - lo) x (C + 3) fp32, DEVICE memory, for the
+ *    sorted points [lo, hi): [d moments (C) | d normal (3)] of point_order[j]
+ *    (stream-ordered on the handle's stream, returns without waiting);
+ *  - dpl_flush_end: rows N x (C + 3) (device, summed over ranks by the caller)
+ *    -> moments N x C / normals N x 3 in the original order; zeroes the
+ *    buffers (reset(), bhtree.cpp:438).
+ * With one rank the three calls give exactly dpl_flush's results. */
+int dpl_flush_begin(dpl_tree_t tree, dpl_gradbuf_t* bufs, int32_t nbuf, double* d_epsilon);
+int dpl_flush_rows(dpl_tree_t tree, dpl_gradbuf_t buf0, int64_t lo, int64_t hi, float* rows);
+int dpl_flush_end(dpl_tree_t tree, dpl_gradbuf_t* bufs, int32_t nbuf, const float* rows,
+                  float* moments, float* normals);
 
 /* ---- render step (renderer.cpp:106-231) ------------------------------------
  * Rays are (origin, dir) fp64 (R x 6). Samples per ray: S; when ts is NULL the

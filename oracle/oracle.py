@@ -152,6 +152,11 @@ def ref_lib():
                                    C.c_int, _dp, _dp, _lp, C.c_int]
         lib.ref_adjoint.argtypes = [vp, C.POINTER(Params), C.c_double, _dp, C.c_int64, _dp, _dp,
                                     C.c_int, _dp, _dp, _dp]
+        lib.ref_bufs_create.argtypes = [vp, C.c_int, C.POINTER(vp)]
+        lib.ref_bufs_free.argtypes = [vp]
+        lib.ref_adjoint_into.argtypes = [vp, C.POINTER(Params), C.c_double, _dp, C.c_int64, _dp,
+                                         vp]
+        lib.ref_bufs_flush.argtypes = [vp, vp, _dp, _dp, _dp]
         lib.ref_naive_sum.argtypes = [vp, C.POINTER(Params), _dp, C.c_int64, C.c_int, C.c_int,
                                       C.c_int, _dp, _dp, C.c_int]
         lib.ref_naive_adjoint.argtypes = [vp, C.POINTER(Params), _dp, C.c_int64, _dp, _dp, _up,
@@ -344,6 +349,12 @@ class OracleTree:
                                              _ptr(nrm), C.byref(de)))
         return mom, nrm, de.value
 
+    def gradient_buffers(self, workers):
+        """Reference backend only: `workers` caller-held GradientBuffers
+        (make_buffer), filled by RefBuffers.adjoint and flushed by RefBuffers.flush."""
+        assert self.backend == "ref"
+        return RefBuffers(self, workers)
+
     def naive_sum(self, params: Params, xs, channel, kind, with_grad=False):
         xs = _d(xs).reshape(-1, 3)
         q = xs.shape[0]
@@ -394,6 +405,37 @@ class OracleTree:
                                   _ptr(rgb), _ptr(mom), _ptr(nrm), C.byref(de), C.byref(dl),
                                   _ptr(dbg))
         return dict(rgb=rgb, moments=mom, normals=nrm, d_eps=de.value, d_lambda=dl.value, d_bg=dbg)
+
+
+class RefBuffers:
+    """One GradientBuffer per worker on a reference tree (bhtree.hpp:38-40)."""
+
+    def __init__(self, tree: "OracleTree", workers):
+        self.tree = tree
+        self.workers = int(workers)
+        h = C.c_void_p()
+        _check_ref(tree._lib.ref_bufs_create(tree._h, self.workers, C.byref(h)))
+        self._h = h.value
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            self.tree._lib.ref_bufs_free(self._h)
+            self._h = None
+
+    def adjoint(self, params: Params, beta, xs, d_out):
+        xs = _d(xs).reshape(-1, 3)
+        q = xs.shape[0]
+        d_out = _d(d_out).reshape(q, self.tree.C)
+        _check_ref(self.tree._lib.ref_adjoint_into(self.tree._h, C.byref(params), beta, _ptr(xs), q,
+                                                   _ptr(d_out), self._h))
+
+    def flush(self, want=True):
+        mom = np.zeros((self.tree.n, self.tree.C)) if want else None
+        nrm = np.zeros((self.tree.n, 3)) if want else None
+        de = C.c_double()
+        _check_ref(self.tree._lib.ref_bufs_flush(self.tree._h, self._h, _ptr(mom), _ptr(nrm),
+                                                 C.byref(de)))
+        return mom, nrm, de.value
 
 
 class RefModel:

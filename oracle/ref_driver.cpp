@@ -15,6 +15,7 @@
 //     (proj/src/renderer.cpp:106-231) on a SceneModel prepared by
 //     SceneModel::prepare (proj/src/fields.cpp:7-18).
 // Nothing here is on the product path; the product never links this file.
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstdint>
@@ -246,6 +247,56 @@ int ref_adjoint(const ref_tree* t, const RefParams* p, double beta, const double
     for (size_t m = 0; m < pg.normals.size(); ++m)
       for (int a = 0; a < 3; ++a) normals[3 * m + a] = pg.normals[m][a];
     *d_eps = pg.d_epsilon;
+  });
+}
+
+// The same adjoint with caller-held buffers, so a benchmark can time the
+// per-query traversal and the (per-step, query-count independent) buffer
+// setup + flush_gradients separately: ref_bufs_create = make_buffer per worker
+// (bhtree.cpp:336-343), ref_adjoint_into = parallel_for over DipoleTree::adjoint
+// into bufs[w] (:345-417), ref_bufs_flush = flush_gradients(span) (:419-459).
+struct ref_bufs {
+  std::vector<GradientBuffer> b;
+};
+
+int ref_bufs_create(const ref_tree* t, int workers, ref_bufs** out) {
+  return guard([&] {
+    auto r = std::make_unique<ref_bufs>();
+    for (int w = 0; w < std::max(1, workers); ++w) r->b.push_back(t->tree.make_buffer());
+    *out = r.release();
+  });
+}
+
+void ref_bufs_free(ref_bufs* b) { delete b; }
+
+int ref_adjoint_into(const ref_tree* t, const RefParams* p, double beta, const double* xs,
+                     int64_t q, const double* d_out, ref_bufs* bufs) {
+  return guard([&] {
+    KernelParams kp = to_kp(p);
+    const int C = t->tree.channels();
+    const int workers = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)bufs->b.size(), q));
+    parallel_for(
+        q,
+        [&](int64_t lo, int64_t hi, int w) {
+          for (int64_t i = lo; i < hi; ++i) {
+            Vec3 x(xs[3 * i], xs[3 * i + 1], xs[3 * i + 2]);
+            t->tree.adjoint(x, kp, beta, std::span<const double>(d_out + i * C, C), {},
+                            bufs->b[w]);
+          }
+        },
+        workers);
+  });
+}
+
+int ref_bufs_flush(const ref_tree* t, ref_bufs* bufs, double* moments, double* normals,
+                   double* d_eps) {
+  return guard([&] {
+    PointGradients pg = t->tree.flush_gradients(bufs->b);
+    if (moments) std::memcpy(moments, pg.moments.data(), pg.moments.size() * sizeof(double));
+    if (normals)
+      for (size_t m = 0; m < pg.normals.size(); ++m)
+        for (int a = 0; a < 3; ++a) normals[3 * m + a] = pg.normals[m][a];
+    if (d_eps) *d_eps = pg.d_epsilon;
   });
 }
 

@@ -128,6 +128,7 @@ class DipoleTree:
         check(lib().dpl_tree_create(int(device), s, C.byref(h)))
         self._h = h.value
         self.device = device
+        self.stream_ptr = s  # None: the library's own (blocking) stream
         self._built = False
         self._kinds = None
         self._async = False
@@ -144,6 +145,7 @@ class DipoleTree:
     def set_stream(self, stream):
         s = stream.cuda_stream if hasattr(stream, "cuda_stream") else stream
         check(lib().dpl_tree_set_stream(self._h, s))
+        self.stream_ptr = s
 
     def synchronize(self):
         check(lib().dpl_tree_sync(self._h))
@@ -378,10 +380,11 @@ class DipoleTree:
 
     def adjoint(self, xs, params: KernelParams, beta_bh: float, d_out, d_grad, buf: GradientBuffer):
         """DipoleTree::adjoint (bhtree.cpp:345-417) for a (Q, 3) batch; d_out (Q, C),
-        d_grad None or (Q, C, 3)."""
-        q = int(xs.shape[0])
+        d_grad None or (Q, C, 3). xs=None reuses the batch of the immediately
+        preceding primal() (its device copy: a host batch is uploaded once)."""
+        q = int(xs.shape[0]) if xs is not None else int(d_out.shape[0])
         Cc = self.channels()
-        xp, k1 = _in(xs, np.float64, (q, 3))
+        xp, k1 = _in(xs, np.float64, (q, 3)) if xs is not None else (None, None)
         dp, k2 = _in(d_out, np.float32, (q, Cc))
         gp, k3 = _in(d_grad, np.float32, (q, Cc, 3)) if d_grad is not None else (None, None)
         check(lib().dpl_adjoint(self._h, C.byref(params), float(beta_bh), xp, q, dp, gp, buf._h))
@@ -414,6 +417,44 @@ class DipoleTree:
         for b in buffers:
             b.dirty = False
         return PointGradients(Cc, mom, nrm, de.value)
+
+
+    # -- flush split for the cross-rank sum (parallel.flush_allreduce) ------------
+    def flush_begin(self, buffers) -> float:
+        """Sum the buffers, node push-down; returns this rank's d_epsilon."""
+        if isinstance(buffers, GradientBuffer):
+            buffers = [buffers]
+        arr = (C.c_void_p * len(buffers))(*[b._h for b in buffers])
+        de = C.c_double()
+        check(lib().dpl_flush_begin(self._h, arr, len(buffers), C.byref(de)))
+        return de.value
+
+    def flush_rows(self, buffer: GradientBuffer, lo: int, hi: int, rows):
+        """Gradient rows [d moments | d normal] (C + 3 wide, fp32 CUDA tensor) of the
+        sorted points [lo, hi), stream-ordered on the tree's stream."""
+        check(lib().dpl_flush_rows(self._h, buffer._h, int(lo), int(hi), rows.data_ptr()))
+
+    def flush_end(self, buffers, rows, out=None, device_out=None) -> tuple:
+        """Rows N x (C + 3) in tree order -> (moments N x C, normals N x 3) in the
+        original order; zeroes the buffers."""
+        if isinstance(buffers, GradientBuffer):
+            buffers = [buffers]
+        n, Cc = self.point_count(), self.channels()
+        arr = (C.c_void_p * len(buffers))(*[b._h for b in buffers])
+        if out is not None:
+            mom, nrm = out
+            mp = mom.data_ptr() if _is_torch(mom) else mom.ctypes.data
+            np_ = nrm.data_ptr() if _is_torch(nrm) else nrm.ctypes.data
+        else:
+            dev = device_out if device_out is not None else rows.device
+            mom = torch.empty((n, Cc), dtype=torch.float32, device=dev)
+            nrm = torch.empty((n, 3), dtype=torch.float32, device=dev)
+            mp, np_ = mom.data_ptr(), nrm.data_ptr()
+        check(lib().dpl_flush_end(self._h, arr, len(buffers), rows.data_ptr(), mp, np_))
+        self._keep.clear()
+        for b in buffers:
+            b.dirty = False
+        return mom, nrm
 
 
 def launch_count() -> int:

@@ -376,6 +376,62 @@ __global__ void k_flush_radial(int64_t n, int C, int Cd, int Cr, const int* __re
   }
 }
 
+// one warp per sorted point j in [lo, hi): row (j - lo) = [d mu (C) | d n (3)],
+// the arithmetic of k_flush_points (lane 0, dipole slots + normal) and
+// k_flush_radial (lanes over radial slots), so rows hold the same values
+__global__ void k_flush_rows(int64_t lo, int64_t hi, int C, int Cd, int Cr,
+                             const int* __restrict__ chmap, const int32_t* __restrict__ order,
+                             const int32_t* __restrict__ pt_leaf, const double* __restrict__ area,
+                             const double* __restrict__ nrm, const double* __restrict__ mu,
+                             const double* __restrict__ gv, const double* __restrict__ gs,
+                             const double* __restrict__ pmud, const double* __restrict__ pmur,
+                             const double* __restrict__ pn, float* __restrict__ rows) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int W = C + 3;
+  for (int64_t j = lo + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5); j < hi; j += nw) {
+    const int64_t m = order[j];
+    const int64_t leaf = pt_leaf[j];
+    const double a = area[m];
+    float* row = rows + (j - lo) * W;
+    for (int k = lane; k < Cr; k += 32)
+      row[chmap[Cd + k]] = (float)(pmur[j * Cr + k] + a * gs[leaf * Cr + k]);
+    if (lane == 0) {
+      double nx = nrm[3 * m], ny = nrm[3 * m + 1], nz = nrm[3 * m + 2];
+      double dn0 = pn[3 * j], dn1 = pn[3 * j + 1], dn2 = pn[3 * j + 2];
+      for (int k = 0; k < Cd; ++k) {
+        int ch = chmap[k];
+        const double* g = gv + (leaf * Cd + k) * 3;
+        double v = pmud[j * Cd + k] + a * (nx * g[0] + ny * g[1] + nz * g[2]);
+        row[ch] = (float)v;
+        double am = a * mu[m * C + ch];
+        dn0 += am * g[0], dn1 += am * g[1], dn2 += am * g[2];
+      }
+      row[C] = (float)dn0, row[C + 1] = (float)dn1, row[C + 2] = (float)dn2;
+    }
+  }
+}
+
+// rows (tree order, C + 3 wide) -> moments N x C / normals N x 3 (original order)
+__global__ void k_unpermute_rows(int64_t n, int C, const int32_t* __restrict__ order,
+                                 const float* __restrict__ rows, float* moments, float* normals) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int W = C + 3;
+  for (int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < n; j += nw) {
+    const int64_t m = order[j];
+    const float* row = rows + j * W;
+    for (int k = lane; k < W; k += 32) {
+      const float v = row[k];
+      if (k < C) {
+        if (moments) moments[m * C + k] = v;
+      } else if (normals) {
+        normals[3 * m + (k - C)] = v;
+      }
+    }
+  }
+}
+
 __global__ void k_axpy_d(double* __restrict__ dst, const double* __restrict__ src, int64_t n) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < n) dst[i] += src[i];
@@ -449,6 +505,40 @@ void gradbuf_accumulate(GradBuf& dst, const GradBuf& src, cudaStream_t s) {
   k_axpy_d<<<(unsigned)((dst.total + 255) / 256), 256, 0, s>>>(dst.mem.as<double>(),
                                                                src.mem.as<double>(), dst.total);
   count_launch();
+}
+
+void flush_pushdown(Tree& t, GradBuf& b) {
+  const int B = 256;
+  int Wv = 3 * t.Cd, Ws = t.Cr, W = Wv + Ws;
+  int levels = (int)t.level_off.size() - 1;
+  for (int d = 0; d < levels && W > 0; ++d) {
+    int64_t off = t.level_off[d], cnt = t.level_off[d + 1] - off;
+    if (!cnt) continue;
+    k_pushdown_level<<<(unsigned)((cnt * W + B - 1) / B), B, 0, t.stream>>>(
+        off, cnt, W, t.node_parent.as<int32_t>(), t.node_area64.as<double>(), b.node_v, Wv,
+        b.node_s, Ws);
+    count_launch();
+  }
+  DPL_CUDA(cudaGetLastError());
+}
+
+void flush_rows(Tree& t, const GradBuf& b, int64_t lo, int64_t hi, float* rows) {
+  if (hi <= lo) return;
+  const int64_t warps = hi - lo;
+  const unsigned blocks = (unsigned)std::min<int64_t>((warps + 7) / 8, 148 * 16);
+  k_flush_rows<<<blocks, 256, 0, t.stream>>>(
+      lo, hi, t.C, t.Cd, t.Cr, t.chmap.as<int>(), t.order.as<int32_t>(), t.pt_leaf.as<int32_t>(),
+      t.area64.as<double>(), t.nrm64.as<double>(), t.mu64.as<double>(), b.node_v, b.node_s,
+      b.pt_mud, b.pt_mur, b.pt_n, rows);
+  count_launch();
+  DPL_CUDA(cudaGetLastError());
+}
+
+void flush_unpermute(Tree& t, const float* rows, float* moments, float* normals) {
+  k_unpermute_rows<<<148 * 16, 256, 0, t.stream>>>(t.n, t.C, t.order.as<int32_t>(), rows, moments,
+                                                  normals);
+  count_launch();
+  DPL_CUDA(cudaGetLastError());
 }
 
 void flush_launch(Tree& t, GradBuf& b, float* moments, float* normals) {

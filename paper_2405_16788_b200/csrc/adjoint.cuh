@@ -40,5 +40,12 @@ void adjoint_launch(const Tree& t, const KParams& kp, const AdjArgs& a, GradBuf&
 bool adjoint2_launch(const Tree& t, const KParams& kp, const AdjArgs& a, GradBuf& b);
 // consumes b's node accumulators (push-down in place); caller zeroes afterwards
 void flush_launch(Tree& t, GradBuf& b, float* moments, float* normals);
+// flush_launch split for cross-rank reduction: the node
+// push-down, then per-point gradient ROWS [moments (C) | normals (3)] in tree
+// order for the sorted-point range [lo, hi) (identical on every rank: the tree
+// is bit-identical), then the scatter of summed rows to the original order.
+void flush_pushdown(Tree& t, GradBuf& b);
+void flush_rows(Tree& t, const GradBuf& b, int64_t lo, int64_t hi, float* rows);
+void flush_unpermute(Tree& t, const float* rows, float* moments, float* normals);
 
 }  // namespace dpl

@@ -55,6 +55,7 @@ struct dpl_tree_s {
     int64_t q = 0;
     double beta = 0;
     bool listed = false;
+    const double* dev = nullptr;  // device copy of that batch (dpl_adjoint xs == NULL)
   } last_fwd;
   bool last_was_fwd = false;
   bool want_lists = false;
@@ -670,6 +671,7 @@ static int forward_common(dpl_tree_t h, const dpl_kernel_params* params, double 
       h->ws_xs.reserve(q * 24);
       h->ws_perm.reserve(q * 4);
       const double* xs_d = xs_host ? h->ws_xs.as<double>() : xs;
+      h->last_fwd.dev = xs_d;
       float* out_d = out;
       if (out_host) {
         h->ws_out.reserve(q * stride * 4);
@@ -721,6 +723,7 @@ static int forward_common(dpl_tree_t h, const dpl_kernel_params* params, double 
     }
     if (h->host_async) h->sync_all();  // the staged path below is synchronous
     const double* xs_d = stage_in(t, xs, (size_t)q * 3, h->ws_xs);
+    h->last_fwd.dev = xs_d;
     h->ws_perm.reserve(q * 4);
     if (!presorted) {
       PhaseTimer pt(t, PH_SORT);
@@ -970,13 +973,20 @@ int dpl_adjoint(dpl_tree_t h, const dpl_kernel_params* params, double beta_bh, c
     check_buf(h, buf);
     require(q >= 0 && q < (int64_t)INT32_MAX, DPL_ERR_USAGE, "bad query count");
     if (q == 0) return;
-    require(xs && d_out, DPL_ERR_USAGE, "null input");
+    require(d_out != nullptr, DPL_ERR_USAGE, "null input");
+    // xs == NULL: the queries of the immediately preceding dpl_primal on this
+    // handle (same q), read from the device copy that call made — a host batch
+    // is uploaded once per primal -> adjoint pair instead of twice
+    const bool reuse = xs == nullptr;
+    require(!reuse || (h->last_was_fwd && h->last_fwd.q == q && h->last_fwd.dev),
+            DPL_ERR_USAGE, "adjoint: xs == NULL needs a preceding primal of the same batch");
+    if (reuse) xs = h->last_fwd.dev;
     Tree& t = h->t;
     DPL_CUDA(cudaSetDevice(t.device));
     KParams kp = make_kparams(params->epsilon, params->desingularized, params->desing_delta);
     tree_ensure_thresholds(t, beta_bh);
     // list policy (see dpl_tree_s)
-    const bool pair = h->last_was_fwd && h->last_fwd.xs == (const void*)xs &&
+    const bool pair = h->last_was_fwd && (reuse || h->last_fwd.xs == (const void*)xs) &&
                       h->last_fwd.q == q && h->last_fwd.beta == beta_bh;
     const bool lists = (pair && h->last_fwd.listed) || ilist_always();
     h->want_lists = pair;
@@ -1027,6 +1037,8 @@ int dpl_adjoint(dpl_tree_t h, const dpl_kernel_params* params, double beta_bh, c
         PhaseTimer pt(t, PH_ADJOINT);
         adjoint_launch(t, kp, a, buf->b);
       });
+      // the primal's staging buffer was read: the next primal's upload waits
+      if (reuse) DPL_CUDA(cudaEventRecord(hazard_event(h->ev_fwd_in), t.stream));
       DPL_CUDA(cudaGetLastError());
       return;
     }
@@ -1055,6 +1067,7 @@ int dpl_adjoint(dpl_tree_t h, const dpl_kernel_params* params, double beta_bh, c
       adjoint_launch(t, kp, a, buf->b);
     }
     DPL_CUDA(cudaGetLastError());
+    if (reuse) DPL_CUDA(cudaEventRecord(hazard_event(h->ev_fwd_in), t.stream));
     if (!is_device_ptr(xs) || !is_device_ptr(d_out)) DPL_CUDA(cudaStreamSynchronize(t.stream));
   });
 }
@@ -1083,6 +1096,62 @@ int dpl_flush(dpl_tree_t h, dpl_gradbuf_t* bufs, int32_t nbuf, float* moments, f
     for (int i = 0; i < nbuf; ++i) gradbuf_zero(bufs[i]->b, t.stream);  // reset() (:438)
     h->sync_all();  // also completes host-async outputs of earlier calls
     if (d_epsilon) *d_epsilon = de;
+  });
+}
+
+int dpl_flush_begin(dpl_tree_t h, dpl_gradbuf_t* bufs, int32_t nbuf, double* d_epsilon) {
+  return guard([&] {
+    check_tree(h);
+    require(nbuf >= 1 && bufs, DPL_ERR_USAGE, "no gradient buffers");
+    for (int i = 0; i < nbuf; ++i) check_buf(h, bufs[i]);
+    Tree& t = h->t;
+    DPL_CUDA(cudaSetDevice(t.device));
+    GradBuf& b0 = bufs[0]->b;
+    for (int i = 1; i < nbuf; ++i) gradbuf_accumulate(b0, bufs[i]->b, t.stream);  // :429-439
+    double de = 0;
+    DPL_CUDA(cudaMemcpyAsync(&de, b0.d_eps, 8, cudaMemcpyDeviceToHost, t.stream));
+    {
+      PhaseTimer pt(t, PH_FLUSH);
+      flush_pushdown(t, b0);
+    }
+    DPL_CUDA(cudaStreamSynchronize(t.stream));
+    if (d_epsilon) *d_epsilon = de;
+  });
+}
+
+int dpl_flush_rows(dpl_tree_t h, dpl_gradbuf_t buf, int64_t lo, int64_t hi, float* rows) {
+  return guard([&] {
+    check_tree(h);
+    check_buf(h, buf);
+    require(0 <= lo && lo <= hi && hi <= h->t.n, DPL_ERR_USAGE, "flush_rows: bad point range");
+    require(hi == lo || is_device_ptr(rows), DPL_ERR_USAGE, "flush_rows: rows must be device memory");
+    Tree& t = h->t;
+    DPL_CUDA(cudaSetDevice(t.device));
+    PhaseTimer pt(t, PH_FLUSH);
+    flush_rows(t, buf->b, lo, hi, rows);
+  });
+}
+
+int dpl_flush_end(dpl_tree_t h, dpl_gradbuf_t* bufs, int32_t nbuf, const float* rows,
+                  float* moments, float* normals) {
+  return guard([&] {
+    check_tree(h);
+    require(nbuf >= 1 && bufs, DPL_ERR_USAGE, "no gradient buffers");
+    for (int i = 0; i < nbuf; ++i) check_buf(h, bufs[i]);
+    require(rows && is_device_ptr(rows), DPL_ERR_USAGE, "flush_end: rows must be device memory");
+    Tree& t = h->t;
+    DPL_CUDA(cudaSetDevice(t.device));
+    Out<float> mo, no;
+    mo.bind(t, moments, t.n * t.C, h->ws_mom);
+    no.bind(t, normals, t.n * 3, h->ws_nrm);
+    {
+      PhaseTimer pt(t, PH_FLUSH);
+      flush_unpermute(t, rows, mo.dev, no.dev);
+    }
+    mo.finish(t);
+    no.finish(t);
+    for (int i = 0; i < nbuf; ++i) gradbuf_zero(bufs[i]->b, t.stream);  // reset() (:438)
+    h->sync_all();
   });
 }
 

@@ -14,6 +14,12 @@ all-gather of the updated parameters, update_moments on every rank
 """
 from __future__ import annotations
 
+import contextlib
+
+
+def _nullctx():
+    return contextlib.nullcontext()
+
 
 def shard_range(total: int, rank: int, world: int):
     """Contiguous [lo, hi) slice of `total` items for `rank` (sizes differ by <= 1)."""
@@ -35,6 +41,57 @@ def allreduce_point_gradients(moments, normals, d_epsilon, group=None):
     e = torch.tensor([float(d_epsilon)], dtype=torch.float64, device=moments.device)
     dist.all_reduce(e, group=group)
     return float(e.item())
+
+
+def flush_allreduce(tree, buffers, rows=None, chunks=8, group=None, out=None):
+    """flush_gradients summed over ranks, overlapped chunk by chunk.
+
+    Every rank holds the bit-identical tree, so gradient rows in TREE order line
+    up across ranks: the push-down runs once (`flush_begin`), then for each of
+    `chunks` contiguous sorted-point ranges the rows are computed on the tree's
+    stream and handed to an asynchronous all-reduce — NCCL waits for that
+    chunk only, so the sum of chunk k runs on the NCCL stream while chunk k+1
+    is computed. The summed rows are scattered back to the original order
+    (`flush_end`, which also zeroes the buffers). Returns
+    (moments N x C, normals N x 3, d_epsilon summed over ranks).
+
+    `rows`: optional preallocated N x (C + 3) fp32 CUDA tensor."""
+    import torch
+    import torch.distributed as dist
+
+    n, C = tree.point_count(), tree.channels()
+    if isinstance(buffers, (list, tuple)):
+        b0 = buffers[0]
+    else:
+        b0, buffers = buffers, [buffers]
+    if rows is None:
+        rows = torch.empty((n, C + 3), dtype=torch.float32,
+                           device=torch.device("cuda", torch.cuda.current_device()))
+    dev = rows.device
+    de = tree.flush_begin(buffers)
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    works = []
+    # torch's collectives order against torch's CURRENT stream: make it the
+    # tree's stream (a library-owned stream is blocking, i.e. ordered with the
+    # legacy default stream already)
+    sp = getattr(tree, "stream_ptr", None)
+    ctx = (torch.cuda.stream(torch.cuda.ExternalStream(sp)) if sp and dev.type == "cuda"
+           else _nullctx())
+    with ctx:
+        e = torch.tensor([de], dtype=torch.float64, device=dev)
+        for k in range(max(1, chunks)):
+            lo, hi = shard_range(n, k, max(1, chunks))
+            if hi <= lo:
+                continue
+            tree.flush_rows(b0, lo, hi, rows[lo:hi])
+            if world > 1:
+                works.append(dist.all_reduce(rows[lo:hi], group=group, async_op=True))
+        if world > 1:
+            works.append(dist.all_reduce(e, group=group, async_op=True))
+        for w in works:
+            w.wait()  # the tree's stream waits on the NCCL stream (no host sync)
+    mom, nrm = tree.flush_end(buffers, rows, out=out)
+    return mom, nrm, float(e.item()) if world > 1 else de
 
 
 def point_chunk(n: int, rank: int, world: int):

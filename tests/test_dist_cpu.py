@@ -170,3 +170,83 @@ def test_sharded_point_update_matches_single(tmp_path, oracle_mod):
         got = np.load(tmp_path / f"sharded{r}.npz")
         assert np.array_equal(got["mu"], ref.mu)
         assert np.array_equal(got["nrm"], ref.nrm)
+
+
+# ---------------------------------------------------------------- chunked flush all-reduce
+class _RowsTree:
+    """The flush split of DipoleTree (flush_begin / flush_rows / flush_end) over
+    one rank's oracle adjoint result: rows in TREE order (the oracle's
+    point_order, identical on every rank), scattered back to the original
+    order at the end — the layout parallel.flush_allreduce relies on."""
+
+    def __init__(self, m, n, de, order):
+        self.m, self.n, self.de, self.order = m, n, de, order
+        self.calls = []
+
+    def point_count(self):
+        return self.m.shape[0]
+
+    def channels(self):
+        return self.m.shape[1]
+
+    def flush_begin(self, buffers):
+        self.calls.append("begin")
+        return self.de
+
+    def flush_rows(self, buf, lo, hi, rows):
+        self.calls.append(("rows", lo, hi))
+        full = np.concatenate([self.m, self.n], 1)[self.order[lo:hi]]
+        rows.copy_(torch.from_numpy(full.astype(np.float32)))
+
+    def flush_end(self, buffers, rows, out=None):
+        self.calls.append("end")
+        C = self.m.shape[1]
+        mom = torch.empty((self.m.shape[0], C), dtype=torch.float32)
+        nrm = torch.empty((self.m.shape[0], 3), dtype=torch.float32)
+        idx = torch.from_numpy(self.order.astype(np.int64))
+        mom[idx] = rows[:, :C]
+        nrm[idx] = rows[:, C:]
+        return mom, nrm
+
+
+def _flush_worker(rank, world, port, out_dir):
+    import sys
+
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle"))
+    import oracle as O
+    from paper_2405_16788_b200.parallel import flush_allreduce
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    pos, nrm, area, mu, xs, d_out = _case()
+    tree = O.OracleTree(O.Cloud(pos, nrm, area, mu))
+    tree.set_kinds(np.array([0, 1, 1, 1], np.uint8))
+    lo, hi = shard_range(xs.shape[0], rank, world)
+    m, n, de = tree.adjoint(O.Params(0.08), 2.0, xs[lo:hi], d_out[lo:hi], threads=1)
+    rt = _RowsTree(m, n, de, tree.export()["order"])
+    rows = torch.empty((m.shape[0], m.shape[1] + 3), dtype=torch.float32)
+    mom, nr, de_sum = flush_allreduce(rt, [None], rows=rows, chunks=3)
+    if rank == 0:
+        np.savez(os.path.join(out_dir, "flush.npz"), m=mom.numpy(), n=nr.numpy(), de=de_sum,
+                 calls=np.array([str(c) for c in rt.calls]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_chunked_flush_allreduce_matches_single(tmp_path, oracle_mod):
+    """parallel.flush_allreduce (the multi-GPU flush bench.py runs under NCCL):
+    push-down once, rows of 3 point chunks each all-reduced asynchronously as
+    soon as they exist, scatter to the original order — equal to the
+    single-process flush of the whole batch (fp32 rows)."""
+    O = oracle_mod
+    mp.spawn(_flush_worker, args=(2, _free_port(), str(tmp_path)), nprocs=2, join=True)
+    got = np.load(tmp_path / "flush.npz")
+    pos, nrm, area, mu, xs, d_out = _case()
+    t = O.OracleTree(O.Cloud(pos, nrm, area, mu))
+    t.set_kinds(np.array([0, 1, 1, 1], np.uint8))
+    m, n, de = t.adjoint(O.Params(0.08), 2.0, xs, d_out, threads=1)
+    assert np.abs(got["m"] - m).max() <= 2e-6 * np.abs(m).max()
+    assert np.abs(got["n"] - n).max() <= 2e-6 * np.abs(n).max()
+    assert abs(float(got["de"]) - de) <= 1e-12 * abs(de)
+    calls = list(got["calls"])
+    assert calls[0] == "begin" and calls[-1] == "end" and len(calls) == 5
