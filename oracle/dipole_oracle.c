@@ -9,6 +9,7 @@
 
 #include <math.h>
 #include <pthread.h>
+#include <unistd.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -470,13 +471,21 @@ static inline int is_near(double r, const ora_params* p) {
 
 /* primal (bhtree.cpp:188-234), primal_channel (:236-274) and
  * primal_with_gradient (:276-334) for one query. */
-static void primal_one(const ora_tree* t, const ora_params* p, double beta, const double* x,
-                       int mode, int channel, double* out, double* grad, ora_counters* cnt) {
+/* out_abs (nc) / grad_abs (3C), test-only and NULL normally: the sum of |terms|
+ * each output accumulated (the tolerance scale of a parity test where the
+ * sum cancels); the outputs are unaffected. */
+static void primal_one_mag(const ora_tree* t, const ora_params* p, double beta, const double* x,
+                           int mode, int channel, double* out, double* grad, ora_counters* cnt,
+                           double* out_abs, double* grad_abs) {
   const int C = t->C;
   int nc = mode == 2 ? 1 : C;
   for (int c = 0; c < nc; ++c) out[c] = 0.0;
   if (grad)
     for (int c = 0; c < 3 * C; ++c) grad[c] = 0.0;
+  if (out_abs)
+    for (int c = 0; c < nc; ++c) out_abs[c] = 0.0;
+  if (grad_abs)
+    for (int c = 0; c < 3 * C; ++c) grad_abs[c] = 0.0;
   double beta2 = beta * beta;
   int singular = p->epsilon <= 0.0 && !p->desingularized;
   int order = mode == 1 ? 1 : 0;
@@ -500,15 +509,23 @@ static void primal_one(const ora_tree* t, const ora_params* p, double beta, cons
         double* o = mode == 2 ? out : out + c;
         const double* v = t->mv + ((size_t)ni * C + c) * 3;
         double s = t->ms[(size_t)ni * C + c];
+        double* oa = out_abs ? (mode == 2 ? out_abs : out_abs + c) : NULL;
         if (t->kinds[c] == 0) {
           double vd = dot3(v, d);
           *o += A * k.W * vd;
+          if (oa) *oa += fabs(A * k.W * vd);
           if (mode == 1)
             for (int a = 0; a < 3; ++a) grad[3 * c + a] -= A * (k.W * v[a] + k.Wp_r * vd * d[a]);
+          if (mode == 1 && grad_abs)
+            for (int a = 0; a < 3; ++a)
+              grad_abs[3 * c + a] += fabs(A) * (fabs(k.W * v[a]) + fabs(k.Wp_r * vd * d[a]));
         } else {
           *o += A * k.R * s;
+          if (oa) *oa += fabs(A * k.R * s);
           if (mode == 1)
             for (int a = 0; a < 3; ++a) grad[3 * c + a] -= A * k.Rp_r * s * d[a];
+          if (mode == 1 && grad_abs)
+            for (int a = 0; a < 3; ++a) grad_abs[3 * c + a] += fabs(A * k.Rp_r * s * d[a]);
         }
       }
     } else if (t->leaf[ni]) {
@@ -527,14 +544,22 @@ static void primal_one(const ora_tree* t, const ora_params* p, double beta, cons
           if (mode == 2 && c != channel) continue;
           double* o = mode == 2 ? out : out + c;
           double A = t->ar[pi] * kInvFourPi * t->mu[pi * C + c];
+          double* oa = out_abs ? (mode == 2 ? out_abs : out_abs + c) : NULL;
           if (t->kinds[c] == 0) {
             *o += A * k.W * ndot;
+            if (oa) *oa += fabs(A * k.W * ndot);
             if (mode == 1)
               for (int a = 0; a < 3; ++a) grad[3 * c + a] -= A * (k.W * nn[a] + k.Wp_r * ndot * dm[a]);
+            if (mode == 1 && grad_abs)
+              for (int a = 0; a < 3; ++a)
+                grad_abs[3 * c + a] += fabs(A) * (fabs(k.W * nn[a]) + fabs(k.Wp_r * ndot * dm[a]));
           } else {
             *o += A * k.R;
+            if (oa) *oa += fabs(A * k.R);
             if (mode == 1)
               for (int a = 0; a < 3; ++a) grad[3 * c + a] -= A * k.Rp_r * dm[a];
+            if (mode == 1 && grad_abs)
+              for (int a = 0; a < 3; ++a) grad_abs[3 * c + a] += fabs(A * k.Rp_r * dm[a]);
           }
         }
       }
@@ -542,6 +567,11 @@ static void primal_one(const ora_tree* t, const ora_params* p, double beta, cons
       for (int32_t c = 0; c < t->ccnt[ni]; ++c) stack[sp++] = t->cbeg[ni] + c;
     }
   }
+}
+
+static void primal_one(const ora_tree* t, const ora_params* p, double beta, const double* x,
+                       int mode, int channel, double* out, double* grad, ora_counters* cnt) {
+  primal_one_mag(t, p, beta, x, mode, channel, out, grad, cnt, NULL, NULL);
 }
 
 typedef struct {
@@ -552,6 +582,7 @@ typedef struct {
   int mode, channel;
   double *out, *grad;
   ora_counters* cnt;
+  double *out_abs, *grad_abs;
 } primal_ctx;
 
 static void primal_body(void* v, int64_t lo, int64_t hi, int w) {
@@ -561,22 +592,37 @@ static void primal_body(void* v, int64_t lo, int64_t hi, int w) {
   int nc = c->mode == 2 ? 1 : C;
   for (int64_t i = lo; i < hi; ++i) {
     ora_counters k = {0, 0, 0, 0, 0};
-    primal_one(c->t, c->p, c->beta, c->xs + 3 * i, c->mode, c->channel, c->out + i * nc,
-               c->grad ? c->grad + i * C * 3 : NULL, c->cnt ? &k : NULL);
+    primal_one_mag(c->t, c->p, c->beta, c->xs + 3 * i, c->mode, c->channel, c->out + i * nc,
+                   c->grad ? c->grad + i * C * 3 : NULL, c->cnt ? &k : NULL,
+                   c->out_abs ? c->out_abs + i * nc : NULL,
+                   c->grad_abs ? c->grad_abs + i * C * 3 : NULL);
     if (c->cnt) c->cnt[i] = k;
   }
+}
+
+void ora_primal_ex(const ora_tree* t, const ora_params* p, double beta, const double* xs,
+                   int64_t q, int mode, int channel, double* out, double* grad,
+                   ora_counters* counters, int threads, double* out_abs, double* grad_abs) {
+  primal_ctx c = {t, p, beta, xs, mode, channel, out, mode == 1 ? grad : NULL, counters,
+                  out_abs, mode == 1 ? grad_abs : NULL};
+  parallel_for(q, threads, primal_body, &c);
 }
 
 void ora_primal(const ora_tree* t, const ora_params* p, double beta, const double* xs, int64_t q,
                 int mode, int channel, double* out, double* grad, ora_counters* counters,
                 int threads) {
-  primal_ctx c = {t, p, beta, xs, mode, channel, out, mode == 1 ? grad : NULL, counters};
-  parallel_for(q, threads, primal_body, &c);
+  ora_primal_ex(t, p, beta, xs, q, mode, channel, out, grad, counters, threads, NULL, NULL);
 }
 
-/* GradientBuffer (bhtree.hpp:40-49) */
+/* GradientBuffer (bhtree.hpp:40-49). Test-only extension (mag != 0): beside
+ * every accumulator, a bound on the SUM OF ABSOLUTE VALUES of the terms that
+ * reach it (vector terms by their Euclidean norm), so a parity test can scale
+ * its tolerance to the cancellation the reference's own sum went through.
+ * The accumulators themselves are untouched by it. */
 typedef struct {
   double *node_v, *node_s, *point_mu, *point_n, d_eps;
+  int mag;
+  double *node_va, *node_sa, *point_mua, *point_na, d_epsa;
 } gradbuf;
 
 static void gradbuf_init(gradbuf* b, const ora_tree* t) {
@@ -586,11 +632,27 @@ static void gradbuf_init(gradbuf* b, const ora_tree* t) {
   b->point_mu = calloc(np, sizeof(double));
   b->point_n = calloc((size_t)t->n * 3, sizeof(double));
   b->d_eps = 0;
+  b->mag = 0;
+  b->node_va = b->node_sa = b->point_mua = b->point_na = NULL;
+  b->d_epsa = 0;
+}
+
+static void gradbuf_init_mag(gradbuf* b, const ora_tree* t) {
+  size_t nn = (size_t)t->nodes * t->C, np = (size_t)t->n * t->C;
+  gradbuf_init(b, t);
+  b->mag = 1;
+  b->node_va = calloc(nn, sizeof(double));
+  b->node_sa = calloc(nn, sizeof(double));
+  b->point_mua = calloc(np, sizeof(double));
+  b->point_na = calloc((size_t)t->n * 3, sizeof(double));
 }
 
 static void gradbuf_free(gradbuf* b) {
   free(b->node_v), free(b->node_s), free(b->point_mu), free(b->point_n);
+  free(b->node_va), free(b->node_sa), free(b->point_mua), free(b->point_na);
 }
+
+static inline double norm3(const double* a) { return sqrt(dot3(a, a)); }
 
 /* adjoint: bhtree.cpp:345-417 */
 static void adjoint_one(const ora_tree* t, const ora_params* p, double beta, const double* x,
@@ -618,6 +680,10 @@ static void adjoint_one(const ora_tree* t, const ora_params* p, double beta, con
           const double* v = t->mv + ((size_t)ni * C + c) * 3;
           double vd = dot3(v, d);
           buf->d_eps += ds * A * k.dW_de * vd;
+          if (buf->mag) {
+            buf->node_va[(size_t)ni * C + c] += fabs(A * k.W * ds) * norm3(d);
+            buf->d_epsa += fabs(ds * A * k.dW_de * vd);
+          }
           if (with_grad) {
             const double* dg = d_grad + 3 * c;
             double gd = dot3(dg, d);
@@ -625,12 +691,22 @@ static void adjoint_one(const ora_tree* t, const ora_params* p, double beta, con
             double u[3];
             for (int a = 0; a < 3; ++a) u[a] = k.dW_de * v[a] + k.dWp_r_de * vd * d[a];
             buf->d_eps -= A * dot3(dg, u);
+            if (buf->mag) {
+              buf->node_va[(size_t)ni * C + c] +=
+                  fabs(A) * (fabs(k.W) * norm3(dg) + fabs(k.Wp_r * gd) * norm3(d));
+              for (int a = 0; a < 3; ++a)
+                buf->d_epsa += fabs(A * dg[a]) * (fabs(k.dW_de * v[a]) + fabs(k.dWp_r_de * vd * d[a]));
+            }
           }
           double* nv = buf->node_v + ((size_t)ni * C + c) * 3;
           for (int a = 0; a < 3; ++a) nv[a] += dv[a];
         } else {
           buf->node_s[(size_t)ni * C + c] += A * k.R * ds;
           buf->d_eps += ds * A * k.dR_de * t->ms[(size_t)ni * C + c];
+          if (buf->mag) {
+            buf->node_sa[(size_t)ni * C + c] += fabs(A * k.R * ds);
+            buf->d_epsa += fabs(ds * A * k.dR_de * t->ms[(size_t)ni * C + c]);
+          }
         }
       }
     } else if (t->leaf[ni]) {
@@ -652,18 +728,33 @@ static void adjoint_one(const ora_tree* t, const ora_params* p, double beta, con
             double dn[3];
             for (int a = 0; a < 3; ++a) dn[a] = ds * A * mu * k.W * dm[a];
             buf->d_eps += ds * A * mu * k.dW_de * ndot;
+            if (buf->mag) {
+              buf->point_mua[pi * C + c] += fabs(dmu);
+              for (int a = 0; a < 3; ++a) buf->point_na[3 * pi + a] += fabs(dn[a]);
+              buf->d_epsa += fabs(ds * A * mu * k.dW_de * ndot);
+            }
             if (with_grad) {
               const double* dg = d_grad + 3 * c;
               double gd = dot3(dg, dm), gn = dot3(dg, nn);
               dmu -= A * (k.W * gn + k.Wp_r * ndot * gd);
               for (int a = 0; a < 3; ++a) dn[a] -= A * mu * (k.W * dg[a] + k.Wp_r * gd * dm[a]);
               buf->d_eps -= A * mu * (k.dW_de * gn + k.dWp_r_de * ndot * gd);
+              if (buf->mag) {
+                buf->point_mua[pi * C + c] += fabs(A) * (fabs(k.W * gn) + fabs(k.Wp_r * ndot * gd));
+                for (int a = 0; a < 3; ++a)
+                  buf->point_na[3 * pi + a] += fabs(A * mu) * (fabs(k.W * dg[a]) + fabs(k.Wp_r * gd * dm[a]));
+                buf->d_epsa += fabs(A * mu) * (fabs(k.dW_de * gn) + fabs(k.dWp_r_de * ndot * gd));
+              }
             }
             buf->point_mu[pi * C + c] += dmu;
             for (int a = 0; a < 3; ++a) buf->point_n[3 * pi + a] += dn[a];
           } else {
             buf->point_mu[pi * C + c] += ds * A * k.R;
             buf->d_eps += ds * A * mu * k.dR_de;
+            if (buf->mag) {
+              buf->point_mua[pi * C + c] += fabs(ds * A * k.R);
+              buf->d_epsa += fabs(ds * A * mu * k.dR_de);
+            }
           }
         }
       }
@@ -673,7 +764,53 @@ static void adjoint_one(const ora_tree* t, const ora_params* p, double beta, con
   }
 }
 
-/* flush_gradients: bhtree.cpp:419-463 */
+/* flush_gradients: bhtree.cpp:419-463. The ancestor walk of each point is
+ * independent of every other point's, so it runs over point ranges on
+ * `threads` workers (the same operations per point, in the same order). */
+typedef struct {
+  const ora_tree* t;
+  const double *node_v, *node_s;  /* summed buffers (value) or magnitudes (mag) */
+  double *moments, *normals;
+  int mag;
+} flush_ctx;
+
+static void flush_body(void* v, int64_t lo, int64_t hi, int w) {
+  (void)w;
+  flush_ctx* fc = v;
+  const ora_tree* t = fc->t;
+  const int C = t->C;
+  for (int64_t m = lo; m < hi; ++m) { /* ancestor walk incl. the leaf, :441-457 */
+    double a = t->ar[m];
+    const double* n = t->nrm + 3 * m;
+    for (int32_t ti = t->leaf_of[m]; ti >= 0; ti = t->parent[ti]) {
+      if (!(t->area[ti] > 0)) continue;
+      double f = a / t->area[ti];
+      for (int c = 0; c < C; ++c) {
+        if (t->kinds[c] == 0) {
+          if (fc->mag) {
+            /* |n . g| <= |g| for the unit normal; each normal component <= the
+             * norm of its vector terms */
+            double g = fc->node_v[(size_t)ti * C + c];
+            fc->moments[m * C + c] += f * g;
+            for (int k = 0; k < 3; ++k) fc->normals[3 * m + k] += f * fabs(t->mu[m * C + c]) * g;
+          } else {
+            const double* g = fc->node_v + ((size_t)ti * C + c) * 3;
+            fc->moments[m * C + c] += f * dot3(n, g);
+            for (int k = 0; k < 3; ++k) fc->normals[3 * m + k] += f * t->mu[m * C + c] * g[k];
+          }
+        } else {
+          fc->moments[m * C + c] += f * fc->node_s[(size_t)ti * C + c];
+        }
+      }
+    }
+  }
+}
+
+static int flush_threads(void) {
+  long n = sysconf(_SC_NPROCESSORS_ONLN);
+  return n > 0 ? (int)n : 1;
+}
+
 static void flush(const ora_tree* t, gradbuf* bufs, int nbuf, double* moments, double* normals,
                   double* d_eps) {
   const int C = t->C;
@@ -693,25 +830,33 @@ static void flush(const ora_tree* t, gradbuf* bufs, int nbuf, double* moments, d
     for (size_t i = 0; i < (size_t)M * 3; ++i) normals[i] += bufs[b].point_n[i];
     *d_eps += bufs[b].d_eps;
   }
-  for (int64_t m = 0; m < M; ++m) { /* ancestor walk incl. the leaf, :441-457 */
-    double a = t->ar[m];
-    const double* n = t->nrm + 3 * m;
-    for (int32_t ti = t->leaf_of[m]; ti >= 0; ti = t->parent[ti]) {
-      if (!(t->area[ti] > 0)) continue;
-      double f = a / t->area[ti];
-      for (int c = 0; c < C; ++c) {
-        if (t->kinds[c] == 0) {
-          const double* g = node_v + ((size_t)ti * C + c) * 3;
-          moments[m * C + c] += f * dot3(n, g);
-          for (int k = 0; k < 3; ++k) normals[3 * m + k] += f * t->mu[m * C + c] * g[k];
-        } else {
-          moments[m * C + c] += f * node_s[(size_t)ti * C + c];
-        }
-      }
-    }
-  }
+  flush_ctx fc = {t, node_v, node_s, moments, normals, 0};
+  parallel_for(M, flush_threads(), flush_body, &fc);
   free(node_v);
   free(node_s);
+}
+
+/* the magnitude bounds through the same flush: Sum|terms| of every flushed output */
+static void flush_mag(const ora_tree* t, gradbuf* bufs, int nbuf, double* mom_a, double* nrm_a,
+                      double* deps_a) {
+  const int C = t->C;
+  const int64_t M = t->n;
+  size_t nn = (size_t)t->nodes * C;
+  double* va = calloc(nn, sizeof(double));
+  double* sa = calloc(nn, sizeof(double));
+  memset(mom_a, 0, (size_t)M * C * sizeof(double));
+  memset(nrm_a, 0, (size_t)M * 3 * sizeof(double));
+  *deps_a = 0;
+  for (int b = 0; b < nbuf; ++b) {
+    for (size_t i = 0; i < nn; ++i) va[i] += bufs[b].node_va[i], sa[i] += bufs[b].node_sa[i];
+    for (size_t i = 0; i < (size_t)M * C; ++i) mom_a[i] += bufs[b].point_mua[i];
+    for (size_t i = 0; i < (size_t)M * 3; ++i) nrm_a[i] += bufs[b].point_na[i];
+    *deps_a += bufs[b].d_epsa;
+  }
+  flush_ctx fc = {t, va, sa, mom_a, nrm_a, 1};
+  parallel_for(M, flush_threads(), flush_body, &fc);
+  free(va);
+  free(sa);
 }
 
 typedef struct {
@@ -730,18 +875,33 @@ static void adjoint_body(void* v, int64_t lo, int64_t hi, int w) {
                 c->d_grad ? c->d_grad + i * C * 3 : NULL, &c->bufs[w]);
 }
 
-void ora_adjoint(const ora_tree* t, const ora_params* p, double beta, const double* xs, int64_t q,
-                 const double* d_out, const double* d_grad, int threads, double* moments,
-                 double* normals, double* d_eps) {
+void ora_adjoint_ex(const ora_tree* t, const ora_params* p, double beta, const double* xs,
+                    int64_t q, const double* d_out, const double* d_grad, int threads,
+                    double* moments, double* normals, double* d_eps, double* mom_abs,
+                    double* nrm_abs, double* deps_abs) {
   if (threads < 1) threads = 1;
   if (threads > q) threads = q > 0 ? (int)q : 1;
+  const int mag = mom_abs != NULL;
   gradbuf* bufs = xrealloc(NULL, sizeof(gradbuf) * (size_t)threads);
-  for (int w = 0; w < threads; ++w) gradbuf_init(&bufs[w], t);
+  for (int w = 0; w < threads; ++w) {
+    if (mag)
+      gradbuf_init_mag(&bufs[w], t);
+    else
+      gradbuf_init(&bufs[w], t);
+  }
   adj_ctx c = {t, p, beta, xs, d_out, d_grad, bufs};
   parallel_for(q, threads, adjoint_body, &c);
+  if (mag) flush_mag(t, bufs, threads, mom_abs, nrm_abs, deps_abs);
   flush(t, bufs, threads, moments, normals, d_eps);
   for (int w = 0; w < threads; ++w) gradbuf_free(&bufs[w]);
   free(bufs);
+}
+
+void ora_adjoint(const ora_tree* t, const ora_params* p, double beta, const double* xs, int64_t q,
+                 const double* d_out, const double* d_grad, int threads, double* moments,
+                 double* normals, double* d_eps) {
+  ora_adjoint_ex(t, p, beta, xs, q, d_out, d_grad, threads, moments, normals, d_eps, NULL, NULL,
+                 NULL);
 }
 
 /* ------------------------------------------------------------ naive sums */
@@ -970,20 +1130,28 @@ static void render_body(void* v, int64_t lo, int64_t hi, int w) {
   free(out), free(grad), free(d_out), free(d_grad), free(tape), free(dp), free(dsig);
 }
 
-void ora_render_step(const ora_tree* t, const ora_params* p, double beta, double lambda,
-                     const double* background, const double* rays, int64_t R, int32_t S,
-                     const double* ts, const double* deltas, const double* target, double scale,
-                     int threads, double* rgb, double* moments, double* normals, double* d_eps,
-                     double* d_lambda, double* d_bg) {
+void ora_render_step_ex(const ora_tree* t, const ora_params* p, double beta, double lambda,
+                        const double* background, const double* rays, int64_t R, int32_t S,
+                        const double* ts, const double* deltas, const double* target,
+                        double scale, int threads, double* rgb, double* moments, double* normals,
+                        double* d_eps, double* d_lambda, double* d_bg, double* mom_abs,
+                        double* nrm_abs, double* deps_abs) {
   if (threads < 1) threads = 1;
   if (threads > R) threads = R > 0 ? (int)R : 1;
+  const int mag = mom_abs != NULL;
   gradbuf* bufs = xrealloc(NULL, sizeof(gradbuf) * (size_t)threads);
   double* dl = calloc((size_t)threads, sizeof(double));
   double* db = calloc((size_t)threads * 3, sizeof(double));
-  for (int w = 0; w < threads; ++w) gradbuf_init(&bufs[w], t);
+  for (int w = 0; w < threads; ++w) {
+    if (mag)
+      gradbuf_init_mag(&bufs[w], t);
+    else
+      gradbuf_init(&bufs[w], t);
+  }
   render_ctx c = {t, p, beta, lambda, background, rays, ts, deltas, target, scale, S,
                   rgb, bufs, dl, db};
   parallel_for(R, threads, render_body, &c);
+  if (mag) flush_mag(t, bufs, threads, mom_abs, nrm_abs, deps_abs);
   flush(t, bufs, threads, moments, normals, d_eps);
   *d_lambda = 0;
   d_bg[0] = d_bg[1] = d_bg[2] = 0;
@@ -993,6 +1161,15 @@ void ora_render_step(const ora_tree* t, const ora_params* p, double beta, double
     gradbuf_free(&bufs[w]);
   }
   free(bufs), free(dl), free(db);
+}
+
+void ora_render_step(const ora_tree* t, const ora_params* p, double beta, double lambda,
+                     const double* background, const double* rays, int64_t R, int32_t S,
+                     const double* ts, const double* deltas, const double* target, double scale,
+                     int threads, double* rgb, double* moments, double* normals, double* d_eps,
+                     double* d_lambda, double* d_bg) {
+  ora_render_step_ex(t, p, beta, lambda, background, rays, R, S, ts, deltas, target, scale,
+                     threads, rgb, moments, normals, d_eps, d_lambda, d_bg, NULL, NULL, NULL);
 }
 
 /* ------------------------------------------------------- mean kNN spacing */

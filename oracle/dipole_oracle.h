@@ -67,6 +67,22 @@ void ora_naive_adjoint(const ora_tree* t, const ora_params* p, const double* xs,
                        const double* d_out, const double* d_grad, double* moments,
                        double* normals, double* d_eps);
 
+void ora_primal_ex(const ora_tree* t, const ora_params* p, double beta, const double* xs,
+                   int64_t q, int mode, int channel, double* out, double* grad,
+                   ora_counters* counters, int threads, double* out_abs, double* grad_abs);
+/* Test-only: the same primal / adjoint / render step, plus for every flushed output a
+ * bound on the sum of |terms| it accumulated (the tolerance scale where the
+ * reference's sum cancels). */
+void ora_adjoint_ex(const ora_tree* t, const ora_params* p, double beta, const double* xs,
+                    int64_t q, const double* d_out, const double* d_grad, int threads,
+                    double* moments, double* normals, double* d_eps, double* mom_abs,
+                    double* nrm_abs, double* deps_abs);
+void ora_render_step_ex(const ora_tree* t, const ora_params* p, double beta, double lambda,
+                        const double* background, const double* rays, int64_t R, int32_t S,
+                        const double* ts, const double* deltas, const double* target,
+                        double scale, int threads, double* rgb, double* moments, double* normals,
+                        double* d_eps, double* d_lambda, double* d_bg, double* mom_abs,
+                        double* nrm_abs, double* deps_abs);
 double ora_uniform(uint64_t seed, uint64_t counter);
 void ora_stratified_samples(int64_t R, int32_t S, double t_near, double t_far, uint64_t seed,
                             int64_t ray_offset, double* ts, double* deltas);

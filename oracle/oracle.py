@@ -85,6 +85,14 @@ def port_lib():
                                    C.c_int, C.c_int, _dp, _dp, C.POINTER(Counters), C.c_int]
         lib.ora_adjoint.argtypes = [C.c_void_p, C.POINTER(Params), C.c_double, _dp, C.c_int64,
                                     _dp, _dp, C.c_int, _dp, _dp, _dp]
+        lib.ora_primal_ex.argtypes = [C.c_void_p, C.POINTER(Params), C.c_double, _dp, C.c_int64,
+                                      C.c_int, C.c_int, _dp, _dp, C.c_void_p, C.c_int, _dp, _dp]
+        lib.ora_adjoint_ex.argtypes = [C.c_void_p, C.POINTER(Params), C.c_double, _dp, C.c_int64,
+                                       _dp, _dp, C.c_int, _dp, _dp, _dp, _dp, _dp, _dp]
+        lib.ora_render_step_ex.argtypes = [C.c_void_p, C.POINTER(Params), C.c_double, C.c_double,
+                                           _dp, _dp, C.c_int64, C.c_int32, _dp, _dp, _dp,
+                                           C.c_double, C.c_int, _dp, _dp, _dp, _dp, _dp, _dp,
+                                           _dp, _dp, _dp]
         lib.ora_naive_sum.argtypes = [C.c_void_p, C.POINTER(Params), _dp, C.c_int64, C.c_int,
                                       C.c_int, _dp, _dp]
         lib.ora_naive_adjoint.argtypes = [C.c_void_p, C.POINTER(Params), _dp, C.c_int64, _dp, _dp,
@@ -349,6 +357,43 @@ class OracleTree:
                                              _ptr(nrm), C.byref(de)))
         return mom, nrm, de.value
 
+    def primal_mag(self, params: Params, beta, xs, mode="values", channel=0, threads=None):
+        """Port only: primal() plus the sum of |terms| of every output (dict:
+        out, out_abs, and grad / grad_abs for mode "grad")."""
+        assert self.backend == "port"
+        xs = _d(xs).reshape(-1, 3)
+        q = xs.shape[0]
+        threads = threads or os.cpu_count() or 1
+        m = {"values": 0, "grad": 1, "channel": 2}[mode]
+        shape = q if m == 2 else (q, self.C)
+        out, out_a = np.zeros(shape), np.zeros(shape)
+        grad = np.zeros((q, self.C, 3)) if m == 1 else None
+        grad_a = np.zeros((q, self.C, 3)) if m == 1 else None
+        self._lib.ora_primal_ex(self._h, C.byref(params), beta, _ptr(xs), q, m, channel, _ptr(out),
+                                _ptr(grad), None, threads, _ptr(out_a), _ptr(grad_a))
+        res = dict(out=out, out_abs=out_a)
+        if m == 1:
+            res.update(grad=grad, grad_abs=grad_a)
+        return res
+
+    def adjoint_mag(self, params: Params, beta, xs, d_out, d_grad=None, threads=None):
+        """Port only: adjoint() plus, per flushed output, a bound on the sum of
+        |terms| it accumulated (dict: moments, normals, d_eps and *_abs)."""
+        assert self.backend == "port"
+        xs = _d(xs).reshape(-1, 3)
+        q = xs.shape[0]
+        threads = threads or os.cpu_count() or 1
+        d_out = _d(d_out).reshape(q, self.C)
+        d_grad = None if d_grad is None else _d(d_grad).reshape(q, self.C, 3)
+        mom, mom_a = np.zeros((self.n, self.C)), np.zeros((self.n, self.C))
+        nrm, nrm_a = np.zeros((self.n, 3)), np.zeros((self.n, 3))
+        de, de_a = C.c_double(), C.c_double()
+        self._lib.ora_adjoint_ex(self._h, C.byref(params), beta, _ptr(xs), q, _ptr(d_out),
+                                 _ptr(d_grad), threads, _ptr(mom), _ptr(nrm), C.byref(de),
+                                 _ptr(mom_a), _ptr(nrm_a), C.byref(de_a))
+        return dict(moments=mom, normals=nrm, d_eps=de.value, moments_abs=mom_a,
+                    normals_abs=nrm_a, d_eps_abs=de_a.value)
+
     def gradient_buffers(self, workers):
         """Reference backend only: `workers` caller-held GradientBuffers
         (make_buffer), filled by RefBuffers.adjoint and flushed by RefBuffers.flush."""
@@ -386,7 +431,7 @@ class OracleTree:
         return mom, nrm, de.value
 
     def render_step(self, params: Params, beta, lam, background, rays, ts, deltas, target, scale,
-                    threads=None):
+                    threads=None, mag=False):
         """render_ray + render_ray_backward (renderer.cpp:106-231), direct-rgb head,
         channel 0 Dipole / 1..C-1 Radial (SceneModel::prepare)."""
         assert self.backend == "port", "use RefModel for the reference render step"
@@ -400,11 +445,18 @@ class OracleTree:
         de, dl = C.c_double(), C.c_double()
         dbg = np.zeros(3)
         bg = _d(background)
-        self._lib.ora_render_step(self._h, C.byref(params), beta, lam, _ptr(bg), _ptr(rays), R, S,
-                                  _ptr(_d(ts)), _ptr(_d(deltas)), _ptr(_d(target)), scale, threads,
-                                  _ptr(rgb), _ptr(mom), _ptr(nrm), C.byref(de), C.byref(dl),
-                                  _ptr(dbg))
-        return dict(rgb=rgb, moments=mom, normals=nrm, d_eps=de.value, d_lambda=dl.value, d_bg=dbg)
+        mom_a = np.zeros((self.n, self.C)) if mag else None
+        nrm_a = np.zeros((self.n, 3)) if mag else None
+        de_a = C.c_double()
+        self._lib.ora_render_step_ex(self._h, C.byref(params), beta, lam, _ptr(bg), _ptr(rays), R,
+                                     S, _ptr(_d(ts)), _ptr(_d(deltas)), _ptr(_d(target)), scale,
+                                     threads, _ptr(rgb), _ptr(mom), _ptr(nrm), C.byref(de),
+                                     C.byref(dl), _ptr(dbg), _ptr(mom_a), _ptr(nrm_a),
+                                     C.byref(de_a) if mag else None)
+        res = dict(rgb=rgb, moments=mom, normals=nrm, d_eps=de.value, d_lambda=dl.value, d_bg=dbg)
+        if mag:
+            res.update(moments_abs=mom_a, normals_abs=nrm_a, d_eps_abs=de_a.value)
+        return res
 
 
 class RefBuffers:

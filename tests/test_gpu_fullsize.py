@@ -14,6 +14,7 @@ query:
 """
 import numpy as np
 import pytest
+from parity import check, counters_equal, scalar
 
 pytestmark = pytest.mark.gpu
 
@@ -53,9 +54,18 @@ def test_config2_full_size_properties(oracle_mod):
 
     # subset of the production batch against the reference's primal
     idx = np.random.default_rng(3).choice(Q, 1500, replace=False)
-    want = r.primal(O.Params(eps), 2.0, w["xs"][idx])
-    bad = np.abs(out[idx] - want) > 1e-6 + 1e-4 * np.abs(want)
-    assert int(bad.sum()) == 0, float(np.abs(out[idx] - want).max())
+    want, wcnt = r.primal(O.Params(eps), 2.0, w["xs"][idx], counters=True)
+    check("config2 full size forward, 1500-query subset of the 4M batch", out[idx], want)
+    _, cnt = t.primal(xs[torch.from_numpy(idx).cuda()], p, 2.0, visited=True)
+    counters_equal("config2 full size subset counters", cnt.cpu().numpy(), wcnt)
+
+    # the whole 4M-query adjoint (fused, then list replay) against the oracle's
+    wa = r.adjoint_mag(O.Params(eps), 2.0, w["xs"], d1.astype(np.float64))
+    for name, g in (("fused", g1), ("list replay", g1b)):
+        tag = f"config2 full size adjoint of all 4M queries ({name})"
+        check(f"{tag} moments", g.moments, wa["moments"], wa["moments_abs"])
+        check(f"{tag} normals", g.normals, wa["normals"], wa["normals_abs"])
+        scalar(f"{tag} d_epsilon", g.d_epsilon, wa["d_eps"], wa["d_eps_abs"])
 
     # duality <d_out, primal> = <d moments, moments> (fp64 sums of fp32 terms)
     lhs = float(np.einsum("qc,qc->", d1.astype(np.float64), out.astype(np.float64)))

@@ -8,6 +8,7 @@ re-targeted at the batched GPU API with fp32 tolerances.
 """
 import numpy as np
 import pytest
+from parity import check, counters_equal, scalar
 
 pytestmark = pytest.mark.gpu
 
@@ -104,12 +105,9 @@ def test_primal_parity_mixed_kernels(eng, oracle_mod, beta):
     p = eng.KernelParams(epsilon=0.05)
     got, cnt = t.primal(xs, p, beta, visited=True)
     want, wcnt = r.primal(O.Params(0.05), beta, xs, counters=True)
-    nbad, mx = close(got, want)
-    assert nbad == 0, (nbad, mx)
+    check(f"primal mixed kinds beta={beta}", got, want)
     # identical opening decisions: visited / far / point counts match exactly
-    assert np.array_equal(cnt[:, 0], wcnt[:, 0])
-    assert np.array_equal(cnt[:, 1] + cnt[:, 2], wcnt[:, 1] + wcnt[:, 2])
-    assert np.array_equal(cnt[:, 3] + cnt[:, 4], wcnt[:, 3] + wcnt[:, 4])
+    counters_equal(f"primal mixed kinds beta={beta} counters", cnt, wcnt)
     # primal_channel(c) == primal()[c] (test_bhtree.cpp:140)
     for c in range(3):
         pc = t.primal_channel(xs, p, beta, c)
@@ -124,14 +122,14 @@ def test_primal_with_gradient_parity(eng, oracle_mod):
     xs = np.random.default_rng(8).uniform(-1.5, 1.5, (2000, 3))
     p = eng.KernelParams(epsilon=0.2)
     v, g = t.primal_with_gradient(xs, p, 2.0)
-    wv, wg = r.primal(O.Params(0.2), 2.0, xs, mode="grad")
-    assert close(v, wv)[0] == 0
-    nbad, mx = close(g, wg)
-    assert nbad == 0, (nbad, mx)
+    w = r.primal_mag(O.Params(0.2), 2.0, xs, mode="grad")
+    check("primal_with_gradient values C=2", v, w["out"], w["out_abs"])
+    check("primal_with_gradient gradients C=2", g, w["grad"], w["grad_abs"])
     # values of primal_with_gradient equal primal (test_bhtree.cpp:215-216), fp32 tolerance
     assert close(v, t.primal(xs, p, 2.0))[0] == 0
     v0, g0 = t.primal_grad0(xs, p, 2.0)
-    assert close(v0, wv)[0] == 0 and close(g0, wg[:, 0])[0] == 0
+    check("primal_grad0 values", v0, w["out"], w["out_abs"])
+    check("primal_grad0 gradient of channel 0", g0, w["grad"][:, 0], w["grad_abs"][:, 0])
 
 
 def test_beta_infinity_equals_naive(eng, oracle_mod):
@@ -143,7 +141,7 @@ def test_beta_infinity_equals_naive(eng, oracle_mod):
     got = t.primal(xs, eng.KernelParams(epsilon=0.15), np.inf)
     for c in range(3):
         want = r.naive_sum(O.Params(0.15), xs, c, int(kinds[c]))
-        assert close(got[:, c], want)[0] == 0
+        check(f"beta=inf vs naive_dipole_sum channel {c}", got[:, c], want)
 
 
 @pytest.mark.parametrize("eps,desing,delta", [(0.0, False, 0.0), (0.0, True, 0.05), (0.3, False, 0.0)])
@@ -155,9 +153,9 @@ def test_kernel_variants(eng, oracle_mod, eps, desing, delta):
     xs = np.random.default_rng(22).uniform(-1.2, 1.2, (1000, 3))
     p = eng.KernelParams(epsilon=eps, desingularized=desing, desing_delta=delta)
     v, g = t.primal_with_gradient(xs, p, 2.0)
-    wv, wg = r.primal(O.Params(eps, desing, delta), 2.0, xs, mode="grad")
-    assert close(v, wv, rtol=3e-4)[0] == 0
-    assert rel_scale_err(g, wg) < 1e-4
+    w = r.primal_mag(O.Params(eps, desing, delta), 2.0, xs, mode="grad")
+    check(f"kernel variant eps={eps} desing={desing} values", v, w["out"], w["out_abs"])
+    check(f"kernel variant eps={eps} desing={desing} gradients", g, w["grad"], w["grad_abs"])
 
 
 def test_config1_slice(eng, oracle_mod):
@@ -171,8 +169,7 @@ def test_config1_slice(eng, oracle_mod):
     xs = w["xs"]
     got = t.primal(xs, eng.KernelParams(epsilon=eps), 2.0)
     want = r.primal(O.Params(eps), 2.0, xs)
-    nbad, mx = close(got, want)
-    assert nbad == 0, (nbad, mx)
+    check("config-1 slice primal", got, want)
 
 
 # ---------------------------------------------------------------- adjoint
@@ -191,13 +188,12 @@ def test_adjoint_flush_parity(eng, oracle_mod, with_grad):
     buf = t.make_buffer()
     t.adjoint(xs, p, 2.0, d_out, d_grad, buf)
     g = t.flush_gradients(buf)
-    wm, wn, we = r.adjoint(O.Params(0.1), 2.0, xs, d_out.astype(np.float64),
-                           None if d_grad is None else d_grad.astype(np.float64))
-    assert rel_scale_err(g.moments, wm) < 1e-5
-    assert rel_scale_err(g.normals, wn) < 1e-5
-    assert abs(g.d_epsilon - we) <= 1e-4 * abs(we) + 1e-6
-    nbad, _ = close(g.moments, wm)
-    assert nbad <= 0.001 * wm.size
+    w = r.adjoint_mag(O.Params(0.1), 2.0, xs, d_out.astype(np.float64),
+                      None if d_grad is None else d_grad.astype(np.float64))
+    tag = f"adjoint+flush d_grad={with_grad}"
+    check(f"{tag} moments", g.moments, w["moments"], w["moments_abs"])
+    check(f"{tag} normals", g.normals, w["normals"], w["normals_abs"])
+    scalar(f"{tag} d_epsilon", g.d_epsilon, w["d_eps"], w["d_eps_abs"])
     # flush zeroes the buffer: a second flush is all zeros (test_bhtree.cpp:297-299)
     g2 = t.flush_gradients(buf)
     assert not np.any(g2.moments) and g2.d_epsilon == 0.0
@@ -217,7 +213,15 @@ def test_multi_buffer_flush_order_independent(eng, oracle_mod):
     for w in range(3):
         t.adjoint(xs[w::3], p, 2.0, ds[w::3], None, bufs[w])
     got = t.flush_gradients(bufs)
-    assert rel_scale_err(got.moments, ref.moments) < 1e-6
+    # the reference asserts 1e-10 in fp64 (test_bhtree.cpp:441); here each
+    # buffer's queries form other warps (other fp32 summation groupings), so
+    # both are held to the oracle's result under the parity bar, and to each other
+    w = oracle_mod.OracleTree(oracle_mod.Cloud(pos, nrm, area, mu))
+    wa = w.adjoint_mag(oracle_mod.Params(0.1), 2.0, xs, ds.astype(np.float64))
+    check("multi-buffer flush (3 buffers) moments", got.moments, wa["moments"], wa["moments_abs"])
+    check("single-buffer flush moments", ref.moments, wa["moments"], wa["moments_abs"])
+    check("multi-buffer vs single-buffer flush moments", got.moments, ref.moments,
+          wa["moments_abs"])
 
 
 def test_zero_adjoint_leaves_accumulators_untouched(eng, oracle_mod):
@@ -263,18 +267,21 @@ def test_render_step_parity(eng, oracle_mod):
     p = eng.KernelParams(epsilon=eps)
     rgb, tape = Rn.render_forward(t, p, rs, rays, S)
     scale = 2.0 / (3.0 * rays.shape[0])
-    d_rgb = (scale * (rgb.astype(np.float64) - target)).astype(np.float32)
+    ts, dlt = O.stratified_samples(rays.shape[0], S, 2.0, 6.0, 3)
+    want = r.render_step(O.Params(eps), 2.0, 20.0, [0, 0, 0], rays, ts, dlt, target, scale,
+                         mag=True)
+    # the loss gradient of the oracle's colours: both backward passes start
+    # from the same d_rgb (the GPU colours are checked separately)
+    d_rgb = (scale * (want["rgb"] - target)).astype(np.float32)
     buf = t.make_buffer()
     dl, dbg = Rn.render_backward(t, p, rs, tape, d_rgb, buf)
     g = t.flush_gradients(buf)
-    ts, dlt = O.stratified_samples(rays.shape[0], S, 2.0, 6.0, 3)
-    want = r.render_step(O.Params(eps), 2.0, 20.0, [0, 0, 0], rays, ts, dlt, target, scale)
-    assert close(rgb, want["rgb"])[0] == 0
-    assert rel_scale_err(g.moments, want["moments"]) < 1e-4
-    assert rel_scale_err(g.normals, want["normals"]) < 1e-4
-    assert abs(g.d_epsilon - want["d_eps"]) <= 1e-4 * abs(want["d_eps"]) + 1e-6
-    assert abs(dl - want["d_lambda"]) <= 1e-4 * abs(want["d_lambda"]) + 1e-8
-    assert np.abs(dbg - want["d_bg"]).max() <= 1e-4 * np.abs(want["d_bg"]).max() + 1e-8
+    check("render C=4 S=32 rgb", rgb, want["rgb"])
+    check("render C=4 S=32 moments", g.moments, want["moments"], want["moments_abs"])
+    check("render C=4 S=32 normals", g.normals, want["normals"], want["normals_abs"])
+    scalar("render C=4 S=32 d_epsilon", g.d_epsilon, want["d_eps"], want["d_eps_abs"])
+    scalar("render C=4 S=32 d_lambda", dl, want["d_lambda"], atol=1e-8)
+    check("render C=4 S=32 d_background", dbg, want["d_bg"], atol=1e-8)
 
 
 def test_render_steps_switch_to_lists(eng, oracle_mod):
@@ -326,22 +333,21 @@ def test_many_channel_forward_adjoint(eng, oracle_mod, C):
     p = eng.KernelParams(epsilon=0.06)
     got = t.primal(xs, p, 2.0)
     want, wcnt = r.primal(O.Params(0.06), 2.0, xs, counters=True)
-    nbad, mx = close(got, want)
-    assert nbad == 0, (nbad, mx)
+    check(f"primal C={C}", got, want)
     # the production (two-phase / tensor-core) path replays the reference's
     # opening decisions exactly: identical visited / far / leaf-point counts
     _, cnt = t.primal(xs, p, 2.0, visited=True)
-    assert np.array_equal(cnt[:, 0], wcnt[:, 0])
-    assert np.array_equal(cnt[:, 1] + cnt[:, 2], wcnt[:, 1] + wcnt[:, 2])
-    assert np.array_equal(cnt[:, 3] + cnt[:, 4], wcnt[:, 3] + wcnt[:, 4])
+    counters_equal(f"primal C={C} counters", cnt, wcnt)
     d_out = rng.standard_normal((q, C)).astype(np.float32)
-    buf = t.make_buffer()
-    t.adjoint(xs, p, 2.0, d_out, None, buf)
-    g = t.flush_gradients(buf)
-    wm, wn, we = r.adjoint(O.Params(0.06), 2.0, xs, d_out.astype(np.float64))
-    assert rel_scale_err(g.moments, wm) < 1e-5
-    assert rel_scale_err(g.normals, wn) < 1e-5
-    assert abs(g.d_epsilon - we) <= 1e-4 * abs(we) + 1e-6
+    w = r.adjoint_mag(O.Params(0.06), 2.0, xs, d_out.astype(np.float64))
+    for rnd in range(2):  # fused walk, then (primal -> adjoint pair) list replay
+        t.primal(xs, p, 2.0)
+        buf = t.make_buffer()
+        t.adjoint(xs, p, 2.0, d_out, None, buf)
+        g = t.flush_gradients(buf)
+        check(f"adjoint C={C} moments (pass {rnd})", g.moments, w["moments"], w["moments_abs"])
+        check(f"adjoint C={C} normals (pass {rnd})", g.normals, w["normals"], w["normals_abs"])
+        scalar(f"adjoint C={C} d_epsilon (pass {rnd})", g.d_epsilon, w["d_eps"], w["d_eps_abs"])
 
 
 @pytest.mark.parametrize("eps", [1e-8, 0.06])
@@ -364,19 +370,17 @@ def test_regularized_specialisation_bounds(eng, oracle_mod, eps):
     p = eng.KernelParams(epsilon=eps)
     want = r.primal(O.Params(eps), 2.0, xs)
     d_out = rng.standard_normal((len(xs), C)).astype(np.float32)
-    wm, wn, we = r.adjoint(O.Params(eps), 2.0, xs, d_out.astype(np.float64))
-    for _ in range(2):  # the second primal -> adjoint pair replays interaction lists
+    w = r.adjoint_mag(O.Params(eps), 2.0, xs, d_out.astype(np.float64))
+    for rnd in range(2):  # the second primal -> adjoint pair replays interaction lists
         got = t.primal(xs, p, 2.0)
-        assert np.isfinite(got).all()
-        nbad, mx = close(got, want)
-        assert nbad == 0, (nbad, mx)
+        check(f"regularized bounds eps={eps} primal (pass {rnd})", got, want)
         buf = t.make_buffer()
         t.adjoint(xs, p, 2.0, d_out, None, buf)
         g = t.flush_gradients(buf)
-        assert np.isfinite(g.moments).all() and np.isfinite(g.normals).all()
-        assert rel_scale_err(g.moments, wm) < 1e-5
-        assert rel_scale_err(g.normals, wn) < 1e-5
-        assert abs(g.d_epsilon - we) <= 1e-4 * abs(we) + 1e-6
+        tag = f"regularized bounds eps={eps} adjoint (pass {rnd})"
+        check(f"{tag} moments", g.moments, w["moments"], w["moments_abs"])
+        check(f"{tag} normals", g.normals, w["normals"], w["normals_abs"])
+        scalar(f"{tag} d_epsilon", g.d_epsilon, w["d_eps"], w["d_eps_abs"])
 
 
 # ---------------------------------------------------------------- errors
@@ -493,12 +497,14 @@ def test_interaction_list_reuse_is_keyed_on_the_batch(eng, oracle_mod):
         b = t.make_buffer()
         t.adjoint(dev, p, beta_a, ddo, None, b)
         g = t.flush_gradients(b)
-        wm, wn, we = r.adjoint(O.Params(0.05), beta_a, xs2, d_out.astype(np.float64))
-        assert rel_scale_err(g.moments, wm) < 1e-5
-        assert rel_scale_err(g.normals, wn) < 1e-5
+        w = r.adjoint_mag(O.Params(0.05), beta_a, xs2, d_out.astype(np.float64))
+        tag = f"list reuse keyed on batch beta {beta_f}->{beta_a}"
+        check(f"{tag} moments", g.moments, w["moments"], w["moments_abs"])
+        check(f"{tag} normals", g.normals, w["normals"], w["normals_abs"])
+        scalar(f"{tag} d_epsilon", g.d_epsilon, w["d_eps"], w["d_eps_abs"])
         # and a primal on the edited buffer matches the oracle too
         got = t.primal(dev, p, beta_a).cpu().numpy()
-        assert close(got, r.primal(O.Params(0.05), beta_a, xs2))[0] == 0
+        check(f"{tag} primal", got, r.primal(O.Params(0.05), beta_a, xs2))
     # rebuilt tree (same queries): lists are rebuilt as well
     pos2 = pos + 0.01
     t.build(eng.OrientedPointCloud(pos2, nrm, area, mu))
