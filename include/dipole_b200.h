@@ -184,6 +184,12 @@ int dpl_sample_rays(dpl_tree_t tree, const dpl_kernel_params* params, double bet
 int dpl_gradbuf_create(dpl_tree_t tree, dpl_gradbuf_t* out);
 int dpl_gradbuf_destroy(dpl_gradbuf_t buf);
 int dpl_gradbuf_zero(dpl_gradbuf_t buf);
+/* The accumulators of a buffer in the reference's GradientBuffer layout
+ * (bhtree.hpp:40-49): node_v nodes x C x 3, node_s nodes x C (a channel of the
+ * other kind reads 0), point_mu N x C and point_n N x 3 in cloud order,
+ * d_epsilon. Any pointer may be NULL. Synchronous (host outputs). */
+int dpl_gradbuf_export(dpl_gradbuf_t buf, double* node_v, double* node_s, double* point_mu,
+                       double* point_n, double* d_epsilon);
 /* DipoleTree::adjoint (bhtree.cpp:345-417) for q queries: d_out q x C,
  * d_grad NULL or q x C x 3 (radial channels ignore d_grad, as the reference).
  * Warp-aggregated accumulation into node / leaf-point buffers; no per-point

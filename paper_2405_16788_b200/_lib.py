@@ -120,6 +120,7 @@ _sig = {
     "dpl_gradbuf_create": (C.c_int, [_vp, C.POINTER(_vp)]),
     "dpl_gradbuf_destroy": (C.c_int, [_vp]),
     "dpl_gradbuf_zero": (C.c_int, [_vp]),
+    "dpl_gradbuf_export": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
     "dpl_adjoint": (C.c_int, [_vp, C.POINTER(KernelParams), C.c_double, _vp, C.c_int64, _vp, _vp,
                               _vp]),
     "dpl_flush": (C.c_int, [_vp, C.POINTER(_vp), C.c_int32, _vp, _vp, C.POINTER(C.c_double)]),

@@ -965,6 +965,62 @@ static void check_buf(dpl_tree_t h, dpl_gradbuf_t b) {
           DPL_ERR_DATA, "gradient buffer does not match the tree (rebuilt or kinds changed)");
 }
 
+int dpl_gradbuf_export(dpl_gradbuf_t b, double* node_v, double* node_s, double* point_mu,
+                       double* point_n, double* d_epsilon) {
+  return guard([&] {
+    require(b != nullptr, DPL_ERR_USAGE, "null buffer");
+    dpl_tree_t h = b->tree;
+    check_tree(h);
+    check_buf(h, b);
+    Tree& t = h->t;
+    DPL_CUDA(cudaSetDevice(t.device));
+    const GradBuf& g = b->b;
+    const int64_t nn = t.nodes, n = t.n;
+    const int C = t.C, Cd = t.Cd, Cr = t.Cr;
+    std::vector<double> nv((size_t)nn * Cd * 3), ns((size_t)nn * Cr), pmd((size_t)n * Cd),
+        pmr((size_t)n * Cr), pn((size_t)n * 3);
+    std::vector<int32_t> order(n);
+    double de = 0;
+    auto get = [&](void* dst, const void* src, size_t bytes) {
+      if (bytes) DPL_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, t.stream));
+    };
+    get(nv.data(), g.node_v, nv.size() * 8);
+    get(ns.data(), g.node_s, ns.size() * 8);
+    get(pmd.data(), g.pt_mud, pmd.size() * 8);
+    get(pmr.data(), g.pt_mur, pmr.size() * 8);
+    get(pn.data(), g.pt_n, pn.size() * 8);
+    get(&de, g.d_eps, 8);
+    get(order.data(), t.order.p, (size_t)n * 4);
+    DPL_CUDA(cudaStreamSynchronize(t.stream));
+    // device slots -> the reference's per-channel layout (a channel of the
+    // other kind keeps its zero entry); points from tree order to cloud order
+    for (int64_t i = 0; i < nn; ++i)
+      for (int c = 0; c < C; ++c) {
+        const int k = t.slot_of[c];
+        if (t.kinds[c] == 0) {
+          if (node_v)
+            for (int a = 0; a < 3; ++a) node_v[(i * C + c) * 3 + a] = nv[((size_t)i * Cd + k) * 3 + a];
+          if (node_s) node_s[i * C + c] = 0.0;
+        } else {
+          if (node_v)
+            for (int a = 0; a < 3; ++a) node_v[(i * C + c) * 3 + a] = 0.0;
+          if (node_s) node_s[i * C + c] = ns[(size_t)i * Cr + k];
+        }
+      }
+    for (int64_t j = 0; j < n; ++j) {
+      const int64_t m = order[j];
+      for (int c = 0; c < C; ++c) {
+        const int k = t.slot_of[c];
+        if (point_mu)
+          point_mu[m * C + c] = t.kinds[c] == 0 ? pmd[(size_t)j * Cd + k] : pmr[(size_t)j * Cr + k];
+      }
+      if (point_n)
+        for (int a = 0; a < 3; ++a) point_n[m * 3 + a] = pn[(size_t)j * 3 + a];
+    }
+    if (d_epsilon) *d_epsilon = de;
+  });
+}
+
 int dpl_adjoint(dpl_tree_t h, const dpl_kernel_params* params, double beta_bh, const double* xs,
                 int64_t q, const float* d_out, const float* d_grad, dpl_gradbuf_t buf) {
   return guard([&] {

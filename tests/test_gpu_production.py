@@ -202,3 +202,31 @@ def test_primal_with_gradient_all_channels_c49(oracle_mod):
     w = r.primal_mag(O.Params(eps), 2.0, xs, mode="grad")
     check("primal_with_gradient C=49 values", v, w["out"], w["out_abs"])
     check("primal_with_gradient C=49 all-channel gradients", g, w["grad"], w["grad_abs"])
+
+
+@pytest.mark.parametrize("n,C,seed", [(1, 1, 0), (64, 2, 23), (3000, 4, 5), (20000, 49, 7)])
+def test_dplt_dump_byte_identical_to_reference(oracle_mod, tmp_path, n, C, seed):
+    """DipoleTree::dump (bhtree.cpp:465-494): the engine's DPLT file equals the
+    reference build's (oracle/_ref, the reference's own bhtree.cpp) byte for
+    byte — node records, point order and both moment arrays in fp64."""
+    import paper_2405_16788_b200 as P
+
+    O = oracle_mod
+    if not O.have_ref():
+        pytest.skip("oracle/_ref not built")
+    rng = np.random.default_rng(seed)
+    pos = rng.uniform(-1, 1, (n, 3)).astype(np.float32).astype(np.float64)
+    nrm = rng.standard_normal((n, 3))
+    nrm /= np.linalg.norm(nrm, axis=1, keepdims=True)
+    area = rng.uniform(0.5, 1, n) / max(n, 1)
+    mu = rng.standard_normal((n, C))
+    t = P.DipoleTree(0)
+    t.build(P.OrientedPointCloud(pos, nrm, area, mu))
+    r = O.OracleTree(O.Cloud(pos, nrm, area, mu), backend="ref")
+    a, b = tmp_path / "gpu.dplt", tmp_path / "ref.dplt"
+    t.dump(str(a))
+    r.dump(str(b))
+    ga, gb = a.read_bytes(), b.read_bytes()
+    assert len(ga) == len(gb)
+    diff = np.flatnonzero(np.frombuffer(ga, np.uint8) != np.frombuffer(gb, np.uint8))
+    assert diff.size == 0, f"{diff.size} bytes differ, first at offset {diff[0]}"
