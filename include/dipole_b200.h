@@ -251,9 +251,19 @@ int dpl_render_backward(dpl_tree_t tree, const dpl_kernel_params* params,
  * for the render step: sizes run from 22 + (C - 1) inputs (x, sh(omega), normal,
  * appearance) to 3 outputs; w: the reference's flat fp64 layout (per layer rows
  * x cols weights then the bias, radiance.cpp:44-57). n_sizes = 0 restores the
- * direct-rgb head. The layers run as fp32 GEMMs (cuBLAS). */
+ * direct-rgb head. The layers run on the tensor cores (dpl_gemm_f32's kernel). */
 int dpl_tree_set_mlp_head(dpl_tree_t tree, const int32_t* sizes, int32_t n_sizes, const double* w,
                           int64_t n_w);
+/* The tiny-MLP head's tensor-core GEMM (tcgen05.mma kind::tf32 with a 3-term
+ * hi/lo split, A in TMEM, TMEM accumulators; fp32-class accuracy), exported for
+ * tests and host code: D[i][j] = sum_l A[i][l] B[j][l] (d: m x n, row stride
+ * ldd), with A read as a[i * lda + l] when a_kcontig else a[l * lda + i], B
+ * likewise. flags bit 0: stage B through a pre-split image (bulk async copies,
+ * the path the head's weights take). Device pointers; stream NULL = the legacy
+ * default stream; synchronous. */
+int dpl_gemm_f32(int device, void* stream, int32_t m, int32_t n, int32_t k, const float* a,
+                 int64_t lda, int32_t a_kcontig, const float* b, int64_t ldb, int32_t b_kcontig,
+                 float* d, int64_t ldd, int32_t flags);
 /* RenderGrads::d_head_w accumulated (fp64) by dpl_render_backward since the
  * last call; the accumulator is reset. */
 int dpl_head_grads(dpl_tree_t tree, double* d_w, int64_t n_w);

@@ -21,6 +21,7 @@
 #include "train.cuh"
 #include "render.cuh"
 #include "sampling.cuh"
+#include "tc_gemm.cuh"
 #include "tree.cuh"
 
 namespace dpl {
@@ -1226,6 +1227,12 @@ int dpl_tape_destroy(dpl_tape_t tp) {
 
 double dpl_uniform(uint64_t seed, uint64_t counter) { return host_uniform(seed, counter); }
 
+// samples per tiny-MLP head pass: large enough that the weight-gradient GEMM's
+// split-K partial sums (fp64 atomics) and the per-layer launches amortise over
+// many samples; the chunk's activations (samples x sum of widths fp32) stay a
+// few GB of HBM
+constexpr int64_t kMlpChunk = 1 << 20;
+
 static void check_render_layout(Tree& t) {
   require(t.C >= 4, DPL_ERR_DATA, "direct-rgb head needs at least 3 appearance channels");
   // every channel, not only the ones the direct-rgb head reads: the render
@@ -1302,7 +1309,7 @@ int dpl_render_forward(dpl_tree_t h, const dpl_kernel_params* params, const dpl_
     }
     if (mlp) {  // head raw outputs, in sample chunks (RadianceHead::eval, radiance.cpp:146-154)
       const int din = h->head.din();
-      const int64_t chunk = std::min<int64_t>(Q, 1 << 16);
+      const int64_t chunk = std::min<int64_t>(Q, kMlpChunk);
       tape->head_raw.reserve(Q * 12);
       tape->mlp_x.reserve((size_t)chunk * din * 4);
       PhaseTimer pt(t, PH_RENDER);
@@ -1369,7 +1376,7 @@ int dpl_render_backward(dpl_tree_t h, const dpl_kernel_params* params, const dpl
                          tape->sums.as<double>());
     if (mlp) {  // head backward (radiance.cpp:176-179) -> appearance / normal adjoints
       const int din = h->head.din();
-      const int64_t chunk = std::min<int64_t>(Q, 1 << 16);
+      const int64_t chunk = std::min<int64_t>(Q, kMlpChunk);
       tape->mlp_x.reserve((size_t)chunk * din * 4);
       tape->mlp_dx.reserve((size_t)chunk * din * 4);
       PhaseTimer pt(t, PH_RENDER);
@@ -1412,6 +1419,33 @@ int dpl_render_backward(dpl_tree_t h, const dpl_kernel_params* params, const dpl
   });
 }
 
+
+// ---------------------------------------------------------------- tensor-core GEMM
+int dpl_gemm_f32(int device, void* stream, int32_t m, int32_t n, int32_t k, const float* a,
+                 int64_t lda, int32_t a_kcontig, const float* b, int64_t ldb, int32_t b_kcontig,
+                 float* d, int64_t ldd, int32_t flags) {
+  return guard([&] {
+    require(m >= 0 && n >= 0 && k >= 0, DPL_ERR_USAGE, "gemm: negative size");
+    require((m == 0 || n == 0) || (a && b && d), DPL_ERR_USAGE, "gemm: null operand");
+    require((a == nullptr || is_device_ptr(a)) && (b == nullptr || is_device_ptr(b)) &&
+                (d == nullptr || is_device_ptr(d)),
+            DPL_ERR_USAGE, "gemm: operands must be device memory");
+    DPL_CUDA(cudaSetDevice(device));
+    TcGemm g;
+    g.M = m, g.N = n, g.K = k;
+    g.A = a, g.lda = lda, g.a_kcontig = a_kcontig != 0;
+    g.B = b, g.ldb = ldb, g.b_kcontig = b_kcontig != 0;
+    g.D = d, g.ldd = ldd;
+    DevBuf img;
+    if (flags & 1) {  // the pre-split image path (bulk copies of B)
+      img.reserve(tc_b_image_bytes(n, k));
+      tc_b_image(b, ldb, b_kcontig != 0, n, k, img.as<uint8_t>(), (cudaStream_t)stream);
+      g.b_image = img.as<uint8_t>();
+    }
+    tc_gemm(g, device, (cudaStream_t)stream);
+    DPL_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  });
+}
 
 // ---------------------------------------------------------------- profiling
 

@@ -4,21 +4,14 @@
 #include <algorithm>
 #include <cstdlib>
 
-#include <dlfcn.h>
-
 #include "mlp_head.cuh"
+#include "tc_gemm.cuh"
 
 #include "../../include/dipole_b200.h"
 
 namespace dpl {
 
 namespace {
-
-#define BLAS(x)                                                                       \
-  do {                                                                                \
-    cublasStatus_t st_ = (x);                                                         \
-    if (st_ != CUBLAS_STATUS_SUCCESS) throw Error(DPL_ERR_CUDA, "cuBLAS call failed"); \
-  } while (0)
 
 inline unsigned blocks_for(int64_t n, int b) {
   return (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + b - 1) / b, 148 * 32));
@@ -81,34 +74,6 @@ __global__ void k_bias_act(float* __restrict__ y, const float* __restrict__ b, i
   }
 }
 
-// ReLU gate of the backward pass: delta = 0 where the layer output <= 0 (:105-107)
-__global__ void k_gate(float* __restrict__ d, const float* __restrict__ out, int64_t n) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    if (out[i] <= 0.f) d[i] = 0.f;
-}
-
-// bias gradient: column sums of delta (q x rows) into db
-__global__ void k_colsum(const float* __restrict__ d, int64_t q, int rows, float* __restrict__ db) {
-  const int c = blockIdx.x;
-  float s = 0.f;
-  for (int64_t i = threadIdx.x; i < q; i += blockDim.x) s += d[i * rows + c];
-  __shared__ float red[256];
-  red[threadIdx.x] = s;
-  __syncthreads();
-  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-    if ((int)threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) db[c] = red[0];
-}
-
-__global__ void k_acc64(double* __restrict__ dst, const float* __restrict__ src, int64_t n) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    dst[i] += (double)src[i];
-}
-
 __global__ void k_to_f32(const double* __restrict__ a, int64_t n, float* __restrict__ b) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -117,9 +82,7 @@ __global__ void k_to_f32(const double* __restrict__ a, int64_t n, float* __restr
 
 }  // namespace
 
-MlpHead::~MlpHead() {
-  if (blas) cublasDestroy(blas);
-}
+MlpHead::~MlpHead() = default;
 
 int MlpHead::widest() const {
   int w = 0;
@@ -146,23 +109,7 @@ void mlp_set(MlpHead& m, const Tree& t, const int* sizes, int n_sizes, const dou
   }
   if (n != n_w) throw Error(DPL_ERR_DATA, "mlp head: weight count does not match the sizes");
   m.n_w = n;
-  if (!m.blas) {
-    BLAS(cublasCreate(&m.blas));
-    // fp32 GEMMs on the tensor cores through cuBLAS's BF16x9 fp32 emulation
-    // (fp32-accurate, Blackwell, cuBLAS >= 12.9) when the process's cuBLAS has
-    // it — a host that loaded an older libcublas.so.12 first (e.g. a framework's
-    // bundled copy) keeps the plain FFMA SGEMM; DPL_MLP_SGEMM=1 forces SGEMM
-    using set_emu_t = cublasStatus_t (*)(cublasHandle_t, cublasEmulationStrategy_t);
-    static const auto set_emu = (set_emu_t)dlsym(RTLD_DEFAULT, "cublasSetEmulationStrategy");
-    static const bool plain = getenv("DPL_MLP_SGEMM") != nullptr || set_emu == nullptr;
-    m.emulated = !plain;
-    if (plain) {
-      BLAS(cublasSetMathMode(m.blas, CUBLAS_DEFAULT_MATH));
-    } else {
-      BLAS(cublasSetMathMode(m.blas, CUBLAS_FP32_EMULATED_BF16X9_MATH));
-      BLAS(set_emu(m.blas, CUBLAS_EMULATION_STRATEGY_EAGER));
-    }
-  }
+  m.device = t.device;
   // fp32 weights: the host fp64 array goes up once, converted on the device
   DevBuf w64;
   w64.reserve(n * 8);
@@ -172,7 +119,23 @@ void mlp_set(MlpHead& m, const Tree& t, const int* sizes, int n_sizes, const dou
   count_launch();
   m.dw64.reserve(n * 8);
   DPL_CUDA(cudaMemsetAsync(m.dw64.p, 0, n * 8, t.stream));
-  m.dw32.reserve(n * 4);
+  // tensor-core B images of every layer's W and W^T (weights change only here)
+  m.img_fwd.clear(), m.img_bwd.clear();
+  size_t ib = 0;
+  for (int l = 0; l + 1 < n_sizes; ++l) {
+    const int rows = m.sizes[l + 1], cols = m.sizes[l];
+    m.img_fwd.push_back(ib);
+    ib += tc_b_image_bytes(rows, cols);
+    m.img_bwd.push_back(ib);
+    ib += tc_b_image_bytes(cols, rows);
+  }
+  m.img.reserve(ib);
+  for (int l = 0; l + 1 < n_sizes; ++l) {
+    const int rows = m.sizes[l + 1], cols = m.sizes[l];
+    const float* W = m.w32.as<float>() + m.offs[l];
+    tc_b_image(W, cols, true, rows, cols, m.img.as<uint8_t>() + m.img_fwd[l], t.stream);
+    tc_b_image(W, cols, false, cols, rows, m.img.as<uint8_t>() + m.img_bwd[l], t.stream);
+  }
   DPL_CUDA(cudaStreamSynchronize(t.stream));
   m.active = true;
 }
@@ -183,18 +146,20 @@ void mlp_inputs(cudaStream_t s, const double* rays, int S, const double* xs, con
   count_launch();
 }
 
-// layer l: out (q x rows) = in (q x cols) . W^T + b  (cuBLAS column-major view)
+// layer l: out (q x rows) = in (q x cols) . W^T + b, ReLU except on the last layer
 static void layer_fwd(MlpHead& m, cudaStream_t s, int l, const float* in, int64_t q, float* out) {
   const int rows = m.sizes[l + 1], cols = m.sizes[l];
-  const float one = 1.f, zero = 0.f;
   const float* W = m.w32.as<float>() + m.offs[l];
-  BLAS(cublasSetStream(m.blas, s));
-  BLAS(cublasSgemm(m.blas, CUBLAS_OP_T, CUBLAS_OP_N, rows, (int)q, cols, &one, W, cols, in, cols,
-                   &zero, out, rows));
   const bool last = l + 2 == (int)m.sizes.size();
-  k_bias_act<<<blocks_for(q * rows, 256), 256, 0, s>>>(out, W + (size_t)rows * cols, q, rows,
-                                                       last ? 0 : 1);
-  count_launch();
+  TcGemm g;
+  g.M = (int)q, g.N = rows, g.K = cols;
+  g.A = in, g.lda = cols;             // in[q][cols]
+  g.B = W, g.ldb = cols;              // W[rows][cols]
+  g.b_image = m.img.as<uint8_t>() + m.img_fwd[l];
+  g.D = out, g.ldd = rows;
+  g.bias = W + (size_t)rows * cols;
+  g.epi = last ? TC_BIAS : TC_BIAS_RELU;
+  tc_gemm(g, m.device, s);
 }
 
 void mlp_forward(MlpHead& m, cudaStream_t s, const float* X, int64_t q, float* raw) {
@@ -227,32 +192,41 @@ void mlp_backward(MlpHead& m, cudaStream_t s, const float* X, int64_t q, const f
   }
   float* dbuf[2] = {p, p + (size_t)q * wide};
   for (int l = 0; l < L; ++l) layer_fwd(m, s, l, act[l], q, act[l + 1]);
-  const float one = 1.f, zero = 0.f;
+  // delta: d loss / d (output of layer l), already through that layer's ReLU
   const float* delta = d_raw;
+  double* dw = m.dw64.as<double>();
   for (int l = L - 1; l >= 0; --l) {
     const int rows = m.sizes[l + 1], cols = m.sizes[l];
-    float* dl = const_cast<float*>(delta);
-    if (l + 1 < L) {  // ReLU gate with this layer's output
-      k_gate<<<blocks_for(q * rows, 256), 256, 0, s>>>(dl, act[l + 1], q * rows);
-      count_launch();
-    }
     const float* W = m.w32.as<float>() + m.offs[l];
-    float* dW = m.dw32.as<float>() + m.offs[l];
-    // dW (rows x cols) = delta^T . in ; db = column sums of delta
-    BLAS(cublasSgemm(m.blas, CUBLAS_OP_N, CUBLAS_OP_T, cols, rows, (int)q, &one, act[l], cols,
-                     delta, rows, &zero, dW, cols));
-    k_colsum<<<rows, 256, 0, s>>>(delta, q, rows, dW + (size_t)rows * cols);
-    count_launch();
-    // d_in (q x cols) = delta . W
-    float* din = l == 0 ? dX : dbuf[l & 1];
-    BLAS(cublasSgemm(m.blas, CUBLAS_OP_N, CUBLAS_OP_N, cols, (int)q, rows, &one, W, cols, delta,
-                     rows, &zero, din, cols));
-    delta = din;
+    // dW (rows x cols) += delta^T . in over the chunk's samples (split-K, fp64
+    // accumulation into RenderGrads::d_head_w)
+    TcGemm gw;
+    gw.M = rows, gw.N = cols, gw.K = (int)q;
+    gw.A = delta, gw.lda = rows, gw.a_kcontig = false;   // A[r][q] = delta[q][r]
+    gw.B = act[l], gw.ldb = cols, gw.b_kcontig = false;  // B[c][q] = in[q][c]
+    gw.D64 = dw + m.offs[l], gw.ldd = cols;
+    gw.epi = TC_ACC64;
+    // one wave of CTAs: the M x N tiles times the K slices ~ the SM count
+    const int tiles = ((rows + 127) / 128) * ((cols + 127) / 128);
+    gw.split_k = (int)std::max<int64_t>(1, std::min<int64_t>(2 * 148 / tiles, q / 1024));
+    // db = column sums of delta, summed by the same CTAs as A's row sums
+    gw.bias_grad = dw + m.offs[l] + (size_t)rows * cols;
+    tc_gemm(gw, m.device, s);
+    // d_in (q x cols) = delta . W, through the ReLU of the layer below (its
+    // output is act[l], Mlp::backward's gate, radiance.cpp:105-107)
+    TcGemm gi;
+    gi.M = (int)q, gi.N = cols, gi.K = rows;
+    gi.A = delta, gi.lda = rows;                      // delta[q][rows]
+    gi.B = W, gi.ldb = cols, gi.b_kcontig = false;    // B[c][r] = W[r][c]
+    gi.b_image = m.img.as<uint8_t>() + m.img_bwd[l];
+    gi.D = l == 0 ? dX : dbuf[l & 1], gi.ldd = cols;
+    if (l > 0) {
+      gi.epi = TC_GATE;
+      gi.aux = act[l], gi.ldaux = cols;
+    }
+    tc_gemm(gi, m.device, s);
+    delta = gi.D;
   }
-  // fold the chunk's fp32 gradient into the fp64 accumulator (RenderGrads::d_head_w)
-  k_acc64<<<blocks_for(m.n_w, 256), 256, 0, s>>>(m.dw64.as<double>(), m.dw32.as<float>(),
-                                                 (int64_t)m.n_w);
-  count_launch();
 }
 
 }  // namespace dpl

@@ -5,12 +5,11 @@
 // sh_encode(omega_head) (16), implicit normal (3), appearance channels (K).
 // Dense ReLU layers, linear last layer, rgb = logistic(raw). Weights keep the
 // reference's flat layout (per layer: rows x cols matrix, then the bias).
-// The layers are fp32 cuBLAS GEMMs (plain library GEMMs) with our own
-// bias / ReLU / gather kernels; the weight gradient accumulates in fp64 over
-// sample chunks like RenderGrads::d_head_w.
+// The layers run on the tensor cores through tc_gemm.cuh (tcgen05, TMEM
+// accumulators, 3xTF32 for fp32-class accuracy) with bias / ReLU / ReLU-gate
+// fused into the epilogue; the weight gradient accumulates in fp64 like
+// RenderGrads::d_head_w.
 #pragma once
-
-#include <cublas_v2.h>
 
 #include <vector>
 
@@ -22,16 +21,18 @@ constexpr int kShDim = 16;
 
 struct MlpHead {
   bool active = false;
-  bool emulated = false;     // GEMMs through cuBLAS's BF16x9 fp32 emulation
+  int device = 0;
   int K = 0;                 // appearance channels (= tree C - 1)
   std::vector<int> sizes;    // sizes[0] = 22 + K, back() = 3
   std::vector<size_t> offs;  // layer offsets into the flat weights
   size_t n_w = 0;
   DevBuf w32;   // fp32 weights, reference layout
   DevBuf dw64;  // fp64 weight gradient accumulator
-  DevBuf dw32;  // one chunk's fp32 weight gradient
   DevBuf ws;    // activations / deltas of one chunk
-  cublasHandle_t blas = nullptr;
+  // per layer: pre-split tensor-core images of W (forward: B[r][c] = W[r][c])
+  // and of W^T (input gradient: B[c][r] = W[r][c]), built by mlp_set
+  std::vector<size_t> img_fwd, img_bwd;  // byte offsets into img
+  DevBuf img;
   ~MlpHead();
   int din() const { return sizes.empty() ? 0 : sizes.front(); }
   int widest() const;
