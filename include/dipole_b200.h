@@ -317,6 +317,18 @@ int dpl_tree_refresh_moments(dpl_tree_t tree);
 int dpl_adam_step(dpl_tree_t tree, float* params, const float* grads, float* m, float* v,
                   int64_t n, double lr, double beta1, double beta2, double eps, int64_t t);
 
+/* ---- debugging: guard zones ---------------------------------------------------
+ * With DPL_GUARD=1 in the environment (read once), every device buffer the
+ * engine allocates gets 4 KB guard zones before and after it, filled with a
+ * byte pattern. dpl_guard_check synchronizes the device and verifies every
+ * live buffer's zones (and reports zones found overwritten when buffers were
+ * released): NumericalError naming the buffer sizes on a hit. live_buffers
+ * (may be NULL) receives the number of guarded buffers checked. */
+int dpl_guard_check(int64_t* live_buffers);
+/* Positive control of the detector: writes 4 bytes past the end of a fresh
+ * guarded buffer and requires dpl_guard_check to report it (DPL_GUARD=1). */
+int dpl_guard_selftest(void);
+
 /* ---- measurement -----------------------------------------------------------
  * Per-phase CUDA-event timing on the handle's stream (phases: 0 query Morton
  * sort, 1 forward traversal, 2 adjoint traversal, 3 flush, 4 render per-ray

@@ -136,6 +136,8 @@ _sig = {
     "dpl_uniform": (C.c_double, [C.c_uint64, C.c_uint64]),
     "dpl_gemm_f32": (C.c_int, [C.c_int, _vp, C.c_int32, C.c_int32, C.c_int32, _vp, C.c_int64,
                                C.c_int32, _vp, C.c_int64, C.c_int32, _vp, C.c_int64, C.c_int32]),
+    "dpl_guard_check": (C.c_int, [C.POINTER(C.c_int64)]),
+    "dpl_guard_selftest": (C.c_int, []),
     "dpl_profile_enable": (C.c_int, [_vp, C.c_int]),
     "dpl_profile_read": (C.c_int, [_vp, _vp, _vp]),
     "dpl_peak_fp32": (C.c_int, [C.c_int, C.POINTER(C.c_double)]),

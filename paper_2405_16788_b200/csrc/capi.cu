@@ -26,7 +26,16 @@
 
 namespace dpl {
 static std::atomic<long long> g_launches{0};
-void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+void count_launch(int n) {
+  g_launches.fetch_add(n, std::memory_order_relaxed);
+  static const bool guard = getenv("DPL_GUARD") != nullptr;
+  if (guard) {  // debug mode: name the launch that failed
+    cudaError_t e = cudaPeekAtLastError();
+    if (e != cudaSuccess)
+      throw Error(4, std::string("launch #") + std::to_string(g_launches.load()) + ": " +
+                         cudaGetErrorString(e));
+  }
+}
 }  // namespace dpl
 
 using namespace dpl;
@@ -1419,6 +1428,34 @@ int dpl_render_backward(dpl_tree_t h, const dpl_kernel_params* params, const dpl
   });
 }
 
+
+// ---------------------------------------------------------------- guard zones
+int dpl_guard_check(int64_t* live_buffers) {
+  return guard([&] {
+    std::string msg;
+    const int bad = guard_check_all(msg);
+    if (live_buffers) *live_buffers = guard_live_count();
+    if (bad) throw Error(DPL_ERR_NUMERICAL, "out-of-bounds device write: " + msg);
+  });
+}
+
+__global__ void k_poke_past_end(unsigned char* p, size_t bytes) { p[bytes + 3] = 0x5a; }
+
+int dpl_guard_selftest(void) {
+  return guard([&] {
+    require(getenv("DPL_GUARD") != nullptr, DPL_ERR_USAGE, "guard selftest needs DPL_GUARD=1");
+    std::string msg;
+    guard_check_all(msg);  // clear earlier findings
+    {
+      DevBuf b;
+      b.reserve(1000);
+      k_poke_past_end<<<1, 1>>>(b.as<unsigned char>(), b.bytes);  // 4 bytes past the end
+      DPL_CUDA(cudaDeviceSynchronize());
+    }  // released here: the overwritten trailing zone must be reported
+    msg.clear();
+    require(guard_check_all(msg) == 1, DPL_ERR_NUMERICAL, "guard selftest: the write past the end went unnoticed");
+  });
+}
 
 // ---------------------------------------------------------------- tensor-core GEMM
 int dpl_gemm_f32(int device, void* stream, int32_t m, int32_t n, int32_t k, const float* a,

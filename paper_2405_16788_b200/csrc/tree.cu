@@ -22,29 +22,146 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
+#include <mutex>
+#include <set>
+#include <string>
 
 #include "tree.cuh"
 
 namespace dpl {
 
+// ---- guard mode (DPL_GUARD=1): every engine allocation gets 4 KB guard zones
+// before and after it, filled with a byte pattern; dpl_guard_check() (and the
+// release of a buffer) verifies them. compute-sanitizer is not available on the
+// GPU pool, so this is the engine's own out-of-bounds-write detector.
+namespace {
+constexpr size_t kGuard = 4096;
+constexpr unsigned char kGuardByte = 0xA5;
+bool guard_mode() {
+  static const bool on = getenv("DPL_GUARD") != nullptr;
+  return on;
+}
+std::mutex& guard_mu() {
+  static std::mutex m;
+  return m;
+}
+std::set<DevBuf*>& guard_live() {
+  static std::set<DevBuf*> s;
+  return s;
+}
+std::string& guard_report() {
+  static std::string r;
+  return r;
+}
+bool guard_intact(const DevBuf& b) {
+  std::vector<unsigned char> h(2 * kGuard);
+  const char* base = static_cast<const char*>(b.p) - kGuard;
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = cudaMemcpy(h.data(), base, kGuard, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess)
+    e = cudaMemcpy(h.data() + kGuard, static_cast<const char*>(b.p) + b.bytes, kGuard,
+                   cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) {
+    cudaGetLastError();  // reported here, not left pending for the next engine call
+    guard_report() += std::string("guard zones of a ") + std::to_string(b.bytes) +
+                      "-byte buffer unreadable (" + cudaGetErrorString(e) + "); ";
+    return true;
+  }
+  for (unsigned char c : h)
+    if (c != kGuardByte) return false;
+  return true;
+}
+}  // namespace
+
 void DevBuf::reserve(size_t b) {
   if (b <= bytes && p) return;
   release();
   size_t a = b ? b : 16;
-  cudaError_t e = cudaMalloc(&p, a);
+  a = (a + 255) & ~(size_t)255;
+  const bool g = guard_mode();
+  if (g) {
+    cudaError_t pe = cudaPeekAtLastError();
+    if (pe != cudaSuccess)
+      throw Error(4, std::string("guard mode: CUDA error pending before an allocation: ") +
+                         cudaGetErrorString(pe));
+  }
+  void* raw = nullptr;
+  cudaError_t e = cudaMalloc(&raw, a + (g ? 2 * kGuard : 0));
   if (e != cudaSuccess) {
     p = nullptr;
     bytes = 0;
     throw Error(4, std::string("cudaMalloc(") + std::to_string(a) + "): " + cudaGetErrorString(e));
   }
+  if (g) {
+    DPL_CUDA(cudaMemset(raw, kGuardByte, kGuard));
+    DPL_CUDA(cudaMemset(static_cast<char*>(raw) + kGuard + a, kGuardByte, kGuard));
+    DPL_CUDA(cudaDeviceSynchronize());
+    p = static_cast<char*>(raw) + kGuard;
+    guarded = true;
+    std::lock_guard<std::mutex> lk(guard_mu());
+    guard_live().insert(this);
+  } else {
+    p = raw;
+  }
   bytes = a;
 }
 
 void DevBuf::release() {
-  if (p) cudaFree(p);
+  if (p) {
+    if (guarded) {
+      std::lock_guard<std::mutex> lk(guard_mu());
+      guard_live().erase(this);
+      if (!guard_intact(*this))
+        guard_report() += "guard zone of a released " + std::to_string(bytes) + "-byte buffer overwritten; ";
+      cudaFree(static_cast<char*>(p) - kGuard);
+    } else {
+      cudaFree(p);
+    }
+  }
   p = nullptr;
   bytes = 0;
+  guarded = false;
+}
+
+void DevBuf::swap(DevBuf& o) {
+  if (guarded || o.guarded) {
+    std::lock_guard<std::mutex> lk(guard_mu());
+    guard_live().erase(this);
+    guard_live().erase(&o);
+    std::swap(p, o.p);
+    std::swap(bytes, o.bytes);
+    std::swap(guarded, o.guarded);
+    if (guarded) guard_live().insert(this);
+    if (o.guarded) guard_live().insert(&o);
+    return;
+  }
+  std::swap(p, o.p);
+  std::swap(bytes, o.bytes);
+}
+
+// number of live guarded buffers whose guard zones were overwritten (plus
+// earlier findings at release time); msg receives a description
+int guard_check_all(std::string& msg) {
+  std::lock_guard<std::mutex> lk(guard_mu());
+  int bad = 0;
+  for (DevBuf* b : guard_live())
+    if (!guard_intact(*b)) {
+      ++bad;
+      msg += "guard zone of a live " + std::to_string(b->bytes) + "-byte buffer overwritten; ";
+    }
+  if (!guard_report().empty()) {
+    ++bad;
+    msg += guard_report();
+    guard_report().clear();
+  }
+  return bad;
+}
+
+int guard_live_count() {
+  std::lock_guard<std::mutex> lk(guard_mu());
+  return (int)guard_live().size();
 }
 
 cudaEvent_t Tree::take_event() {
@@ -630,7 +747,8 @@ void tree_build(Tree& t, const double* pos, const double* nrm, const double* are
   if (C < 1 || C > DPL_MAX_CHANNELS) throw Error(1, "dpl_tree_build: channel count out of range");
   max_leaf = std::max(1, max_leaf);   // :162
   max_depth = std::max(0, max_depth); // :163
-  if (max_depth > 21) throw Error(1, "dpl_tree_build: max_depth > 21 not supported on GPU (63-bit keys)");
+  if (max_depth > DPL_MAX_DEPTH)
+    throw Error(1, "dpl_tree_build: max_depth > 21 not supported on GPU (63-bit keys)");
   t.n = n;
   t.C = C;
   t.max_leaf = max_leaf;
@@ -693,7 +811,7 @@ void tree_build(Tree& t, const double* pos, const double* nrm, const double* are
       if (olds[k]->p && have)
         DPL_CUDA(cudaMemcpyAsync(nb_[k].p, olds[k]->p, have * szs[k], cudaMemcpyDeviceToDevice, s));
     }
-    for (int k = 0; k < 6; ++k) std::swap(olds[k]->p, nb_[k].p), std::swap(olds[k]->bytes, nb_[k].bytes);
+    for (int k = 0; k < 6; ++k) olds[k]->swap(nb_[k]);
     DPL_CUDA(cudaStreamSynchronize(s));  // old buffers freed by nb_ destructors
     cap = c;
   };

@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <string>
+#include <utility>
 #include <vector>
 
 #include "dpl_internal.cuh"
@@ -14,8 +16,10 @@ namespace dpl {
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
+  bool guarded = false;  // allocated with guard zones (DPL_GUARD=1)
   void reserve(size_t b);
   void release();
+  void swap(DevBuf& o);  // exchanges the allocations (and their guard registrations)
   template <typename T>
   T* as() const {
     return static_cast<T*>(p);
@@ -25,6 +29,10 @@ struct DevBuf {
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
 };
+
+// DPL_GUARD=1: guard zones around every DevBuf (tree.cu)
+int guard_check_all(std::string& msg);
+int guard_live_count();
 
 struct Tree {
   int device = 0;

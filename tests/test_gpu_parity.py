@@ -531,3 +531,73 @@ def test_primal_channel_bitwise_equals_primal(eng, oracle_mod, C):
         assert np.array_equal(t.primal_channel(xs, p, 2.0, c), full[:, c]), c
     want = r.primal(O.Params(0.04), 2.0, xs)
     assert close(full, want)[0] == 0
+
+
+def _branchy_cloud(depth):
+    """A cloud whose octree has 8 non-empty children at EVERY level on the path
+    to a cluster at p (7 decoy points at the centres of the sibling cells, built
+    with the reference's cell arithmetic, bhtree.cpp:43-50,77-78,93-95), and
+    more than 8 points at p so the path reaches `depth`: the traversal stack
+    peaks at 1 + 7 * depth entries."""
+    pts = [(-1.0, -1.0, -1.0), (1.0, 1.0, 1.0)]  # bbox [-1, 1]^3: root centre 0
+    p = np.array([0.30011, 0.20017, 0.10029])
+    c = np.zeros(3)
+    h = 1.0 * (1.0 + 1e-7)
+    for _ in range(depth):
+        inside = [p[a] >= c[a] for a in range(3)]
+        for o in range(8):
+            sgn = [1.0 if (o >> a) & 1 else -1.0 for a in range(3)]
+            child = tuple(c[a] + (0.5 * h) * sgn[a] for a in range(3))
+            if [((o >> a) & 1) == 1 for a in range(3)] == inside:
+                nxt = np.array(child)
+            else:
+                pts.append(child)
+        c = nxt
+        h = 0.5 * h
+    for k in range(12):  # > max_leaf points at p (distinct, far below the last cell)
+        pts.append(tuple(p + 1e-13 * k))
+    return np.array(pts), p
+
+
+def test_deepest_tree_branchy_path_stack(eng, oracle_mod):
+    """max_depth = 21 (the deepest the GPU build supports) on a cloud that
+    fills every level of the path: the per-warp stack reaches its worst case
+    (1 + 7 * 21 = 148 <= 192) in every kernel family; results and opening
+    decisions equal the oracle's."""
+    O = oracle_mod
+    depth = 21
+    pos, p = _branchy_cloud(depth)
+    n = pos.shape[0]
+    rng = np.random.default_rng(5)
+    nrm = rng.standard_normal((n, 3))
+    nrm /= np.linalg.norm(nrm, axis=1, keepdims=True)
+    area = np.full(n, 1.0 / n)
+    C = 5
+    mu = rng.standard_normal((n, C))
+    kinds = np.array([0, 1, 1, 1, 1], np.uint8)
+    t, r = make(eng, O, pos, nrm, area, mu, kinds, max_leaf=8, max_depth=depth)
+    a, b = t.export(), r.export()
+    for k in ("topo", "order", "leaf_of", "geo"):
+        assert np.array_equal(a[k], b[k]), k
+    # queries around p open the whole path
+    xs = p + rng.normal(0, 1e-9, (256, 3))
+    xs = np.concatenate([xs, rng.uniform(-1, 1, (256, 3))])
+    prm = eng.KernelParams(epsilon=1e-7)
+    got, cnt = t.primal(xs, prm, 2.0, visited=True)
+    want, wcnt = r.primal(O.Params(1e-7), 2.0, xs, counters=True)
+    counters_equal("deepest tree counters", cnt, wcnt)
+    # queries 1e-9 from a cluster whose terms cancel to ~1e-4 of their sum:
+    # the Sum|terms|-scaled bar applies (tests/parity.py)
+    wm = r.primal_mag(O.Params(1e-7), 2.0, xs)
+    check("deepest tree (depth 21, 8 children per path node) primal", got, want, wm["out_abs"])
+    d_out = rng.standard_normal((xs.shape[0], C)).astype(np.float32)
+    w = r.adjoint_mag(O.Params(1e-7), 2.0, xs, d_out.astype(np.float64))
+    for rnd in range(2):  # fused walk, then list replay
+        t.primal(xs, prm, 2.0)
+        buf = t.make_buffer()
+        t.adjoint(xs, prm, 2.0, d_out, None, buf)
+        g = t.flush_gradients(buf)
+        check(f"deepest tree adjoint moments (pass {rnd})", g.moments, w["moments"], w["moments_abs"])
+        check(f"deepest tree adjoint normals (pass {rnd})", g.normals, w["normals"], w["normals_abs"])
+    with pytest.raises(eng.UsageError):
+        t.build(eng.OrientedPointCloud(pos, nrm, area, mu), 8, 22)
