@@ -47,6 +47,49 @@ def timed(fn, steps, tree):
     return 1e3 * wall, {k: v[0] / steps for k, v in prof.items() if v[1]}
 
 
+def flops_fwd_adj(tot, Cd, Cr):
+    """SURVEY §8(d) cost model v1 (bench.flops_model)."""
+    sys.path.insert(0, ROOT)
+    import bench
+
+    return bench.flops_model(tot, Cd, Cr)
+
+
+def flops_render(tot, Cd, Cr):
+    """Render path: forward values + channel-0 gradient (radial
+    gradient terms count 0), adjoint with d_grad[0]. tot = (V, Fn, Ff, Pn, Pf)."""
+    V, Fn, Ff, Pn, Pf = [float(x) for x in tot]
+    fwd, adj = flops_fwd_adj(tot, Cd, Cr)
+    K1n, K1f = 26.0, 12.0
+    fwd += Fn * (K1n + 1 + 13 * Cd) + Ff * (K1f + 1 + 13 * Cd) + Pn * (K1n + 13 + 6 * Cd) + Pf * (K1f + 13 + 6 * Cd)
+    adj += Fn * (K1n + 30) + Ff * (K1f + 30) + Pn * (K1n + 30) + Pf * (K1f + 30)
+    return fwd, adj
+
+
+def sample_counts(tree, p, rays, S, t_near, t_far, seed, max_rays=65536):
+    """Per-sample (V, Fn, Ff, Pn, Pf) means over the render step's sample
+    positions (the stratified sampler's fp64 t, o + t dir) of a ray subset."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+
+    R = min(rays.shape[0], max_rays)
+    tot = np.zeros(5)
+    for r0 in range(0, R, 8192):
+        r1 = min(R, r0 + 8192)
+        ts, _ = O.stratified_samples(r1 - r0, S, t_near, t_far, seed, ray_offset=r0)
+        o, d = rays[r0:r1, :3], rays[r0:r1, 3:]
+        xs = (o[:, None, :] + ts[:, :, None] * d[:, None, :]).reshape(-1, 3)
+        _, cnt = tree.primal(torch.from_numpy(np.ascontiguousarray(xs)).cuda(), p, 2.0, visited=True)
+        tot += cnt.sum(dim=0).cpu().numpy()
+    return tot / (R * S)
+
+
+def roofline(flops, ms, peak):
+    ach = flops / (ms * 1e-3) / 1e12
+    return {"flops_per_launch": flops, "ms": ms, "achieved_tflops": ach, "peak_tflops": peak,
+            "frac": ach / peak, "peak_source": "measured FFMA microbenchmark (dpl_peak_fp32)"}
+
+
 def build(cloud, kinds, dev):
     t = P.DipoleTree(0, stream=torch.cuda.current_stream())
     t0 = time.perf_counter()
@@ -61,6 +104,7 @@ def main():
     ap.add_argument("--config", type=int, required=True)
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--scale", type=float, default=1.0)
+    ap.add_argument("--cpu", action="store_true", help="also time the reference CPU path (SURVEY 8(d) subsets)")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     res = {"config": args.config, "scale": args.scale}
@@ -88,9 +132,30 @@ def main():
         ms, ph = timed(lambda: tree.primal(nxt(), p, 2.0, out=out), args.steps, tree)
         res.update(points=c.size, nodes=tree.node_count(), queries=Q, channels=C,
                    forward_ms=ms, forward_phases=ph, forward_qps=Q / (ms * 1e-3))
+        _, cnt = tree.primal(xs_b[0], p, 2.0, visited=True)
+        tot = cnt.sum(dim=0).cpu().numpy()
+        del cnt
+        peak = B.peak_fp32(0)
+        f_fwd, f_adj = flops_fwd_adj(tot, 1, C - 1)
+        res["visited_per_query"] = float(tot[0] / Q)
+        res["interactions_per_query"] = float(tot[1:].sum() / Q)
+        fw = ph.get("forward", ms)
+        res["roofline_forward"] = roofline(f_fwd, fw, peak)
         if args.config == 1:
             ms, _ = timed(lambda: tree.primal_channel(nxt(), p, 2.0, 0), args.steps, tree)
             res["primal_channel_ms"] = ms
+            if args.cpu:  # the reference's primal over the full 1M-query batch, all cores
+                sys.path.insert(0, os.path.join(ROOT, "oracle"))
+                import oracle as O
+
+                rt = O.OracleTree(O.Cloud(c.positions, c.normals, c.areas, c.moments), backend="ref")
+                rt.set_kinds(w["kinds"])
+                cores = O.ref_lib().ref_hardware_concurrency()
+                t0 = time.perf_counter()
+                rt.primal(O.Params(eps), 2.0, w["xs"], threads=cores)
+                dt = time.perf_counter() - t0
+                res["reference_cpu"] = {"queries": Q, "s": dt, "queries_per_s": Q / dt,
+                                        "cores": cores, "speedup_gpu": (Q / dt) and (dt / (fw * 1e-3))}
         else:
             g = torch.Generator(device=dev).manual_seed(7)
             d_out = torch.randn((Q, C), device=dev, generator=g)
@@ -104,8 +169,9 @@ def main():
                 tree.adjoint(x, p, 2.0, d_out, None, buf)
                 tree.flush_gradients(buf, out=(mom, nrm))
 
-            ms, ph = timed(step, args.steps, tree)
-            res.update(step_ms=ms, step_phases=ph, step_qps=Q / (ms * 1e-3))
+            ms, ph2 = timed(step, args.steps, tree)
+            res.update(step_ms=ms, step_phases=ph2, step_qps=Q / (ms * 1e-3))
+            res["roofline_adjoint"] = roofline(f_adj, ph2.get("adjoint", ms), peak)
     elif args.config in (6, 7):
         # SURVEY 8(f) rows on the config-3 scene (config-1 sphere cloud, C=4):
         # 6 = sample_ray over its 65,536 camera rays (probe_count 1024, [2, 6]),
@@ -242,6 +308,33 @@ def main():
         Q = R * S
         res.update(points=c.size, nodes=tree.node_count(), rays=R, samples=S, queries=Q,
                    channels=c.channels, step_ms=ms, phases=ph, samples_per_s=Q / (ms * 1e-3))
+        # roofline: the direct-rgb render step evaluates channels 0..3 (values)
+        # and the channel-0 gradient, and adjoints channels 0..3 with d_grad[0]
+        # (renderer.cpp:125-127, radiance.cpp:133-145) — the 4-channel rate
+        per = sample_counts(tree, p, rays, S, 2.0, 6.0, 3)
+        f_fwd, f_adj = flops_render(per * Q, 1, 3)
+        peak = B.peak_fp32(0)
+        res["counters_per_sample"] = per.tolist()
+        res["roofline_forward"] = roofline(f_fwd, ph.get("forward", ms), peak)
+        res["roofline_adjoint"] = roofline(f_adj, ph.get("adjoint", ms), peak)
+        res["channels_computed"] = "0..3 of %d (the direct-rgb head's inputs; the reference evaluates all %d, the rest never reach the output)" % (c.channels, c.channels)
+        if args.cpu:  # the reference's render_ray + render_ray_backward on a 4,096-ray subset
+            sys.path.insert(0, os.path.join(ROOT, "oracle"))
+            import oracle as O
+
+            nr = min(R, 4096)
+            t0 = time.perf_counter()
+            ref = O.RefModel(O.Cloud(c.positions, c.normals, c.areas, c.moments), eps, beta=2.0)
+            t_build = time.perf_counter() - t0
+            ts, dlt = O.stratified_samples(nr, S, 2.0, 6.0, 3)
+            tgt = np.random.default_rng(4).uniform(0, 1, (nr, 3))
+            t0 = time.perf_counter()
+            ref.render_step(rays[:nr], ts, dlt, tgt, 2.0 / (3.0 * nr))
+            dt = time.perf_counter() - t0
+            res["reference_cpu"] = {"rays": nr, "samples": nr * S, "s": dt,
+                                    "samples_per_s": nr * S / dt, "tree_build_s": t_build,
+                                    "cores": O.ref_lib().ref_hardware_concurrency(),
+                                    "note": "render_ray + render_ray_backward per ray (all channels), one flush"}
     print(json.dumps(res), flush=True)
 
 
