@@ -136,6 +136,7 @@ def _config5_like(n, px_per_cam, seed=5):
 
     pos, nrm, area, rng = W.shapes_cloud(n, seed)
     mu = rng.standard_normal((n, 49))
+    mu[:, 0] = 1.0  # geometry moment 1: the shapes' winding-number field (visible surfaces)
     c = W.cloud(pos, nrm, area, mu)
     kinds = np.ones(49, np.uint8)
     kinds[0] = 0

@@ -274,6 +274,7 @@ def main():
             n = max(64, int(4_000_000 * args.scale))
             pos, nrm_, area, rng = W.shapes_cloud(n, 5)
             mu = rng.standard_normal((n, 49))
+            mu[:, 0] = 1.0  # geometry moment 1 (winding-number field: the shapes are opaque)
             c = W.cloud(pos, nrm_, area, mu)
             kinds = np.ones(49, np.uint8)
             kinds[0] = 0
