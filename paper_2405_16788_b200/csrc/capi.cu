@@ -1317,16 +1317,15 @@ int dpl_render_forward(dpl_tree_t h, const dpl_kernel_params* params, const dpl_
       forward_launch(t, kp, a);
     }
     if (mlp) {  // head raw outputs, in sample chunks (RadianceHead::eval, radiance.cpp:146-154)
-      const int din = h->head.din();
       const int64_t chunk = std::min<int64_t>(Q, kMlpChunk);
       tape->head_raw.reserve(Q * 12);
-      tape->mlp_x.reserve((size_t)chunk * din * 4);
+      tape->mlp_x.reserve((size_t)chunk * h->head.ldx() * 4);
       PhaseTimer pt(t, PH_RENDER);
       for (int64_t q0 = 0; q0 < Q; q0 += chunk) {
         const int64_t qc = std::min(chunk, Q - q0);
         mlp_inputs(t.stream, tape->rays.as<double>(), S, tape->xs.as<double>(),
                    tape->vals.as<float>(), t.C, tape->g0.as<float>(), q0, qc, h->head.K,
-                   tape->mlp_x.as<float>());
+                   tape->mlp_x.as<float>(), h->head.ldx());
         mlp_forward(h->head, t.stream, tape->mlp_x.as<float>(), qc,
                     tape->head_raw.as<float>() + 3 * q0);
       }
@@ -1386,14 +1385,14 @@ int dpl_render_backward(dpl_tree_t h, const dpl_kernel_params* params, const dpl
     if (mlp) {  // head backward (radiance.cpp:176-179) -> appearance / normal adjoints
       const int din = h->head.din();
       const int64_t chunk = std::min<int64_t>(Q, kMlpChunk);
-      tape->mlp_x.reserve((size_t)chunk * din * 4);
+      tape->mlp_x.reserve((size_t)chunk * h->head.ldx() * 4);
       tape->mlp_dx.reserve((size_t)chunk * din * 4);
       PhaseTimer pt(t, PH_RENDER);
       for (int64_t q0 = 0; q0 < Q; q0 += chunk) {
         const int64_t qc = std::min(chunk, Q - q0);
         mlp_inputs(t.stream, tape->rays.as<double>(), S, tape->xs.as<double>(),
                    tape->vals.as<float>(), t.C, tape->g0.as<float>(), q0, qc, h->head.K,
-                   tape->mlp_x.as<float>());
+                   tape->mlp_x.as<float>(), h->head.ldx());
         mlp_backward(h->head, t.stream, tape->mlp_x.as<float>(), qc,
                      tape->d_raw.as<float>() + 3 * q0, tape->mlp_dx.as<float>());
         render_mlp_scatter(t.stream, tape->mlp_dx.as<float>(), din, q0, qc, h->head.K,

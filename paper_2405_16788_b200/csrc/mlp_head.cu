@@ -42,14 +42,13 @@ __device__ __forceinline__ void sh_encode(double x, double y, double z, float* o
 // as render_ray builds them, renderer.cpp:111,128-130)
 __global__ void k_inputs(const double* __restrict__ rays, int S, const double* __restrict__ xs,
                          const float* __restrict__ vals, int C, const float* __restrict__ g0,
-                         int64_t q0, int64_t q, int K, float* __restrict__ X) {
-  const int din = 22 + K;
+                         int64_t q0, int64_t q, int K, float* __restrict__ X, int ldx) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < q;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t g = q0 + i;
     const double* dir = rays + 6 * (g / S) + 3;
     const double ox = -dir[0], oy = -dir[1], oz = -dir[2];
-    float* row = X + i * din;
+    float* row = X + i * ldx;
     row[0] = (float)xs[3 * g], row[1] = (float)xs[3 * g + 1], row[2] = (float)xs[3 * g + 2];
     sh_encode(ox, oy, oz, row + 3);
     const double gx = -(double)g0[3 * g], gy = -(double)g0[3 * g + 1], gz = -(double)g0[3 * g + 2];
@@ -141,19 +140,20 @@ void mlp_set(MlpHead& m, const Tree& t, const int* sizes, int n_sizes, const dou
 }
 
 void mlp_inputs(cudaStream_t s, const double* rays, int S, const double* xs, const float* vals,
-                int C, const float* g0, int64_t q0, int64_t q, int K, float* X) {
-  k_inputs<<<blocks_for(q, 256), 256, 0, s>>>(rays, S, xs, vals, C, g0, q0, q, K, X);
+                int C, const float* g0, int64_t q0, int64_t q, int K, float* X, int ldx) {
+  k_inputs<<<blocks_for(q, 256), 256, 0, s>>>(rays, S, xs, vals, C, g0, q0, q, K, X, ldx);
   count_launch();
 }
 
 // layer l: out (q x rows) = in (q x cols) . W^T + b, ReLU except on the last layer
 static void layer_fwd(MlpHead& m, cudaStream_t s, int l, const float* in, int64_t q, float* out) {
   const int rows = m.sizes[l + 1], cols = m.sizes[l];
+  const int lda = l == 0 ? m.ldx() : cols;  // the input rows X are padded to 16 bytes
   const float* W = m.w32.as<float>() + m.offs[l];
   const bool last = l + 2 == (int)m.sizes.size();
   TcGemm g;
   g.M = (int)q, g.N = rows, g.K = cols;
-  g.A = in, g.lda = cols;             // in[q][cols]
+  g.A = in, g.lda = lda;              // in[q][cols]
   g.B = W, g.ldb = cols;              // W[rows][cols]
   g.b_image = m.img.as<uint8_t>() + m.img_fwd[l];
   g.D = out, g.ldd = rows;
@@ -203,7 +203,7 @@ void mlp_backward(MlpHead& m, cudaStream_t s, const float* X, int64_t q, const f
     TcGemm gw;
     gw.M = rows, gw.N = cols, gw.K = (int)q;
     gw.A = delta, gw.lda = rows, gw.a_kcontig = false;   // A[r][q] = delta[q][r]
-    gw.B = act[l], gw.ldb = cols, gw.b_kcontig = false;  // B[c][q] = in[q][c]
+    gw.B = act[l], gw.ldb = l == 0 ? m.ldx() : cols, gw.b_kcontig = false;  // B[c][q] = in[q][c]
     gw.D64 = dw + m.offs[l], gw.ldd = cols;
     gw.epi = TC_ACC64;
     // one wave of CTAs: the M x N tiles times the K slices ~ the SM count

@@ -35,6 +35,9 @@ struct MlpHead {
   DevBuf img;
   ~MlpHead();
   int din() const { return sizes.empty() ? 0 : sizes.front(); }
+  // row stride of the input rows X: din rounded up to 4 floats, so the first
+  // layer's A rows are 16-byte aligned (the tensor-core GEMM's cp.async path)
+  int ldx() const { return (din() + 3) & ~3; }
   int widest() const;
 };
 
@@ -45,7 +48,7 @@ void mlp_set(MlpHead& m, const Tree& t, const int* sizes, int n_sizes, const dou
 // -dir, n_hat from the channel-0 gradient (renderer.cpp:124-130), appearance
 // = channels 1..K of vals (q x C)
 void mlp_inputs(cudaStream_t s, const double* rays, int S, const double* xs, const float* vals,
-                int C, const float* g0, int64_t q0, int64_t q, int K, float* X);
+                int C, const float* g0, int64_t q0, int64_t q, int K, float* X, int ldx);
 
 // raw outputs (q x 3, fp32) of the samples [q0, q0 + q)
 void mlp_forward(MlpHead& m, cudaStream_t s, const float* X, int64_t q, float* raw);

@@ -18,6 +18,7 @@
 // The fp32 accumulator (128 lanes x BN columns of TMEM) is read back by the
 // warp owning each lane quadrant (tcgen05.ld 32x32b) for the fused epilogue.
 #include <algorithm>
+#include <cstdlib>
 #include <atomic>
 
 #include "dpl_internal.cuh"
@@ -402,6 +403,223 @@ __global__ void __launch_bounds__(128, 2) k_tc_gemm(TcGemm g) {
                  : "memory");
 }
 
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// Persistent, warp-specialised variant for K-contiguous A and a pre-split B
+// image (the MLP head's forward and input-gradient GEMMs). One CTA per SM
+// walks the tiles round-robin:
+//   warps 0-3  A producers: cp.async of the chunk into a 3-deep swizzled fp32
+//              staging ring (two chunks in flight), split into tf32 hi / lo,
+//              tcgen05.st into one of 4 TMEM A stages (warp w -> lanes 32w..);
+//              thread 0 also issues the chunk's B bulk copy;
+//   warp 8     MMA issuer (one thread): 12 tcgen05.mma per chunk into one of two
+//              TMEM accumulators, commit -> stage free; after a tile's last
+//              chunk, commit -> accumulator full;
+//   warps 4-7  epilogue: tcgen05.ld of the finished accumulator (warp 4 + q ->
+//              lane quadrant q), fused bias / ReLU / gate, stores, release.
+// The epilogue of tile i and the producers of tile i + 1 run while the tensor
+// core works, so per-tile fixed costs (TMEM allocation, barrier setup, the
+// first loads, the drain) are paid once per SM instead of once per tile.
+// TMEM: accumulators 2 x BN (<= 256) + A stages 4 x 64 = 512 columns.
+constexpr int kWsStages = 4;
+constexpr int kWsRing = 3;  // A staging ring (prefetch distance 2)
+constexpr int kWsThreads = 9 * 32;
+
+template <int BN, int EPI>
+__global__ void __launch_bounds__(kWsThreads, 1) k_tc_gemm_ws(TcGemm g) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  constexpr int BBYTES = BN * kRowBytes;
+  constexpr int STAGEB = 2 * BBYTES;
+  constexpr int ABYTES = kTileM * kRowBytes;
+  uint8_t* bst = sm;                          // kWsStages x (hi | lo)
+  uint8_t* ast = sm + kWsStages * STAGEB;     // kWsRing x raw fp32 A chunk
+  __shared__ __align__(8) uint64_t afull[kWsStages], bfull[kWsStages], empty[kWsStages],
+      dfull[2], dempty[2];
+  __shared__ uint32_t tmem_slot;
+  constexpr uint32_t TM_A = 256;  // A stages at columns 256 + 64 s (hi), + 32 (lo)
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                     smem_addr(&tmem_slot)),
+                 "r"(512u)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+  }
+  if (tid == 0) {
+    for (int i = 0; i < kWsStages; ++i) {
+      mbar_init(smem_addr(&afull[i]), 128);
+      mbar_init(smem_addr(&bfull[i]), 1);
+      mbar_init(smem_addr(&empty[i]), 1);
+    }
+    for (int i = 0; i < 2; ++i) mbar_init(smem_addr(&dfull[i]), 1), mbar_init(smem_addr(&dempty[i]), 128);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+
+  const int mtiles = (g.M + kTileM - 1) / kTileM, ntiles = (g.N + BN - 1) / BN;
+  const int ntotal = mtiles * ntiles;
+  const int nkc = (g.K + kChunkK - 1) / kChunkK;  // chunks per tile (K > 0)
+
+  if (warp < 4) {
+    // ---------------- A producers (+ B bulk copies by thread 0)
+    const int row = tid;  // tile row = TMEM lane (warp w owns lanes 32w..32w+31)
+    const uint32_t lane_base = (uint32_t)(32 * warp) << 16;
+    // chunk cursor for the cp.async prefetch (two chunks ahead of consumption)
+    int pf_t = blockIdx.x, pf_c = 0;
+    auto issue = [&](int slot) {
+      if (pf_t < ntotal) {
+        const int m0 = (pf_t / ntiles) * kTileM, k0 = pf_c * kChunkK;
+        uint8_t* dst0 = ast + slot * ABYTES;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int idx = tid + 128 * i, r = idx >> 3, j = idx & 7;
+          const int grr = m0 + r, gk = k0 + 4 * j;
+          const int bytes = grr < g.M ? max(0, min(16, (g.K - gk) * 4)) : 0;
+          const float* src = bytes ? g.A + (int64_t)grr * g.lda + gk : g.A;
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(
+                           smem_addr(dst0 + r * kRowBytes + ((j ^ (r & 7)) << 4))),
+                       "l"(src), "r"(bytes)
+                       : "memory");
+        }
+        if (++pf_c == nkc) pf_c = 0, pf_t += gridDim.x;
+      }
+      asm volatile("cp.async.commit_group;\n" ::: "memory");  // (possibly empty) group
+    };
+    issue(0);
+    issue(1);
+    int gc = 0;  // chunks consumed by this CTA
+    for (int t = blockIdx.x; t < ntotal; t += gridDim.x) {
+      const int nt = t % ntiles;
+      for (int c = 0; c < nkc; ++c, ++gc) {
+        const int s = gc % kWsStages;
+        const uint32_t ph = (uint32_t)(gc / kWsStages) & 1u;
+        mbar_wait(smem_addr(&empty[s]), ph ^ 1u);  // the MMAs of chunk gc - 4 are done
+        if (tid == 0) {
+          const uint8_t* src = g.b_image + ((size_t)nt * nkc + c) * STAGEB;
+          mbar_expect_tx(smem_addr(&bfull[s]), STAGEB);
+          bulk_copy(smem_addr(bst + s * STAGEB), src, STAGEB, smem_addr(&bfull[s]));
+        }
+        asm volatile("cp.async.wait_group 1;\n" ::: "memory");  // chunk gc has landed (own copies)
+        asm volatile("bar.sync 1, 128;\n" ::: "memory");        // ... everyone's; ring slot gc-1 read
+        issue((gc + 2) % kWsRing);
+        const uint8_t* src = ast + (gc % kWsRing) * ABYTES + row * kRowBytes;
+        float x[32];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float4 v = *reinterpret_cast<const float4*>(src + ((j ^ (row & 7)) << 4));
+          x[4 * j] = v.x, x[4 * j + 1] = v.y, x[4 * j + 2] = v.z, x[4 * j + 3] = v.w;
+        }
+        store_a(tmem + lane_base + TM_A + 64u * s, x);
+        asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+        tc_fence_before();
+        mbar_arrive(smem_addr(&afull[s]));
+      }
+    }
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  } else if (warp == 8) {
+    // ---------------- MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t IDESC = idesc_tf32(kTileM, BN);
+      int gc = 0, i = 0;
+      for (int t = blockIdx.x; t < ntotal; t += gridDim.x, ++i) {
+        const int b = i & 1;
+        mbar_wait(smem_addr(&dempty[b]), ((uint32_t)(i >> 1) & 1u) ^ 1u);  // epilogue drained it
+        tc_fence_after();
+        const uint32_t d = tmem + (uint32_t)(b * BN);
+        for (int c = 0; c < nkc; ++c, ++gc) {
+          const int s = gc % kWsStages;
+          const uint32_t ph = (uint32_t)(gc / kWsStages) & 1u;
+          mbar_wait(smem_addr(&afull[s]), ph);
+          mbar_wait(smem_addr(&bfull[s]), ph);
+          tc_fence_after();
+          const uint32_t b_hi = smem_addr(bst + s * STAGEB), b_lo = b_hi + BBYTES;
+          const uint32_t a_hi = tmem + TM_A + 64u * s, a_lo = a_hi + 32u;
+#pragma unroll
+          for (int ks = 0; ks < kChunkK / 8; ++ks) {
+            mma_ts(d, a_hi + 8u * ks, sw128_desc(b_hi + 32u * ks), IDESC, (c | ks) != 0);
+            mma_ts(d, a_hi + 8u * ks, sw128_desc(b_lo + 32u * ks), IDESC, 1u);
+            mma_ts(d, a_lo + 8u * ks, sw128_desc(b_hi + 32u * ks), IDESC, 1u);
+          }
+          mma_commit(smem_addr(&empty[s]));
+        }
+        mma_commit(smem_addr(&dfull[b]));
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---------------- epilogue (warps 4-7 -> lane quadrants 0-3)
+    const int q = warp - 4;
+    const uint32_t lane_base = (uint32_t)(32 * q) << 16;
+    const bool vec_d = (g.ldd & 3) == 0 && ((reinterpret_cast<uintptr_t>(g.D) & 15) == 0) &&
+                       (EPI != TC_GATE || ((g.ldaux & 3) == 0 &&
+                                           (reinterpret_cast<uintptr_t>(g.aux) & 15) == 0));
+    int i = 0;
+    for (int t = blockIdx.x; t < ntotal; t += gridDim.x, ++i) {
+      const int b = i & 1;
+      const int m0 = (t / ntiles) * kTileM, n0 = (t % ntiles) * BN;
+      const int gr = m0 + 32 * q + lane;
+      mbar_wait(smem_addr(&dfull[b]), (uint32_t)(i >> 1) & 1u);
+      tc_fence_after();
+#pragma unroll 1
+      for (int cb = 0; cb < BN; cb += 16) {
+        float v[16];
+        tmem_ld16(tmem + lane_base + (uint32_t)(b * BN + cb), v);
+        if (gr >= g.M) continue;
+        const int nb = n0 + cb;
+        if (vec_d && nb + 16 <= g.N) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            float x = v[j];
+            if (EPI == TC_BIAS_RELU) x = fmaxf(x + __ldg(g.bias + nb + j), 0.f);
+            if (EPI == TC_BIAS) x += __ldg(g.bias + nb + j);
+            v[j] = x;
+          }
+          if (EPI == TC_GATE) {
+            const float4* ax = reinterpret_cast<const float4*>(g.aux + (int64_t)gr * g.ldaux + nb);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const float4 a4 = __ldg(ax + j);
+              v[4 * j] = a4.x > 0.f ? v[4 * j] : 0.f;
+              v[4 * j + 1] = a4.y > 0.f ? v[4 * j + 1] : 0.f;
+              v[4 * j + 2] = a4.z > 0.f ? v[4 * j + 2] : 0.f;
+              v[4 * j + 3] = a4.w > 0.f ? v[4 * j + 3] : 0.f;
+            }
+          }
+          float4* dst = reinterpret_cast<float4*>(g.D + (int64_t)gr * g.ldd + nb);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) dst[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          continue;
+        }
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int n = nb + j;
+          if (n >= g.N) break;
+          float x = v[j];
+          if (EPI == TC_BIAS_RELU) x = fmaxf(x + __ldg(g.bias + n), 0.f);
+          if (EPI == TC_BIAS) x += __ldg(g.bias + n);
+          if (EPI == TC_GATE) x = __ldg(g.aux + (int64_t)gr * g.ldaux + n) > 0.f ? x : 0.f;
+          g.D[(int64_t)gr * g.ldd + n] = x;
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(smem_addr(&dempty[b]));
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(512u)
+                 : "memory");
+}
+
 // B image: [n-tile][k-chunk] blocks of (BN x 128 B hi | BN x 128 B lo), swizzled
 __global__ void k_b_image(const float* __restrict__ B, int64_t ldb, int kcontig, int N, int K,
                           int BN, int ntiles, int nkc, uint8_t* __restrict__ img) {
@@ -447,8 +665,37 @@ void launch_n(const TcGemm& g, int device, cudaStream_t s) {
   }
 }
 
+template <int BN, int EPI>
+void launch_ws(const TcGemm& g, int device, cudaStream_t s) {
+  constexpr size_t smem = 1024 + (size_t)kWsStages * 2 * BN * kRowBytes +
+                          (size_t)kWsRing * kTileM * kRowBytes;
+  static std::atomic<unsigned long long> attr{0};
+  ensure_max_dyn_smem(k_tc_gemm_ws<BN, EPI>, device, smem, attr);
+  int sms = 148;
+  DPL_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  const int64_t tiles = (int64_t)((g.M + kTileM - 1) / kTileM) * ((g.N + BN - 1) / BN);
+  k_tc_gemm_ws<BN, EPI><<<(unsigned)std::min<int64_t>(tiles, sms), kWsThreads, smem, s>>>(g);
+  count_launch();
+}
+
+bool ws_enabled() {
+  static const bool off = getenv("DPL_TC_GEMM_SIMPLE") != nullptr;  // A/B switch for tests
+  return !off;
+}
+
 template <int EPI>
 void launch_epi(const TcGemm& g, int device, cudaStream_t s) {
+  if constexpr (EPI != TC_ACC64) {
+    const bool vec = g.a_kcontig && (g.lda & 3) == 0 && ((reinterpret_cast<uintptr_t>(g.A) & 15) == 0);
+    if (g.b_image && vec && g.K > 0 && ws_enabled()) {  // persistent warp-specialised path
+      switch (pick_bn(g.N)) {
+        case 16: return launch_ws<16, EPI>(g, device, s);
+        case 32: return launch_ws<32, EPI>(g, device, s);
+        case 64: return launch_ws<64, EPI>(g, device, s);
+        default: return launch_ws<128, EPI>(g, device, s);
+      }
+    }
+  }
   if (g.b_image) {  // the layout of the image does not depend on B's order any more
     if (g.a_kcontig) return launch_n<true, true, true, EPI>(g, device, s);
     return launch_n<false, true, true, EPI>(g, device, s);

@@ -5,7 +5,8 @@ d_background and the head-weight gradient RenderGrads::d_head_w."""
 import numpy as np
 import pytest
 
-from test_gpu_parity import close, make, rel_scale_err
+from parity import check, scalar
+from test_gpu_parity import make
 
 pytestmark = pytest.mark.gpu
 
@@ -20,7 +21,7 @@ def he_weights(sizes, seed):
     return np.concatenate(w)
 
 
-@pytest.mark.parametrize("hidden", [(32,), (64, 64)])
+@pytest.mark.parametrize("hidden", [(32,), (64, 64), (256, 256)])
 def test_render_step_tiny_mlp_head(oracle_mod, hidden):
     import paper_2405_16788_b200 as eng
     from paper_2405_16788_b200 import renderer as Rn
@@ -46,22 +47,25 @@ def test_render_step_tiny_mlp_head(oracle_mod, hidden):
     rs = Rn.RenderSettings(t_near=2.0, t_far=6.0, seed=3)
     p = eng.KernelParams(epsilon=eps)
     rgb, tape = Rn.render_forward(t, p, rs, rays, S)
-    scale = 2.0 / (3.0 * rays.shape[0])
-    d_rgb = (scale * (rgb.astype(np.float64) - target)).astype(np.float32)
+    # L = (1/3) sum ||rgb - target||^2 (no batch mean: O(1) gradients, so the
+    # 1e-6 absolute floor does not hide them); both sides use the reference's
+    # colours for the loss gradient, the GPU colours are checked on their own
+    scale = 2.0 / 3.0
+    ts, dlt = O.stratified_samples(rays.shape[0], S, 2.0, 6.0, 3)
+    want = ref.render_step(rays, ts, dlt, target, scale)
+    d_rgb = (scale * (want["rgb"] - target)).astype(np.float32)
     buf = t.make_buffer()
     dl, dbg = Rn.render_backward(t, p, rs, tape, d_rgb, buf)
     g = t.flush_gradients(buf)
     dw = t.head_grads()
-
-    ts, dlt = O.stratified_samples(rays.shape[0], S, 2.0, 6.0, 3)
-    want = ref.render_step(rays, ts, dlt, target, scale)
-    assert close(rgb, want["rgb"])[0] == 0
-    assert rel_scale_err(g.moments, want["moments"]) < 1e-4
-    assert rel_scale_err(g.normals, want["normals"]) < 1e-4
-    assert abs(g.d_epsilon - want["d_eps"]) <= 1e-4 * abs(want["d_eps"]) + 1e-6
-    assert abs(dl - want["d_lambda"]) <= 1e-4 * abs(want["d_lambda"]) + 1e-8
-    assert np.abs(dbg - want["d_bg"]).max() <= 1e-4 * np.abs(want["d_bg"]).max() + 1e-8
-    assert rel_scale_err(dw, ref.head_grads()) < 1e-4
+    tag = f"tiny-MLP head {sizes}"
+    check(f"{tag} rgb", rgb, want["rgb"])
+    check(f"{tag} moments", g.moments, want["moments"])
+    check(f"{tag} normals", g.normals, want["normals"])
+    scalar(f"{tag} d_epsilon", g.d_epsilon, want["d_eps"])
+    scalar(f"{tag} d_lambda", dl, want["d_lambda"], atol=1e-8)
+    check(f"{tag} d_background", dbg, want["d_bg"], atol=1e-8)
+    check(f"{tag} d_head_w (RenderGrads::d_head_w)", dw, ref.head_grads())
     # the accumulator was reset; the direct-rgb head is restored by an empty size list
     assert np.all(t.head_grads() == 0)
     t.set_mlp_head((), ())
