@@ -83,6 +83,12 @@ int dpl_tree_sync(dpl_tree_t tree);
  * dpl_tree_sync() or dpl_flush() (which synchronizes everything) returns; use
  * pinned host memory for real overlap. Off: every call is synchronous. */
 int dpl_tree_set_host_async(dpl_tree_t tree, int on);
+/* Host-async mode: start uploading the NEXT primal's host query batch now (on
+ * the H2D copy stream, e.g. while the current adjoint runs); the next
+ * dpl_primal / dpl_primal_channel / dpl_primal_grad0 given the same host
+ * pointer and count uses it instead of uploading. The batch must stay
+ * unchanged until that call. No-op outside host-async mode. */
+int dpl_tree_prefetch(dpl_tree_t tree, const double* xs, int64_t q);
 
 /* DipoleTree::build (bhtree.cpp:158-169): GPU Morton-digit sort + level-by-level
  * BFS numbering reproduces build_structure (:36-105) bit-exactly; geometry
@@ -201,7 +207,10 @@ int dpl_adjoint(dpl_tree_t tree, const dpl_kernel_params* params, double beta_bh
                 dpl_gradbuf_t buf);
 /* DipoleTree::flush_gradients (bhtree.cpp:419-463): sums nbuf buffers, pushes
  * node accumulators down to points (top-down, O(nodes*C + N*C)), zeroes the
- * buffers. moments N x C, normals N x 3 (fp32, any may be NULL), d_epsilon. */
+ * buffers. moments N x C, normals N x 3 (fp32, any may be NULL), d_epsilon.
+ * Host-async mode with host outputs: d_epsilon is returned at once, the
+ * moments / normals arrive on the D2H copy stream while later calls run and
+ * are complete after dpl_tree_sync (otherwise: complete on return). */
 int dpl_flush(dpl_tree_t tree, dpl_gradbuf_t* bufs, int32_t nbuf, float* moments,
               float* normals, double* d_epsilon);
 

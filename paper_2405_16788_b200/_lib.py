@@ -124,6 +124,7 @@ _sig = {
     "dpl_adjoint": (C.c_int, [_vp, C.POINTER(KernelParams), C.c_double, _vp, C.c_int64, _vp, _vp,
                               _vp]),
     "dpl_flush": (C.c_int, [_vp, C.POINTER(_vp), C.c_int32, _vp, _vp, C.POINTER(C.c_double)]),
+    "dpl_tree_prefetch": (C.c_int, [_vp, _vp, C.c_int64]),
     "dpl_flush_begin": (C.c_int, [_vp, C.POINTER(_vp), C.c_int32, C.POINTER(C.c_double)]),
     "dpl_flush_rows": (C.c_int, [_vp, _vp, C.c_int64, C.c_int64, _vp]),
     "dpl_flush_end": (C.c_int, [_vp, C.POINTER(_vp), C.c_int32, _vp, _vp, _vp]),

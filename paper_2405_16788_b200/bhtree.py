@@ -160,6 +160,14 @@ class DipoleTree:
         if not on:
             self._keep.clear()
 
+    def prefetch(self, xs):
+        """Host-async mode: upload the NEXT primal's host batch now (dpl_tree_prefetch);
+        the primal given the same array skips its own upload."""
+        q = int(xs.shape[0])
+        xp, keep = _in(xs, np.float64, (q, 3))
+        check(lib().dpl_tree_prefetch(self._h, xp, q))
+        self._hold(keep)
+
     def _hold(self, *objs):
         if self._async:
             self._keep.append(objs)
@@ -413,7 +421,10 @@ class DipoleTree:
             mp, np_ = mom.ctypes.data, nrm.ctypes.data
         de = C.c_double()
         check(lib().dpl_flush(self._h, arr, len(buffers), mp, np_, C.byref(de)))
-        self._keep.clear()  # dpl_flush synchronizes every stream of the handle
+        if self._async:  # host outputs complete after synchronize()
+            self._hold(mom, nrm)
+        else:
+            self._keep.clear()  # dpl_flush synchronizes every stream of the handle
         for b in buffers:
             b.dirty = False
         return PointGradients(Cc, mom, nrm, de.value)

@@ -73,6 +73,16 @@ struct dpl_tree_s {
   // a listed forward whose tape no backward consumed switches them off
   bool render_lists = false, render_unconsumed = false;
   cudaEvent_t ev_fwd_in = nullptr, ev_fwd_out = nullptr, ev_adj_in = nullptr;
+  // dpl_tree_prefetch: the next primal's host query batch, uploaded early into
+  // ws_xs_next (swapped in by the primal that names the same host batch)
+  DevBuf ws_xs_next;
+  struct {
+    const void* host = nullptr;
+    int64_t q = 0;
+    bool pending = false;
+  } pf;
+  cudaEvent_t ev_pf_done = nullptr, ev_xs_free = nullptr, ev_flush_done = nullptr,
+              ev_mom_free = nullptr;
   void sync_all() {
     if (copy) DPL_CUDA(cudaStreamSynchronize(copy));
     if (copy_out) DPL_CUDA(cudaStreamSynchronize(copy_out));
@@ -81,7 +91,8 @@ struct dpl_tree_s {
   ~dpl_tree_s() {
     if (copy) cudaStreamSynchronize(copy);
     if (copy_out) cudaStreamSynchronize(copy_out);
-    for (cudaEvent_t e : {ev_fwd_in, ev_fwd_out, ev_adj_in})
+    for (cudaEvent_t e : {ev_fwd_in, ev_fwd_out, ev_adj_in, ev_pf_done, ev_xs_free, ev_flush_done,
+                          ev_mom_free})
       if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : pipe_ev) cudaEventDestroy(e);
     if (copy) cudaStreamDestroy(copy);
@@ -678,6 +689,15 @@ static int forward_common(dpl_tree_t h, const dpl_kernel_params* params, double 
       // pipelined host path
       const int stride = channel >= 0 ? 1 : t.C;
       const int gstride = grad_mode == 1 ? t.C * 3 : 3;
+      bool prefetched = false;
+      if (h->pf.pending) {
+        h->pf.pending = false;
+        if (xs_host && h->host_async && h->pf.host == (const void*)xs && h->pf.q == q) {
+          h->ws_xs.swap(h->ws_xs_next);  // the batch uploaded by dpl_tree_prefetch
+          DPL_CUDA(cudaStreamWaitEvent(t.stream, h->ev_pf_done, 0));
+          prefetched = true;
+        }
+      }
       h->ws_xs.reserve(q * 24);
       h->ws_perm.reserve(q * 4);
       const double* xs_d = xs_host ? h->ws_xs.as<double>() : xs;
@@ -693,7 +713,7 @@ static int forward_common(dpl_tree_t h, const dpl_kernel_params* params, double 
         grad_d = h->ws_grad.as<float>();
       }
       std::vector<HostSeg> ins, outs;
-      if (xs_host) ins.push_back({(const char*)xs, (char*)xs_d, 24});
+      if (xs_host && !prefetched) ins.push_back({(const char*)xs, (char*)xs_d, 24});
       if (out_host) outs.push_back({(const char*)out_d, (char*)out, (size_t)stride * 4});
       if (grad_host) outs.push_back({(const char*)grad_d, (char*)grad, (size_t)gstride * 4});
       int* ovf = overflow_flag(h);
@@ -727,6 +747,7 @@ static int forward_common(dpl_tree_t h, const dpl_kernel_params* params, double 
         PhaseTimer pt(t, PH_FORWARD);
         forward_launch(t, kp, a);
       });
+      DPL_CUDA(cudaEventRecord(hazard_event(h->ev_xs_free), t.stream));
       DPL_CUDA(cudaGetLastError());
       if (!h->host_async) check_overflow(h);  // async: reported by dpl_tree_sync
       return;
@@ -1105,6 +1126,7 @@ int dpl_adjoint(dpl_tree_t h, const dpl_kernel_params* params, double beta_bh, c
       });
       // the primal's staging buffer was read: the next primal's upload waits
       if (reuse) DPL_CUDA(cudaEventRecord(hazard_event(h->ev_fwd_in), t.stream));
+      DPL_CUDA(cudaEventRecord(hazard_event(h->ev_xs_free), t.stream));
       DPL_CUDA(cudaGetLastError());
       return;
     }
@@ -1134,7 +1156,30 @@ int dpl_adjoint(dpl_tree_t h, const dpl_kernel_params* params, double beta_bh, c
     }
     DPL_CUDA(cudaGetLastError());
     if (reuse) DPL_CUDA(cudaEventRecord(hazard_event(h->ev_fwd_in), t.stream));
+    DPL_CUDA(cudaEventRecord(hazard_event(h->ev_xs_free), t.stream));
     if (!is_device_ptr(xs) || !is_device_ptr(d_out)) DPL_CUDA(cudaStreamSynchronize(t.stream));
+  });
+}
+
+int dpl_tree_prefetch(dpl_tree_t h, const double* xs, int64_t q) {
+  return guard([&] {
+    check_tree(h);
+    require(q >= 0, DPL_ERR_USAGE, "negative query count");
+    h->pf.pending = false;
+    // only a host batch that the next primal would upload itself (host-async
+    // pipelined path) gains from an early upload
+    if (!h->host_async || !xs || q <= (1 << 18) || is_device_ptr(xs)) return;
+    Tree& t = h->t;
+    DPL_CUDA(cudaSetDevice(t.device));
+    h->ws_xs_next.reserve((size_t)q * 24);
+    cudaStream_t cin = copy_stream(h, 0);
+    // the kernels queued so far may still read the buffer being refilled
+    DPL_CUDA(cudaStreamWaitEvent(cin, hazard_event(h->ev_xs_free), 0));
+    DPL_CUDA(cudaMemcpyAsync(h->ws_xs_next.p, xs, (size_t)q * 24, cudaMemcpyHostToDevice, cin));
+    DPL_CUDA(cudaEventRecord(hazard_event(h->ev_pf_done), cin));
+    h->pf.host = xs;
+    h->pf.q = q;
+    h->pf.pending = true;
   });
 }
 
@@ -1147,6 +1192,39 @@ int dpl_flush(dpl_tree_t h, dpl_gradbuf_t* bufs, int32_t nbuf, float* moments, f
     Tree& t = h->t;
     DPL_CUDA(cudaSetDevice(t.device));
     GradBuf& b0 = bufs[0]->b;
+    const bool host_out = (moments && !is_device_ptr(moments)) || (normals && !is_device_ptr(normals));
+    if (h->host_async && host_out && (!moments || !is_device_ptr(moments)) &&
+        (!normals || !is_device_ptr(normals))) {
+      // host-async mode: d_epsilon is returned now (it waits for the adjoint
+      // kernels), the point gradients reach the host on the D2H copy stream
+      // while the next call's kernels run; complete after dpl_tree_sync
+      for (int i = 1; i < nbuf; ++i) gradbuf_accumulate(b0, bufs[i]->b, t.stream);
+      double de = 0;
+      DPL_CUDA(cudaMemcpyAsync(&de, b0.d_eps, 8, cudaMemcpyDeviceToHost, t.stream));
+      DPL_CUDA(cudaStreamSynchronize(t.stream));
+      h->ws_mom.reserve(std::max<size_t>(1, (size_t)t.n * t.C * 4));
+      h->ws_nrm.reserve(std::max<size_t>(1, (size_t)t.n * 12));
+      // the previous asynchronous download out of the staging arrays is done
+      DPL_CUDA(cudaStreamWaitEvent(t.stream, hazard_event(h->ev_mom_free), 0));
+      {
+        PhaseTimer pt(t, PH_FLUSH);
+        flush_launch(t, b0, moments ? h->ws_mom.as<float>() : nullptr,
+                     normals ? h->ws_nrm.as<float>() : nullptr);
+      }
+      DPL_CUDA(cudaEventRecord(hazard_event(h->ev_flush_done), t.stream));
+      cudaStream_t cout = copy_stream(h, 1);
+      DPL_CUDA(cudaStreamWaitEvent(cout, h->ev_flush_done, 0));
+      if (moments)
+        DPL_CUDA(cudaMemcpyAsync(moments, h->ws_mom.p, (size_t)t.n * t.C * 4,
+                                 cudaMemcpyDeviceToHost, cout));
+      if (normals)
+        DPL_CUDA(cudaMemcpyAsync(normals, h->ws_nrm.p, (size_t)t.n * 12, cudaMemcpyDeviceToHost,
+                                 cout));
+      DPL_CUDA(cudaEventRecord(hazard_event(h->ev_mom_free), cout));
+      for (int i = 0; i < nbuf; ++i) gradbuf_zero(bufs[i]->b, t.stream);  // reset() (:438)
+      if (d_epsilon) *d_epsilon = de;
+      return;
+    }
     for (int i = 1; i < nbuf; ++i) gradbuf_accumulate(b0, bufs[i]->b, t.stream);  // :429-439
     Out<float> mo, no;
     mo.bind(t, moments, t.n * t.C, h->ws_mom);

@@ -144,6 +144,7 @@ def test_adjoint_reuses_primal_batch(host_async):
         t.primal(xs_h, p, 2.0, out=out_h)
         t.adjoint(None, p, 2.0, do_h, None, b)
         got = t.flush_gradients(b)
+        t.synchronize()  # host-async: outputs complete after synchronize()
         assert np.array_equal(out_h.numpy(), want_out)
         same(got.moments, want.moments)
         same(got.normals, want.normals)
@@ -160,3 +161,46 @@ def test_adjoint_reuse_requires_preceding_primal():
     t.primal(xs, p, 2.0)
     with pytest.raises(P.UsageError):  # different batch size
         t.adjoint(None, p, 2.0, d_out[:500], None, b)
+
+
+def test_prefetch_and_async_flush_pipeline():
+    """Host-async training loop as bench.py's e2e runs it: the next batch is
+    prefetched while the adjoint runs and the point gradients of a flush arrive
+    while the next step's kernels run — the results equal the synchronous
+    loop's, batch by batch."""
+    import torch
+
+    P, t, xs, d_out = _setup(q=400_000, seed=8)
+    p = P.KernelParams(epsilon=0.04)
+    C, n = t.channels(), t.point_count()
+    rng = np.random.default_rng(9)
+    batches = [xs, rng.uniform(-1.3, 1.3, xs.shape).astype(np.float32).astype(np.float64)]
+    xs_h = [torch.from_numpy(b).pin_memory() for b in batches]
+    do_h = torch.from_numpy(d_out).pin_memory()
+    b = t.make_buffer()
+    want = []
+    for k in range(2):  # synchronous reference results per batch
+        out = torch.empty((xs.shape[0], C), dtype=torch.float32).pin_memory()
+        t.primal(xs_h[k], p, 2.0, out=out)
+        t.adjoint(None, p, 2.0, do_h, None, b)
+        g = t.flush_gradients(b)
+        want.append((out.numpy().copy(), g.moments.copy(), g.normals.copy(), g.d_epsilon))
+    t.set_host_async(True)
+    outs = [torch.empty((xs.shape[0], C), dtype=torch.float32).pin_memory() for _ in range(2)]
+    moms = [torch.empty((n, C), dtype=torch.float32).pin_memory() for _ in range(2)]
+    nrms = [torch.empty((n, 3), dtype=torch.float32).pin_memory() for _ in range(2)]
+    deps = []
+    for step in range(4):
+        k = step % 2
+        t.primal(xs_h[k], p, 2.0, out=outs[k])
+        t.adjoint(None, p, 2.0, do_h, None, b)
+        t.prefetch(xs_h[(step + 1) % 2])
+        deps.append(t.flush_gradients(b, out=(moms[k], nrms[k])).d_epsilon)
+    t.synchronize()
+    t.set_host_async(False)
+    for k in range(2):
+        assert np.array_equal(outs[k].numpy(), want[k][0])
+        same(moms[k].numpy(), want[k][1])
+        same(nrms[k].numpy(), want[k][2])
+    for step, de in enumerate(deps):
+        assert abs(de - want[step % 2][3]) <= 1e-12 * abs(want[step % 2][3])
