@@ -66,6 +66,7 @@ struct dpl_tree_s {
     double beta = 0;
     bool listed = false;
     const double* dev = nullptr;  // device copy of that batch (dpl_adjoint xs == NULL)
+    bool sorted = false;          // ws_perm holds that batch's curve order
   } last_fwd;
   bool last_was_fwd = false;
   bool want_lists = false;
@@ -681,6 +682,7 @@ static int forward_common(dpl_tree_t h, const dpl_kernel_params* params, double 
     if (h->last_was_fwd && h->last_fwd.listed) h->want_lists = false;  // unconsumed
     const bool lists = (h->want_lists || ilist_always()) && grad_mode == 0 && !counters;
     h->last_fwd = {xs, q, beta, lists};
+    h->last_fwd.sorted = !presorted;
     h->last_was_fwd = true;
     const bool xs_host = !is_device_ptr(xs);
     const bool out_host = !is_device_ptr(out);
@@ -1075,6 +1077,10 @@ int dpl_adjoint(dpl_tree_t h, const dpl_kernel_params* params, double beta_bh, c
     // list policy (see dpl_tree_s)
     const bool pair = h->last_was_fwd && (reuse || h->last_fwd.xs == (const void*)xs) &&
                       h->last_fwd.q == q && h->last_fwd.beta == beta_bh;
+    // the primal of the same batch left its curve order in ws_perm: no second
+    // sort (any order gives the same results; a batch edited in place between
+    // the calls is only traversed less coherently)
+    const bool keep_perm = pair && h->last_fwd.sorted;
     const bool lists = (pair && h->last_fwd.listed) || ilist_always();
     h->want_lists = pair;
     h->last_was_fwd = false;
@@ -1106,7 +1112,7 @@ int dpl_adjoint(dpl_tree_t h, const dpl_kernel_params* params, double beta_bh, c
       run_chunked(h, q, pipe_chunk(q), ins, {}, h->ev_adj_in, nullptr,
                   [&](int64_t c0, int64_t qc) {
         int32_t* perm = h->ws_perm.as<int32_t>() + c0;
-        {
+        if (!keep_perm) {
           PhaseTimer pt(t, PH_SORT);
           morton_order(t, xs_d + 3 * c0, qc, perm, h->ws_morton);
         }
@@ -1127,6 +1133,9 @@ int dpl_adjoint(dpl_tree_t h, const dpl_kernel_params* params, double beta_bh, c
       // the primal's staging buffer was read: the next primal's upload waits
       if (reuse) DPL_CUDA(cudaEventRecord(hazard_event(h->ev_fwd_in), t.stream));
       DPL_CUDA(cudaEventRecord(hazard_event(h->ev_xs_free), t.stream));
+      // lists rebuilt here (a batch edited in place) follow the kept order, which
+      // a later primal's fresh sort need not reproduce: no reuse across that
+      if (keep_perm) h->il.valid = false;
       DPL_CUDA(cudaGetLastError());
       return;
     }
@@ -1135,7 +1144,7 @@ int dpl_adjoint(dpl_tree_t h, const dpl_kernel_params* params, double beta_bh, c
     const float* dout_d = stage_in(t, d_out, (size_t)q * t.C, h->ws_dout);
     const float* dg_d = d_grad ? stage_in(t, d_grad, (size_t)q * t.C * 3, h->ws_dgrad) : nullptr;
     h->ws_perm.reserve(q * 4);
-    {
+    if (!keep_perm) {
       PhaseTimer pt(t, PH_SORT);
       morton_order(t, xs_d, q, h->ws_perm.as<int32_t>(), h->ws_morton);
     }
@@ -1157,6 +1166,7 @@ int dpl_adjoint(dpl_tree_t h, const dpl_kernel_params* params, double beta_bh, c
     DPL_CUDA(cudaGetLastError());
     if (reuse) DPL_CUDA(cudaEventRecord(hazard_event(h->ev_fwd_in), t.stream));
     DPL_CUDA(cudaEventRecord(hazard_event(h->ev_xs_free), t.stream));
+    if (keep_perm) h->il.valid = false;  // see the pipelined path above
     if (!is_device_ptr(xs) || !is_device_ptr(d_out)) DPL_CUDA(cudaStreamSynchronize(t.stream));
   });
 }
