@@ -411,22 +411,23 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
 // Persistent, warp-specialised variant for K-contiguous A and a pre-split B
 // image (the MLP head's forward and input-gradient GEMMs). One CTA per SM
 // walks the tiles round-robin:
-//   warps 0-3  A producers: cp.async of the chunk into a 3-deep swizzled fp32
-//              staging ring (two chunks in flight), split into tf32 hi / lo,
-//              tcgen05.st into one of 4 TMEM A stages (warp w -> lanes 32w..);
-//              thread 0 also issues the chunk's B bulk copy;
-//   warp 8     MMA issuer (one thread): 12 tcgen05.mma per chunk into one of two
+//   warps 0-7  A producers in two sets of 4 warps taking alternate chunks:
+//              cp.async of the chunk into the set's swizzled fp32 staging ring
+//              (the set's next chunk in flight), split into tf32 hi / lo,
+//              tcgen05.st into one of 4 TMEM A stages (warps w, w + 4 -> lanes
+//              32w..); the set's thread 0 also issues the chunk's B bulk copy;
+//   warp 12    MMA issuer (one thread): 12 tcgen05.mma per chunk into one of two
 //              TMEM accumulators, commit -> stage free; after a tile's last
 //              chunk, commit -> accumulator full;
-//   warps 4-7  epilogue: tcgen05.ld of the finished accumulator (warp 4 + q ->
+//   warps 8-11 epilogue: tcgen05.ld of the finished accumulator (warp 8 + q ->
 //              lane quadrant q), fused bias / ReLU / gate, stores, release.
 // The epilogue of tile i and the producers of tile i + 1 run while the tensor
 // core works, so per-tile fixed costs (TMEM allocation, barrier setup, the
 // first loads, the drain) are paid once per SM instead of once per tile.
 // TMEM: accumulators 2 x BN (<= 256) + A stages 4 x 64 = 512 columns.
 constexpr int kWsStages = 4;
-constexpr int kWsRing = 3;  // A staging ring (prefetch distance 2)
-constexpr int kWsThreads = 9 * 32;
+constexpr int kWsRing = 2;  // per producer set: A staging ring (prefetch distance 1)
+constexpr int kWsThreads = 13 * 32;
 
 template <int BN, int EPI>
 __global__ void __launch_bounds__(kWsThreads, 1) k_tc_gemm_ws(TcGemm g) {
@@ -436,7 +437,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tc_gemm_ws(TcGemm g) {
   constexpr int STAGEB = 2 * BBYTES;
   constexpr int ABYTES = kTileM * kRowBytes;
   uint8_t* bst = sm;                          // kWsStages x (hi | lo)
-  uint8_t* ast = sm + kWsStages * STAGEB;     // kWsRing x raw fp32 A chunk
+  uint8_t* ast = sm + kWsStages * STAGEB;     // 2 sets x kWsRing x raw fp32 A chunk
   __shared__ __align__(8) uint64_t afull[kWsStages], bfull[kWsStages], empty[kWsStages],
       dfull[2], dempty[2];
   __shared__ uint32_t tmem_slot;
@@ -468,19 +469,32 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tc_gemm_ws(TcGemm g) {
   const int ntotal = mtiles * ntiles;
   const int nkc = (g.K + kChunkK - 1) / kChunkK;  // chunks per tile (K > 0)
 
-  if (warp < 4) {
-    // ---------------- A producers (+ B bulk copies by thread 0)
-    const int row = tid;  // tile row = TMEM lane (warp w owns lanes 32w..32w+31)
-    const uint32_t lane_base = (uint32_t)(32 * warp) << 16;
-    // chunk cursor for the cp.async prefetch (two chunks ahead of consumption)
-    int pf_t = blockIdx.x, pf_c = 0;
-    auto issue = [&](int slot) {
-      if (pf_t < ntotal) {
-        const int m0 = (pf_t / ntiles) * kTileM, k0 = pf_c * kChunkK;
-        uint8_t* dst0 = ast + slot * ABYTES;
+  if (warp < 8) {
+    // ---------------- A producers (+ B bulk copies): two sets of 4 warps take
+    // alternate chunks (set = warp / 4; warps w and w + 4 share lane quadrant w)
+    const int set = warp >> 2, ptid = tid & 127;
+    const int row = ptid;  // tile row = TMEM lane of quadrant warp % 4
+    const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
+    uint8_t* ring = ast + set * kWsRing * ABYTES;
+    // (tile, chunk) cursors over this set's chunks: every second chunk of the
+    // CTA's sequence, starting at chunk `set`
+    struct Cursor {
+      int t, c;
+    };
+    auto step = [&](Cursor& k) {
+      if (++k.c == nkc) k.c = 0, k.t += gridDim.x;
+    };
+    Cursor pf{(int)blockIdx.x, 0};
+    if (set) step(pf);
+    Cursor cs = pf;
+    int pf_n = 0;  // chunks issued so far by this set
+    auto issue = [&]() {
+      if (pf.t < ntotal) {
+        const int m0 = (pf.t / ntiles) * kTileM, k0 = pf.c * kChunkK;
+        uint8_t* dst0 = ring + (pf_n % kWsRing) * ABYTES;
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          const int idx = tid + 128 * i, r = idx >> 3, j = idx & 7;
+          const int idx = ptid + 128 * i, r = idx >> 3, j = idx & 7;
           const int grr = m0 + r, gk = k0 + 4 * j;
           const int bytes = grr < g.M ? max(0, min(16, (g.K - gk) * 4)) : 0;
           const float* src = bytes ? g.A + (int64_t)grr * g.lda + gk : g.A;
@@ -489,42 +503,42 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tc_gemm_ws(TcGemm g) {
                        "l"(src), "r"(bytes)
                        : "memory");
         }
-        if (++pf_c == nkc) pf_c = 0, pf_t += gridDim.x;
+        step(pf);
+        step(pf);
       }
+      ++pf_n;
       asm volatile("cp.async.commit_group;\n" ::: "memory");  // (possibly empty) group
     };
-    issue(0);
-    issue(1);
-    int gc = 0;  // chunks consumed by this CTA
-    for (int t = blockIdx.x; t < ntotal; t += gridDim.x) {
-      const int nt = t % ntiles;
-      for (int c = 0; c < nkc; ++c, ++gc) {
-        const int s = gc % kWsStages;
-        const uint32_t ph = (uint32_t)(gc / kWsStages) & 1u;
-        mbar_wait(smem_addr(&empty[s]), ph ^ 1u);  // the MMAs of chunk gc - 4 are done
-        if (tid == 0) {
-          const uint8_t* src = g.b_image + ((size_t)nt * nkc + c) * STAGEB;
-          mbar_expect_tx(smem_addr(&bfull[s]), STAGEB);
-          bulk_copy(smem_addr(bst + s * STAGEB), src, STAGEB, smem_addr(&bfull[s]));
-        }
-        asm volatile("cp.async.wait_group 1;\n" ::: "memory");  // chunk gc has landed (own copies)
-        asm volatile("bar.sync 1, 128;\n" ::: "memory");        // ... everyone's; ring slot gc-1 read
-        issue((gc + 2) % kWsRing);
-        const uint8_t* src = ast + (gc % kWsRing) * ABYTES + row * kRowBytes;
-        float x[32];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const float4 v = *reinterpret_cast<const float4*>(src + ((j ^ (row & 7)) << 4));
-          x[4 * j] = v.x, x[4 * j + 1] = v.y, x[4 * j + 2] = v.z, x[4 * j + 3] = v.w;
-        }
-        store_a(tmem + lane_base + TM_A + 64u * s, x);
-        asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
-        tc_fence_before();
-        mbar_arrive(smem_addr(&afull[s]));
+    issue();  // prefetch distance 1 within the set (2 chunks of the CTA's sequence)
+    for (int n = 0; cs.t < ntotal; ++n) {
+      const int gc = 2 * n + set;
+      const int s = gc % kWsStages;
+      const uint32_t ph = (uint32_t)(gc / kWsStages) & 1u;
+      mbar_wait(smem_addr(&empty[s]), ph ^ 1u);  // the MMAs of chunk gc - 4 are done
+      if (ptid == 0) {
+        const uint8_t* src = g.b_image + ((size_t)(cs.t % ntiles) * nkc + cs.c) * STAGEB;
+        mbar_expect_tx(smem_addr(&bfull[s]), STAGEB);
+        bulk_copy(smem_addr(bst + s * STAGEB), src, STAGEB, smem_addr(&bfull[s]));
       }
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");  // this set's chunk n has landed
+      asm volatile("bar.sync %0, 128;\n" ::"r"(1 + set) : "memory");  // ... everyone's; slot n-1 read
+      issue();
+      const uint8_t* src = ring + (n % kWsRing) * ABYTES + row * kRowBytes;
+      float x[32];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float4 v = *reinterpret_cast<const float4*>(src + ((j ^ (row & 7)) << 4));
+        x[4 * j] = v.x, x[4 * j + 1] = v.y, x[4 * j + 2] = v.z, x[4 * j + 3] = v.w;
+      }
+      store_a(tmem + lane_base + TM_A + 64u * s, x);
+      asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+      tc_fence_before();
+      mbar_arrive(smem_addr(&afull[s]));
+      step(cs);
+      step(cs);
     }
     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-  } else if (warp == 8) {
+  } else if (warp == 12) {
     // ---------------- MMA issuer
     if (lane == 0) {
       constexpr uint32_t IDESC = idesc_tf32(kTileM, BN);
@@ -555,8 +569,8 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tc_gemm_ws(TcGemm g) {
     }
     __syncwarp();
   } else {
-    // ---------------- epilogue (warps 4-7 -> lane quadrants 0-3)
-    const int q = warp - 4;
+    // ---------------- epilogue (warps 8-11 -> lane quadrants 0-3)
+    const int q = warp - 8;
     const uint32_t lane_base = (uint32_t)(32 * q) << 16;
     const bool vec_d = (g.ldd & 3) == 0 && ((reinterpret_cast<uintptr_t>(g.D) & 15) == 0) &&
                        (EPI != TC_GATE || ((g.ldaux & 3) == 0 &&
@@ -668,7 +682,7 @@ void launch_n(const TcGemm& g, int device, cudaStream_t s) {
 template <int BN, int EPI>
 void launch_ws(const TcGemm& g, int device, cudaStream_t s) {
   constexpr size_t smem = 1024 + (size_t)kWsStages * 2 * BN * kRowBytes +
-                          (size_t)kWsRing * kTileM * kRowBytes;
+                          2 * (size_t)kWsRing * kTileM * kRowBytes;
   static std::atomic<unsigned long long> attr{0};
   ensure_max_dyn_smem(k_tc_gemm_ws<BN, EPI>, device, smem, attr);
   int sms = 148;
