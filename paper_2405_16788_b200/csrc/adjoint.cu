@@ -495,6 +495,12 @@ static void adj_plan(const Tree& t, const KParams& kp, const AdjArgs& a, GradBuf
 
 void adjoint_launch(const Tree& t, const KParams& kp, const AdjArgs& a, GradBuf& b) {
   static const bool single_phase = getenv("DPL_ADJOINT_SINGLE_PHASE") != nullptr;
+  // tensor-memory adjoint (adjoint_tm.cu: tcgen05.mma, accumulators in TMEM) for
+  // 4 < Cr <= 48: parity-tested, measured SLOWER than the register-tile FFMA2
+  // kernel on B200 (config 2: 23.7 ms vs 13.6 ms, profiles/r02_adjoint_tmem.md),
+  // so it is opt-in with DPL_ADJOINT_TMEM=1
+  static const bool tmem = getenv("DPL_ADJOINT_TMEM") != nullptr;
+  if (!single_phase && tmem && adjoint_tm_launch(t, kp, a, b)) return;
   if (!single_phase && adjoint2_launch(t, kp, a, b)) return;
   if (a.grad_mode == 0) return adj_plan<0>(t, kp, a, b);
   if (a.grad_mode == 1) return adj_plan<1>(t, kp, a, b);

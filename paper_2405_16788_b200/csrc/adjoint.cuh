@@ -38,6 +38,8 @@ void gradbuf_accumulate(GradBuf& dst, const GradBuf& src, cudaStream_t s);
 void adjoint_launch(const Tree& t, const KParams& kp, const AdjArgs& a, GradBuf& b);
 // two-phase kernel for one Dipole + <= 64 Radial channels (adjoint2.cu)
 bool adjoint2_launch(const Tree& t, const KParams& kp, const AdjArgs& a, GradBuf& b);
+// tcgen05 / TMEM kernel for one Dipole + (4, 48] Radial channels (adjoint_tm.cu)
+bool adjoint_tm_launch(const Tree& t, const KParams& kp, const AdjArgs& a, GradBuf& b);
 // consumes b's node accumulators (push-down in place); caller zeroes afterwards
 void flush_launch(Tree& t, GradBuf& b, float* moments, float* normals);
 // flush_launch split for cross-rank reduction: the node
