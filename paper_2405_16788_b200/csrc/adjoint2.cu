@@ -206,10 +206,20 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
     const float* g = GM == 1 ? d_grad + (qi * dstride + ch0) * 3 : d_grad + qi * 3;
     dg0 = g[0], dg1 = g[1], dg2 = g[2];
   }
-  // FFMA phase B: transposed radial tile in registers (lanes = channels)
+  // FFMA phase B: transposed radial tile in registers. Lane (h, g) = (lane >> 4,
+  // lane & 15) owns channels g, 16 + g, .. (NG groups of 16) for the 16 queries
+  // of half-warp h: each entry's weights are then 4 LDS.128 with a
+  // half-warp-uniform address (8 shared-memory wavefronts) instead of 12
+  // warp-uniform ones (24) — shared-memory wavefronts, not issue slots, bound
+  // this kernel (profiles/r02_smem_wavefronts.md) — and the two halves' partial
+  // sums meet through one shuffle per channel-group pair.
   constexpr bool FF = MT == 0;
-  float colA[FF && !VR ? 32 : 1];
-  float colB[FF ? (NB == 2 ? 32 : (NB == 1 ? 16 : 1)) : 1];
+  constexpr int NG = NB == 0 ? 2 : (NB == 1 ? 3 : (NB == 2 ? 4 : 1));
+  const int hw = lane >> 4, g16 = lane & 15;
+  float col[FF && !VR ? NG : 1][16];
+  bool okg[NG];
+#pragma unroll
+  for (int k = 0; k < NG; ++k) okg[k] = FF && !VR && 16 * k + g16 < nr;
   // VR: this lane's own radial upstream gradients (slots >= nr read as 0)
   float dsr[4] = {0.f, 0.f, 0.f, 0.f};
   if constexpr (VR) {
@@ -217,30 +227,20 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
     for (int c = 0; c < 4; ++c)
       if (valid && c < nr) dsr[c] = __ldg(d_out + qi * dstride + __ldg(chmap + 1 + c));
   }
-  const bool okA = lane < nr;
-  const int slotB = NB == 1 ? 32 + (lane & 15) : 32 + lane;
-  const bool okB = FF && NB > 0 && slotB < nr;
   // tensor-core phase B: A = d_out tile^T [channel][query] as TF32 fragments
   uint32_t ahi[MT ? MT : 1][4][4];
   if constexpr (FF && !VR) {
-    const int chA = okA ? __ldg(chmap + 1 + lane) : 0;
-    const int chB = okB ? __ldg(chmap + 1 + slotB) : 0;
+    int chg[NG];
 #pragma unroll
-    for (int l = 0; l < 32; ++l) {
-      const int64_t ql = __shfl_sync(FULL_MASK, qi, l);
-      const bool vl = (active >> l) & 1u;
-      colA[l] = (okA && vl) ? __ldg(d_out + ql * dstride + chA) : 0.f;
-      if (NB == 2) colB[l] = (okB && vl) ? __ldg(d_out + ql * dstride + chB) : 0.f;
-    }
-    if (NB == 1) {
-      const int h = lane >> 4;
+    for (int k = 0; k < NG; ++k) chg[k] = okg[k] ? __ldg(chmap + 1 + 16 * k + g16) : 0;
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const int l = 16 * h + i;
-        const int64_t ql = __shfl_sync(FULL_MASK, qi, l);  // all lanes participate
-        const bool vl = (active >> l) & 1u;
-        colB[i] = (okB && vl) ? __ldg(d_out + ql * dstride + chB) : 0.f;
-      }
+    for (int i = 0; i < 16; ++i) {
+      const int srcl = 16 * hw + i;
+      const int64_t ql = __shfl_sync(FULL_MASK, qi, srcl);
+      const bool vl = (active >> srcl) & 1u;
+#pragma unroll
+      for (int k = 0; k < NG; ++k)
+        col[k][i] = (okg[k] && vl) ? __ldg(d_out + ql * dstride + chg[k]) : 0.f;
     }
   } else {
     // coalesced staging of the tile T[query l][slot c] (c < 16 MT), then
@@ -357,39 +357,41 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
     for (int e = 0; e < nent; ++e) {
       const int m = meta[e];
       if constexpr (FF && !VR) {
-        const float4* wr4 = reinterpret_cast<const float4*>(wR + e * WS);
+        const float4* wr4 = reinterpret_cast<const float4*>(wR + e * WS + 16 * hw);
         // even / odd query partial sums on the packed FMA pipe (FFMA2)
-        float2 pA = make_float2(0.f, 0.f), pB = make_float2(0.f, 0.f);
+        float2 p[NG];
 #pragma unroll
-        for (int l4 = 0; l4 < 8; ++l4) {
-          const float4 ww = wr4[l4];
-          fma2(pA, make_float2(ww.x, ww.y), make_float2(colA[4 * l4], colA[4 * l4 + 1]));
-          fma2(pA, make_float2(ww.z, ww.w), make_float2(colA[4 * l4 + 2], colA[4 * l4 + 3]));
-          if (NB == 2) {
-            fma2(pB, make_float2(ww.x, ww.y), make_float2(colB[4 * l4], colB[4 * l4 + 1]));
-            fma2(pB, make_float2(ww.z, ww.w), make_float2(colB[4 * l4 + 2], colB[4 * l4 + 3]));
+        for (int k = 0; k < NG; ++k) p[k] = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int i4 = 0; i4 < 4; ++i4) {
+          const float4 ww = wr4[i4];
+#pragma unroll
+          for (int k = 0; k < NG; ++k) {
+            fma2(p[k], make_float2(ww.x, ww.y), make_float2(col[k][4 * i4], col[k][4 * i4 + 1]));
+            fma2(p[k], make_float2(ww.z, ww.w), make_float2(col[k][4 * i4 + 2], col[k][4 * i4 + 3]));
           }
         }
-        if (NB == 1) {
-          // half-warp split: lanes 0-15 cover queries 0-15, lanes 16-31 queries 16-31
-          const float* wh = wR + e * WS + 16 * (lane >> 4);
+        float sg[NG];
 #pragma unroll
-          for (int i4 = 0; i4 < 4; ++i4) {
-            const float4 ww = reinterpret_cast<const float4*>(wh)[i4];
-            fma2(pB, make_float2(ww.x, ww.y), make_float2(colB[4 * i4], colB[4 * i4 + 1]));
-            fma2(pB, make_float2(ww.z, ww.w), make_float2(colB[4 * i4 + 2], colB[4 * i4 + 3]));
-          }
-        }
-        const float sA = pA.x + pA.y;
-        float sB = pB.x + pB.y;
-        if (NB == 1) sB += __shfl_xor_sync(FULL_MASK, sB, 16);
+        for (int k = 0; k < NG; ++k) sg[k] = p[k].x + p[k].y;
+        // half 0 completes groups 0 (and 2), half 1 groups 1 (and 3): each lane
+        // sends the partial its partner completes, so group pair (0, 1) ends as
+        // channel `lane` in lane `lane`
+        const float t01 = (hw ? sg[1] : sg[0]) + __shfl_xor_sync(FULL_MASK, hw ? sg[0] : sg[1], 16);
         double* dst_s = dptr[e];
-        if (NB > 0)  // nr > 32: every lane owns an A channel; no predicate, no branch
-          red_add_f32(dst_s + lane, sA);
+        if (NB > 0)  // nr > 32: every lane owns a channel; no predicate, no branch
+          red_add_f32(dst_s + lane, t01);
         else
-          red_add_f32_if(dst_s + lane, sA, okA && sA != 0.f);
-        const bool ownB = NB == 2 ? okB : (NB == 1 ? (okB && lane < 16) : false);
-        if (NB > 0) red_add_f32_if(dst_s + slotB, sB, ownB && sB != 0.f);
+          red_add_f32_if(dst_s + lane, t01, lane < nr && t01 != 0.f);
+        if constexpr (NG == 3) {
+          const float t2 = sg[2] + __shfl_xor_sync(FULL_MASK, sg[2], 16);
+          red_add_f32_if(dst_s + 32 + g16, t2, hw == 0 && okg[2] && t2 != 0.f);
+        }
+        if constexpr (NG == 4) {
+          const float t23 = (hw ? sg[NG - 1] : sg[2]) +
+                            __shfl_xor_sync(FULL_MASK, hw ? sg[2] : sg[NG - 1], 16);
+          red_add_f32_if(dst_s + 32 + lane, t23, 32 + lane < nr && t23 != 0.f);
+        }
       }
     }
     if constexpr (FF && !VR) {
@@ -399,28 +401,25 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
       while (nm) {
         const int e = __ffs(nm) - 1;
         nm &= nm - 1;
-        const bool ownB = NB == 2 ? okB : (NB == 1 ? (okB && lane < 16) : false);
-        const float4* we4 = reinterpret_cast<const float4*>(wE + e * WS);
-        float eA = 0.f, eB = 0.f;
+        const float4* we4 = reinterpret_cast<const float4*>(wE + e * WS + 16 * hw);
+        float ev[NG];
 #pragma unroll
-        for (int l4 = 0; l4 < 8; ++l4) {
-          const float4 ww = we4[l4];
+        for (int k = 0; k < NG; ++k) ev[k] = 0.f;
+#pragma unroll
+        for (int i4 = 0; i4 < 4; ++i4) {
+          const float4 ww = we4[i4];
           const float wv[4] = {ww.x, ww.y, ww.z, ww.w};
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            eA = fmaf(wv[u], colA[4 * l4 + u], eA);
-            if (NB == 2) eB = fmaf(wv[u], colB[4 * l4 + u], eB);
-          }
-        }
-        if (NB == 1) {
-          const float* wh = wE + e * WS + 16 * (lane >> 4);
+          for (int u = 0; u < 4; ++u)
 #pragma unroll
-          for (int i = 0; i < 16; ++i) eB = fmaf(wh[i], colB[i], eB);
-          eB += __shfl_xor_sync(FULL_MASK, eB, 16);
+            for (int k = 0; k < NG; ++k) ev[k] = fmaf(wv[u], col[k][4 * i4 + u], ev[k]);
         }
+        // each half's partial sum times the channel's moment: no cross-half step
+        // (eps_acc is reduced over the warp at the end)
         const float* rad = reinterpret_cast<const float*>(rows + e * F4 + 1);
-        if (okA) eps_acc += (double)(eA * rad[lane]);
-        if (ownB) eps_acc += (double)(eB * rad[slotB]);
+#pragma unroll
+        for (int k = 0; k < NG; ++k)
+          if (okg[k]) eps_acc += (double)(ev[k] * rad[16 * k + g16]);
       }
     }
     // vector quantities of the whole batch: lane L sums pair (e, k) = (L / VQ, L % VQ)

@@ -105,15 +105,17 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
   constexpr int F4 = 1 + TR / 4;               // global row float4 (dipole + radial)
   constexpr int RSF = row_stride_floats(F4);   // padded smem row stride (floats)
   constexpr int WSTR = 40;                     // padded Wr row stride (floats)
-  constexpr int WARP_FLOATS = ENT * 32 * 4 + ENT * WSTR + ENT * RSF + 2 * DPL_STACK_PER_WARP;
+  // the dipole slot is accumulated in phase A (its moment float4 arrives with the
+  // node-record window, vb), so no per-lane dipole weights go through shared memory
+  constexpr int WARP_FLOATS = ENT * WSTR + ENT * RSF + 2 * DPL_STACK_PER_WARP + 32 * 4;
   extern __shared__ float4 smem_f4[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int g = lane >> 2, tq = lane & 3;  // mma fragment coordinates
   float* base = reinterpret_cast<float*>(smem_f4) + (size_t)w * WARP_FLOATS;
-  float4* wd = reinterpret_cast<float4*>(base);  // [ENT][32] (A W d, -)
-  float* wr = base + ENT * 128;                  // [ENT][WSTR]  A R
-  float* rows = wr + ENT * WSTR;                 // [ENT][RSF]
+  float* wr = base;                 // [ENT][WSTR]  A R
+  float* rows = wr + ENT * WSTR;    // [ENT][RSF] (the dipole float4 of each row is not staged)
   int2* stk = reinterpret_cast<int2*>(rows + ENT * RSF);
+  float4* vb = reinterpret_cast<float4*>(stk + DPL_STACK_PER_WARP);  // [32] window dipole moments
   const uint32_t s_rows = smem_u32(rows) + 16u * lane;
 
   const int64_t sidx = ((int64_t)blockIdx.x * WARPS + w) * 32 + lane;
@@ -144,18 +146,9 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
 
   auto evaluate = [&]() {
     // zero-fill the batch tail so the K=8 steps read zeros
-    for (int e = nent; e < ((nent + 7) & ~7); ++e) {
-      wr[e * WSTR + lane] = 0.f;
-      wd[e * 32 + lane] = make_float4(0.f, 0.f, 0.f, 0.f);
-    }
+    for (int e = nent; e < ((nent + 7) & ~7); ++e) wr[e * WSTR + lane] = 0.f;
     cp_async_wait_all();
     __syncwarp();
-    // dipole slot on the FP32 pipe
-    for (int e = 0; e < nent; ++e) {
-      const float4 wv = wd[e * 32 + lane];
-      const float4 v = *reinterpret_cast<const float4*>(rows + e * RSF);
-      accd = fmaf(wv.x, v.x, fmaf(wv.y, v.y, fmaf(wv.z, v.z, accd)));
-    }
     // radial channels on the tensor cores
     const int ksteps = NT > 0 ? (nent + 7) >> 3 : 0;
     for (int ks = 0; ks < ksteps; ++ks) {
@@ -191,15 +184,18 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
     nent = 0;
   };
 
-  auto store_entry = [&](float4 wv, const float4* rowsrc) {  // nent < ENT
-    wd[nent * 32 + lane] = make_float4(wv.x, wv.y, wv.z, 0.f);
+  // v: the source's dipole moment (first float4 of its row); the dipole slot is
+  // three FMAs on the FP32 pipe, in entry order (bitwise the batch loop it replaces)
+  auto store_entry = [&](float4 wv, const float4* rowsrc, float4 v) {  // nent < ENT
+    accd = fmaf(wv.x, v.x, fmaf(wv.y, v.y, fmaf(wv.z, v.z, accd)));
     wr[nent * WSTR + lane] = wv.w;
-    if (lane < F4) cp_async16(s_rows + 4u * RSF * nent, rowsrc + lane);
+    if (lane >= 1 && lane < F4) cp_async16(s_rows + 4u * RSF * nent, rowsrc + lane);
     ++nent;
   };
   auto append = [&](float4 wv, const float4* rowsrc) {
+    const float4 v = __ldg(rowsrc);
     if (nent == ENT) evaluate();
-    store_entry(wv, rowsrc);
+    store_entry(wv, rowsrc, v);
   };
 
   // COUNT: per-query replay counters (visited, far near/far, point near/far)
@@ -213,6 +209,7 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
     // (unused) stack region with cp.async, read back as broadcast LDS.128
     NodeRec* rb = reinterpret_cast<NodeRec*>(stk);
     const uint32_t s_rb = smem_u32(stk) + 48u * lane;
+    const uint32_t s_vb = smem_u32(vb) + 16u * lane;
     const double* xq = xs + 3 * qi;
     int chunk = (int)wg;
     for (int base = 0; base < total; base += 32) {
@@ -225,6 +222,7 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
         cp_async16(s_rb, &r->hi);
         cp_async16(s_rb + 16u, &r->lo);
         cp_async16(s_rb + 32u, &r->topo);
+        if (!(my.x & IL_LEAF)) cp_async16(s_vb, node_row + (size_t)(my.x & IL_NODE) * F4g);
       }
       cp_async_wait_all();
       // the entry itself goes into its record's unused child fields (topo.x/y;
@@ -248,15 +246,15 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
           const bool fa = ((unsigned)tpi.y >> lane) & 1u, fb = ((unsigned)tb.y >> lane) & 1u;
           if (REG) {  // one select on the area per entry (see rsqrt_far)
             store_entry(fwd_w_far_m(ax, ay, az, sa, sel0(fa, la.w), kp.near2),
-                        node_row + (size_t)(src & IL_NODE) * F4g);
+                        node_row + (size_t)(src & IL_NODE) * F4g, vb[i]);
             store_entry(fwd_w_far_m(bx, by, bz, sb, sel0(fb, lb.w), kp.near2),
-                        node_row + (size_t)((uint32_t)tb.x & IL_NODE) * F4g);
+                        node_row + (size_t)((uint32_t)tb.x & IL_NODE) * F4g, vb[i + 1]);
           } else {
             const float4 wa = fwd_w_far(ax, ay, az, sa, la.w), wb = fwd_w_far(bx, by, bz, sb, lb.w);
             store_entry(make_float4(fa ? wa.x : 0.f, fa ? wa.y : 0.f, fa ? wa.z : 0.f, fa ? wa.w : 0.f),
-                        node_row + (size_t)(src & IL_NODE) * F4g);
+                        node_row + (size_t)(src & IL_NODE) * F4g, vb[i]);
             store_entry(make_float4(fb ? wb.x : 0.f, fb ? wb.y : 0.f, fb ? wb.z : 0.f, fb ? wb.w : 0.f),
-                        node_row + (size_t)((uint32_t)tb.x & IL_NODE) * F4g);
+                        node_row + (size_t)((uint32_t)tb.x & IL_NODE) * F4g, vb[i + 1]);
           }
           ++i;
           continue;
@@ -278,7 +276,8 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
             wv.x = mine ? f.x : 0.f, wv.y = mine ? f.y : 0.f;
             wv.z = mine ? f.z : 0.f, wv.w = mine ? f.w : 0.f;
           }
-          append(wv, node_row + (size_t)node * F4g);
+          if (nent == ENT) evaluate();
+          store_entry(wv, node_row + (size_t)node * F4g, vb[i]);
         } else {
           const int4 tp = tpi;
           for (int j = tp.z; j < tp.w; ++j) {
@@ -389,7 +388,7 @@ static void launch_tc1(const Tree& t, const KParams& kp, const FwdArgs& a, int n
                        IListView lv = {}) {
   constexpr int F4 = 1 + 2 * NT;
   constexpr int RSF = row_stride_floats(F4);
-  constexpr int WARP_FLOATS = ENT * 32 * 4 + ENT * 40 + ENT * RSF + 2 * DPL_STACK_PER_WARP;
+  constexpr int WARP_FLOATS = ENT * 40 + ENT * RSF + 2 * DPL_STACK_PER_WARP + 32 * 4;
   const size_t smem = (size_t)WARPS * WARP_FLOATS * 4;
   static std::atomic<unsigned long long> attr{0};
   ensure_max_dyn_smem(k_forward_tc<NT, WARPS, ENT, MAXR, COUNT, LIST, REG>, t.device, smem, attr);
