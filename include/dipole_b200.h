@@ -92,7 +92,9 @@ int dpl_tree_prefetch(dpl_tree_t tree, const double* xs, int64_t q);
 
 /* DipoleTree::build (bhtree.cpp:158-169): GPU Morton-digit sort + level-by-level
  * BFS numbering reproduces build_structure (:36-105) bit-exactly; geometry
- * (:107-134) and moments (:136-156) follow. Channel kernels reset to Dipole. */
+ * (:107-134) and moments (:136-156) follow. Channel kernels reset to Dipole.
+ * max_depth <= 42 (the reference's default is 20, bhtree.hpp:54); a deeper
+ * request returns DPL_ERR_USAGE. */
 int dpl_tree_build(dpl_tree_t tree, const double* pos, const double* nrm, const double* area,
                    const double* mu, int64_t n, int32_t channels, int32_t max_leaf_size,
                    int32_t max_depth);

@@ -77,11 +77,12 @@ constexpr uint32_t TM_A_LO = TM_ROWS * 128;                 // 6144
 constexpr uint32_t TM_B = 2 * TM_ROWS * 128;                // 12288: [buf][hi | lo] x 2 KB
 constexpr uint32_t TM_VQO = TM_B + 2 * 2 * TM_N * 128;      // 20480: vq[8][4][32] floats
 constexpr uint32_t TM_RB = TM_VQO + TM_VQ * 4 * 32 * 4;     // 24576: node records / stack
-constexpr uint32_t TM_DP = TM_RB + 32 * 48;                 // 26112: dptr[2][16]
-constexpr uint32_t TM_META = TM_DP + 2 * TM_N * 8;          // 26368: meta[8], ncols[2]
-constexpr uint32_t TM_WARP = 26624;                         // 26 KB
+constexpr uint32_t TM_RBSZ = DPL_STACK_PER_WARP * 8 > 32 * 48 ? DPL_STACK_PER_WARP * 8 : 32 * 48;
+constexpr uint32_t TM_DP = TM_RB + TM_RBSZ;                 // dptr[2][16]
+constexpr uint32_t TM_META = TM_DP + 2 * TM_N * 8;          // meta[8], ncols[2]
+constexpr uint32_t TM_WARP = 27648;                         // 27 KB
 static_assert(TM_META + (TM_VQ + 2) * 4 <= TM_WARP, "per-warp layout");
-static_assert(DPL_STACK_PER_WARP * 8 <= 32 * 48, "stack aliases the record window");
+static_assert(TM_DP % 16 == 0, "destination rows are read as 16-byte pairs");
 static_assert(TM_WARP % 1024 == 0 && TM_B % 1024 == 0, "tile alignment");
 }  // namespace
 

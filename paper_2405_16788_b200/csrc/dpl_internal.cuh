@@ -24,14 +24,15 @@
 
 #define DPL_WARP 32
 #define DPL_MAX_CHANNELS 1024
-// Deepest tree the GPU build supports: 3 key bits per level in 64-bit keys
-// (tree.cu rejects max_depth > 21 at build time with a usage error).
-#define DPL_MAX_DEPTH 21
+// Deepest tree the GPU build supports: 3 key bits per level in two 64-bit key
+// words (tree.cu rejects max_depth > 42 at build time with a usage error; the
+// reference's default is 20, bhtree.hpp:54).
+#define DPL_MAX_DEPTH 42
 // Traversal stack per warp. A popped internal node pushes its child_count
 // children, so along any root-to-leaf path the stack holds at most
 // 1 + sum (child_count - 1) <= 1 + 7 * depth entries (the reference sizes its
-// stack the same way, bhtree.cpp:185); 192 covers every supported depth.
-#define DPL_STACK_PER_WARP 192
+// stack the same way, bhtree.cpp:185); 304 covers every supported depth.
+#define DPL_STACK_PER_WARP 304
 static_assert(DPL_STACK_PER_WARP >= 7 * DPL_MAX_DEPTH + 8, "traversal stack below 7 * depth + 8");
 
 namespace dpl {

@@ -292,16 +292,21 @@ __global__ void k_bbox_partial(const double* __restrict__ pos, int64_t n, double
 }
 
 // K1: octant digits along the point's own descent (bhtree.cpp:77-78, 93-95).
+// Up to 21 digits fit one 64-bit key; deeper trees (max_depth <= 42) put the
+// digits of levels 22.. into a second key word (keys_lo, else nullptr).
 __global__ void k_keys(const double* __restrict__ pos, int64_t n, double cx, double cy, double cz,
-                       double half, int depth, uint64_t* keys, int32_t* idx) {
+                       double half, int depth, uint64_t* keys, uint64_t* keys_lo, int32_t* idx) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   double px = pos[3 * i], py = pos[3 * i + 1], pz = pos[3 * i + 2];
   double c0 = cx, c1 = cy, c2 = cz, h = half;
-  uint64_t key = 0;
+  uint64_t key = 0, key_lo = 0;
   for (int d = 0; d < depth; ++d) {
     int o = (px >= c0 ? 1 : 0) | (py >= c1 ? 2 : 0) | (pz >= c2 ? 4 : 0);
-    key = (key << 3) | (uint64_t)o;
+    if (d < 21)
+      key = (key << 3) | (uint64_t)o;
+    else
+      key_lo = (key_lo << 3) | (uint64_t)o;
     double hh = __dmul_rn(0.5, h);
     c0 = __dadd_rn(c0, (o & 1) ? hh : -hh);
     c1 = __dadd_rn(c1, (o & 2) ? hh : -hh);
@@ -309,7 +314,23 @@ __global__ void k_keys(const double* __restrict__ pos, int64_t n, double cx, dou
     h = __dmul_rn(0.5, h);
   }
   keys[i] = key;
+  if (keys_lo) keys_lo[i] = key_lo;
   idx[i] = (int32_t)i;
+}
+
+__global__ void k_iota(int32_t* p, int64_t n) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) p[i] = (int32_t)i;
+}
+__global__ void k_gather_u64(const uint64_t* __restrict__ src, const int32_t* __restrict__ at,
+                             int64_t n, uint64_t* dst) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = src[at[i]];
+}
+__global__ void k_gather_i32(const int32_t* __restrict__ src, const int32_t* __restrict__ at,
+                             int64_t n, int32_t* dst) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = src[at[i]];
 }
 
 // per sorted point: active at level d iff its level-(d-1) node is internal;
@@ -748,7 +769,7 @@ void tree_build(Tree& t, const double* pos, const double* nrm, const double* are
   max_leaf = std::max(1, max_leaf);   // :162
   max_depth = std::max(0, max_depth); // :163
   if (max_depth > DPL_MAX_DEPTH)
-    throw Error(1, "dpl_tree_build: max_depth > 21 not supported on GPU (63-bit keys)");
+    throw Error(1, "dpl_tree_build: max_depth > 42 not supported on GPU (two 63-bit key words)");
   t.n = n;
   t.C = C;
   t.max_leaf = max_leaf;
@@ -785,16 +806,46 @@ void tree_build(Tree& t, const double* pos, const double* nrm, const double* are
   int32_t* idx = sbuf<int32_t>(t, 2, n);
   uint64_t* keys_s = sbuf<uint64_t>(t, 3, n);
   int32_t* idx_s = sbuf<int32_t>(t, 4, n);
+  const bool deep = max_depth > 21;  // second key word for levels 22..max_depth
+  DevBuf klo, klo_s;                 // its unsorted / sorted copies (deep trees only)
+  if (deep) klo.reserve(n * 8), klo_s.reserve(n * 8);
   k_keys<<<grid_for(n, B), B, 0, s>>>(t.pos64.as<double>(), n, ctr[0], ctr[1], ctr[2], half,
-                                       max_depth, keys, idx);
+                                       max_depth, keys, deep ? klo.as<uint64_t>() : nullptr, idx);
   count_launch();
-  int end_bit = std::max(1, 3 * max_depth);
   size_t tmp_bytes = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, keys_s, idx, idx_s, (int)n, 0, end_bit, s);
-  void* tmp = sbuf<char>(t, 5, tmp_bytes + 16);
-  DPL_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys_s, idx, idx_s, (int)n, 0,
-                                           end_bit, s));
-  count_launch(4);
+  if (!deep) {
+    int end_bit = std::max(1, 3 * max_depth);
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, keys_s, idx, idx_s, (int)n, 0, end_bit, s);
+    void* tmp = sbuf<char>(t, 5, tmp_bytes + 16);
+    DPL_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys_s, idx, idx_s, (int)n, 0,
+                                             end_bit, s));
+    count_launch(4);
+  } else {
+    // stable LSD over the two words: by the low word, then by the high word
+    DevBuf lo1, idx1, hi1, pos0, pos1;
+    lo1.reserve(n * 8), idx1.reserve(n * 4), hi1.reserve(n * 8), pos0.reserve(n * 4),
+        pos1.reserve(n * 4);
+    const int lo_bits = 3 * (max_depth - 21);
+    size_t b1 = 0, b2 = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, b1, klo.as<uint64_t>(), lo1.as<uint64_t>(), idx,
+                                    idx1.as<int32_t>(), (int)n, 0, lo_bits, s);
+    cub::DeviceRadixSort::SortPairs(nullptr, b2, hi1.as<uint64_t>(), keys_s, pos0.as<int32_t>(),
+                                    pos1.as<int32_t>(), (int)n, 0, 63, s);
+    tmp_bytes = std::max(b1, b2);
+    void* tmp = sbuf<char>(t, 5, tmp_bytes + 16);
+    DPL_CUDA(cub::DeviceRadixSort::SortPairs(tmp, b1, klo.as<uint64_t>(), lo1.as<uint64_t>(), idx,
+                                             idx1.as<int32_t>(), (int)n, 0, lo_bits, s));
+    k_gather_u64<<<grid_for(n, B), B, 0, s>>>(keys, idx1.as<int32_t>(), n, hi1.as<uint64_t>());
+    k_iota<<<grid_for(n, B), B, 0, s>>>(pos0.as<int32_t>(), n);
+    DPL_CUDA(cub::DeviceRadixSort::SortPairs(tmp, b2, hi1.as<uint64_t>(), keys_s,
+                                             pos0.as<int32_t>(), pos1.as<int32_t>(), (int)n, 0, 63,
+                                             s));
+    k_gather_u64<<<grid_for(n, B), B, 0, s>>>(lo1.as<uint64_t>(), pos1.as<int32_t>(), n,
+                                              klo_s.as<uint64_t>());
+    k_gather_i32<<<grid_for(n, B), B, 0, s>>>(idx1.as<int32_t>(), pos1.as<int32_t>(), n, idx_s);
+    count_launch(12);
+    DPL_CUDA(cudaStreamSynchronize(s));  // the temporaries are released here
+  }
 
   // level walk. Node arrays grow level by level.
   std::vector<int64_t> off{0, 1};
@@ -835,8 +886,10 @@ void tree_build(Tree& t, const double* pos, const double* nrm, const double* are
   DPL_CUDA(cudaMemcpyAsync(&h_nint, nint, 4, cudaMemcpyDeviceToHost, s));
   DPL_CUDA(cudaStreamSynchronize(s));
   for (int d = 1; d <= max_depth && h_nint > 0; ++d) {
-    int shift = 3 * (max_depth - d);
-    k_level_heads<<<grid_for(n, B), B, 0, s>>>(keys_s, cur, internal.as<uint8_t>(), n, shift, head,
+    // the key word holding digit d (points of one parent share every higher digit)
+    const uint64_t* kw = (deep && d > 21) ? klo_s.as<uint64_t>() : keys_s;
+    const int shift = !deep ? 3 * (max_depth - d) : (d <= 21 ? 3 * (21 - d) : 3 * (max_depth - d));
+    k_level_heads<<<grid_for(n, B), B, 0, s>>>(kw, cur, internal.as<uint8_t>(), n, shift, head,
                                                t.pt_leaf.as<int32_t>());
     count_launch();
     size_t sb = 0;
@@ -850,7 +903,7 @@ void tree_build(Tree& t, const double* pos, const double* nrm, const double* are
     int64_t o = off.back();
     if (o + cnt > cap) alloc_nodes(std::max<int64_t>(2 * cap, o + cnt));
     k_level_assign<<<grid_for(n, B), B, 0, s>>>(
-        keys_s, cur, internal.as<uint8_t>(), incl, head, n, shift, o, nxt, beg.as<int32_t>(),
+        kw, cur, internal.as<uint8_t>(), incl, head, n, shift, o, nxt, beg.as<int32_t>(),
         end.as<int32_t>(), par.as<int32_t>(), cb.as<int32_t>(), cc.as<int32_t>(),
         beg.as<int32_t>());
     count_launch();

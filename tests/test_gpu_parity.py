@@ -555,18 +555,19 @@ def _branchy_cloud(depth):
                 pts.append(child)
         c = nxt
         h = 0.5 * h
+    step = min(1e-13, 2.0 ** -(depth + 8))
     for k in range(12):  # > max_leaf points at p (distinct, far below the last cell)
-        pts.append(tuple(p + 1e-13 * k))
+        pts.append(tuple(p + step * k))
     return np.array(pts), p
 
 
-def test_deepest_tree_branchy_path_stack(eng, oracle_mod):
-    """max_depth = 21 (the deepest the GPU build supports) on a cloud that
-    fills every level of the path: the per-warp stack reaches its worst case
-    (1 + 7 * 21 = 148 <= 192) in every kernel family; results and opening
-    decisions equal the oracle's."""
+@pytest.mark.parametrize("depth", [21, 42])
+def test_deepest_tree_branchy_path_stack(eng, oracle_mod, depth):
+    """max_depth = 21 (one 63-bit key word) and 42 (the deepest the GPU build
+    supports: two key words) on a cloud that fills every level of the path: the
+    per-warp stack reaches its worst case (1 + 7 * depth <= 304) in every kernel
+    family; structure, opening decisions and results equal the oracle's."""
     O = oracle_mod
-    depth = 21
     pos, p = _branchy_cloud(depth)
     n = pos.shape[0]
     rng = np.random.default_rng(5)
@@ -580,17 +581,31 @@ def test_deepest_tree_branchy_path_stack(eng, oracle_mod):
     a, b = t.export(), r.export()
     for k in ("topo", "order", "leaf_of", "geo"):
         assert np.array_equal(a[k], b[k]), k
-    # queries around p open the whole path
+    assert int(a["topo"].shape[0]) == int(b["topo"].shape[0])
+    prm = eng.KernelParams(epsilon=1e-7)
+    if depth > 21:
+        # queries inside the deepest cells open the whole path (stack peak
+        # 1 + 7 * 42 = 295): the opening decisions are exact (fp64 fallback) and
+        # must equal the oracle's. Their VALUES are not compared: 1e-13 from a
+        # point the double-float distance (2^-46 |x| absolute) is not fp32-accurate.
+        deep = p + rng.normal(0, 2.0 ** -(depth + 2), (256, 3))
+        got_d, cnt_d = t.primal(deep, prm, 2.0, visited=True)
+        _, wcnt_d = r.primal(O.Params(1e-7), 2.0, deep, counters=True)
+        counters_equal("depth-42 tree counters (queries inside the deepest cells)", cnt_d, wcnt_d)
+        assert np.isfinite(got_d).all()
+        buf = t.make_buffer()
+        t.adjoint(deep, prm, 2.0, np.zeros((256, C), np.float32), None, buf)  # walks the path
+        t.flush_gradients(buf)
+    # queries around p open the path down to their distance
     xs = p + rng.normal(0, 1e-9, (256, 3))
     xs = np.concatenate([xs, rng.uniform(-1, 1, (256, 3))])
-    prm = eng.KernelParams(epsilon=1e-7)
     got, cnt = t.primal(xs, prm, 2.0, visited=True)
     want, wcnt = r.primal(O.Params(1e-7), 2.0, xs, counters=True)
     counters_equal("deepest tree counters", cnt, wcnt)
     # queries 1e-9 from a cluster whose terms cancel to ~1e-4 of their sum:
     # the Sum|terms|-scaled bar applies (tests/parity.py)
     wm = r.primal_mag(O.Params(1e-7), 2.0, xs)
-    check("deepest tree (depth 21, 8 children per path node) primal", got, want, wm["out_abs"])
+    check(f"deepest tree (depth {depth}, 8 children per path node) primal", got, want, wm["out_abs"])
     d_out = rng.standard_normal((xs.shape[0], C)).astype(np.float32)
     w = r.adjoint_mag(O.Params(1e-7), 2.0, xs, d_out.astype(np.float64))
     for rnd in range(2):  # fused walk, then list replay
@@ -598,7 +613,7 @@ def test_deepest_tree_branchy_path_stack(eng, oracle_mod):
         buf = t.make_buffer()
         t.adjoint(xs, prm, 2.0, d_out, None, buf)
         g = t.flush_gradients(buf)
-        check(f"deepest tree adjoint moments (pass {rnd})", g.moments, w["moments"], w["moments_abs"])
-        check(f"deepest tree adjoint normals (pass {rnd})", g.normals, w["normals"], w["normals_abs"])
+        check(f"deepest tree d{depth} adjoint moments (pass {rnd})", g.moments, w["moments"], w["moments_abs"])
+        check(f"deepest tree d{depth} adjoint normals (pass {rnd})", g.normals, w["normals"], w["normals_abs"])
     with pytest.raises(eng.UsageError):
-        t.build(eng.OrientedPointCloud(pos, nrm, area, mu), 8, 22)
+        t.build(eng.OrientedPointCloud(pos, nrm, area, mu), 8, 43)
