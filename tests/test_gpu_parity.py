@@ -516,6 +516,41 @@ def test_interaction_list_reuse_is_keyed_on_the_batch(eng, oracle_mod):
     assert close(got, r2.primal(O.Params(0.05), 2.0, xs2))[0] == 0
 
 
+@pytest.mark.parametrize("C", [2, 49])
+def test_list_replay_is_bitwise_the_tree_walk(eng, oracle_mod, C):
+    """K9 records the entries in the reference's pop order (bhtree.cpp:188-234):
+    a primal that replays the lists returns bit-for-bit what the primal that
+    walked the tree itself returned, on a deep clustered cloud (every lane-mask
+    and sibling-order case) and with partial warps."""
+    import torch
+
+    O = oracle_mod
+    rng = np.random.default_rng(77)
+    base = rng.uniform(-1, 1, (40, 3))
+    pos = np.concatenate([base[rng.integers(0, 40, 6000)] + rng.normal(0, 0.02, (6000, 3)),
+                          rng.uniform(-1, 1, (3000, 3))])
+    n = pos.shape[0]
+    nrm = rng.standard_normal((n, 3))
+    nrm /= np.linalg.norm(nrm, axis=1, keepdims=True)
+    area = rng.uniform(0.5, 1.0, n) / n
+    mu = rng.standard_normal((n, C))
+    kinds = np.ones(C, np.uint8)
+    kinds[0] = 0
+    t, r = make(eng, O, pos, nrm, area, mu, kinds, max_leaf=4)
+    q = 5000 + 13  # a partial last warp
+    xs = rng.uniform(-1.3, 1.3, (q, 3))
+    p = eng.KernelParams(epsilon=0.03)
+    dev = torch.from_numpy(xs).cuda()
+    walked = t.primal(dev, p, 2.0).cpu().numpy()  # no lists yet: the kernel walks the tree
+    b = t.make_buffer()
+    t.adjoint(dev, p, 2.0, torch.zeros((q, C), dtype=torch.float32, device="cuda"), None, b)
+    listed = t.primal(dev, p, 2.0).cpu().numpy()   # primal -> adjoint pair seen: lists
+    again = t.primal(dev, p, 2.0).cpu().numpy()
+    assert np.array_equal(walked, listed)
+    assert np.array_equal(listed, again)
+    check(f"list replay C={C} primal", listed, r.primal(O.Params(0.03), 2.0, xs))
+
+
 @pytest.mark.parametrize("C", [1, 2, 3, 17, 33, 49])
 def test_primal_channel_bitwise_equals_primal(eng, oracle_mod, C):
     """primal_channel(c) == primal()[c] bitwise (test_bhtree.cpp:140) for every
