@@ -148,6 +148,35 @@ template <int ROWS, bool KCONTIG>
 __device__ __forceinline__ void stage_b(const float* __restrict__ X, int64_t ld, int nrows, int r0,
                                         int kend, int k0, uint8_t* hi, uint8_t* lo, int tid) {
   constexpr int PER = ROWS * kChunkK / 128;
+  if constexpr (!KCONTIG && ROWS % 32 == 0) {
+    // B[k][n] (n contiguous, the weight-gradient GEMM's activations). A warp
+    // covers 8 consecutive rows x 4 consecutive k per step: 32-byte row segments
+    // of 4 k-lines from global memory, and 32 distinct banks in the swizzled
+    // tile (row r's 16-byte chunk is XORed with r & 7, k & 3 picks the word; 32
+    // consecutive rows at one k would hit every bank four times). Step i of
+    // warp w: row octet w + 4 (i % (ROWS / 32)), k quad i / (ROWS / 32) — all
+    // compile-time but the lane part, so a full tile needs one pointer, one
+    // shared-memory base and immediate offsets.
+    if (r0 + ROWS <= nrows && k0 + kChunkK <= kend) {
+      constexpr int RO = ROWS / 32;  // row-octet steps per k quad
+      const int w = tid >> 5, ln = tid & 31;
+      const int rl = 8 * w + (ln & 7), kl = ln >> 3;
+      const float* src = X + (int64_t)(k0 + kl) * ld + (r0 + rl);
+      const uint32_t ob = (uint32_t)rl * kRowBytes + ((uint32_t)kl << 2);
+      const uint32_t sw = (uint32_t)(ln & 7);
+      float x[PER];
+#pragma unroll
+      for (int i = 0; i < PER; ++i) x[i] = __ldg(src + (int64_t)(4 * (i / RO)) * ld + 32 * (i % RO));
+#pragma unroll
+      for (int i = 0; i < PER; ++i) {
+        const uint32_t o = ob + (uint32_t)(32 * (i % RO)) * kRowBytes + ((((uint32_t)(i / RO)) ^ sw) << 4);
+        const uint32_t h = tf32_hi(x[i]);
+        *reinterpret_cast<uint32_t*>(hi + o) = h;
+        *reinterpret_cast<float*>(lo + o) = x[i] - __uint_as_float(h);
+      }
+      return;
+    }
+  }
 #pragma unroll 8
   for (int i = 0; i < PER; ++i) {
     const int idx = tid + 128 * i;
@@ -155,7 +184,9 @@ __device__ __forceinline__ void stage_b(const float* __restrict__ X, int64_t ld,
     if (KCONTIG) {
       r = idx >> 5, k = idx & 31;  // a warp reads 32 consecutive k of one row
     } else {
-      k = idx / ROWS, r = idx % ROWS;  // a warp reads 32 consecutive rows at one k
+      const int blk = idx >> 5, ln = idx & 31;  // 8 rows x 4 k per warp step (see above)
+      r = (blk % (ROWS / 8)) * 8 + (ln & 7);
+      k = (blk / (ROWS / 8)) * 4 + (ln >> 3);
     }
     const int gr = r0 + r, gk = k0 + k;
     float x = 0.f;
@@ -186,9 +217,15 @@ __device__ __forceinline__ void load_a(const TcGemm& g, int gr, int k0, int kend
       for (int j = 0; j < 32; ++j) x[j] = (gr < g.M && k0 + j < kend) ? __ldg(src + j) : 0.f;
     }
   } else {  // A[k][m]: consecutive threads read consecutive m at each k (coalesced)
+    const int64_t ld = g.lda;
+    const float* src = g.A + (int64_t)k0 * ld + gr;
+    if (gr < g.M && k0 + 32 <= kend) {  // full chunk: one pointer, strided loads
 #pragma unroll
-    for (int j = 0; j < 32; ++j)
-      x[j] = (gr < g.M && k0 + j < kend) ? __ldg(g.A + (int64_t)(k0 + j) * g.lda + gr) : 0.f;
+      for (int j = 0; j < 32; ++j) x[j] = __ldg(src + j * ld);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) x[j] = (gr < g.M && k0 + j < kend) ? __ldg(src + j * ld) : 0.f;
+    }
   }
 }
 
