@@ -73,6 +73,70 @@ __global__ void k_bias_act(float* __restrict__ y, const float* __restrict__ b, i
   }
 }
 
+// Narrow layers (<= 4 output rows: the rgb layer) are HBM-bound, not GEMM-shaped:
+// a 128-row MMA tile would be 97 % padding, so their two backward products run
+// on the FP32 pipe at memory speed.
+// d_in[q][c] = gate(act[q][c]) * sum_r delta[q][r] W[r][c]   (Mlp::backward, radiance.cpp:105-112)
+template <int R>
+__global__ void k_narrow_dx(const float* __restrict__ delta, const float* __restrict__ W,
+                            const float* __restrict__ gate, int64_t q, int cols,
+                            float* __restrict__ out) {
+  const int c4n = cols >> 2;
+  const int64_t n4 = q * c4n;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t qi = i / c4n;
+    const int c4 = (int)(i - qi * c4n);
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const float d = __ldg(delta + qi * R + r);
+      const float4 w = __ldg(reinterpret_cast<const float4*>(W + (size_t)r * cols) + c4);
+      v.x = fmaf(d, w.x, v.x), v.y = fmaf(d, w.y, v.y), v.z = fmaf(d, w.z, v.z), v.w = fmaf(d, w.w, v.w);
+    }
+    if (gate) {
+      const float4 a = __ldg(reinterpret_cast<const float4*>(gate + qi * cols) + c4);
+      v.x = a.x > 0.f ? v.x : 0.f, v.y = a.y > 0.f ? v.y : 0.f;
+      v.z = a.z > 0.f ? v.z : 0.f, v.w = a.w > 0.f ? v.w : 0.f;
+    }
+    reinterpret_cast<float4*>(out + qi * cols)[c4] = v;
+  }
+}
+
+// dW[r][c] += sum_q delta[q][r] in[q][c], db[r] += sum_q delta[q][r] (fp64
+// accumulators, RenderGrads::d_head_w): thread = input column, a block walks
+// a contiguous slice of the samples, fp32 partial sums of at most 1024 samples
+// per fp64 atomic
+template <int R>
+__global__ void k_narrow_dw(const float* __restrict__ delta, const float* __restrict__ in,
+                            int64_t q, int cols, int ldin, double* __restrict__ dW,
+                            double* __restrict__ db) {
+  const int64_t per = (q + gridDim.x - 1) / gridDim.x;
+  const int64_t q0 = (int64_t)blockIdx.x * per, q1 = q0 + per < q ? q0 + per : q;
+  for (int c = threadIdx.x; c < cols; c += blockDim.x) {
+    for (int64_t b0 = q0; b0 < q1; b0 += 1024) {
+      const int64_t b1 = b0 + 1024 < q1 ? b0 + 1024 : q1;
+      float acc[R], sb[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) acc[r] = sb[r] = 0.f;
+      for (int64_t qi = b0; qi < b1; ++qi) {
+        const float x = __ldg(in + qi * ldin + c);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const float d = __ldg(delta + qi * R + r);
+          acc[r] = fmaf(d, x, acc[r]);
+          sb[r] += d;
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        if (acc[r] != 0.f) atomicAdd(dW + (size_t)r * cols + c, (double)acc[r]);
+        if (c == 0 && sb[r] != 0.f) atomicAdd(db + r, (double)sb[r]);
+      }
+    }
+  }
+}
+
 __global__ void k_to_f32(const double* __restrict__ a, int64_t n, float* __restrict__ b) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -198,6 +262,18 @@ void mlp_backward(MlpHead& m, cudaStream_t s, const float* X, int64_t q, const f
   for (int l = L - 1; l >= 0; --l) {
     const int rows = m.sizes[l + 1], cols = m.sizes[l];
     const float* W = m.w32.as<float>() + m.offs[l];
+    // narrow output (the rgb layer): both products at memory speed on the FP32 pipe
+    if (rows == 3 && (cols & 3) == 0) {
+      const int ldin = l == 0 ? m.ldx() : cols;
+      k_narrow_dw<3><<<std::max(1, 148 * 8 / ((cols + 255) / 256)), std::min(256, cols), 0, s>>>(
+          delta, act[l], q, cols, ldin, dw + m.offs[l], dw + m.offs[l] + (size_t)rows * cols);
+      float* out = l == 0 ? dX : dbuf[l & 1];
+      k_narrow_dx<3><<<blocks_for(q * (cols >> 2), 256), 256, 0, s>>>(
+          delta, W, l > 0 ? act[l] : nullptr, q, cols, out);
+      count_launch(2);
+      delta = out;
+      continue;
+    }
     // dW (rows x cols) += delta^T . in over the chunk's samples (split-K, fp64
     // accumulation into RenderGrads::d_head_w)
     TcGemm gw;
