@@ -118,6 +118,11 @@ struct dpl_tape_s {
   double t_near = 0;
   DevBuf rays, ts, deltas, xs, perm, vals, g0, tape, dout, dgrad, sums, morton, head_raw, d_raw,
       mlp_x, mlp_dx;
+  // tiny-MLP head activations of the whole forward, kept for the backward when
+  // HBM allows (else the backward recomputes them chunk by chunk)
+  DevBuf mlp_acts;
+  uint64_t acts_version = 0;  // head version the activations belong to (0: none kept)
+  int64_t acts_q = 0;
   int vstride = 4;  // values per sample in vals (4: direct-rgb head, C: tiny-MLP head)
   bool has_deltas = false;
   bool listed = false;  // render_forward built interaction lists for xs
@@ -1408,6 +1413,23 @@ int dpl_render_forward(dpl_tree_t h, const dpl_kernel_params* params, const dpl_
       const int64_t chunk = std::min<int64_t>(Q, kMlpChunk);
       tape->head_raw.reserve(Q * 12);
       tape->mlp_x.reserve((size_t)chunk * h->head.ldx() * 4);
+      // keep the activations for the backward when they fit beside everything
+      // else (8 GB of headroom); DPL_MLP_RECOMPUTE=1 forces the recompute path
+      static const bool recompute = getenv("DPL_MLP_RECOMPUTE") != nullptr;
+      const size_t aps = h->head.acts_per_sample();
+      const size_t need = (size_t)Q * aps * 4;
+      bool keep = !recompute;
+      if (keep && tape->mlp_acts.bytes < need) {
+        size_t free_b = 0, total_b = 0;
+        DPL_CUDA(cudaMemGetInfo(&free_b, &total_b));
+        keep = free_b + tape->mlp_acts.bytes > need + ((size_t)8 << 30);
+      }
+      tape->acts_version = 0;
+      if (keep) {
+        tape->mlp_acts.reserve(need);
+        tape->acts_version = h->head.version;
+        tape->acts_q = Q;
+      }
       PhaseTimer pt(t, PH_RENDER);
       for (int64_t q0 = 0; q0 < Q; q0 += chunk) {
         const int64_t qc = std::min(chunk, Q - q0);
@@ -1415,7 +1437,8 @@ int dpl_render_forward(dpl_tree_t h, const dpl_kernel_params* params, const dpl_
                    tape->vals.as<float>(), t.C, tape->g0.as<float>(), q0, qc, h->head.K,
                    tape->mlp_x.as<float>(), h->head.ldx());
         mlp_forward(h->head, t.stream, tape->mlp_x.as<float>(), qc,
-                    tape->head_raw.as<float>() + 3 * q0);
+                    tape->head_raw.as<float>() + 3 * q0,
+                    keep ? tape->mlp_acts.as<float>() + (size_t)q0 * aps : nullptr);
       }
     }
     Out<float> o;
@@ -1481,8 +1504,11 @@ int dpl_render_backward(dpl_tree_t h, const dpl_kernel_params* params, const dpl
         mlp_inputs(t.stream, tape->rays.as<double>(), S, tape->xs.as<double>(),
                    tape->vals.as<float>(), t.C, tape->g0.as<float>(), q0, qc, h->head.K,
                    tape->mlp_x.as<float>(), h->head.ldx());
+        const bool kept = tape->acts_version == h->head.version && tape->acts_q == Q;
         mlp_backward(h->head, t.stream, tape->mlp_x.as<float>(), qc,
-                     tape->d_raw.as<float>() + 3 * q0, tape->mlp_dx.as<float>());
+                     tape->d_raw.as<float>() + 3 * q0, tape->mlp_dx.as<float>(),
+                     kept ? tape->mlp_acts.as<float>() + (size_t)q0 * h->head.acts_per_sample()
+                          : nullptr);
         render_mlp_scatter(t.stream, tape->mlp_dx.as<float>(), din, q0, qc, h->head.K,
                            tape->g0.as<float>(), tape->dout.as<float>(), t.C,
                            tape->dgrad.as<float>());

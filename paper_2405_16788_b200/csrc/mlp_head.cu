@@ -201,6 +201,7 @@ void mlp_set(MlpHead& m, const Tree& t, const int* sizes, int n_sizes, const dou
   }
   DPL_CUDA(cudaStreamSynchronize(t.stream));
   m.active = true;
+  ++m.version;
 }
 
 void mlp_inputs(cudaStream_t s, const double* rays, int S, const double* xs, const float* vals,
@@ -226,12 +227,22 @@ static void layer_fwd(MlpHead& m, cudaStream_t s, int l, const float* in, int64_
   tc_gemm(g, m.device, s);
 }
 
-void mlp_forward(MlpHead& m, cudaStream_t s, const float* X, int64_t q, float* raw) {
+void mlp_forward(MlpHead& m, cudaStream_t s, const float* X, int64_t q, float* raw, float* keep) {
   const int L = (int)m.sizes.size() - 1;
   const size_t wide = (size_t)m.widest();
+  const float* in = X;
+  if (keep) {  // layer-major block: act[l] at keep + q * (sizes[1] + .. + sizes[l-1])
+    float* p = keep;
+    for (int l = 0; l < L; ++l) {
+      float* out = l + 1 == L ? raw : p;
+      layer_fwd(m, s, l, in, q, out);
+      in = out;
+      p += (size_t)q * m.sizes[l + 1];
+    }
+    return;
+  }
   m.ws.reserve(2 * (size_t)q * wide * 4);
   float* buf[2] = {m.ws.as<float>(), m.ws.as<float>() + (size_t)q * wide};
-  const float* in = X;
   for (int l = 0; l < L; ++l) {
     float* out = l + 1 == L ? raw : buf[l & 1];
     layer_fwd(m, s, l, in, q, out);
@@ -240,22 +251,25 @@ void mlp_forward(MlpHead& m, cudaStream_t s, const float* X, int64_t q, float* r
 }
 
 void mlp_backward(MlpHead& m, cudaStream_t s, const float* X, int64_t q, const float* d_raw,
-                  float* dX) {
+                  float* dX, const float* kept) {
   const int L = (int)m.sizes.size() - 1;
   // recompute the chunk's activations (Mlp::Tape), then walk back (:95-119)
   size_t acts = 0;
   for (int l = 1; l <= L; ++l) acts += (size_t)m.sizes[l];
   const size_t wide = (size_t)m.widest();
-  m.ws.reserve(((size_t)q * acts + 2 * (size_t)q * wide) * 4);
+  m.ws.reserve(((kept ? 0 : (size_t)q * acts) + 2 * (size_t)q * wide) * 4);
   std::vector<float*> act(L + 1);
   act[0] = const_cast<float*>(X);
-  float* p = m.ws.as<float>();
+  float* p = kept ? const_cast<float*>(kept) : m.ws.as<float>();
   for (int l = 1; l <= L; ++l) {
-    act[l] = p;
+    act[l] = p;  // act[L] (the raw outputs) is never read by the backward
     p += (size_t)q * m.sizes[l];
   }
-  float* dbuf[2] = {p, p + (size_t)q * wide};
-  for (int l = 0; l < L; ++l) layer_fwd(m, s, l, act[l], q, act[l + 1]);
+  float* dbuf[2];
+  dbuf[0] = kept ? m.ws.as<float>() : p;
+  dbuf[1] = dbuf[0] + (size_t)q * wide;
+  if (!kept)
+    for (int l = 0; l < L; ++l) layer_fwd(m, s, l, act[l], q, act[l + 1]);
   // delta: d loss / d (output of layer l), already through that layer's ReLU
   const float* delta = d_raw;
   double* dw = m.dw64.as<double>();

@@ -33,6 +33,13 @@ struct MlpHead {
   // and of W^T (input gradient: B[c][r] = W[r][c]), built by mlp_set
   std::vector<size_t> img_fwd, img_bwd;  // byte offsets into img
   DevBuf img;
+  uint64_t version = 0;  // bumped by mlp_set (kept activations belong to one set of weights)
+  // fp32 activations per sample that a backward needs (outputs of layers 1..L-1... L)
+  size_t acts_per_sample() const {
+    size_t a = 0;
+    for (size_t l = 1; l < sizes.size(); ++l) a += (size_t)sizes[l];
+    return a;
+  }
   ~MlpHead();
   int din() const { return sizes.empty() ? 0 : sizes.front(); }
   // row stride of the input rows X: din rounded up to 4 floats, so the first
@@ -50,11 +57,17 @@ void mlp_set(MlpHead& m, const Tree& t, const int* sizes, int n_sizes, const dou
 void mlp_inputs(cudaStream_t s, const double* rays, int S, const double* xs, const float* vals,
                 int C, const float* g0, int64_t q0, int64_t q, int K, float* X, int ldx);
 
-// raw outputs (q x 3, fp32) of the samples [q0, q0 + q)
-void mlp_forward(MlpHead& m, cudaStream_t s, const float* X, int64_t q, float* raw);
+// raw outputs (q x 3, fp32) of the samples [q0, q0 + q). keep != nullptr: the
+// chunk's activations (q x acts_per_sample floats, layer-major) are written
+// there for the backward — with 180 GB of HBM the render tape can hold them
+// (34 GB for 8.4M samples of a 4 x 256 head) instead of recomputing the forward.
+void mlp_forward(MlpHead& m, cudaStream_t s, const float* X, int64_t q, float* raw,
+                 float* keep = nullptr);
 
-// backward of a chunk: d_raw (q x 3) -> d_X (q x din); accumulates dW (fp64)
+// backward of a chunk: d_raw (q x 3) -> d_X (q x din); accumulates dW (fp64).
+// kept: the activations mlp_forward stored for this chunk, or nullptr to
+// recompute them (Mlp::Tape, radiance.cpp:59-93)
 void mlp_backward(MlpHead& m, cudaStream_t s, const float* X, int64_t q, const float* d_raw,
-                  float* dX);
+                  float* dX, const float* kept = nullptr);
 
 }  // namespace dpl

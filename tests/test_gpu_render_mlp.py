@@ -71,3 +71,18 @@ def test_render_step_tiny_mlp_head(oracle_mod, hidden):
     t.set_mlp_head((), ())
     rgb2, _ = Rn.render_forward(t, p, rs, rays, S)
     assert not np.allclose(rgb2, rgb)
+
+
+def test_recompute_path_of_the_head_backward():
+    """DPL_MLP_RECOMPUTE=1 (the path taken when HBM cannot hold the forward's
+    activations on the render tape): the head backward recomputes them chunk by
+    chunk and passes the same reference-TinyMlp parity tests."""
+    import os
+    import subprocess
+    import sys
+
+    r = subprocess.run(
+        [sys.executable, "-m", "pytest", os.path.abspath(__file__), "-q", "-x", "-m", "gpu",
+         "-k", "tiny_mlp_head"],
+        env=dict(os.environ, DPL_MLP_RECOMPUTE="1"), capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]

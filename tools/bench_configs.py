@@ -249,9 +249,13 @@ def main():
         ms, ph = timed(step, args.steps, tree)
         tree.head_grads()
         Q = R * S
-        flops = 2 * Q * sum(a * b for a, b in zip(sizes[:-1], sizes[1:])) * 4  # fwd, fwd again, 2x bwd
+        # executed GEMM passes: forward, weight gradient, input gradient (+ the forward
+        # again when the backward recomputes the activations, DPL_MLP_RECOMPUTE=1)
+        passes = 4 if os.environ.get("DPL_MLP_RECOMPUTE") else 3
+        flops = 2 * Q * sum(a * b for a, b in zip(sizes[:-1], sizes[1:])) * passes
         res.update(points=c.size, rays=R, samples=S, queries=Q, mlp=sizes, step_ms=ms, phases=ph,
-                   samples_per_s=Q / (ms * 1e-3), mlp_tflops=flops / (ph.get("render", ms) * 1e-3) / 1e12)
+                   samples_per_s=Q / (ms * 1e-3), mlp_tflops=flops / (ph.get("render", ms) * 1e-3) / 1e12,
+                   mlp_gemm_passes=passes)
         sys.path.insert(0, os.path.join(ROOT, "oracle"))
         import oracle as O
 
