@@ -17,8 +17,8 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def _run(code):
-    env = dict(os.environ, DPL_GUARD="1")
+def _run(code, **extra):
+    env = dict(os.environ, DPL_GUARD="1", **extra)
     return subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
                           timeout=600, cwd=ROOT)
 
@@ -28,7 +28,11 @@ def test_guard_detector_positive_control():
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
 
 
-def test_no_out_of_bounds_writes_in_any_kernel_family():
-    r = _run("import runpy; runpy.run_path('tools/sanitize_case.py', run_name='__main__')")
+@pytest.mark.parametrize("extra", [{}, {"DPL_ADJOINT_TMEM": "1"}, {"DPL_MLP_RECOMPUTE": "1"}],
+                         ids=["default", "tmem-adjoint", "mlp-recompute"])
+def test_no_out_of_bounds_writes_in_any_kernel_family(extra):
+    """Default kernels, then the opt-in tcgen05 / TMEM adjoint and the head
+    backward's recompute path under the same guard zones."""
+    r = _run("import runpy; runpy.run_path('tools/sanitize_case.py', run_name='__main__')", **extra)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
     assert "guard zones intact" in r.stdout, r.stdout
