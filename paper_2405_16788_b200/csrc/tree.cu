@@ -499,21 +499,36 @@ __global__ void __launch_bounds__(WARPS * 32)
                     int64_t nodes, const double* __restrict__ pt_pos64,
                     const int32_t* __restrict__ order, const double* __restrict__ area,
                     double* ctr, double* narea, double* nrad, uint8_t* flag, float4* geo) {
-  __shared__ double4 stage[WARPS][32];
+  // batches of 128 points (4 per lane): while lane 0 runs the chains of one
+  // batch (~10 cycles per point, bound by the fp64 add latency), the loads of
+  // the next batch — including the area gather through point_order — are in
+  // flight in every lane's registers
+  constexpr int PER = 4;
+  __shared__ double4 stage[WARPS][32 * PER];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t i = (int64_t)blockIdx.x * WARPS + w;
   if (i >= nodes) return;
   const int32_t b = beg[i], e = end[i];
   if (e - b <= GEO_BIG) return;
   double asum = 0, px = 0, py = 0, pz = 0, mx = 0, my = 0, mz = 0;
-  for (int32_t base = b; base < e; base += 32) {
-    const int32_t j = base + lane;
-    if (j < e)
-      stage[w][lane] = make_double4(area[order[j]], pt_pos64[3 * (size_t)j],
-                                    pt_pos64[3 * (size_t)j + 1], pt_pos64[3 * (size_t)j + 2]);
+  auto fetch = [&](int32_t base, double4 (&v)[PER]) {
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int32_t j = base + 32 * u + lane;
+      if (j < e)
+        v[u] = make_double4(area[order[j]], pt_pos64[3 * (size_t)j], pt_pos64[3 * (size_t)j + 1],
+                            pt_pos64[3 * (size_t)j + 2]);
+    }
+  };
+  double4 nxt[PER];
+  fetch(b, nxt);
+  for (int32_t base = b; base < e; base += 32 * PER) {
+#pragma unroll
+    for (int u = 0; u < PER; ++u) stage[w][32 * u + lane] = nxt[u];
     __syncwarp();
+    if (base + 32 * PER < e) fetch(base + 32 * PER, nxt);
     if (lane == 0) {
-      const int n = min(32, e - base);
+      const int n = min(32 * PER, e - base);
       for (int k = 0; k < n; ++k) {
         const double4 v = stage[w][k];
         asum = __dadd_rn(asum, v.x);
