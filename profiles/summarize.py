@@ -56,6 +56,10 @@ def summarize(path, dst, title):
                 v = f"{fv * sc:.4g}"
             except (ValueError, AttributeError):
                 pass
+            if v == "" and "_op_" in k:
+                # op-count metrics are not in `--set full`; they come from the
+                # separate `--metrics` pass summarised in profiles/r02_opcounts.md
+                continue
             lines.append(f"| {label} (`{k}`) | {v} |")
         stalls = sorted(((float(d[i]), h) for i, h in enumerate(hdr)
                          if h.startswith("smsp__average_warps_issue_stalled_")
