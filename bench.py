@@ -22,7 +22,8 @@ N=1) exceed the 126 MB L2, so no explicit flush.
 `python bench.py --gpus N` without WORLD_SIZE in the environment launches N
 ranks itself (torch.distributed.run on 127.0.0.1); under torchrun it is one
 rank. --config 2 selects BASELINE config 2 (N=1e6, Q=4e6) instead; at N=1 the
-config-4 line also carries config 2 under "extra".
+config-4 line also carries config 2 (forward + adjoint) and config 5 (the full
+render + Adam step) under "extra".
 
 --impl reference: the reference's own CPU path (oracle/_ref, compiled from the
 reference's sources unmodified) on the box's host cores, on a fixed 1M-query
@@ -61,7 +62,7 @@ def parse():
     ap.add_argument("--chunks", type=int, default=8, help="point chunks of the overlapped all-reduce")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--no-extra", action="store_true", help="skip the config-2 extra line")
+    ap.add_argument("--no-extra", action="store_true", help="skip the config-2 / config-5 extra lines")
     ap.add_argument("--ref-subset", type=int, default=1_000_000,
                     help="reference arm: queries of the fixed subset covered by the timed steps")
     ap.add_argument("--ref-workers", type=int, default=4,
@@ -595,6 +596,11 @@ def run_ours(args):
             line["extra"] = {"config2": extra_config2(args, dev, local, peak32)}
         except Exception as e:
             line["extra"] = {"config2": {"error": str(e)}}
+        try:
+            del tree, wl
+            line["extra"]["config5"] = extra_config5(args, dev, local)
+        except Exception as e:
+            line["extra"]["config5"] = {"error": str(e)}
     emit(line)
     if dist is not None:
         dist.destroy_process_group()
@@ -618,6 +624,83 @@ def extra_config2(args, dev, local, peak32):
             "ms_per_step": m["ms"], "phase_ms": m["phases"], "roofline_frac": roof["frac"],
             "roofline_achieved_tflops": roof["achieved"], "gpu_launches": m["launches"],
             "clocks": m["clocks"]}
+
+
+def extra_config5(args, dev, local):
+    """BASELINE config 5 on the same GPU, N=1: the full differentiable render
+    step (render forward -> L2 d_rgb -> render backward / adjoint -> flush ->
+    Adam on beta, alpha, n -> update_moments) on N=4e6 points, C=49, 1,048,576
+    rays x 192 samples, direct-rgb head. Timed with CUDA events on the tree's
+    stream; rays and targets device-resident (tools/bench_configs.py --config 5
+    is the same step with its roofline and CPU baseline)."""
+    import numpy as np
+    import torch
+
+    import paper_2405_16788_b200 as P
+    from paper_2405_16788_b200 import bhtree as B
+    from paper_2405_16788_b200 import renderer as Rn
+    from paper_2405_16788_b200 import workloads as W
+
+    n = max(64, int(4_000_000 * args.scale))
+    pos, nrm_, area, rng = W.shapes_cloud(n, 5)
+    mu = rng.standard_normal((n, 49))
+    mu[:, 0] = 1.0  # geometry moment 1: the shapes' winding-number field (opaque surfaces)
+    c = W.cloud(pos, nrm_, area, mu)
+    kinds = np.ones(49, np.uint8)
+    kinds[0] = 0
+    rays = W.camera_rays(64, 1024, max(1, int(16384 * args.scale)), seed=2)
+    S = 192
+    eps = B.default_epsilon(c)
+    tree = P.DipoleTree(local, stream=torch.cuda.current_stream())
+    tree.build(c)
+    tree.set_channel_kernels(kinds)
+    R = rays.shape[0]
+    rays_d = torch.from_numpy(rays).to(dev)
+    target = torch.rand((R, 3), device=dev, generator=torch.Generator(device=dev).manual_seed(4))
+    p = P.KernelParams(epsilon=eps)
+    rs = Rn.RenderSettings(t_near=2.0, t_far=6.0, seed=3)
+    buf = tree.make_buffer()
+    mom = torch.empty((c.size, c.channels), device=dev)
+    nrm = torch.empty((c.size, 3), device=dev)
+    opt = B.PointAdam(tree, lr=1e-2)
+    tape = Rn.Tape()
+    scale = 2.0 / (3.0 * R)
+
+    def step():
+        rgb, _ = Rn.render_forward(tree, p, rs, rays_d, S, tape=tape)
+        d_rgb = (scale * (rgb - target)).float()
+        Rn.render_backward(tree, p, rs, tape, d_rgb, buf)
+        opt.step(tree.flush_gradients(buf, out=(mom, nrm)))
+
+    for _ in range(max(3, args.warmup)):  # the list policy settles after one step
+        step()
+    torch.cuda.synchronize()
+    B.profile_read(tree)
+    B.profile_enable(tree, True)
+    l0 = B.launch_count() if hasattr(B, "launch_count") else None
+    k = max(3, min(args.steps, 5))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(k):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / k
+    prof = B.profile_read(tree)
+    B.profile_enable(tree, False)
+    Q = R * S
+    out = {"workload": f"config5: N={n} shapes cloud, C=49, {R} rays x {S} samples = {Q} queries "
+                       "per step; render forward + composite + L2 adjoint + flush + Adam(beta, "
+                       "alpha, n) + update_moments; direct-rgb head",
+           "value": Q / (ms * 1e-3), "unit": "ray samples/s", "ms_per_step": ms, "steps": k,
+           "phase_ms": {key: v[0] / k for key, v in prof.items() if v[1]},
+           "channels_computed": "0..3 of 49: the direct-rgb head reads only these "
+                                "(radiance.cpp:133-145); the reference interpolates all 49 "
+                                "(renderer.cpp:125), the other 45 never reach the output and "
+                                "receive exactly zero adjoint"}
+    if l0 is not None:
+        out["gpu_launches"] = B.launch_count() - l0
+    return out
 
 
 # ------------------------------------------------------------------ launcher
