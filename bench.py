@@ -22,8 +22,8 @@ N=1) exceed the 126 MB L2, so no explicit flush.
 `python bench.py --gpus N` without WORLD_SIZE in the environment launches N
 ranks itself (torch.distributed.run on 127.0.0.1); under torchrun it is one
 rank. --config 2 selects BASELINE config 2 (N=1e6, Q=4e6) instead; at N=1 the
-config-4 line also carries config 2 (forward + adjoint) and config 5 (the full
-render + Adam step) under "extra".
+config-4 line also carries configs 1, 2, 3 and 5 under "extra" (every BASELINE
+configuration in one driver-run line).
 
 --impl reference: the reference's own CPU path (oracle/_ref, compiled from the
 reference's sources unmodified) on the box's host cores, on a fixed 1M-query
@@ -596,11 +596,13 @@ def run_ours(args):
             line["extra"] = {"config2": extra_config2(args, dev, local, peak32)}
         except Exception as e:
             line["extra"] = {"config2": {"error": str(e)}}
-        try:
-            del tree, wl
-            line["extra"]["config5"] = extra_config5(args, dev, local)
-        except Exception as e:
-            line["extra"]["config5"] = {"error": str(e)}
+        del tree, wl
+        for name, fn in (("config1", extra_config1), ("config3", lambda a, d, l: extra_render(a, d, l, 3)),
+                         ("config5", lambda a, d, l: extra_render(a, d, l, 5))):
+            try:
+                line["extra"][name] = fn(args, dev, local)
+            except Exception as e:
+                line["extra"][name] = {"error": str(e)}
     emit(line)
     if dist is not None:
         dist.destroy_process_group()
@@ -626,13 +628,48 @@ def extra_config2(args, dev, local, peak32):
             "clocks": m["clocks"]}
 
 
-def extra_config5(args, dev, local):
-    """BASELINE config 5 on the same GPU, N=1: the full differentiable render
-    step (render forward -> L2 d_rgb -> render backward / adjoint -> flush ->
-    Adam on beta, alpha, n -> update_moments) on N=4e6 points, C=49, 1,048,576
-    rays x 192 samples, direct-rgb head. Timed with CUDA events on the tree's
-    stream; rays and targets device-resident (tools/bench_configs.py --config 5
-    is the same step with its roofline and CPU baseline)."""
+def extra_config1(args, dev, local):
+    """BASELINE config 1 on the same GPU: forward-only, N=1e5 sphere, C=2,
+    Q=1e6 uniform queries (two alternating batches: no list reuse), CUDA events
+    on the tree's stream, inputs device-resident."""
+    import torch
+
+    import paper_2405_16788_b200 as P
+    from paper_2405_16788_b200 import workloads as W
+
+    w = W.config1(scale=args.scale)
+    c = w["cloud"]
+    tree = P.DipoleTree(local, stream=torch.cuda.current_stream())
+    tree.build(c)
+    tree.set_channel_kernels(w["kinds"])
+    Q, C = w["xs"].shape[0], c.channels
+    xs_b = [torch.from_numpy(w["xs"]).to(dev), torch.from_numpy(W.step_queries(w, 0, 1)).to(dev)]
+    out = torch.empty((Q, C), device=dev)
+    p = P.KernelParams(epsilon=W.epsilon_for("config1", args.scale))
+    for i in range(max(3, args.warmup)):
+        tree.primal(xs_b[i % 2], p, BETA, out=out)
+    k = max(10, args.steps)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(k):
+        tree.primal(xs_b[i % 2], p, BETA, out=out)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / k
+    return {"workload": f"config1: N={c.size} sphere, C={C}, Q={Q} uniform queries in [-1.5,1.5]^3, "
+                        "forward only (query sort + traversal)",
+            "value": Q / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms, "steps": k}
+
+
+def extra_render(args, dev, local, config):
+    """BASELINE configs 3 and 5 on the same GPU, N=1. Config 3: render step on
+    the config-1 cloud (C=4), 65,536 rays x 128 samples: render forward -> L2
+    d_rgb -> render backward / adjoint -> flush. Config 5: the full
+    differentiable step on N=4e6 points, C=49, 1,048,576 rays x 192 samples, also
+    Adam on beta, alpha, n and update_moments. Direct-rgb head. Timed with CUDA
+    events on the tree's stream; rays and targets device-resident
+    (tools/bench_configs.py --config 3|5 is the same step with its roofline and
+    CPU baseline)."""
     import numpy as np
     import torch
 
@@ -641,15 +678,21 @@ def extra_config5(args, dev, local):
     from paper_2405_16788_b200 import renderer as Rn
     from paper_2405_16788_b200 import workloads as W
 
-    n = max(64, int(4_000_000 * args.scale))
-    pos, nrm_, area, rng = W.shapes_cloud(n, 5)
-    mu = rng.standard_normal((n, 49))
-    mu[:, 0] = 1.0  # geometry moment 1: the shapes' winding-number field (opaque surfaces)
-    c = W.cloud(pos, nrm_, area, mu)
-    kinds = np.ones(49, np.uint8)
-    kinds[0] = 0
-    rays = W.camera_rays(64, 1024, max(1, int(16384 * args.scale)), seed=2)
-    S = 192
+    if config == 3:
+        w = W.config3(scale=args.scale)
+        c, rays, S, kinds = w["cloud"], w["rays"], w["S"], w["kinds"]
+        what = "config-1 sphere cloud"
+    else:
+        n = max(64, int(4_000_000 * args.scale))
+        pos, nrm_, area, rng = W.shapes_cloud(n, 5)
+        mu = rng.standard_normal((n, 49))
+        mu[:, 0] = 1.0  # geometry moment 1: the shapes' winding-number field (opaque surfaces)
+        c = W.cloud(pos, nrm_, area, mu)
+        kinds = np.ones(49, np.uint8)
+        kinds[0] = 0
+        rays = W.camera_rays(64, 1024, max(1, int(16384 * args.scale)), seed=2)
+        S = 192
+        what = "shapes cloud"
     eps = B.default_epsilon(c)
     tree = P.DipoleTree(local, stream=torch.cuda.current_stream())
     tree.build(c)
@@ -662,7 +705,7 @@ def extra_config5(args, dev, local):
     buf = tree.make_buffer()
     mom = torch.empty((c.size, c.channels), device=dev)
     nrm = torch.empty((c.size, 3), device=dev)
-    opt = B.PointAdam(tree, lr=1e-2)
+    opt = B.PointAdam(tree, lr=1e-2) if config == 5 else None
     tape = Rn.Tape()
     scale = 2.0 / (3.0 * R)
 
@@ -670,15 +713,17 @@ def extra_config5(args, dev, local):
         rgb, _ = Rn.render_forward(tree, p, rs, rays_d, S, tape=tape)
         d_rgb = (scale * (rgb - target)).float()
         Rn.render_backward(tree, p, rs, tape, d_rgb, buf)
-        opt.step(tree.flush_gradients(buf, out=(mom, nrm)))
+        g = tree.flush_gradients(buf, out=(mom, nrm))
+        if opt is not None:
+            opt.step(g)
 
     for _ in range(max(3, args.warmup)):  # the list policy settles after one step
         step()
     torch.cuda.synchronize()
     B.profile_read(tree)
     B.profile_enable(tree, True)
-    l0 = B.launch_count() if hasattr(B, "launch_count") else None
-    k = max(3, min(args.steps, 5))
+    l0 = B.launch_count()
+    k = max(3, min(args.steps, 5)) if config == 5 else max(10, args.steps)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(k):
@@ -689,18 +734,17 @@ def extra_config5(args, dev, local):
     prof = B.profile_read(tree)
     B.profile_enable(tree, False)
     Q = R * S
-    out = {"workload": f"config5: N={n} shapes cloud, C=49, {R} rays x {S} samples = {Q} queries "
-                       "per step; render forward + composite + L2 adjoint + flush + Adam(beta, "
-                       "alpha, n) + update_moments; direct-rgb head",
-           "value": Q / (ms * 1e-3), "unit": "ray samples/s", "ms_per_step": ms, "steps": k,
-           "phase_ms": {key: v[0] / k for key, v in prof.items() if v[1]},
-           "channels_computed": "0..3 of 49: the direct-rgb head reads only these "
-                                "(radiance.cpp:133-145); the reference interpolates all 49 "
-                                "(renderer.cpp:125), the other 45 never reach the output and "
-                                "receive exactly zero adjoint"}
-    if l0 is not None:
-        out["gpu_launches"] = B.launch_count() - l0
-    return out
+    tail = (" + Adam(beta, alpha, n) + update_moments" if config == 5 else "")
+    return {"workload": f"config{config}: N={c.size} {what}, C={c.channels}, {R} rays x {S} samples "
+                        f"= {Q} queries per step; render forward + composite + L2 adjoint + flush"
+                        f"{tail}; direct-rgb head",
+            "value": Q / (ms * 1e-3), "unit": "ray samples/s", "ms_per_step": ms, "steps": k,
+            "phase_ms": {key: v[0] / k for key, v in prof.items() if v[1]},
+            "gpu_launches": B.launch_count() - l0,
+            "channels_computed": f"0..3 of {c.channels}: the direct-rgb head reads only these "
+                                 "(radiance.cpp:133-145); the reference interpolates every channel "
+                                 "(renderer.cpp:125), the others never reach the output and "
+                                 "receive exactly zero adjoint"}
 
 
 # ------------------------------------------------------------------ launcher
