@@ -312,7 +312,11 @@ def run_reference(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * timed / K, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": f"synthetic (seeded config-{wl.config} generator)",
-        "config": {"workload": wl.desc, "subset_queries": sub, "queries_per_timed_step": s},
+        # the same workload keys as the GPU arm's line; what was sampled is in "sample"
+        "config": {"workload": wl.desc, "points": int(wl.cloud.size), "queries": int(Q),
+                   "channels": int(C), "epsilon": wl.eps, "nodes": int(tree.node_count())},
+        "sample": {"subset_queries": sub, "queries_per_timed_step": s, "timed_steps": K,
+                   "adjoint_workers": workers, "threads": cores},
         "ms_per_step_note": "measured: the timed region (K sample steps + the flush) / K",
         "extrapolated_full_step_ms": 1e3 * full,
         "forward_qps": sub / t_f, "adjoint_qps": sub / t_a,

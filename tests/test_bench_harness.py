@@ -51,5 +51,6 @@ def test_reference_arm_runs_on_cpu(tmp_path, oracle_mod):
     assert r.returncode == 0, r.stderr[-2000:]
     line = json.loads(r.stdout.strip().splitlines()[-1])
     assert line["impl"] == "reference" and line["value"] > 0
-    assert line["config"]["subset_queries"] == 2000
+    assert line["sample"]["subset_queries"] == 2000
+    assert {"workload", "points", "queries", "channels", "epsilon"} <= set(line["config"])
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["cpu_baseline"]["kind"] == "reference"
