@@ -600,13 +600,23 @@ def run_ours(args):
             line["extra"] = {"config2": extra_config2(args, dev, local, peak32)}
         except Exception as e:
             line["extra"] = {"config2": {"error": str(e)}}
-        del tree, wl
+        # release the config-4 tree (its staging buffers), the gradient buffer that
+        # references it and torch's cached blocks before the larger extras
+        import gc
+
+        tree = wl = c = None
+        buf = rows = mom_h = nrm_h = None  # noqa: F841 (set in the e2e leg)
+        gc.collect()
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
         for name, fn in (("config1", extra_config1), ("config3", lambda a, d, l: extra_render(a, d, l, 3)),
                          ("config5", lambda a, d, l: extra_render(a, d, l, 5))):
             try:
                 line["extra"][name] = fn(args, dev, local)
             except Exception as e:
                 line["extra"][name] = {"error": str(e)}
+            gc.collect()
+            torch.cuda.empty_cache()
     emit(line)
     if dist is not None:
         dist.destroy_process_group()

@@ -56,6 +56,9 @@ def test_config2_full_size_properties(oracle_mod):
     idx = np.random.default_rng(3).choice(Q, 1500, replace=False)
     want, wcnt = r.primal(O.Params(eps), 2.0, w["xs"][idx], counters=True)
     check("config2 full size forward, 1500-query subset of the 4M batch", out[idx], want)
+    # and every output of the whole 4M-query batch (list replay pass)
+    check("config2 full size forward, all 4M queries x 49 channels", out,
+          r.primal(O.Params(eps), 2.0, w["xs"]))
     _, cnt = t.primal(xs[torch.from_numpy(idx).cuda()], p, 2.0, visited=True)
     counters_equal("config2 full size subset counters", cnt.cpu().numpy(), wcnt)
 
