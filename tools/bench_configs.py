@@ -1,5 +1,6 @@
 #!/usr/bin/env python
-"""Per-configuration timings beyond bench.py's headline (config 2).
+"""Per-configuration timings with rooflines and CPU baselines (bench.py carries the
+config-4 headline and plain timings of configs 1, 2, 3, 5 under "extra").
 
     python tools/bench_configs.py --config 1|3|4|5 [--steps K] [--scale s]
 
