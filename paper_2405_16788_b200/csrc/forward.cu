@@ -444,6 +444,8 @@ static void launch_one(const Tree& t, const KParams& kp, FwdArgs& a, int d0, int
 void forward_launch(const Tree& t, const KParams& kp, FwdArgs a) {
   static const bool single_phase = getenv("DPL_FORWARD_SINGLE_PHASE") != nullptr;
   static const bool no_tc = getenv("DPL_FORWARD_NO_TC") != nullptr;
+  // accumulator in tensor memory (forward_tm.cu), opt-in with DPL_FORWARD_TMEM=1
+  if (!single_phase && !no_tc && forward_tmem_enabled() && forward_tm_launch(t, kp, a)) return;
   if (!single_phase && !no_tc && forward_tc_launch(t, kp, a)) return;
   if (!single_phase && forward2_launch(t, kp, a)) return;
   const int Cd = a.only_dip >= 0 ? 1 : (a.only_rad >= 0 ? 0 : t.Cd);

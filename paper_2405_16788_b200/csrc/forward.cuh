@@ -32,6 +32,8 @@ void forward_launch(const Tree& t, const KParams& kp, FwdArgs a);
 bool forward2_launch(const Tree& t, const KParams& kp, const FwdArgs& a);
 // tensor-core (3xTF32 mma.sync) values-only kernel (forward_tc.cu)
 bool forward_tc_launch(const Tree& t, const KParams& kp, const FwdArgs& a);
+// tcgen05 / TMEM values-only kernel for one Dipole + 48 Radial slots (forward_tm.cu)
+bool forward_tm_launch(const Tree& t, const KParams& kp, const FwdArgs& a);
 void morton_order(Tree& t, const double* xs_dev, int64_t q, int32_t* perm_out, DevBuf& ws);
 
 }  // namespace dpl

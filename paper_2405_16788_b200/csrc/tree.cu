@@ -226,6 +226,10 @@ TreeView Tree::view() const {
   v.pt_geo = pt_geo.as<float4>();
   v.pt_row = pt_row.as<float4>();
   v.pt_rec = pt_rec.as<PtRec>();
+  v.node_row_hi = node_row_hi.as<float4>();
+  v.node_row_lo = node_row_lo.as<float4>();
+  v.pt_row_hi = pt_row_hi.as<float4>();
+  v.pt_row_lo = pt_row_lo.as<float4>();
   v.pt_nrm = pt_nrm.as<float>();
   v.pt_mu = pt_mud.as<float>();
   v.P = PR;
@@ -687,6 +691,23 @@ __global__ void k_moments_normalise(int64_t nodes, int Cd, int Cr, int F4,
 
 // ---------------------------------------------------------------- host
 
+bool forward_tmem_enabled() {
+  static const bool v = getenv("DPL_FORWARD_TMEM") != nullptr;
+  return v;
+}
+
+// hi = v truncated to tf32 (10 mantissa bits), lo = v - hi (exact)
+__global__ void k_rows_split(const float* __restrict__ rows, float* __restrict__ hi,
+                             float* __restrict__ lo, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float v = rows[i];
+    const float h = __uint_as_float(__float_as_uint(v) & 0xffffe000u);
+    hi[i] = h;
+    lo[i] = v - h;
+  }
+}
+
 template <typename T>
 static T* sbuf(Tree& t, int slot, size_t count) {
   t.scratch[slot].reserve(count * sizeof(T));
@@ -731,6 +752,18 @@ void tree_compute_moments(Tree& t) {
       t.nodes, t.Cd, t.Cr, t.F4, t.node_area64.as<double>(), t.node_sumv.as<double>(),
       t.node_sums.as<double>(), t.node_row.as<float4>());
   count_launch();
+  if (forward_tmem_enabled()) {
+    const size_t nn = (size_t)(t.nodes + 1) * t.F4, np = (size_t)(t.n + 1) * t.F4;
+    t.node_row_hi.reserve(sizeof(float4) * nn);
+    t.node_row_lo.reserve(sizeof(float4) * nn);
+    t.pt_row_hi.reserve(sizeof(float4) * np);
+    t.pt_row_lo.reserve(sizeof(float4) * np);
+    k_rows_split<<<8 * 148, 256, 0, t.stream>>>(t.node_row.as<float>(), t.node_row_hi.as<float>(),
+                                                 t.node_row_lo.as<float>(), (int64_t)t.nodes * t.F4 * 4);
+    k_rows_split<<<8 * 148, 256, 0, t.stream>>>(t.pt_row.as<float>(), t.pt_row_hi.as<float>(),
+                                                 t.pt_row_lo.as<float>(), (int64_t)t.n * t.F4 * 4);
+    count_launch(2);
+  }
   DPL_CUDA(cudaGetLastError());
 }
 

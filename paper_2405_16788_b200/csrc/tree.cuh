@@ -60,6 +60,8 @@ struct Tree {
   DevBuf node_row, node_rec;  // fp32 payload rows (nodes x F4 float4), packed node records
   // sorted point data
   DevBuf pt_pos64, pt_geo, pt_row, pt_nrm, pt_mud, pt_rec;
+  // tf32 hi / lo split of node_row / pt_row for the TMEM forward (DPL_FORWARD_TMEM)
+  DevBuf node_row_hi, node_row_lo, pt_row_hi, pt_row_lo;
   DevBuf chmap;  // int32 [Cd dip ids | Cr rad ids]
   // scratch
   DevBuf scratch[8];
@@ -83,6 +85,9 @@ void tree_build(Tree& t, const double* pos, const double* nrm, const double* are
 void tree_update_points(Tree& t, const double* pos, const double* nrm, const double* area,
                         const double* mu);  // device pointers, original order
 void tree_compute_moments(Tree& t);
+// DPL_FORWARD_TMEM set: the tensor-memory forward (forward_tm.cu) is selected and
+// tree_compute_moments also writes the split rows
+bool forward_tmem_enabled();
 void tree_refresh_sorted_positions(Tree& t);  // pt_pos64 / pt_geo from pos64 / area64
 void tree_set_kinds(Tree& t, const uint8_t* kinds);
 void tree_ensure_thresholds(Tree& t, double beta);

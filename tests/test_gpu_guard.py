@@ -28,10 +28,11 @@ def test_guard_detector_positive_control():
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
 
 
-@pytest.mark.parametrize("extra", [{}, {"DPL_ADJOINT_TMEM": "1"}, {"DPL_MLP_RECOMPUTE": "1"}],
-                         ids=["default", "tmem-adjoint", "mlp-recompute"])
+@pytest.mark.parametrize("extra", [{}, {"DPL_ADJOINT_TMEM": "1"}, {"DPL_FORWARD_TMEM": "1"},
+                                   {"DPL_MLP_RECOMPUTE": "1"}],
+                         ids=["default", "tmem-adjoint", "tmem-forward", "mlp-recompute"])
 def test_no_out_of_bounds_writes_in_any_kernel_family(extra):
-    """Default kernels, then the opt-in tcgen05 / TMEM adjoint and the head
+    """Default kernels, then the opt-in tcgen05 / TMEM adjoint and forward and the head
     backward's recompute path under the same guard zones."""
     r = _run("import runpy; runpy.run_path('tools/sanitize_case.py', run_name='__main__')", **extra)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]

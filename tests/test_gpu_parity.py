@@ -449,7 +449,7 @@ def test_host_pointer_pipeline_matches_device_path(eng, oracle_mod):
 
 
 @pytest.mark.parametrize("env", ["DPL_ADJOINT_TMEM", "DPL_ADJOINT_TC", "DPL_ADJOINT_SINGLE_PHASE",
-                                 "DPL_FORWARD_NO_TC", "DPL_FORWARD_SINGLE_PHASE",
+                                 "DPL_FORWARD_TMEM", "DPL_FORWARD_NO_TC", "DPL_FORWARD_SINGLE_PHASE",
                                  "DPL_NO_ILIST", "DPL_ILIST_POOL", "DPL_ILIST_ALWAYS"])
 def test_alternate_kernel_paths(env):
     """The opt-in / fallback kernels (selected once per process from the

@@ -8,16 +8,18 @@
 // per entry, a warp's 32 weights are contiguous per entry), so it needs the
 // instruction descriptor's a_major / b_major = MN.
 //
-// Result on B200 (driver 580.159, CUDA 12.9): MODE 2 (both operands K-major,
-// SWIZZLE_128B, the layout tc_gemm.cu / adjoint_tm.cu use) reproduces the fp64
-// reference exactly (0 of 2048 mismatches, and confirms the M = 64 row -> TMEM
-// lane map 32 (m / 16) + m % 16); every MN-major variant — no-swizzle with either
-// LBO / SBO assignment (MODE 0, 1), SWIZZLE_128B atoms (MODE 3, 4), and even A
-// K-major with only B MN-major (MODE 5) — leaves the accumulator all zero,
-// without an error. With K-major operands the node rows would need a transposing
-// 4-byte scatter per entry (bank-conflicted, 6 warp instructions) instead of one
-// 16-byte cp.async per chunk, which removes the gain; the forward stays on
-// mma.sync.
+// Result on B200 (driver 580.159, CUDA 12.9), D checked against fp64:
+//   MODE 2  both operands K-major, SWIZZLE_128B (the layout tc_gemm.cu and
+//           adjoint_tm.cu use): exact; confirms the M = 64 row -> TMEM lane map
+//           32 (m / 16) + m % 16.
+//   MODE 0, 1  MN-major, no swizzle (either LBO / SBO assignment): accumulator
+//           all zero, no error.
+//   MODE 3, 4  MN-major, SWIZZLE_128B atoms (8 k-rows x 128 B): all zero.
+//   MODE 5  A K-major, only B MN-major SWIZZLE_128B: all zero.
+//   MODE 7  MN-major, SWIZZLE_128B_BASE32B (layout type 1: atoms of 4 k-rows x
+//           128 B, the 32-byte chunk c of row k stored at c ^ (k & 3); LBO = MN
+//           atom stride, SBO = stride of the 4-row k groups): EXACT. This is the
+//           layout forward_tm.cu uses. MODE 8 (LBO / SBO swapped) faults.
 #include <cstdio>
 #include <cstdlib>
 #include <cmath>
@@ -172,6 +174,66 @@ __global__ void kmn128(const float* A, const float* B, float* D, int variant) {
   __syncthreads();
   if (w == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(32));
 }
+__global__ void kmn32(const float* A, const float* B, float* D, int variant) {
+  __shared__ __align__(1024) uint8_t sa[KT][2048], sb[KT][1024];
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ uint32_t slot;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  for (int i = tid; i < KT * K * M; i += blockDim.x) {
+    int kt = i / (K * M), kk = (i / M) % K, m = i % M;
+    int atom = m / 32, c = (m % 32) / 8;
+    *reinterpret_cast<float*>(&sa[kt][atom * 1024 + (kk / 4) * 512 + (kk % 4) * 128 + ((c ^ (kk & 3)) << 5) + (m % 8) * 4]) = A[(kt * K + kk) * M + m];
+  }
+  for (int i = tid; i < KT * K * N; i += blockDim.x) {
+    int kt = i / (K * N), kk = (i / N) % K, n = i % N;
+    int c = n / 8;
+    *reinterpret_cast<float*>(&sb[kt][(kk / 4) * 512 + (kk % 4) * 128 + ((c ^ (kk & 3)) << 5) + (n % 8) * 4]) = B[(kt * K + kk) * N + n];
+  }
+  if (w == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_addr(&slot)), "r"(32));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_addr(&bar)), "r"(1));
+    asm volatile("fence.mbarrier_init.release.cluster;\n");
+  }
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n");
+  const uint32_t tmem = slot;
+  if (tid == 0) {
+    for (int kt = 0; kt < KT; ++kt) {
+      uint32_t lbo = 1024, sbo = 512;
+      if (variant == 1) { lbo = 512; sbo = 1024; }
+      uint64_t da = desc_mn128(smem_addr(sa[kt]), lbo, sbo), db = desc_mn128(smem_addr(sb[kt]), lbo, sbo);
+      da = (da & ~((uint64_t)7 << 61)) | ((uint64_t)1 << 61);
+      db = (db & ~((uint64_t)7 << 61)) | ((uint64_t)1 << 61);
+      uint32_t acc = kt != 0;
+      asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                   "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem), "l"(da), "l"(db),
+                   "r"(idesc(M, N, 1, 1)), "r"(acc) : "memory");
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_addr(&bar)) : "memory");
+  }
+  uint32_t done = 0;
+  while (!done)
+    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}\n" : "=r"(done) : "r"(smem_addr(&bar)), "r"(0) : "memory");
+  asm volatile("tcgen05.fence::after_thread_sync;\n");
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]),
+        "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+        "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]),
+        "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(tmem + ((uint32_t)(32 * w) << 16)));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+  for (int c = 0; c < 32; ++c) D[(32 * w + lane) * 32 + c] = __uint_as_float(r[c]);
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  if (w == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(32));
+}
 __global__ void k(const float* A, const float* B, float* D, int swap_lbo_sbo) {
   // A[kk][m] (MN-major: m contiguous), B[kk][n]
   __shared__ __align__(128) uint8_t sa[KT][16 * CS], sb[KT][8 * CS];
@@ -241,7 +303,7 @@ int main(int argc, char** argv) {
   cudaMalloc(&dA, sizeof hA); cudaMalloc(&dB, sizeof hB); cudaMalloc(&dD, sizeof hD);
   cudaMemcpy(dA, hA, sizeof hA, cudaMemcpyHostToDevice); cudaMemcpy(dB, hB, sizeof hB, cudaMemcpyHostToDevice);
   cudaMemset(dD, 0, sizeof hD);
-  if (swap == 3 || swap == 4) kmn128<<<1, 128>>>(dA, dB, dD, swap - 3); else if (swap == 2 || swap == 5) kref<<<1, 128>>>(dA, dB, dD, swap == 5); else k<<<1, 128>>>(dA, dB, dD, swap);
+  if (swap == 7 || swap == 8) kmn32<<<1, 128>>>(dA, dB, dD, swap - 7); else if (swap == 3 || swap == 4) kmn128<<<1, 128>>>(dA, dB, dD, swap - 3); else if (swap == 2 || swap == 5) kref<<<1, 128>>>(dA, dB, dD, swap == 5); else k<<<1, 128>>>(dA, dB, dD, swap);
   cudaError_t e = cudaDeviceSynchronize();
   printf("kernel: %s\n", cudaGetErrorString(e));
   cudaMemcpy(hD, dD, sizeof hD, cudaMemcpyDeviceToHost);
