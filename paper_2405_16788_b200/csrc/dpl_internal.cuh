@@ -103,12 +103,11 @@ struct TreeView {
   const double* pt_pos64;
   const float4* pt_geo;
   const float4* pt_row;     // N x F4 (sorted order)
-  // tf32 split of the payload rows (hi = row truncated to tf32, lo = row - hi),
-  // only when the TMEM forward is enabled (forward_tm.cu); null otherwise
-  const float4* node_row_hi;
-  const float4* node_row_lo;
-  const float4* pt_row_hi;
-  const float4* pt_row_lo;
+  // tf32 split of the payload rows, [row][hi F4 float4 | lo F4 float4] (hi = row
+  // truncated to tf32, lo = row - hi), only when the TMEM forward is enabled
+  // (forward_tm.cu); null otherwise
+  const float4* node_row_split;
+  const float4* pt_row_split;
   const float* pt_nrm;  // N x 3 sorted
   const float* pt_mu;   // N x C sorted (reference channel order)
   int P;                // radial pad (floats, multiple of 4)

@@ -18,8 +18,10 @@
 // accumulator zero on B200): atoms of 4 k-rows x 128 B (32 MN elements), the
 // 32-byte chunk c of row k stored at c ^ (k & 3); LBO = stride of MN atoms,
 // SBO = stride of the 4-row k groups. A source's row is 12 cp.async chunks of
-// 16 B (the split rows node_row_hi / _lo are precomputed with the moments), its
+// 16 B (the split rows [hi | lo] are precomputed with the moments), its
 // weights one conflict-free STS per lane.
+#include <algorithm>
+
 #include "forward.cuh"
 #include "tc05.cuh"
 #include "traverse.cuh"
@@ -166,16 +168,21 @@ __global__ void __launch_bounds__(FT_WARPS * 32, FT_NS == 1 ? 4 : 3)
     const bool singular = kp.mode == KM_SINGULAR;
     const float4* __restrict__ node_row = tv.node_row;
     const float4* __restrict__ pt_row = tv.pt_row;
-    // split rows: the same index space as node_row / pt_row
-    const ptrdiff_t node_hi = tv.node_row_hi - tv.node_row, node_lo = tv.node_row_lo - tv.node_row;
-    const ptrdiff_t pt_hi = tv.pt_row_hi - tv.pt_row, pt_lo = tv.pt_row_lo - tv.pt_row;
+    // split rows [row][hi | lo]: row r starts at float4 index 2 F4 r
+    const float4* __restrict__ node_split = tv.node_row_split;
+    const float4* __restrict__ pt_split = tv.pt_row_split;
     int2* stk = reinterpret_cast<int2*>(wb + FT_STK);
     float4* vb = reinterpret_cast<float4*>(wb + FT_VB);
     const uint32_t s_a = smem_addr(wb + FT_A_HI), s_b = smem_addr(wb + FT_B_HI);
-    // this lane's place in a tile row: weights by query, row chunk j = lane - 1
-    const uint32_t b_c = (uint32_t)lane >> 3, b_in = ((uint32_t)lane & 7u) * 4u;
+    // Tile offsets. Row k of a tile starts at (k >> 2) 512 + (k & 3) 128 and its
+    // 32-byte chunks are permuted by XOR with (k & 3): every field sits in its own
+    // bits, so an element's offset is (lane constant) ^ U(k) with the warp-uniform
+    // U(k) = (k >> 2) 512 + (k & 3) (128 + 32). Weights: lane n is element n of the
+    // row; source rows: lane L in 1..12 copies 16-byte chunk j = L - 1 (radial
+    // channels 4 j .. 4 j + 3; MN atom j >> 3).
+    const uint32_t b0 = (((uint32_t)lane >> 3) << 5) + ((uint32_t)lane & 7u) * 4u;
     const uint32_t j = (uint32_t)(lane - 1) & 15u;
-    const uint32_t a_base = (j >> 3) * 1024u + (j & 1u) * 16u, a_c = (j & 7u) >> 1;
+    const uint32_t a0 = (j >> 3) * 1024u + (((j & 7u) >> 1) << 5) + (j & 1u) * 16u;
     const bool a_lane = lane >= 1 && lane < F4;
     constexpr uint32_t IDESC = ft_idesc(64, 32);
     int nent = 0;
@@ -196,8 +203,7 @@ __global__ void __launch_bounds__(FT_WARPS * 32, FT_NS == 1 ? 4 : 3)
     // the batch's 8 sources -> three MMAs into the warp's accumulator
     auto evaluate = [&]() {
       for (int k = nent; k < 8; ++k) {  // rows without a source: zero weights
-        const uint32_t off = (uint32_t)(k >> 2) * 512u + (uint32_t)(k & 3) * 128u +
-                             ((b_c ^ (uint32_t)(k & 3)) << 5) + b_in;
+        const uint32_t off = b0 ^ ((uint32_t)(k >> 2) * 512u + (uint32_t)(k & 3) * 160u);
         *reinterpret_cast<float*>(tb + FT_B_HI + off) = 0.f;
         *reinterpret_cast<float*>(tb + FT_B_LO + off) = 0.f;
       }
@@ -221,29 +227,27 @@ __global__ void __launch_bounds__(FT_WARPS * 32, FT_NS == 1 ? 4 : 3)
       st = (st + 1u) % (uint32_t)FT_NS;
       tb = wb + st * FT_STAGE;
     };
-    // v: the source's dipole moment; rowsrc indexes node_row / pt_row, d_hi / d_lo
-    // are the offsets of its split copies
-    auto store_entry = [&](float4 wv, const float4* rowsrc, ptrdiff_t d_hi, ptrdiff_t d_lo,
-                           float4 v) {  // nent < 8
+    // v: the source's dipole moment; split: the source's [hi | lo] row
+    auto store_entry = [&](float4 wv, const float4* split, float4 v) {  // nent < 8
       if (nent == 0) stage_free(st);  // the MMAs that last read these tiles are done
       accd = fmaf(wv.x, v.x, fmaf(wv.y, v.y, fmaf(wv.z, v.z, accd)));
-      const uint32_t kr = (uint32_t)(nent >> 2) * 512u + (uint32_t)(nent & 3) * 128u;
-      const uint32_t ks = (uint32_t)(nent & 3);
-      const uint32_t offb = kr + ((b_c ^ ks) << 5) + b_in;
+      const uint32_t u = (uint32_t)(nent >> 2) * 512u + (uint32_t)(nent & 3) * 160u;
+      const uint32_t offb = b0 ^ u;
       const float wh = __uint_as_float(__float_as_uint(wv.w) & 0xffffe000u);
       *reinterpret_cast<float*>(tb + FT_B_HI + offb) = wh;
       *reinterpret_cast<float*>(tb + FT_B_LO + offb) = wv.w - wh;
       if (a_lane) {
-        const uint32_t offa = st * FT_STAGE + a_base + kr + ((a_c ^ ks) << 5);
-        cp_async16(s_a + offa, rowsrc + d_hi + lane);
-        cp_async16(s_a + 2048u + offa, rowsrc + d_lo + lane);
+        const uint32_t offa = st * FT_STAGE + (a0 ^ u);
+        const float4* src = split + lane;
+        cp_async16(s_a + offa, src);
+        cp_async16(s_a + 2048u + offa, src + F4);
       }
       ++nent;
     };
-    auto append = [&](float4 wv, const float4* rowsrc, ptrdiff_t d_hi, ptrdiff_t d_lo) {
+    auto append = [&](float4 wv, const float4* rowsrc, const float4* split) {
       const float4 v = __ldg(rowsrc);
       if (nent == 8) evaluate();
-      store_entry(wv, rowsrc, d_hi, d_lo, v);
+      store_entry(wv, split, v);
     };
 
     const int64_t wg = (int64_t)blockIdx.x * FT_WARPS + w;
@@ -286,18 +290,16 @@ __global__ void __launch_bounds__(FT_WARPS * 32, FT_NS == 1 ? 4 : 3)
             const bool fa = ((unsigned)tpi.y >> lane) & 1u, fb = ((unsigned)tb.y >> lane) & 1u;
             if (REG) {
               store_entry(fwd_w_far_m(ax, ay, az, sa, sel0(fa, la.w), kp.near2),
-                          node_row + (size_t)(src & IL_NODE) * F4, node_hi, node_lo, vb[i]);
+                          node_split + (size_t)(src & IL_NODE) * (2 * F4), vb[i]);
               store_entry(fwd_w_far_m(bx, by, bz, sb, sel0(fb, lb.w), kp.near2),
-                          node_row + (size_t)((uint32_t)tb.x & IL_NODE) * F4, node_hi, node_lo,
-                          vb[i + 1]);
+                          node_split + (size_t)((uint32_t)tb.x & IL_NODE) * (2 * F4), vb[i + 1]);
             } else {
               const float4 wa = fwd_w_far(ax, ay, az, sa, la.w), wbv = fwd_w_far(bx, by, bz, sb, lb.w);
               store_entry(make_float4(fa ? wa.x : 0.f, fa ? wa.y : 0.f, fa ? wa.z : 0.f, fa ? wa.w : 0.f),
-                          node_row + (size_t)(src & IL_NODE) * F4, node_hi, node_lo, vb[i]);
+                          node_split + (size_t)(src & IL_NODE) * (2 * F4), vb[i]);
               store_entry(make_float4(fb ? wbv.x : 0.f, fb ? wbv.y : 0.f, fb ? wbv.z : 0.f,
                                       fb ? wbv.w : 0.f),
-                          node_row + (size_t)((uint32_t)tb.x & IL_NODE) * F4, node_hi, node_lo,
-                          vb[i + 1]);
+                          node_split + (size_t)((uint32_t)tb.x & IL_NODE) * (2 * F4), vb[i + 1]);
             }
             ++i;
             continue;
@@ -320,7 +322,7 @@ __global__ void __launch_bounds__(FT_WARPS * 32, FT_NS == 1 ? 4 : 3)
               wv.z = mine ? f.z : 0.f, wv.w = mine ? f.w : 0.f;
             }
             if (nent == 8) evaluate();
-            store_entry(wv, node_row + (size_t)node * F4, node_hi, node_lo, vb[i]);
+            store_entry(wv, node_split + (size_t)node * (2 * F4), vb[i]);
           } else {
             for (int jp = tpi.z; jp < tpi.w; ++jp) {
               float4 wv = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -332,7 +334,7 @@ __global__ void __launch_bounds__(FT_WARPS * 32, FT_NS == 1 ? 4 : 3)
                 if (!(singular && r2 == 0.f && coincident_exact(tv.pt_pos64 + 3 * (size_t)jp, xq)))
                   wv = fwd_w(dx, dy, dz, r2, ph.w, kp);
               }
-              append(wv, pt_row + (size_t)jp * F4, pt_hi, pt_lo);
+              append(wv, pt_row + (size_t)jp * F4, pt_split + (size_t)jp * (2 * F4));
             }
           }
         }
@@ -359,7 +361,7 @@ __global__ void __launch_bounds__(FT_WARPS * 32, FT_NS == 1 ? 4 : 3)
       const unsigned farm = __ballot_sync(FULL_MASK, far);
       if (farm && A > 0.f) {  // area > 0 (bhtree.cpp:205)
         const float4 wv = far ? fwd_w(dx, dy, dz, s, A, kp) : make_float4(0.f, 0.f, 0.f, 0.f);
-        append(wv, node_row + (size_t)node * F4, node_hi, node_lo);
+        append(wv, node_row + (size_t)node * F4, node_split + (size_t)node * (2 * F4));
       }
       const unsigned openm = mask & ~farm;
       if (openm) {
@@ -374,7 +376,7 @@ __global__ void __launch_bounds__(FT_WARPS * 32, FT_NS == 1 ? 4 : 3)
               if (!(singular && r2 == 0.f && coincident_exact(tv.pt_pos64 + 3 * (size_t)jp, x)))
                 wv = fwd_w(dx, dy, dz, r2, ph.w, kp);
             }
-            append(wv, pt_row + (size_t)jp * F4, pt_hi, pt_lo);
+            append(wv, pt_row + (size_t)jp * F4, pt_split + (size_t)jp * (2 * F4));
           }
         } else {
           if (sp + tp.y > DPL_STACK_PER_WARP) {
@@ -436,7 +438,11 @@ __global__ void __launch_bounds__(FT_WARPS * 32, FT_NS == 1 ? 4 : 3)
 
 template <bool LIST, bool REG>
 static void launch_ftm(const Tree& t, const KParams& kp, const FwdArgs& a, int nr, IListView lv) {
-  const size_t smem = (size_t)FT_WARPS * FT_WARP + 1024;
+  // 128 TMEM columns per CTA: at most 4 CTAs of an SM can hold their accumulators.
+  // The request is padded so that no fifth CTA becomes resident: it would spin in
+  // tcgen05.alloc (9 % of the issued instructions in the first ncu capture) with
+  // its other warps parked at the barrier behind it.
+  const size_t smem = std::max<size_t>((size_t)FT_WARPS * FT_WARP + 1024, 47 * 1024);
   static std::atomic<unsigned long long> attr{0};
   ensure_max_dyn_smem(k_forward_tm<LIST, REG>, t.device, smem, attr);
   const unsigned blocks = (unsigned)((a.q + FT_WARPS * 32 - 1) / (FT_WARPS * 32));
@@ -450,7 +456,7 @@ static void launch_ftm(const Tree& t, const KParams& kp, const FwdArgs& a, int n
 // range (the caller falls back to forward_tc / forward2).
 bool forward_tm_launch(const Tree& t, const KParams& kp, const FwdArgs& a) {
   if (a.grad_mode != 0 || a.counters || (a.single && a.only_ch < 0)) return false;
-  if (t.Cd != 1 || t.PR != 48 || t.F4 != FT_F4 || !t.node_row_hi.p) return false;
+  if (t.Cd != 1 || t.PR != 48 || t.F4 != FT_F4 || !t.node_row_split.p) return false;
   if (a.only_ch >= 0 && t.kinds[a.only_ch] == 0) return false;  // dipole-only variant: forward_tc
   const int nr = a.nr_limit >= 0 ? std::min(a.nr_limit, t.Cr) : t.Cr;
   const bool reg = kp.mode == KM_REGULARIZED && kp.near2 >= REG_MIN_NEAR2;

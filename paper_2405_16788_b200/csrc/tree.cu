@@ -226,10 +226,8 @@ TreeView Tree::view() const {
   v.pt_geo = pt_geo.as<float4>();
   v.pt_row = pt_row.as<float4>();
   v.pt_rec = pt_rec.as<PtRec>();
-  v.node_row_hi = node_row_hi.as<float4>();
-  v.node_row_lo = node_row_lo.as<float4>();
-  v.pt_row_hi = pt_row_hi.as<float4>();
-  v.pt_row_lo = pt_row_lo.as<float4>();
+  v.node_row_split = node_row_split.as<float4>();
+  v.pt_row_split = pt_row_split.as<float4>();
   v.pt_nrm = pt_nrm.as<float>();
   v.pt_mu = pt_mud.as<float>();
   v.P = PR;
@@ -696,15 +694,17 @@ bool forward_tmem_enabled() {
   return v;
 }
 
-// hi = v truncated to tf32 (10 mantissa bits), lo = v - hi (exact)
-__global__ void k_rows_split(const float* __restrict__ rows, float* __restrict__ hi,
-                             float* __restrict__ lo, int64_t n) {
+// out[row] = [hi | lo] with hi = v truncated to tf32 (10 mantissa bits), lo = v - hi
+// (exact); W floats per row
+__global__ void k_rows_split(const float* __restrict__ rows, float* __restrict__ out, int64_t n,
+                             int W) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const float v = rows[i];
     const float h = __uint_as_float(__float_as_uint(v) & 0xffffe000u);
-    hi[i] = h;
-    lo[i] = v - h;
+    const int64_t r = i / W, c = i - r * W;
+    out[2 * r * W + c] = h;
+    out[(2 * r + 1) * W + c] = v - h;
   }
 }
 
@@ -753,15 +753,13 @@ void tree_compute_moments(Tree& t) {
       t.node_sums.as<double>(), t.node_row.as<float4>());
   count_launch();
   if (forward_tmem_enabled()) {
-    const size_t nn = (size_t)(t.nodes + 1) * t.F4, np = (size_t)(t.n + 1) * t.F4;
-    t.node_row_hi.reserve(sizeof(float4) * nn);
-    t.node_row_lo.reserve(sizeof(float4) * nn);
-    t.pt_row_hi.reserve(sizeof(float4) * np);
-    t.pt_row_lo.reserve(sizeof(float4) * np);
-    k_rows_split<<<8 * 148, 256, 0, t.stream>>>(t.node_row.as<float>(), t.node_row_hi.as<float>(),
-                                                 t.node_row_lo.as<float>(), (int64_t)t.nodes * t.F4 * 4);
-    k_rows_split<<<8 * 148, 256, 0, t.stream>>>(t.pt_row.as<float>(), t.pt_row_hi.as<float>(),
-                                                 t.pt_row_lo.as<float>(), (int64_t)t.n * t.F4 * 4);
+    const int Wf = 4 * t.F4;
+    t.node_row_split.reserve(sizeof(float) * 2 * (size_t)(t.nodes + 1) * Wf);
+    t.pt_row_split.reserve(sizeof(float) * 2 * (size_t)(t.n + 1) * Wf);
+    k_rows_split<<<8 * 148, 256, 0, t.stream>>>(t.node_row.as<float>(), t.node_row_split.as<float>(),
+                                                 (int64_t)t.nodes * Wf, Wf);
+    k_rows_split<<<8 * 148, 256, 0, t.stream>>>(t.pt_row.as<float>(), t.pt_row_split.as<float>(),
+                                                 (int64_t)t.n * Wf, Wf);
     count_launch(2);
   }
   DPL_CUDA(cudaGetLastError());

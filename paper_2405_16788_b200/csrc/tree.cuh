@@ -61,7 +61,7 @@ struct Tree {
   // sorted point data
   DevBuf pt_pos64, pt_geo, pt_row, pt_nrm, pt_mud, pt_rec;
   // tf32 hi / lo split of node_row / pt_row for the TMEM forward (DPL_FORWARD_TMEM)
-  DevBuf node_row_hi, node_row_lo, pt_row_hi, pt_row_lo;
+  DevBuf node_row_split, pt_row_split;  // [row][hi | lo]
   DevBuf chmap;  // int32 [Cd dip ids | Cr rad ids]
   // scratch
   DevBuf scratch[8];
