@@ -353,6 +353,10 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
         }
       }
     }
+    // NG == 3: channel group 2 (16 channels) of two consecutive entries shares one
+    // exchange and one full-warp RED: half 0 completes the even entry, half 1 the odd
+    float sg2_prev = 0.f;
+    double* dst_prev = nullptr;
 #pragma unroll 2
     for (int e = 0; e < nent; ++e) {
       const int m = meta[e];
@@ -384,14 +388,26 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
         else
           red_add_f32_if(dst_s + lane, t01, lane < nr && t01 != 0.f);
         if constexpr (NG == 3) {
-          const float t2 = sg[2] + __shfl_xor_sync(FULL_MASK, sg[2], 16);
-          red_add_f32_if(dst_s + 32 + g16, t2, hw == 0 && okg[2] && t2 != 0.f);
+          if (e & 1) {  // own partial + the partner's, as the one-entry form: the same sums
+            const float mine = hw ? sg[2] : sg2_prev;
+            const float t2 = mine + __shfl_xor_sync(FULL_MASK, hw ? sg2_prev : sg[2], 16);
+            red_add_f32_if((hw ? dst_s : dst_prev) + 32 + g16, t2, okg[2] && t2 != 0.f);
+          } else {
+            sg2_prev = sg[2];
+            dst_prev = dst_s;
+          }
         }
         if constexpr (NG == 4) {
           const float t23 = (hw ? sg[NG - 1] : sg[2]) +
                             __shfl_xor_sync(FULL_MASK, hw ? sg[2] : sg[NG - 1], 16);
           red_add_f32_if(dst_s + 32 + lane, t23, 32 + lane < nr && t23 != 0.f);
         }
+      }
+    }
+    if constexpr (FF && !VR && NG == 3) {
+      if (nent & 1) {  // the last entry of an odd batch has no partner
+        const float t2 = sg2_prev + __shfl_xor_sync(FULL_MASK, sg2_prev, 16);
+        red_add_f32_if(dst_prev + 32 + g16, t2, hw == 0 && okg[2] && t2 != 0.f);
       }
     }
     if constexpr (FF && !VR) {
