@@ -138,9 +138,6 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = acc[mt][nt][2] = acc[mt][nt][3] = 0.f;
 
-  // the staged rows start as zeros (see evaluate: unpredicated reads of the tail slots)
-  for (int i = lane; i < ENT * RSF; i += 32) rows[i] = 0.f;
-  __syncwarp();
   const bool singular = kp.mode == KM_SINGULAR;
   const float4* __restrict__ node_row = tv.node_row;
   const float4* __restrict__ pt_row = tv.pt_row;
@@ -171,10 +168,8 @@ __global__ void __launch_bounds__(WARPS * 32) __maxnreg__(MAXR)
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
         uint32_t bh0, bl0, bh1, bl1;
-        // slots >= nent hold zeros or an earlier source's (finite) row; their
-        // weights are zero (tail fill above), so they add exact zeros: no predicate
-        const float v0 = r0[8 * nt];
-        const float v1 = r1[8 * nt];
+        const float v0 = (e0 + tq < nent) ? r0[8 * nt] : 0.f;
+        const float v1 = (e0 + tq + 4 < nent) ? r1[8 * nt] : 0.f;
         split_tf32(v0, bh0, bl0);
         split_tf32(v1, bh1, bl1);
 #pragma unroll
